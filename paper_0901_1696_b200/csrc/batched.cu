@@ -1,0 +1,192 @@
+// Batched small-n RFP Cholesky (BASELINE config 4: 65,536 x n = 64).
+//
+// One CTA per matrix.  The whole RFP buffer (nt doubles, 16,640 B at n = 64)
+// is read from HBM once with coalesced loads into shared memory, factored
+// (and, for the fused entry point, the n x nrhs right-hand side solved) in
+// shared memory, and written back once -- so HBM traffic is the algorithmic
+// 2*nt*8 (+2*n*nrhs*8) bytes per matrix.  Inside shared memory the factor is
+// computed on the logical lower triangle (for uplo 'U' the stored upper
+// triangle is its transpose, U = L^T, the identity used by blas_potrf), so
+// all eight RFP layouts share one code path; the index map is the RFP cell
+// map of SURVEY Appendix B (layout.py:127-163).
+#include "../../include/rfpk_b200.h"
+#include "rfp.cuh"
+
+namespace rfpk {
+
+constexpr int BMAX = 64;       // largest order handled by the batched kernels
+constexpr int BLD = BMAX + 1;  // smem column stride of the expanded triangle
+
+__device__ __forceinline__ i64 rfp_off(const RfpDesc& r, int i, int j) {
+  // (i, j) of the *stored* triangle (i >= j for 'L', i <= j for 'U')
+  i64 row, col;
+  if (r.lower) {
+    if (j < r.n1) { row = i + r.d; col = j; }
+    else { row = j - r.n1; col = i - r.n1 + 1 - r.d; }
+  } else {
+    if (j >= r.n2) { row = i; col = j - r.n2; }
+    else { row = j + r.n2 + 1; col = i; }
+  }
+  return r.trans ? row * r.n1 + col : col * r.ldar + row;
+}
+
+template <int NT>
+__device__ void batched_body(const RfpDesc r, double* __restrict__ arf, int nrhs,
+                             double* __restrict__ b, i64 ldb, int* info_out, bool factor,
+                             bool solve) {
+  __shared__ double L[BMAX * BLD];
+  __shared__ double X[BMAX * 8];
+  __shared__ int fail;
+  const int n = (int)r.n, tid = threadIdx.x;
+  if (tid == 0) fail = 0;
+  // expand: L(i, j) for i >= j of the logical lower triangle
+  for (int e = tid; e < n * n; e += NT) {
+    int i = e % n, j = e / n;
+    if (i >= j) L[i + j * BLD] = r.lower ? arf[rfp_off(r, i, j)] : arf[rfp_off(r, j, i)];
+  }
+  __syncthreads();
+  if (factor) {
+    for (int k = 0; k < n; ++k) {
+      double d = L[k + k * BLD];
+      if (!(d > 0.0)) {
+        if (tid == 0) fail = k + 1;
+        break;
+      }
+      d = sqrt(d);
+      for (int i = k + 1 + tid; i < n; i += NT) L[i + k * BLD] /= d;
+      __syncthreads();
+      const int m = n - k - 1;
+      for (int e = tid; e < m * m; e += NT) {
+        int i = k + 1 + e % m, j = k + 1 + e / m;
+        if (j <= i) L[i + j * BLD] = fma(-L[i + k * BLD], L[j + k * BLD], L[i + j * BLD]);
+      }
+      if (tid == 0) L[k + k * BLD] = d;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (tid == 0) *info_out = fail;
+    if (fail) return;
+    // compress the factor back into the RFP buffer
+    for (int e = tid; e < n * n; e += NT) {
+      int i = e % n, j = e / n;
+      if (i >= j) {
+        if (r.lower) arf[rfp_off(r, i, j)] = L[i + j * BLD];
+        else arf[rfp_off(r, j, i)] = L[i + j * BLD];
+      }
+    }
+  }
+  if (!solve || nrhs == 0) return;
+  // X = B (n x nrhs, column-major); L L^T X = B, one column per thread group
+  for (int c0 = 0; c0 < nrhs; c0 += 8) {
+    const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
+    for (int e = tid; e < n * cw; e += NT) {
+      int i = e % n, c = e / n;
+      X[i + c * BMAX] = b[i + (i64)(c0 + c) * ldb];
+    }
+    __syncthreads();
+    // forward substitution L y = b: rows processed in order, columns in parallel
+    for (int i = 0; i < n; ++i) {
+      if (tid < cw) X[i + tid * BMAX] /= L[i + i * BLD];
+      __syncthreads();
+      for (int e = tid; e < (n - i - 1) * cw; e += NT) {
+        int rr = i + 1 + e % (n - i - 1), c = e / (n - i - 1);
+        X[rr + c * BMAX] = fma(-L[rr + i * BLD], X[i + c * BMAX], X[rr + c * BMAX]);
+      }
+      __syncthreads();
+    }
+    // back substitution L^T x = y
+    for (int i = n - 1; i >= 0; --i) {
+      if (tid < cw) X[i + tid * BMAX] /= L[i + i * BLD];
+      __syncthreads();
+      for (int e = tid; e < i * cw; e += NT) {
+        int rr = e % i, c = e / i;
+        X[rr + c * BMAX] = fma(-L[i + rr * BLD], X[i + c * BMAX], X[rr + c * BMAX]);
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < n * cw; e += NT) {
+      int i = e % n, c = e / n;
+      b[i + (i64)(c0 + c) * ldb] = X[i + c * BMAX];
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64 stride_arf,
+                                                     int nrhs, double* b, i64 ldb, i64 stride_b,
+                                                     int* info, int factor, int solve) {
+  const i64 k = blockIdx.x;
+  int* inf = info + k;
+  batched_body<NT>(r, arf + k * stride_arf, nrhs, b ? b + k * stride_b : nullptr, ldb, inf,
+                   factor != 0, solve != 0);
+}
+
+int batched_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, int nrhs, double* b,
+                   i64 ldb, i64 stride_b, int* info, bool factor, bool solve, cudaStream_t st) {
+  if (batch == 0) return 0;
+  cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int) * batch, st);
+  if (e != cudaSuccess) return (int)e;
+  if (r.n == 0) return 0;
+  batched_kernel<128><<<(unsigned)batch, 128, 0, st>>>(r, arf, stride_arf, nrhs, b, ldb, stride_b,
+                                                       info, factor, solve);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace rfpk
+
+using namespace rfpk;
+
+namespace {
+char upc(char c) { return (c >= 'a' && c <= 'z') ? (char)(c - 32) : c; }
+int check(char& transr, char& uplo, int64_t n) {
+  transr = upc(transr);
+  uplo = upc(uplo);
+  if (!(transr == 'N' || transr == 'T' || transr == 'C')) return -1;
+  if (!(uplo == 'L' || uplo == 'U')) return -2;
+  if (n < 0 || n > BMAX) return -3;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int rfpk_dpftrf_batched(char transr, char uplo, int64_t n, double* arf, int64_t stride_arf,
+                        int64_t batch, int* info, rfpk_stream_t s) {
+  if (int rc = check(transr, uplo, n)) return rc;
+  if (stride_arf < n * (n + 1) / 2) return -5;
+  if (batch < 0) return -6;
+  if (!info) return -7;
+  return batched_launch(rfp_desc(n, uplo, transr), arf, stride_arf, batch, 0, nullptr, 1, 0, info,
+                        true, false, reinterpret_cast<cudaStream_t>(s));
+}
+
+int rfpk_dpftrs_batched(char transr, char uplo, int64_t n, int64_t nrhs, const double* arf,
+                        int64_t stride_arf, double* b, int64_t ldb, int64_t stride_b,
+                        int64_t batch, int* info, rfpk_stream_t s) {
+  if (int rc = check(transr, uplo, n)) return rc;
+  if (nrhs < 0) return -4;
+  if (stride_arf < n * (n + 1) / 2) return -6;
+  if (ldb < (n > 1 ? n : 1)) return -8;
+  if (batch < 0) return -10;
+  if (!info) return -11;
+  return batched_launch(rfp_desc(n, uplo, transr), const_cast<double*>(arf), stride_arf, batch,
+                        (int)nrhs, b, ldb, stride_b, info, false, true,
+                        reinterpret_cast<cudaStream_t>(s));
+}
+
+int rfpk_dpftrf_pftrs_batched(char transr, char uplo, int64_t n, int64_t nrhs, double* arf,
+                              int64_t stride_arf, double* b, int64_t ldb, int64_t stride_b,
+                              int64_t batch, int* info, rfpk_stream_t s) {
+  if (int rc = check(transr, uplo, n)) return rc;
+  if (nrhs < 0) return -4;
+  if (stride_arf < n * (n + 1) / 2) return -6;
+  if (ldb < (n > 1 ? n : 1)) return -8;
+  if (batch < 0) return -10;
+  if (!info) return -11;
+  return batched_launch(rfp_desc(n, uplo, transr), arf, stride_arf, batch, (int)nrhs, b, ldb,
+                        stride_b, info, true, true, reinterpret_cast<cudaStream_t>(s));
+}
+
+}  // extern "C"

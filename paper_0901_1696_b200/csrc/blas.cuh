@@ -1,0 +1,43 @@
+// Full-format FP64/complex128 kernels on strided device views, with the
+// reference's flag semantics (kernels.py).  Everything is stream-ordered and
+// asynchronous; failures are reported through a device int (`info`), which
+// also acts as a skip flag for every later kernel of the same chain, so a
+// host never synchronises inside a factorisation.
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace rfpk {
+
+struct Ctx {
+  cudaStream_t st;
+  int* info;  // device int: 0 = ok; >0 = 1-based failure index (also skips work)
+};
+
+// Leaf size of the recursive drivers (diagonal blocks factored in one CTA).
+constexpr int LEAF = 64;
+
+// --- reference-API level (flags as characters, like kernels.py) ---------
+// gemm: C <- alpha op(A) op(B) + beta C                       (kernels.py:129)
+template <typename T>
+int blas_gemm(Ctx c, char transa, char transb, T alpha, View<T> A, View<T> B, T beta, View<T> C);
+// trsm: op(A) X = alpha B (side L) / X op(A) = alpha B (side R) (kernels.py:218)
+//       zero diagonal -> *info = 1-based index, B untouched
+template <typename T>
+int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B,
+              bool scan = true);
+// trmm: B <- alpha op(A) B / alpha B op(A)                     (kernels.py:307)
+template <typename T>
+int blas_trmm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B);
+// syrk/herk on the uplo triangle of C (real alpha/beta)        (kernels.py:405)
+template <typename T>
+int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta, View<T> C,
+              bool herm);
+// potrf: L L^H (uplo L) / U^H U (uplo U); *info = base + first failing pivot
+template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base);
+// trtri: in-place inverse; zero diagonal -> *info (matrix untouched) (kernels.py:515)
+template <typename T> int blas_trtri(Ctx c, char uplo, char diag, View<T> A, int base);
+// lauum: L^H L (uplo L) / U U^H (uplo U)                        (kernels.py:575)
+template <typename T> int blas_lauum(Ctx c, char uplo, View<T> A);
+
+}  // namespace rfpk

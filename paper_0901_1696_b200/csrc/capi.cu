@@ -1,0 +1,328 @@
+// extern "C" boundary (include/rfpk_b200.h): argument checking, info reset,
+// and dispatch into the templated drivers.  No allocations, no host syncs.
+#include "../../include/rfpk_b200.h"
+#include "rfp.cuh"
+
+using namespace rfpk;
+
+namespace {
+
+char up(char c) { return (c >= 'a' && c <= 'z') ? (char)(c - 32) : c; }
+bool one_of(char c, const char* set) {
+  for (; *set; ++set)
+    if (c == *set) return true;
+  return false;
+}
+cudaStream_t S(rfpk_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int reset_info(int* info, cudaStream_t st) {
+  if (!info) return 0;
+  cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int), st);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+template <typename T> View<T> V(const void* p, int64_t r, int64_t c, int64_t rs, int64_t cs) {
+  return View<T>{reinterpret_cast<T*>(const_cast<void*>(p)), r, c, rs, cs};
+}
+bool unit_stride(int64_t r, int64_t c, int64_t rs, int64_t cs) {
+  return rs == 1 || cs == 1 || r <= 1 || c <= 1;
+}
+
+// ---------------------------------------------------------------- conversions
+template <typename T>
+int trttf_t(char transr, char uplo, int64_t n, const void* a, int64_t lda, void* arf,
+            cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (lda < (n > 1 ? n : 1)) return -5;
+  Storage src{ST_FULL, lda, rfp_desc(n, uplo, transr)};
+  Storage dst{ST_RFP, 0, rfp_desc(n, uplo, transr)};
+  return convert<T>(src, (const T*)a, dst, (T*)arf, false, st);
+}
+template <typename T>
+int tfttr_t(char transr, char uplo, int64_t n, const void* arf, void* a, int64_t lda,
+            cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (lda < (n > 1 ? n : 1)) return -6;
+  Storage src{ST_RFP, 0, rfp_desc(n, uplo, transr)};
+  Storage dst{ST_FULL, lda, rfp_desc(n, uplo, transr)};
+  return convert<T>(src, (const T*)arf, dst, (T*)a, true, st);
+}
+template <typename T>
+int tpttf_t(char transr, char uplo, int64_t n, const void* ap, void* arf, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  Storage src{ST_PACKED, 0, rfp_desc(n, uplo, transr)};
+  Storage dst{ST_RFP, 0, rfp_desc(n, uplo, transr)};
+  return convert<T>(src, (const T*)ap, dst, (T*)arf, false, st);
+}
+template <typename T>
+int tfttp_t(char transr, char uplo, int64_t n, const void* arf, void* ap, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  Storage src{ST_RFP, 0, rfp_desc(n, uplo, transr)};
+  Storage dst{ST_PACKED, 0, rfp_desc(n, uplo, transr)};
+  return convert<T>(src, (const T*)arf, dst, (T*)ap, false, st);
+}
+template <typename T>
+int trttp_t(char uplo, int64_t n, const void* a, int64_t lda, void* ap, cudaStream_t st) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  Storage src{ST_FULL, lda, rfp_desc(n, uplo, 'N')};
+  Storage dst{ST_PACKED, 0, rfp_desc(n, uplo, 'N')};
+  return convert<T>(src, (const T*)a, dst, (T*)ap, false, st);
+}
+template <typename T>
+int tpttr_t(char uplo, int64_t n, const void* ap, void* a, int64_t lda, cudaStream_t st) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -5;
+  Storage src{ST_PACKED, 0, rfp_desc(n, uplo, 'N')};
+  Storage dst{ST_FULL, lda, rfp_desc(n, uplo, 'N')};
+  return convert<T>(src, (const T*)ap, dst, (T*)a, true, st);
+}
+
+// ---------------------------------------------------------------- RFP ops
+template <typename T>
+int pftrf_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (!info) return -5;
+  if (int rc = reset_info(info, st)) return rc;
+  return pftrf<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (T*)arf);
+}
+template <typename T>
+int pftrs_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* arf, void* b,
+            int64_t rsb, int64_t csb, int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (nrhs < 0) return -4;
+  if (!unit_stride(n, nrhs, rsb, csb)) return -7;
+  if (!info) return -8;
+  if (int rc = reset_info(info, st)) return rc;
+  return pftrs<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (const T*)arf,
+                  V<T>(b, n, nrhs, rsb, csb));
+}
+template <typename T>
+int tftri_t(char transr, char uplo, char diag, int64_t n, void* arf, int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo); diag = up(diag);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (!one_of(diag, "NU")) return -3;
+  if (n < 0) return -4;
+  if (!info) return -6;
+  if (int rc = reset_info(info, st)) return rc;
+  return tftri<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), diag, (T*)arf);
+}
+template <typename T>
+int pftri_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (!info) return -5;
+  if (int rc = reset_info(info, st)) return rc;
+  return pftri<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (T*)arf);
+}
+
+Z zc(double re, double im) { return Z{re, im}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* rfpk_version(void) { return "rfpk_b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+int rfpk_device_sms(void) {
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return -(int)e;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return e == cudaSuccess ? sms : -(int)e;
+}
+
+int rfpk_dtrttf(char t, char u, int64_t n, const double* a, int64_t lda, double* arf, rfpk_stream_t s) { return trttf_t<double>(t, u, n, a, lda, arf, S(s)); }
+int rfpk_ztrttf(char t, char u, int64_t n, const void* a, int64_t lda, void* arf, rfpk_stream_t s) { return trttf_t<Z>(t, u, n, a, lda, arf, S(s)); }
+int rfpk_dtfttr(char t, char u, int64_t n, const double* arf, double* a, int64_t lda, rfpk_stream_t s) { return tfttr_t<double>(t, u, n, arf, a, lda, S(s)); }
+int rfpk_ztfttr(char t, char u, int64_t n, const void* arf, void* a, int64_t lda, rfpk_stream_t s) { return tfttr_t<Z>(t, u, n, arf, a, lda, S(s)); }
+int rfpk_dtpttf(char t, char u, int64_t n, const double* ap, double* arf, rfpk_stream_t s) { return tpttf_t<double>(t, u, n, ap, arf, S(s)); }
+int rfpk_ztpttf(char t, char u, int64_t n, const void* ap, void* arf, rfpk_stream_t s) { return tpttf_t<Z>(t, u, n, ap, arf, S(s)); }
+int rfpk_dtfttp(char t, char u, int64_t n, const double* arf, double* ap, rfpk_stream_t s) { return tfttp_t<double>(t, u, n, arf, ap, S(s)); }
+int rfpk_ztfttp(char t, char u, int64_t n, const void* arf, void* ap, rfpk_stream_t s) { return tfttp_t<Z>(t, u, n, arf, ap, S(s)); }
+int rfpk_dtrttp(char u, int64_t n, const double* a, int64_t lda, double* ap, rfpk_stream_t s) { return trttp_t<double>(u, n, a, lda, ap, S(s)); }
+int rfpk_ztrttp(char u, int64_t n, const void* a, int64_t lda, void* ap, rfpk_stream_t s) { return trttp_t<Z>(u, n, a, lda, ap, S(s)); }
+int rfpk_dtpttr(char u, int64_t n, const double* ap, double* a, int64_t lda, rfpk_stream_t s) { return tpttr_t<double>(u, n, ap, a, lda, S(s)); }
+int rfpk_ztpttr(char u, int64_t n, const void* ap, void* a, int64_t lda, rfpk_stream_t s) { return tpttr_t<Z>(u, n, ap, a, lda, S(s)); }
+
+int rfpk_dpftrf(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftrf_t<double>(t, u, n, arf, info, S(s)); }
+int rfpk_zpftrf(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftrf_t<Z>(t, u, n, arf, info, S(s)); }
+int rfpk_dpftrs(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) {
+  if (ldb < (n > 1 ? n : 1)) return -7;
+  return pftrs_t<double>(t, u, n, nrhs, arf, b, 1, ldb, info, S(s));
+}
+int rfpk_zpftrs(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) {
+  if (ldb < (n > 1 ? n : 1)) return -7;
+  return pftrs_t<Z>(t, u, n, nrhs, arf, b, 1, ldb, info, S(s));
+}
+int rfpk_dpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pftrs_t<double>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
+int rfpk_zpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pftrs_t<Z>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
+int rfpk_dtftri(char t, char u, char d, int64_t n, double* arf, int* info, rfpk_stream_t s) { return tftri_t<double>(t, u, d, n, arf, info, S(s)); }
+int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_stream_t s) { return tftri_t<Z>(t, u, d, n, arf, info, S(s)); }
+int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftri_t<double>(t, u, n, arf, info, S(s)); }
+int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftri_t<Z>(t, u, n, arf, info, S(s)); }
+
+// ---------------------------------------------------------------- dense kernels
+int rfpk_dgemm(char ta, char tb, double alpha, const double* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
+               const double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, double beta,
+               double* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+  ta = up(ta); tb = up(tb);
+  if (!one_of(ta, "NTC")) return -1;
+  if (!one_of(tb, "NTC")) return -2;
+  if (!unit_stride(ar, ac, ars, acs)) return -4;
+  if (!unit_stride(br, bc, brs, bcs)) return -9;
+  if (!unit_stride(cr, cc, crs, ccs)) return -15;
+  View<double> A = V<double>(a, ar, ac, ars, acs), B = V<double>(b, br, bc, brs, bcs),
+               C = V<double>(c, cr, cc, crs, ccs);
+  int64_t m = ta == 'N' ? ar : ac, k = ta == 'N' ? ac : ar;
+  int64_t kb = tb == 'N' ? br : bc, nn = tb == 'N' ? bc : br;
+  if (alpha != 0 && (m != cr || nn != cc || k != kb)) return -4;
+  return blas_gemm<double>(Ctx{S(s), nullptr}, ta, tb, alpha, A, B, beta, C);
+}
+int rfpk_zgemm(char ta, char tb, double are, double aim, const void* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
+               const void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, double bre, double bim,
+               void* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+  ta = up(ta); tb = up(tb);
+  if (!one_of(ta, "NTC")) return -1;
+  if (!one_of(tb, "NTC")) return -2;
+  if (!unit_stride(ar, ac, ars, acs)) return -5;
+  if (!unit_stride(br, bc, brs, bcs)) return -10;
+  if (!unit_stride(cr, cc, crs, ccs)) return -17;
+  View<Z> A = V<Z>(a, ar, ac, ars, acs), B = V<Z>(b, br, bc, brs, bcs), C = V<Z>(c, cr, cc, crs, ccs);
+  int64_t m = ta == 'N' ? ar : ac, k = ta == 'N' ? ac : ar;
+  int64_t kb = tb == 'N' ? br : bc, nn = tb == 'N' ? bc : br;
+  if (!(are == 0 && aim == 0) && (m != cr || nn != cc || k != kb)) return -5;
+  return blas_gemm<Z>(Ctx{S(s), nullptr}, ta, tb, zc(are, aim), A, B, zc(bre, bim), C);
+}
+
+#define TRI_ARGS_CHECK()                          \
+  side = up(side); uplo = up(uplo); trans = up(trans); diag = up(diag); \
+  if (!one_of(side, "LR")) return -1;             \
+  if (!one_of(uplo, "LU")) return -2;             \
+  if (!one_of(trans, "NTC")) return -3;           \
+  if (!one_of(diag, "NU")) return -4;             \
+  if (!unit_stride(an, an, ars, acs)) return -6;  \
+  if (!unit_stride(br, bc, brs, bcs)) return -10; \
+  if ((side == 'L' ? br : bc) != an) return -7;
+
+int rfpk_dtrsm(char side, char uplo, char trans, char diag, double alpha, const double* a, int64_t an, int64_t ars, int64_t acs,
+               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) {
+  TRI_ARGS_CHECK();
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_trsm<double>(Ctx{S(s), info}, side, uplo, trans, diag, alpha, V<double>(a, an, an, ars, acs),
+                           V<double>(b, br, bc, brs, bcs), info != nullptr);
+}
+int rfpk_ztrsm(char side, char uplo, char trans, char diag, double are, double aim, const void* a, int64_t an, int64_t ars, int64_t acs,
+               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) {
+  TRI_ARGS_CHECK();
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_trsm<Z>(Ctx{S(s), info}, side, uplo, trans, diag, zc(are, aim), V<Z>(a, an, an, ars, acs),
+                      V<Z>(b, br, bc, brs, bcs), info != nullptr);
+}
+int rfpk_dtrmm(char side, char uplo, char trans, char diag, double alpha, const double* a, int64_t an, int64_t ars, int64_t acs,
+               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) {
+  TRI_ARGS_CHECK();
+  return blas_trmm<double>(Ctx{S(s), nullptr}, side, uplo, trans, diag, alpha, V<double>(a, an, an, ars, acs),
+                           V<double>(b, br, bc, brs, bcs));
+}
+int rfpk_ztrmm(char side, char uplo, char trans, char diag, double are, double aim, const void* a, int64_t an, int64_t ars, int64_t acs,
+               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) {
+  TRI_ARGS_CHECK();
+  return blas_trmm<Z>(Ctx{S(s), nullptr}, side, uplo, trans, diag, zc(are, aim), V<Z>(a, an, an, ars, acs),
+                      V<Z>(b, br, bc, brs, bcs));
+}
+int rfpk_dsyrk(char uplo, char trans, double alpha, const double* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
+               double beta, double* c, int64_t cn, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+  uplo = up(uplo); trans = up(trans);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!one_of(trans, "NTC")) return -2;
+  if (!unit_stride(ar, ac, ars, acs)) return -4;
+  if (!unit_stride(cn, cn, crs, ccs)) return -10;
+  if (alpha != 0 && (trans == 'N' ? ar : ac) != cn) return -4;
+  return blas_syrk<double>(Ctx{S(s), nullptr}, uplo, trans, alpha, V<double>(a, ar, ac, ars, acs), beta,
+                           V<double>(c, cn, cn, crs, ccs), false);
+}
+int rfpk_zsyrk(char uplo, char trans, double alpha, const void* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
+               double beta, void* c, int64_t cn, int64_t crs, int64_t ccs, int hermitian, rfpk_stream_t s) {
+  uplo = up(uplo); trans = up(trans);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!one_of(trans, "NTC")) return -2;
+  if (!unit_stride(ar, ac, ars, acs)) return -4;
+  if (!unit_stride(cn, cn, crs, ccs)) return -10;
+  if (alpha != 0 && (trans == 'N' ? ar : ac) != cn) return -4;
+  return blas_syrk<Z>(Ctx{S(s), nullptr}, uplo, trans, alpha, V<Z>(a, ar, ac, ars, acs), beta,
+                      V<Z>(c, cn, cn, crs, ccs), hermitian != 0);
+}
+int rfpk_dpotrf(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!unit_stride(n, n, rs, cs)) return -4;
+  if (!info) return -6;
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_potrf<double>(Ctx{S(s), info}, uplo, V<double>(a, n, n, rs, cs), 0);
+}
+int rfpk_zpotrf(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!unit_stride(n, n, rs, cs)) return -4;
+  if (!info) return -6;
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_potrf<Z>(Ctx{S(s), info}, uplo, V<Z>(a, n, n, rs, cs), 0);
+}
+int rfpk_dtrtri(char uplo, char diag, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+  uplo = up(uplo); diag = up(diag);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!one_of(diag, "NU")) return -2;
+  if (!unit_stride(n, n, rs, cs)) return -5;
+  if (!info) return -7;
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_trtri<double>(Ctx{S(s), info}, uplo, diag, V<double>(a, n, n, rs, cs), 0);
+}
+int rfpk_ztrtri(char uplo, char diag, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+  uplo = up(uplo); diag = up(diag);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!one_of(diag, "NU")) return -2;
+  if (!unit_stride(n, n, rs, cs)) return -5;
+  if (!info) return -7;
+  if (int rc = reset_info(info, S(s))) return rc;
+  return blas_trtri<Z>(Ctx{S(s), info}, uplo, diag, V<Z>(a, n, n, rs, cs), 0);
+}
+int rfpk_dlauum(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!unit_stride(n, n, rs, cs)) return -4;
+  return blas_lauum<double>(Ctx{S(s), nullptr}, uplo, V<double>(a, n, n, rs, cs));
+}
+int rfpk_zlauum(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (!unit_stride(n, n, rs, cs)) return -4;
+  return blas_lauum<Z>(Ctx{S(s), nullptr}, uplo, V<Z>(a, n, n, rs, cs));
+}
+
+}  // extern "C"

@@ -1,0 +1,434 @@
+// FP64 / complex128 DMMA GEMM for sm_100a (see gemm.cuh for the contract).
+#include "gemm.cuh"
+
+namespace rfpk {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+// D += A(16x4, row) * B(4x8, col); fragments per the PTX m16n8k4 f64 layout
+// (verified on the B200 by tools/probe_mma.cu): a0=(g,t) a1=(g+8,t), b=(t,g),
+// c0..c3 = (g,2t) (g,2t+1) (g+8,2t) (g+8,2t+1) with g = lane/4, t = lane%4.
+__device__ __forceinline__ void dmma16x8x4(double* c, double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+__device__ __forceinline__ void tri_tile(int mode, int tiles, int& tm, int& tn) {
+  // blockIdx.x enumerates the tiles (ti >= tj) of a lower-triangular tile grid
+  long long b = blockIdx.x;
+  int ti = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while ((long long)(ti + 1) * (ti + 2) / 2 <= b) ++ti;
+  while ((long long)ti * (ti + 1) / 2 > b) --ti;
+  int tj = (int)(b - (long long)ti * (ti + 1) / 2);
+  if (mode == TRI_LOWER) { tm = ti; tn = tj; } else { tm = tj; tn = ti; }
+  (void)tiles;
+}
+
+__device__ __forceinline__ bool tri_keep(int mode, int row, int col) {
+  return mode == TRI_FULL || (mode == TRI_LOWER ? row >= col : row <= col);
+}
+
+// ------------------------------------------------------------ real kernel
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    dgemm_kernel(GemmArgs<double> g) {
+  constexpr int WARPS_M = BM / WM;
+  constexpr int NT = WARPS_M * (BN / WN) * 32;
+  constexpr int PA = BM + 4, PB = BN + 4;  // == 4 (mod 16): conflict-free fragment loads
+  constexpr int MI = WM / 16, NI = WN / 8;
+  extern __shared__ __align__(16) double smem_d[];
+  double* As = smem_d;
+  double* Bs = smem_d + STAGES * BK * PA;
+  if (g.skip && *g.skip) return;
+  int tm, tn;
+  if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
+  else tri_tile(MODE, g.tiles_m, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int M = g.M, N = g.N, K = g.K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  double acc[MI][NI][4];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+  const double* __restrict__ Ag = g.A;
+  const double* __restrict__ Bg = g.B;
+  const i64 lda = g.lda, ldb = g.ldb;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * BK * PA;
+    double* bs = Bs + stage * BK * PB;
+#pragma unroll
+    for (int i = tid; i < BM * BK; i += NT) {
+      int m, k;
+      if (AK) { k = i % BK; m = i / BK; } else { m = i % BM; k = i / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < M && gk < K;
+      const double* src = ok ? (AK ? Ag + (i64)gm * lda + gk : Ag + gm + (i64)gk * lda) : Ag;
+      cp_async8(as + k * PA + m, src, ok);
+    }
+#pragma unroll
+    for (int i = tid; i < BN * BK; i += NT) {
+      int n, k;
+      if (BKM) { k = i % BK; n = i / BK; } else { n = i % BN; k = i / BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      const bool ok = gn < N && gk < K;
+      const double* src = ok ? (BKM ? Bg + gk + (i64)gn * ldb : Bg + (i64)gk * ldb + gn) : Bg;
+      cp_async8(bs + k * PB + n, src, ok);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) load_stage(nk % STAGES, nk);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
+    const double* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[MI][2], bf[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        af[i][0] = as[(kk + tq) * PA + i * 16];
+        af[i][1] = as[(kk + tq) * PA + i * 16 + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < NI; ++j) bf[j] = bs[(kk + tq) * PB + j * 8];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm * WM + i * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * WN + j * 8 + 2 * tq + (r & 1);
+        if (row < M && col < N && tri_keep(MODE, row, col)) {
+          double* c = g.C + row + (i64)col * g.ldc;
+          double v = alpha * acc[i][j][r];
+          if (beta != 0.0) v = fma(beta, *c, v);
+          *c = v;
+        }
+      }
+}
+
+// ------------------------------------------------------------ complex kernel
+// Complex product from 4 real DMMAs per fragment pair on interleaved smem
+// tiles: Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br (conjugation = sign flip).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    zgemm_kernel(GemmArgs<Z> g) {
+  constexpr int WARPS_M = BM / WM;
+  constexpr int NT = WARPS_M * (BN / WN) * 32;
+  constexpr int PA = BM + 2, PB = BN + 2;  // == 2 (mod 8) complex: conflict-free LDS.128
+  constexpr int MI = WM / 16, NI = WN / 8;
+  extern __shared__ __align__(16) double smem_d[];
+  Z* As = reinterpret_cast<Z*>(smem_d);
+  Z* Bs = As + STAGES * BK * PA;
+  if (g.skip && *g.skip) return;
+  int tm, tn;
+  if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
+  else tri_tile(MODE, g.tiles_m, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int M = g.M, N = g.N, K = g.K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int gq = lane >> 2, tq = lane & 3;
+  const double sa = g.conjA ? -1.0 : 1.0, sb = g.conjB ? -1.0 : 1.0;
+
+  double re[MI][NI][4], im[MI][NI][4];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) re[i][j][r] = im[i][j][r] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+  const Z* __restrict__ Ag = g.A;
+  const Z* __restrict__ Bg = g.B;
+  const i64 lda = g.lda, ldb = g.ldb;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    Z* as = As + stage * BK * PA;
+    Z* bs = Bs + stage * BK * PB;
+#pragma unroll
+    for (int i = tid; i < BM * BK; i += NT) {
+      int m, k;
+      if (AK) { k = i % BK; m = i / BK; } else { m = i % BM; k = i / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < M && gk < K;
+      const Z* src = ok ? (AK ? Ag + (i64)gm * lda + gk : Ag + gm + (i64)gk * lda) : Ag;
+      cp_async16(as + k * PA + m, src, ok);
+    }
+#pragma unroll
+    for (int i = tid; i < BN * BK; i += NT) {
+      int n, k;
+      if (BKM) { k = i % BK; n = i / BK; } else { n = i % BN; k = i / BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      const bool ok = gn < N && gk < K;
+      const Z* src = ok ? (BKM ? Bg + gk + (i64)gn * ldb : Bg + (i64)gk * ldb + gn) : Bg;
+      cp_async16(bs + k * PB + n, src, ok);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) load_stage(nk % STAGES, nk);
+    cp_async_commit();
+    const Z* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
+    const Z* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[MI][2], ai[MI][2], nai[MI][2], br[NI], bi[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        Z v0 = as[(kk + tq) * PA + i * 16];
+        Z v1 = as[(kk + tq) * PA + i * 16 + 8];
+        ar[i][0] = v0.x; ai[i][0] = sa * v0.y;
+        ar[i][1] = v1.x; ai[i][1] = sa * v1.y;
+        nai[i][0] = -ai[i][0]; nai[i][1] = -ai[i][1];
+      }
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        Z w = bs[(kk + tq) * PB + j * 8];
+        br[j] = w.x; bi[j] = sb * w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          dmma16x8x4(re[i][j], ar[i][0], ar[i][1], br[j]);
+          dmma16x8x4(re[i][j], nai[i][0], nai[i][1], bi[j]);
+          dmma16x8x4(im[i][j], ar[i][0], ar[i][1], bi[j]);
+          dmma16x8x4(im[i][j], ai[i][0], ai[i][1], br[j]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  const Z alpha = g.alpha, beta = g.beta;
+  const bool use_beta = !(beta.x == 0.0 && beta.y == 0.0);
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm * WM + i * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * WN + j * 8 + 2 * tq + (r & 1);
+        if (row < M && col < N && tri_keep(MODE, row, col)) {
+          Z* c = g.C + row + (i64)col * g.ldc;
+          Z v = alpha * Z{re[i][j][r], im[i][j][r]};
+          if (use_beta) v = v + beta * (*c);
+          if (MODE != TRI_FULL && g.herm_diag && row == col) v.y = 0.0;
+          *c = v;
+        }
+      }
+}
+
+// ------------------------------------------------------------ scale kernel
+template <typename T>
+__global__ void scale_kernel(View<T> C, T beta, int mode, int herm_diag, const int* skip) {
+  if (skip && *skip) return;
+  i64 total = C.m * C.n;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    i64 i = e % C.m, j = e / C.m;
+    if (!tri_keep(mode, (int)i, (int)j)) continue;
+    T* c = C.at(i, j);
+    T v = is_zero(beta) ? sc_from<T>(0.0) : beta * (*c);
+    if constexpr (is_cplx<T>::value) {
+      if (herm_diag && i == j) v.y = 0.0;
+    }
+    *c = v;
+  }
+}
+
+template <typename T>
+int scale_view(View<T> C, T beta, int tri_mode, bool herm_diag, const int* skip, cudaStream_t st) {
+  if (C.empty()) return 0;
+  i64 total = C.m * C.n;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  scale_kernel<T><<<blocks, 256, 0, st>>>(C, beta, tri_mode, herm_diag ? 1 : 0, skip);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+// ------------------------------------------------------------ dispatch
+namespace {
+
+struct OperandLayout {
+  bool kmajor;  // contiguous along K
+  i64 ld;
+  bool ok;
+};
+
+// A is an M x K view (or B a K x N view, passed transposed as N x K): report
+// whether it is contiguous along its first dim (MN-major) or its second (K).
+template <typename T> OperandLayout classify(const View<T>& v) {
+  if (v.rs == 1 || v.m == 1) {
+    i64 ld = (v.n == 1) ? (v.m > 0 ? v.m : 1) : v.cs;
+    return {false, ld, true};
+  }
+  if (v.cs == 1 || v.n == 1) {
+    i64 ld = (v.m == 1) ? (v.n > 0 ? v.n : 1) : v.rs;
+    return {true, ld, true};
+  }
+  return {false, 0, false};
+}
+
+template <typename T, int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int MODE>
+int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int PA = BM + (is_cplx<T>::value ? 2 : 4), PB = BN + (is_cplx<T>::value ? 2 : 4);
+  constexpr size_t smem = (size_t)ST * BK * (PA + PB) * sizeof(T);
+  auto kern = [] {
+    if constexpr (is_cplx<T>::value) return zgemm_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
+    else return dgemm_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
+  }();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
+  GemmArgs<T> g = a;
+  g.tiles_m = tm;
+  if (MODE == TRI_FULL) {
+    dim3 grid(tm, tn);
+    kern<<<grid, NT, smem, st>>>(g);
+  } else {
+    long long nb = (long long)tm * (tm + 1) / 2;
+    kern<<<(unsigned)nb, NT, smem, st>>>(g);
+  }
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename T, int BM, int BN, int BK, int WM, int WN, int ST, int MODE>
+int launch_major(const GemmArgs<T>& a, bool ak, bool bk, cudaStream_t st) {
+  if (ak) {
+    return bk ? launch_one<T, BM, BN, BK, WM, WN, ST, true, true, MODE>(a, st)
+              : launch_one<T, BM, BN, BK, WM, WN, ST, true, false, MODE>(a, st);
+  }
+  return bk ? launch_one<T, BM, BN, BK, WM, WN, ST, false, true, MODE>(a, st)
+            : launch_one<T, BM, BN, BK, WM, WN, ST, false, false, MODE>(a, st);
+}
+
+template <typename T, int BM, int BN, int BK, int WM, int WN, int ST>
+int launch_mode(const GemmArgs<T>& a, int mode, bool ak, bool bk, cudaStream_t st) {
+  switch (mode) {
+    case TRI_LOWER: return launch_major<T, BM, BN, BK, WM, WN, ST, TRI_LOWER>(a, ak, bk, st);
+    case TRI_UPPER: return launch_major<T, BM, BN, BK, WM, WN, ST, TRI_UPPER>(a, ak, bk, st);
+    default: return launch_major<T, BM, BN, BK, WM, WN, ST, TRI_FULL>(a, ak, bk, st);
+  }
+}
+
+}  // namespace
+
+template <typename T>
+int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T beta,
+         View<T> C, bool herm_diag, const int* skip, cudaStream_t st) {
+  if (C.empty()) return 0;
+  if (A.n == 0 || is_zero(alpha)) {
+    bool unit_beta;
+    if constexpr (is_cplx<T>::value) unit_beta = beta.x == 1.0 && beta.y == 0.0;
+    else unit_beta = beta == 1.0;
+    if (unit_beta && !herm_diag) return 0;
+    return scale_view(C, beta, tri_mode, herm_diag, skip, st);
+  }
+  if (!(C.rs == 1 || C.n == 1)) {
+    // C row-major: solve C^T = op(B)^T op(A)^T (column-major)
+    View<T> At = B.t(), Bt = A.t();
+    A = At; B = Bt;
+    bool c = conjA; conjA = conjB; conjB = c;
+    C = C.t();
+    if (tri_mode == TRI_LOWER) tri_mode = TRI_UPPER;
+    else if (tri_mode == TRI_UPPER) tri_mode = TRI_LOWER;
+  }
+  OperandLayout la = classify(A);
+  OperandLayout lb = classify(B.t());  // B^T is N x K
+  if (!la.ok || !lb.ok || !(C.rs == 1 || C.n == 1)) return -100;
+  GemmArgs<T> g;
+  g.M = (int)C.m; g.N = (int)C.n; g.K = (int)A.n;
+  g.A = A.p; g.lda = la.ld;
+  g.B = B.p; g.ldb = lb.ld;
+  g.C = C.p; g.ldc = (C.n == 1) ? (C.m > 0 ? C.m : 1) : C.cs;
+  g.alpha = alpha; g.beta = beta;
+  g.conjA = conjA; g.conjB = conjB;
+  g.herm_diag = herm_diag ? 1 : 0;
+  g.skip = skip;
+  g.tiles_m = 0;
+  // operand "K-major": A contiguous along K  <=> la.kmajor; for B, B^T (N x K)
+  // contiguous along K <=> lb.kmajor.
+  const bool ak = la.kmajor, bk = lb.kmajor;
+  if constexpr (is_cplx<T>::value) {
+    long long tiles = (long long)((g.M + 63) / 64) * ((g.N + 63) / 64);
+    if (tiles >= num_sms())
+      return launch_mode<T, 64, 64, 8, 32, 32, 3>(g, tri_mode, ak, bk, st);
+    return launch_mode<T, 32, 32, 8, 16, 16, 3>(g, tri_mode, ak, bk, st);
+  } else {
+    long long tiles = (long long)((g.M + 127) / 128) * ((g.N + 127) / 128);
+    if (tiles >= (num_sms() * 3) / 4)
+      return launch_mode<T, 128, 128, 16, 64, 32, 3>(g, tri_mode, ak, bk, st);
+    return launch_mode<T, 64, 64, 16, 32, 32, 3>(g, tri_mode, ak, bk, st);
+  }
+}
+
+template int gemm<double>(int, double, View<double>, bool, View<double>, bool, double,
+                          View<double>, bool, const int*, cudaStream_t);
+template int gemm<Z>(int, Z, View<Z>, bool, View<Z>, bool, Z, View<Z>, bool, const int*,
+                     cudaStream_t);
+template int scale_view<double>(View<double>, double, int, bool, const int*, cudaStream_t);
+template int scale_view<Z>(View<Z>, Z, int, bool, const int*, cudaStream_t);
+
+}  // namespace rfpk

@@ -1,0 +1,248 @@
+// RFP drivers (rfp.py) and full/packed/RFP conversion kernels (convert.py).
+#include "rfp.cuh"
+
+namespace rfpk {
+
+RfpDesc rfp_desc(i64 n, char uplo, char transr) {
+  RfpDesc d;
+  d.n = n;
+  d.n1 = (n + 1) / 2;
+  d.n2 = n - d.n1;
+  d.nt = n * (n + 1) / 2;
+  d.ldar = (n % 2) ? n : n + 1;
+  d.d = (n % 2) ? 0 : 1;
+  d.lower = uplo == 'L';
+  d.trans = transr != 'N';
+  return d;
+}
+
+template <typename T>
+void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2, View<T>& s1) {
+  const i64 rs = d.trans ? d.n1 : 1, cs = d.trans ? 1 : d.ldar;
+  auto mk = [&](i64 r0, i64 c0, i64 m, i64 n) { return View<T>{buf + r0 * rs + c0 * cs, m, n, rs, cs}; };
+  const i64 n1 = d.n1, n2 = d.n2, sh = d.d;
+  if (d.lower) {
+    t1 = mk(sh, 0, n1, n1);
+    t2 = mk(0, 1 - sh, n2, n2);
+    s1 = mk(n1 + sh, 0, n2, n1);
+  } else {
+    t1 = mk(n2 + 1, 0, n2, n2);
+    t2 = mk(n2, 0, n1, n1);
+    s1 = mk(0, 0, n2, n1);
+  }
+}
+
+template <typename T> static T one() { return sc_from<T>(1.0); }
+template <typename T> static T m_one() { return sc_from<T>(-1.0); }
+
+#define TRY(x)              \
+  do {                      \
+    int rc_ = (x);          \
+    if (rc_) return rc_;    \
+  } while (0)
+
+// SRPA factorization (rfp.py:55-91)
+template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
+  if (d.n == 0) return 0;
+  const bool herm = is_cplx<T>::value;
+  View<T> t1, t2, s1;
+  rfp_blocks(d, arf, t1, t2, s1);
+  if (d.lower) {
+    TRY(blas_potrf(c, 'L', t1, 0));
+    if (d.n2) {
+      TRY(blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false));
+      TRY(blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm));
+      TRY(blas_potrf(c, 'U', t2, (int)d.n1));
+    }
+    return 0;
+  }
+  if (d.n2) {
+    TRY(blas_potrf(c, 'L', t1, 0));
+    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false));
+    TRY(blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm));
+  }
+  return blas_potrf(c, 'U', t2, (int)d.n2);
+}
+
+// forward/back substitution through T1/S1/T2 (rfp.py:106-136)
+template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b) {
+  if (d.n == 0 || b.n == 0) return 0;
+  View<T> t1, t2, s1;
+  rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
+  const i64 n1 = d.n1, n2 = d.n2, r = b.n;
+  if (d.lower) {
+    View<T> b1 = b.sub(0, 0, n1, r), b2 = b.sub(n1, 0, n2, r);
+    TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false));
+    if (n2) {
+      TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+      TRY(blas_trsm(c, 'L', 'U', 'T', 'N', one<T>(), t2, b2, false));
+      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false));
+      TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+    }
+    return blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false);
+  }
+  View<T> b1 = b.sub(0, 0, n2, r), b2 = b.sub(n2, 0, n1, r);
+  if (n2) {
+    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false));
+    TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+  }
+  TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t2, b2, false));
+  TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false));
+  if (n2) {
+    TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+    TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false));
+  }
+  return 0;
+}
+
+// triangular inverse in RFP (rfp.py:286-325)
+template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf) {
+  if (d.n == 0) return 0;
+  View<T> t1, t2, s1;
+  rfp_blocks(d, arf, t1, t2, s1);
+  if (d.lower) {
+    TRY(blas_trtri(c, 'L', diag, t1, 0));
+    if (d.n2) {
+      TRY(blas_trmm(c, 'R', 'L', 'N', diag, m_one<T>(), t1, s1));
+      TRY(blas_trtri(c, 'U', diag, t2, (int)d.n1));
+      TRY(blas_trmm(c, 'L', 'U', 'T', diag, one<T>(), t2, s1));
+    }
+    return 0;
+  }
+  if (d.n2) {
+    TRY(blas_trtri(c, 'L', diag, t1, 0));
+    TRY(blas_trmm(c, 'L', 'L', 'T', diag, m_one<T>(), t1, s1));
+    TRY(blas_trtri(c, 'U', diag, t2, (int)d.n2));
+    TRY(blas_trmm(c, 'R', 'U', 'N', diag, one<T>(), t2, s1));
+    return 0;
+  }
+  return blas_trtri(c, 'U', diag, t2, 0);
+}
+
+// inverse from the Cholesky factor: tftri + lauum stage (rfp.py:328-360)
+template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf) {
+  TRY(tftri(c, d, 'N', arf));
+  if (d.n == 0) return 0;
+  const bool herm = is_cplx<T>::value;
+  View<T> t1, t2, s1;
+  rfp_blocks(d, arf, t1, t2, s1);
+  if (d.lower) {
+    TRY(blas_lauum(c, 'L', t1));
+    if (d.n2) {
+      TRY(blas_syrk(c, 'L', 'C', 1.0, s1, 1.0, t1, herm));
+      TRY(blas_trmm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), s1));
+      TRY(blas_lauum(c, 'U', t2));
+    }
+    return 0;
+  }
+  if (d.n2) {
+    TRY(blas_lauum(c, 'L', t1));
+    TRY(blas_syrk(c, 'L', 'C', 1.0, s1.t(), 1.0, t1, herm));
+    TRY(blas_trmm(c, 'R', 'U', 'C', 'N', one<T>(), t2, s1));
+  }
+  return blas_lauum(c, 'U', t2);
+}
+
+// ============================================================ conversions
+// Element (i, j) of the logical triangle -> offset in a storage, plus whether
+// consecutive i are consecutive in memory ("i-fast").  RFP cells follow
+// SURVEY Appendix B (convert.py:174-185, layout.py:127-163).
+__device__ __forceinline__ i64 storage_addr(const Storage& s, i64 i, i64 j, bool& ifast) {
+  if (s.kind == ST_FULL) { ifast = true; return i + j * s.ld; }
+  const RfpDesc& r = s.r;
+  if (s.kind == ST_PACKED) {
+    ifast = true;
+    return r.lower ? j * r.n - j * (j - 1) / 2 + (i - j) : j * (j + 1) / 2 + i;
+  }
+  i64 row, col;
+  bool rowvar;
+  if (r.lower) {
+    if (j < r.n1) { row = i + r.d; col = j; rowvar = true; }
+    else { row = j - r.n1; col = i - r.n1 + 1 - r.d; rowvar = false; }
+  } else {
+    if (j >= r.n2) { row = i; col = j - r.n2; rowvar = true; }
+    else { row = j + r.n2 + 1; col = i; rowvar = false; }
+  }
+  if (!r.trans) { ifast = rowvar; return col * r.ldar + row; }
+  ifast = !rowvar;
+  return row * r.n1 + col;
+}
+
+// One 32x32 tile of the logical (i, j) space per CTA (256 threads).  Loads
+// are issued with an i-fast or j-fast thread mapping according to the
+// source's contiguity at each element, staged through shared memory, and
+// stored with the destination's contiguity -- so both sides are coalesced
+// even where RFP stores a block transposed.
+template <typename T>
+__global__ void __launch_bounds__(256) convert_kernel(Storage src, const T* __restrict__ sp,
+                                                      Storage dst, T* __restrict__ dp, i64 n,
+                                                      i64 rows_total, int lower, int zero_fill) {
+  __shared__ T tile[32][33];
+  const i64 i0 = (i64)blockIdx.x * 32, j0 = (i64)blockIdx.y * 32;
+  if (!zero_fill && (lower ? (i0 + 31 < j0) : (i0 > j0 + 31))) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool want_ifast = pass == 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int a = tx, b = ty + 8 * r;
+      const int ii = want_ifast ? a : b, jj = want_ifast ? b : a;
+      const i64 i = i0 + ii, j = j0 + jj;
+      const bool in = i < n && j < n && (lower ? i >= j : i <= j);
+      if (in) {
+        bool f;
+        i64 off = storage_addr(src, i, j, f);
+        if (f == want_ifast) tile[jj][ii] = sp[off];
+      } else if (want_ifast) {
+        tile[jj][ii] = sc_from<T>(0.0);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool want_ifast = pass == 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int a = tx, b = ty + 8 * r;
+      const int ii = want_ifast ? a : b, jj = want_ifast ? b : a;
+      const i64 i = i0 + ii, j = j0 + jj;
+      const bool in = i < n && j < n && (lower ? i >= j : i <= j);
+      if (zero_fill) {
+        // full destination, i-fast: every element of the ld x n array
+        if (want_ifast && i < rows_total && j < n) dp[i + j * dst.ld] = tile[jj][ii];
+      } else if (in) {
+        bool f;
+        i64 off = storage_addr(dst, i, j, f);
+        if (f == want_ifast) dp[off] = tile[jj][ii];
+      }
+    }
+  }
+}
+
+template <typename T>
+int convert(const Storage& src, const T* s, const Storage& dst, T* dptr, bool zero_fill,
+            cudaStream_t st) {
+  const i64 n = src.r.n;
+  if (n == 0 && !(zero_fill && dst.kind == ST_FULL)) return 0;
+  const i64 rows = (zero_fill && dst.kind == ST_FULL) ? dst.ld : n;
+  if (rows == 0 || n == 0) return 0;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((n + 31) / 32));
+  convert_kernel<T><<<grid, 256, 0, st>>>(src, s, dst, dptr, n, rows, src.r.lower ? 1 : 0,
+                                          zero_fill ? 1 : 0);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+#define RFPK_RFP_INST(T)                                                                     \
+  template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
+  template int pftrf<T>(Ctx, const RfpDesc&, T*);                                            \
+  template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>);                             \
+  template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
+  template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \
+  template int convert<T>(const Storage&, const T*, const Storage&, T*, bool, cudaStream_t);
+RFPK_RFP_INST(double)
+RFPK_RFP_INST(Z)
+
+}  // namespace rfpk

@@ -1,0 +1,42 @@
+// RFP-level drivers: the SRPA compositions of pftrf / pftrs / tftri / pftri
+// over the T1 / T2 / S1 views of one flat RFP buffer, and the full / packed /
+// RFP conversion kernels.
+#pragma once
+#include "blas.cuh"
+
+namespace rfpk {
+
+struct RfpDesc {
+  i64 n, n1, n2, nt, ldar;
+  int d;       // 1 for even n (layout.py:75-78)
+  bool lower;  // uplo 'L'
+  bool trans;  // transr 'T' (or 'C', its verbatim alias)
+};
+
+RfpDesc rfp_desc(i64 n, char uplo, char transr);
+
+// T1, T2, S1 as views of the normal ldar x n1 rectangle (convert.py:142-153)
+template <typename T> void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2,
+                                      View<T>& s1);
+
+template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf);
+template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b);
+template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf);
+template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf);
+
+// Storage descriptors for the conversion kernel.
+enum StorageKind : int { ST_FULL = 0, ST_PACKED = 1, ST_RFP = 2 };
+struct Storage {
+  int kind;
+  i64 ld;  // full: leading dimension
+  RfpDesc r;
+};
+
+// Copy the triangle between two storages (verbatim).  When dst is ST_FULL and
+// zero_fill is set, every other element of the ld x n destination is +0.0
+// (convert.py:200, packed.py:62).
+template <typename T>
+int convert(const Storage& src, const T* s, const Storage& dst, T* dptr, bool zero_fill,
+            cudaStream_t st);
+
+}  // namespace rfpk

@@ -1,0 +1,142 @@
+"""GPU parity of the full-format device kernels (kernels.py surface) against
+the CPU oracle on random strided views: every side/uplo/trans/diag flag
+combination, real and complex, column- and row-major operands."""
+
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import rfp_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return float(np.abs(a - b).max()) / max(float(np.abs(b).max()), 1e-300)
+
+
+def rnd(shape, cplx, seed, rowmajor=False):
+    g = np.random.default_rng(seed)
+    x = g.standard_normal(shape) + (1j * g.standard_normal(shape) if cplx else 0)
+    return np.ascontiguousarray(x) if rowmajor else np.asfortranarray(x)
+
+
+def dev(x):
+    t = torch.from_numpy(x).cuda()
+    return t
+
+
+def tri_matrix(n, cplx, seed, rowmajor):
+    t = rnd((n, n), cplx, seed, rowmajor)
+    t[np.diag_indices(n)] += 2 * n  # well conditioned triangles
+    return t
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_0901_1696_b200 import kernels
+    return kernels
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("ta,tb", list(itertools.product("NTC", "NTC")))
+@pytest.mark.parametrize("m,n,k", [(70, 45, 33), (200, 130, 257)])
+def test_gemm(K, cplx, ta, tb, m, n, k):
+    a = rnd((m, k) if ta == "N" else (k, m), cplx, 1, rowmajor=(m % 2 == 0))
+    b = rnd((k, n) if tb == "N" else (n, k), cplx, 2)
+    c = rnd((m, n), cplx, 3, rowmajor=(k % 2 == 1))
+    want = c.copy()
+    O.gemm(ta, tb, -1.0, a, b, 0.5, want)
+    cd = dev(c)
+    K.gemm(ta, tb, -1.0, dev(a), dev(b), 0.5, cd)
+    assert rel(cd, want) <= TOL
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("side,uplo,trans,diag", list(itertools.product("LR", "LU", "NTC", "NU")))
+def test_trsm_trmm(K, cplx, side, uplo, trans, diag):
+    n, r = 150, 37
+    a = tri_matrix(n, cplx, 5, rowmajor=(uplo == "U"))
+    b = rnd((n, r) if side == "L" else (r, n), cplx, 6, rowmajor=(trans == "T"))
+    want = b.copy()
+    O.trsm(side, uplo, trans, diag, 2.0, a, want)
+    bd = dev(b)
+    K.trsm(side, uplo, trans, diag, 2.0, dev(a), bd)
+    assert rel(bd, want) <= TOL
+    want = b.copy()
+    O.trmm(side, uplo, trans, diag, -1.5, a, want)
+    bd = dev(b)
+    K.trmm(side, uplo, trans, diag, -1.5, dev(a), bd)
+    assert rel(bd, want) <= TOL
+
+
+def test_trsm_singular(K):
+    a = tri_matrix(80, False, 1, False)
+    a[70, 70] = 0.0
+    a[10, 10] = 0.0
+    with pytest.raises(K.SingularMatrixError) as e:
+        K.trsm("L", "L", "N", "N", 1.0, dev(a), dev(rnd((80, 3), False, 2)))
+    assert e.value.index == 11
+    with pytest.raises(K.SingularMatrixError) as e:
+        K.trsm("L", "U", "N", "N", 1.0, dev(a), dev(rnd((80, 3), False, 2)))
+    assert e.value.index == 71
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("uplo,trans", list(itertools.product("LU", "NTC")))
+def test_syrk_herk(K, cplx, uplo, trans):
+    n, k = 190, 77
+    a = rnd((n, k) if trans == "N" else (k, n), cplx, 7)
+    c = rnd((n, n), cplx, 8, rowmajor=(uplo == "L"))
+    for herm in ([False, True] if cplx else [False]):
+        want = c.copy()
+        O.syrk_herk(uplo, trans, -1.0, a, 1.0, want, herm)
+        cd = dev(c)
+        K.syrk_herk(uplo, trans, -1.0, dev(a), 1.0, cd, hermitian=herm)
+        assert rel(cd, want) <= TOL
+        # the other triangle is bit-identical
+        other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+        assert np.array_equal(cd.cpu().numpy()[other], c[other])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("n", [1, 50, 64, 65, 200, 333])
+def test_potrf_trtri_lauum(K, cplx, uplo, n):
+    g = rnd((n, n), cplx, n)
+    a = np.asfortranarray(g @ np.conj(g.T) + n * np.eye(n))
+    want = a.copy(order="F")
+    assert O.potrf(uplo, want) == 0
+    ad = dev(a)
+    assert K.potrf_ref(uplo, ad) == 0
+    assert rel(ad, want) <= TOL
+    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+    assert np.array_equal(ad.cpu().numpy()[other], a[other])
+    for diag in "NU":
+        w2 = want.copy(order="F")
+        assert O.trtri(uplo, diag, w2) == 0
+        td = dev(want.copy(order="F"))
+        assert K.trtri_ref(uplo, diag, td) == 0
+        assert rel(td, w2) <= TOL
+    w3 = want.copy(order="F")
+    O.lauum(uplo, w3)
+    ld = dev(want.copy(order="F"))
+    K.lauum_ref(uplo, ld)
+    assert rel(ld, w3) <= TOL
+
+
+def test_potrf_failure_and_trtri_zero(K):
+    n = 150
+    a = np.eye(n) * 4.0
+    a[120, 120] = -1.0
+    ad = dev(np.asfortranarray(a))
+    assert K.potrf_ref("L", ad) == O.potrf("L", a.copy()) == 121
+    t = np.asfortranarray(np.tril(rnd((n, n), False, 3)) + 10 * np.eye(n))
+    t[77, 77] = 0.0
+    td = dev(t)
+    assert K.trtri_ref("L", "N", td) == 78
+    assert np.array_equal(td.cpu().numpy(), t)  # untouched (kernels.py:526-529)

@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Conversions must be bit-exact; factors,
+solutions and inverses within 1e-10 max-relative of the oracle
+(BASELINE.json north_star tolerance); info codes identical."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import rfp_oracle as O
+from tests.conftest import golden_cases, GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+with np.load(GOLDEN) as _z:
+    CASES = golden_cases({k: None for k in _z.files})
+
+TOL = 1e-10
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else np.asarray(b)
+    if a.size == 0:
+        return 0.0
+    return float(np.abs(a - b).max()) / max(float(np.abs(b).max()), 1e-300)
+
+
+def bits(t):
+    return t.detach().cpu().numpy().tobytes()
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_0901_1696_b200 as pkg
+    from paper_0901_1696_b200 import convert, packed, rfp, kernels  # noqa: F401
+    assert torch.cuda.is_available()
+    return pkg
+
+
+@pytest.mark.parametrize("key,dt,uplo,transr,n", CASES, ids=[c[0] for c in CASES])
+def test_conversions_bit_exact(P, golden, key, dt, uplo, transr, n):
+    conv, packed = P.convert, P.packed
+    a = golden[key + "_A"]
+    r = conv.trttf(a, uplo, transr)
+    assert r.data.is_cuda
+    assert bits(r.data) == golden[key + "_rfp"].tobytes()
+    full = conv.tfttr(r)
+    assert full.stride(0) == 1 or n <= 1
+    assert bits(full.t().contiguous().t()) == np.asfortranarray(golden[key + "_tfttr"]).tobytes()
+    full7 = conv.tfttr(r, ld=n + 7)
+    assert full7.shape == (n + 7, n) and float(full7[n:].abs().sum()) == 0.0
+    p = packed.pack(a, uplo)
+    assert bits(p.data) == golden[key + "_packed"].tobytes()
+    assert bits(conv.tpttf(p, transr).data) == golden[key + "_tpttf"].tobytes()
+    assert bits(conv.tfttp(r).data) == golden[key + "_tfttp"].tobytes()
+    back = packed.unpack(p)
+    assert bits(back.t().contiguous().t()) == np.asfortranarray(golden[key + "_tfttr"]).tobytes()
+
+
+@pytest.mark.parametrize("key,dt,uplo,transr,n", CASES, ids=[c[0] for c in CASES])
+def test_pftrf_pftrs_pftri_match_reference(P, golden, key, dt, uplo, transr, n):
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    d = layout.make_descriptor(n, uplo, transr)
+    r = conv.RfpTriangle(golden[key + "_rfp"], d)
+    assert rfp.pftrf(r) == int(golden[key + "_pftrf_info"])
+    assert r.state is conv.FactorState.CHOLESKY
+    assert rel(r.data, golden[key + "_factor"]) <= TOL
+    b = torch.from_numpy(golden[key + "_B"]).cuda()
+    x = b.clone()
+    rfp.pftrs(r, x)
+    assert rel(x, golden[key + "_X"]) <= TOL
+    # row-major RHS and 1-D RHS
+    xr = torch.from_numpy(np.ascontiguousarray(golden[key + "_B"])).cuda()
+    rfp.pftrs(r, xr)
+    assert rel(xr, golden[key + "_X"]) <= TOL
+    if n:
+        x1 = torch.from_numpy(golden[key + "_B"][:, 0].copy()).cuda()
+        rfp.pftrs(r, x1)
+        assert rel(x1, golden[key + "_X"][:, 0]) <= TOL
+    t = r.copy()
+    assert rfp.tftri(t) == int(golden[key + "_tftri_info"])
+    assert rel(t.data, golden[key + "_tftri"]) <= TOL
+    inv = r.copy()
+    assert rfp.pftri(inv) == int(golden[key + "_pftri_info"])
+    assert inv.state is conv.FactorState.FULL_INVERSE
+    assert rel(inv.data, golden[key + "_pftri"]) <= TOL
+
+
+def test_failure_info_matches_reference(P, golden):
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    keys = [k[:-5] for k in golden if k.startswith("fail_") and k.endswith("_info")]
+    for base in keys:
+        _, dt, ut, nn, *_ = base.split("_")
+        n = int(nn[1:])
+        r = conv.RfpTriangle(golden[base + "_rfp"], layout.make_descriptor(n, ut[0], ut[1]))
+        assert rfp.pftrf(r) == int(golden[base + "_info"]), base
+        assert r.state is conv.FactorState.UNFACTORED
+
+
+def test_state_machine_and_errors(P):
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    r = conv.trttf(O.spd_matrix(5, 1), "L", "N")
+    with pytest.raises(ValueError, match="pftrs needs a Cholesky factor"):
+        rfp.pftrs(r, torch.zeros(5, 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="pftri needs a Cholesky factor"):
+        rfp.pftri(r)
+    assert rfp.pftrf(r) == 0
+    with pytest.raises(ValueError, match="does not match order"):
+        rfp.pftrs(r, torch.zeros(4, 1, dtype=torch.float64, device="cuda"))
+    z = conv.trttf(O.spd_matrix(5, 2, complex_=True), "U", "C")
+    assert z.desc.transr == "T"
+    assert rfp.pftrf(z) == 0
+    with pytest.raises(ValueError, match="complex system"):
+        rfp.pftrs(z, torch.zeros(5, 1, dtype=torch.float64, device="cuda"))
+    e = conv.RfpTriangle(torch.zeros(0, dtype=torch.float64), layout.make_descriptor(0, "L", "N"))
+    assert rfp.pftrf(e) == 0 and e.state is conv.FactorState.CHOLESKY
+    assert rfp.pftri(e) == 0 and e.state is conv.FactorState.FULL_INVERSE
+    with pytest.raises(ValueError):
+        conv.RfpTriangle(torch.zeros(7, dtype=torch.float64), layout.make_descriptor(3, "L", "N"))
+
+
+def test_host_rhs_is_solved_in_place(P):
+    conv, rfp = P.convert, P.rfp
+    a = O.spd_matrix(9, 3)
+    r = conv.trttf(a, "U", "T")
+    assert rfp.pftrf(r) == 0
+    b = np.asfortranarray(np.random.default_rng(0).standard_normal((9, 2)))
+    x = b.copy(order="F")
+    rfp.pftrs(r, x)
+    assert np.abs(a @ x - b).max() < 1e-12
+    # real factor with complex RHS (rfp.py:101 allows it)
+    bc = torch.from_numpy(b + 1j * b[::-1]).cuda()
+    xc = bc.clone()
+    rfp.pftrs(r, xc)
+    ac = torch.from_numpy(a).cuda().to(torch.complex128)
+    assert float((ac @ xc - bc).abs().max()) < 1e-12
+
+
+@pytest.mark.parametrize("n", [65, 128, 130, 257, 600])
+@pytest.mark.parametrize("uplo,transr", [("L", "N"), ("U", "T"), ("L", "T"), ("U", "N")])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_recursive_sizes_vs_oracle(P, n, uplo, transr, cplx):
+    """Sizes beyond the 64 leaf exercise the recursive drivers and GEMMs."""
+    conv, rfp = P.convert, P.rfp
+    a = O.spd_matrix(n, 100 + n, "n", complex_=cplx)
+    buf = O.trttf(a, uplo, transr)
+    f = buf.copy()
+    assert O.pftrf(f, n, uplo, transr) == 0
+    r = conv.trttf(a, uplo, transr)
+    assert bits(r.data) == buf.tobytes()
+    assert rfp.pftrf(r) == 0
+    assert rel(r.data, f) <= TOL
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, 7)) + (1j * rng.standard_normal((n, 7)) if cplx else 0)
+    b = np.asfortranarray(b)
+    xo = b.copy(order="F")
+    O.pftrs(f, n, uplo, transr, xo)
+    x = torch.from_numpy(b).cuda()
+    rfp.pftrs(r, x)
+    assert rel(x, xo) <= TOL
+    inv_o = f.copy()
+    O.pftri(inv_o, n, uplo, transr)
+    assert rfp.pftri(r) == 0
+    assert rel(r.data, inv_o) <= TOL
+
+
+def test_batched_vs_oracle(P):
+    rfp = P.rfp
+    for n, uplo, transr, nrhs in [(64, "U", "N", 8), (64, "L", "T", 3), (33, "L", "N", 1),
+                                  (1, "U", "T", 2), (17, "U", "C", 8), (64, "L", "N", 0)]:
+        batch = 37
+        bufs, facs, xs, bs = [], [], [], []
+        for k in range(batch):
+            a = O.spd_matrix(n, 1000 + k, "n")
+            buf = O.trttf(a, uplo, transr)
+            bufs.append(buf)
+            f = buf.copy()
+            assert O.pftrf(f, n, uplo, transr) == 0
+            facs.append(f)
+            b = np.asfortranarray(np.random.default_rng(k).standard_normal((n, max(nrhs, 1))))
+            bs.append(b)
+            x = b.copy(order="F")
+            O.pftrs(f, n, uplo, transr, x)
+            xs.append(x)
+        arf = torch.from_numpy(np.stack(bufs)).cuda()
+        arf2 = arf.clone()
+        bt = torch.from_numpy(np.stack([b.T for b in bs])).cuda().transpose(1, 2)[:, :, :nrhs]
+        info = rfp.pftrf_pftrs_batched(arf, bt, n, uplo, transr)
+        assert int(info.abs().sum()) == 0
+        assert rel(arf, np.stack(facs)) <= TOL
+        if nrhs:
+            assert rel(bt, np.stack(xs)[:, :, :nrhs]) <= TOL
+        # unfused
+        info2 = rfp.pftrf_batched(arf2, n, uplo, transr)
+        assert int(info2.abs().sum()) == 0
+        assert rel(arf2, np.stack(facs)) <= TOL
+        if nrhs:
+            b2 = torch.from_numpy(np.stack(bs)).cuda()[:, :, :nrhs].contiguous()
+            rfp.pftrs_batched(arf2, b2, n, uplo, transr)
+            assert rel(b2, np.stack(xs)[:, :, :nrhs]) <= TOL
+
+
+def test_batched_failure_info(P):
+    rfp = P.rfp
+    n, batch = 64, 8
+    bufs, want = [], []
+    for k in range(batch):
+        a = O.spd_matrix(n, k, "n")
+        if k % 3 == 1:
+            a[k + 5, k + 5] = -1e9
+            a[:, k + 5] = 0.0
+            a[k + 5, :] = 0.0
+            a[k + 5, k + 5] = -1.0
+        buf = O.trttf(a, "U", "N")
+        want.append(O.pftrf(buf.copy(), n, "U", "N"))
+        bufs.append(buf)
+    arf = torch.from_numpy(np.stack(bufs)).cuda()
+    info = rfp.pftrf_batched(arf, n, "U", "N")
+    assert info.cpu().tolist() == want
