@@ -15,6 +15,7 @@
 // conjugating B in place.  potrf/trtri/lauum with uplo 'U' are run as the
 // lower algorithm on the transposed view (exact identities, see blas_potrf).
 #include "blas.cuh"
+#include "leaf.cuh"
 
 namespace rfpk {
 
@@ -66,64 +67,85 @@ template <typename T> __device__ __forceinline__ T real_part_as(T v);
 template <> __device__ __forceinline__ double real_part_as(double v) { return v; }
 template <> __device__ __forceinline__ Z real_part_as(Z v) { return Z{v.x, 0.0}; }
 
-// Lower Cholesky of an n x n (n <= LEAF) block in shared memory: right-looking,
-// two barriers per pivot.  `not d > 0` (catches NaN) -> info = base + k + 1
-// (kernels.py:441-442).  Only the lower triangle is read or written.
+// 64-leaf Cholesky + inverse: L (lower, in place) and W = L^{-1} (64 x 64,
+// zero upper part, column-major ld 64) for the in-place GEMM trsm leaves.
+// info <- base + first failing pivot (kernels.py:441-442); on failure
+// nothing is written back.
 template <typename T>
-__global__ void __launch_bounds__(256) potf2_kernel(View<T> A, int* info, int base) {
+__global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* info, int base) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
+  T* Ws = S + 64 * LD64;
+  __shared__ int fail;
   if (*info) return;
   const int n = (int)A.m;
-  constexpr int LD = LEAF + 1;
-  smem_load(S, LD, A, n, n, 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) fail = 0;
+  leaf_load_lower(S, A, n);
   __syncthreads();
-  int fail = 0;
-  for (int k = 0; k < n; ++k) {
-    double d = sc_re(S[k + k * LD]);
-    if (!(d > 0.0)) { fail = k + 1; break; }
-    d = sqrt(d);
-    const double rd = 1.0 / d;
-    (void)rd;
-    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) S[i + k * LD] = S[i + k * LD] / d;
-    __syncthreads();
-    const int r = n - k - 1;
-    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-      int i = k + 1 + e % r, j = k + 1 + e / r;
-      if (j <= i) S[i + j * LD] = fnmac(S[i + k * LD], conj_(S[j + k * LD]), S[i + j * LD]);
-    }
-    if (threadIdx.x == 0) S[k + k * LD] = sc_from<T>(d);
-    __syncthreads();
+  if (warp == 0) {
+    const int f = chol32_warp(S, 0);
+    if (lane == 0 && f) fail = f;
   }
+  __syncthreads();
   if (fail) {
     if (threadIdx.x == 0) *info = base + fail;
     return;
   }
-  smem_store(S, LD, A, n, n, 1, false);
-}
-
-// In-place inverse of an n x n lower triangle (n <= LEAF): thread j owns
-// column j of W = L^{-1} and runs the row recurrence with no barriers.
-template <typename T>
-__global__ void __launch_bounds__(LEAF) trtri_leaf_kernel(View<T> A, int unit, const int* skip) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* L = reinterpret_cast<T*>(smem_raw);
-  constexpr int LD = LEAF + 1;
-  T* W = L + LD * LEAF;
-  if (skip && *skip) return;
-  const int n = (int)A.m;
-  smem_load(L, LD, A, n, n, 1);
+  if (warp == 0) inv32_warp(S, 0, Ws, 0, false);
   __syncthreads();
-  const int j = threadIdx.x;
-  if (j < n) {
-    for (int i = j; i < n; ++i) {
-      T s = sc_from<T>(i == j ? 1.0 : 0.0);
-      for (int k = j; k < i; ++k) s = fnmac(L[i + k * LD], W[k + j * LD], s);
-      W[i + j * LD] = unit ? s : s / L[i + i * LD];
-    }
+  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
+  T acc[8];
+  mm32<T, true, true>(S, 32, 0, Ws, 0, 0, acc);  // L21 = A21 W11^H
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) S[(32 + i) + (jg + q) * LD64] = acc[q];
+  __syncthreads();
+  mm32<T, true, true>(S, 32, 0, S, 32, 0, acc);  // L21 L21^H
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
+  __syncthreads();
+  if (warp == 0) {
+    const int f = chol32_warp(S, 32);
+    if (lane == 0 && f) fail = 32 + f;
   }
   __syncthreads();
-  smem_store(W, LD, A, n, n, 1, unit != 0);
+  if (fail) {
+    if (threadIdx.x == 0) *info = base + fail;
+    return;
+  }
+  if (warp == 1) inv32_warp(S, 32, Ws, 32, false);
+  __syncthreads();
+  if (W) inv64_block(S, Ws, false, true);
+  __syncthreads();
+  leaf_store_lower(S, A, n, false);
+  if (W)
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) W[e] = Ws[(e & 63) + (e >> 6) * LD64];
+}
+
+// Inverses of all 64-leaves of a lower-triangular view (one CTA per leaf):
+// into the W slabs (W != null, slab b at W + 64*64*b) or in place.
+template <typename T>
+__global__ void __launch_bounds__(128) trtri_leaves_kernel(View<T> A, T* W, int unit,
+                                                           const int* skip) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  T* Ws = S + 64 * LD64;
+  if (skip && *skip) return;
+  const i64 r0 = (i64)blockIdx.x * 64;
+  const int len = (int)((A.m - r0) < 64 ? (A.m - r0) : 64);
+  View<T> blk = A.sub(r0, r0, len, len);
+  leaf_load_lower(S, blk, len);
+  __syncthreads();
+  inv64_block(S, Ws, unit != 0, false);
+  __syncthreads();
+  if (W) {
+    T* dst = W + r0 * 64;
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) dst[e] = Ws[(e & 63) + (e >> 6) * LD64];
+  } else {
+    leaf_store_lower(Ws, blk, len, unit != 0);
+  }
 }
 
 // In-place A <- L^H L on an n x n lower triangle (n <= LEAF)  (kernels.py:554-572)
@@ -147,83 +169,6 @@ __global__ void __launch_bounds__(256) lauum_leaf_kernel(View<T> A, const int* s
   }
   __syncthreads();
   smem_store(X, LD, A, n, n, 1, false);
-}
-
-// Triangular solve conj?(T) X = B for an n x n (n <= LEAF) triangle against a
-// chunk of CW columns of B; one thread per column.
-constexpr int TRSM_CW = 64;
-template <typename T>
-__global__ void __launch_bounds__(TRSM_CW)
-    trsm_leaf_kernel(View<T> Tm, View<T> B, int lower, int conj, int unit, const int* skip) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);
-  constexpr int LD = LEAF + 1;
-  T* X = S + LD * LEAF;  // X[i + c*LD]
-  if (skip && *skip) return;
-  const int n = (int)Tm.m;
-  const i64 c0 = (i64)blockIdx.x * TRSM_CW;
-  const int cw = (int)((B.n - c0) < TRSM_CW ? (B.n - c0) : TRSM_CW);
-  View<T> Bc = B.sub(0, c0, B.m, cw);
-  smem_load(S, LD, Tm, n, n, lower ? 1 : 2);
-  smem_load(X, LD, Bc, n, cw, 0);
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (c < cw) {
-    T* x = X + c * LD;
-    if (lower) {
-      for (int i = 0; i < n; ++i) {
-        T s = x[i];
-        for (int k = 0; k < i; ++k) s = fnmac(cj(S[i + k * LD], conj), x[k], s);
-        x[i] = unit ? s : s / cj(S[i + i * LD], conj);
-      }
-    } else {
-      for (int i = n - 1; i >= 0; --i) {
-        T s = x[i];
-        for (int k = i + 1; k < n; ++k) s = fnmac(cj(S[i + k * LD], conj), x[k], s);
-        x[i] = unit ? s : s / cj(S[i + i * LD], conj);
-      }
-    }
-  }
-  __syncthreads();
-  smem_store(X, LD, Bc, n, cw, 0, false);
-}
-
-// B <- alpha conj?(T) B for an n x n triangle against CW columns of B.
-template <typename T>
-__global__ void __launch_bounds__(TRSM_CW) trmm_leaf_kernel(View<T> Tm, View<T> B, int lower,
-                                                            int conj, int unit, T alpha,
-                                                            const int* skip) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);
-  constexpr int LD = LEAF + 1;
-  T* X = S + LD * LEAF;
-  if (skip && *skip) return;
-  const int n = (int)Tm.m;
-  const i64 c0 = (i64)blockIdx.x * TRSM_CW;
-  const int cw = (int)((B.n - c0) < TRSM_CW ? (B.n - c0) : TRSM_CW);
-  View<T> Bc = B.sub(0, c0, B.m, cw);
-  smem_load(S, LD, Tm, n, n, lower ? 1 : 2);
-  smem_load(X, LD, Bc, n, cw, 0);
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (c < cw) {
-    T* x = X + c * LD;
-    if (lower) {
-      for (int i = n - 1; i >= 0; --i) {
-        T s = unit ? x[i] : cj(S[i + i * LD], conj) * x[i];
-        for (int k = 0; k < i; ++k) s = fmac(cj(S[i + k * LD], conj), x[k], s);
-        x[i] = alpha * s;
-      }
-    } else {
-      for (int i = 0; i < n; ++i) {
-        T s = unit ? x[i] : cj(S[i + i * LD], conj) * x[i];
-        for (int k = i + 1; k < n; ++k) s = fmac(cj(S[i + k * LD], conj), x[k], s);
-        x[i] = alpha * s;
-      }
-    }
-  }
-  __syncthreads();
-  smem_store(X, LD, Bc, n, cw, 0, false);
 }
 
 // Zero-diagonal scan: first (lowest, mode 0) or last (highest, mode 1)
@@ -259,10 +204,14 @@ template <typename K> void allow_smem(K kern, size_t bytes) {
                                               (int)bytes);
 }
 
+// Recursive split: n1 is a multiple of 64 (128 for large n), so every leaf
+// starts at a multiple of 64 and all leaves but the last are exactly 64 wide.
+// potrf, trsm, trmm, trtri and lauum split identically, which lets a trsm
+// reuse the leaf inverses its potrf produced (W slab b <-> rows 64b..64b+63).
 i64 split_point(i64 n) {
-  const i64 q = n > 512 ? 128 : (n > 128 ? 64 : 32);
+  const i64 q = n > 512 ? 128 : 64;
   i64 n1 = ((n / 2 + q - 1) / q) * q;
-  if (n1 >= n) n1 = n / 2;
+  if (n1 >= n) n1 = ((n - 1) / 64) * 64;
   return n1;
 }
 
@@ -272,6 +221,23 @@ template <typename T> bool is_one(T v) {
   if constexpr (is_cplx<T>::value) return v.x == 1.0 && v.y == 0.0;
   else return v == 1.0;
 }
+
+}  // namespace
+
+// workspace for the leaf inverses of an order-n triangle (64 x 64 per leaf)
+template <typename T> size_t leaf_ws_elems(i64 n) { return (size_t)((n + 63) / 64) * 64 * 64; }
+
+template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st) {
+  *p = nullptr;
+  if (n <= 0) return 0;
+  cudaError_t e = cudaMallocAsync((void**)p, leaf_ws_elems<T>(n) * sizeof(T), st);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+template <typename T> void ws_free(T* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+namespace {
 
 // ----------------------------------------------------------- canonical ops
 // herk/syrk on the `tri` triangle of C: C <- alpha G op(G) + beta C where
@@ -285,58 +251,78 @@ int herk_core(Ctx c, int tri, double alpha, View<T> Gv, bool gconj, double beta,
                  cplx && herm, c.info, c.st);
 }
 
+// Inverses of all 64-leaves of the lower-in-view triangle L into W slabs.
+template <typename T> int leaf_inverses(Ctx c, View<T> L, bool unit, T* W) {
+  if (L.m == 0) return 0;
+  const size_t sm = leaf_smem<T>(2);
+  auto k = trtri_leaves_kernel<T>;
+  allow_smem(k, sm);
+  k<<<(unsigned)((L.m + 63) / 64), 128, sm, c.st>>>(L, W, unit ? 1 : 0, c.info);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+// Solve conj?(T) X = B (T lower or upper in its view) with the leaf inverses
+// W: W slab b holds inv(leaf b) of T (wtrans == false) or of T^T (wtrans).
+// Leaves are in-place 64-row GEMMs X_b = W_b B_b; updates are GEMMs.
 template <typename T>
-int trsm_rec(Ctx c, bool lower, bool conj, bool unit, View<T> Tm, View<T> B) {
+int trsm_rec(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
   const i64 n = Tm.m;
   if (n == 0 || B.n == 0) return 0;
   if (n <= LEAF) {
-    const size_t sm = leaf_smem<T>(2);
-    auto k = trsm_leaf_kernel<T>;
-    allow_smem(k, sm);
-    unsigned grid = (unsigned)((B.n + TRSM_CW - 1) / TRSM_CW);
-    k<<<grid, TRSM_CW, sm, c.st>>>(Tm, B, lower, conj, unit, c.info);
-    RFPK_CHECK_LAUNCH();
-    return 0;
+    View<T> Wv{W, n, n, 1, 64};
+    if (wtrans) Wv = Wv.t();
+    return gemm<T>(TRI_FULL, one<T>(), Wv, conj, B, false, sc_from<T>(0.0), B, false, c.info,
+                   c.st, A_FULL, true);
   }
   const i64 n1 = split_point(n), n2 = n - n1;
   View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
+  T* W2 = W + n1 * 64;
   int rc;
   if (lower) {
-    if ((rc = trsm_rec(c, lower, conj, unit, Tm.sub(0, 0, n1, n1), B1))) return rc;
+    if ((rc = trsm_rec(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans))) return rc;
     if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(n1, 0, n2, n1), conj, B1, false, one<T>(), B2,
                       false, c.info, c.st)))
       return rc;
-    return trsm_rec(c, lower, conj, unit, Tm.sub(n1, n1, n2, n2), B2);
+    return trsm_rec(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans);
   }
-  if ((rc = trsm_rec(c, lower, conj, unit, Tm.sub(n1, n1, n2, n2), B2))) return rc;
+  if ((rc = trsm_rec(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans))) return rc;
   if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(0, n1, n1, n2), conj, B2, false, one<T>(), B1,
                     false, c.info, c.st)))
     return rc;
-  return trsm_rec(c, lower, conj, unit, Tm.sub(0, 0, n1, n1), B1);
+  return trsm_rec(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans);
 }
 
+// conj?(T) X = alpha B.  If W is null the leaf inverses are computed here.
 template <typename T>
-int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
-  if (B.empty()) return 0;
+int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B, T* W) {
+  if (B.empty() || Tm.m == 0) return 0;
   if (!is_one(alpha)) {
     int rc = scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
     if (rc || is_zero(alpha)) return rc;
   }
-  return trsm_rec(c, lower, conj, unit, Tm, B);
+  T* own = nullptr;
+  int rc;
+  if (!W) {
+    if ((rc = ws_alloc(&own, Tm.m, c.st))) return rc;
+    if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
+    W = own;
+  }
+  rc = trsm_rec(c, lower, conj, Tm, B, W, !lower);
+  ws_free(own, c.st);
+  return rc;
 }
 
+// B <- alpha conj?(T) B; leaves are in-place 64-row GEMMs with a masked
+// (triangular) A operand; unit diagonal = strict mask + beta = alpha.
 template <typename T>
 int trmm_rec(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
   const i64 n = Tm.m;
   if (n == 0 || B.n == 0) return 0;
   if (n <= LEAF) {
-    const size_t sm = leaf_smem<T>(2);
-    auto k = trmm_leaf_kernel<T>;
-    allow_smem(k, sm);
-    unsigned grid = (unsigned)((B.n + TRSM_CW - 1) / TRSM_CW);
-    k<<<grid, TRSM_CW, sm, c.st>>>(Tm, B, lower, conj, unit, alpha, c.info);
-    RFPK_CHECK_LAUNCH();
-    return 0;
+    const int mask = lower ? (unit ? A_SLOWER : A_LOWER) : (unit ? A_SUPPER : A_UPPER);
+    return gemm<T>(TRI_FULL, alpha, Tm, conj, B, false, unit ? alpha : sc_from<T>(0.0), B, false,
+                   c.info, c.st, mask, true);
   }
   const i64 n1 = split_point(n), n2 = n - n1;
   View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
@@ -362,50 +348,51 @@ int trmm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
   return trmm_rec(c, lower, conj, unit, alpha, Tm, B);
 }
 
-// A = L L^H, lower triangle of the view (recursive; leaves in one CTA)
-template <typename T> int potrf_lower(Ctx c, View<T> A, int base) {
-  const i64 n = A.m;
-  if (n == 0) return 0;
-  if (n <= LEAF) {
-    const size_t sm = leaf_smem<T>(1);
-    auto k = potf2_kernel<T>;
-    allow_smem(k, sm);
-    k<<<1, 256, sm, c.st>>>(A, c.info, base);
-    RFPK_CHECK_LAUNCH();
-    return 0;
-  }
-  const i64 n1 = split_point(n), n2 = n - n1;
-  View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
-  int rc;
-  if ((rc = potrf_lower(c, A11, base))) return rc;
-  // A21 <- A21 L11^{-H}  <=>  conj(L11) A21^T = A21^T
-  if ((rc = trsm_rec(c, true, is_cplx<T>::value, false, A11, A21.t()))) return rc;
-  // A22 <- A22 - A21 A21^H (lower triangle)
-  if ((rc = herk_core(c, TRI_LOWER, -1.0, A21, false, 1.0, A22, true))) return rc;
-  return potrf_lower(c, A22, base + (int)n1);
-}
-
-// A <- L^{-1} in place, lower triangle
-template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
+// A = L L^H, lower triangle of the view; W receives the leaf inverses (slab
+// b <-> rows 64b..), reused by the trsm steps of this recursion and by the
+// caller (pftrf's S1 solve).
+template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
   const i64 n = A.m;
   if (n == 0) return 0;
   if (n <= LEAF) {
     const size_t sm = leaf_smem<T>(2);
-    auto k = trtri_leaf_kernel<T>;
+    auto k = potf2_inv64_kernel<T>;
     allow_smem(k, sm);
-    k<<<1, LEAF, sm, c.st>>>(A, unit ? 1 : 0, c.info);
+    k<<<1, 128, sm, c.st>>>(A, W, c.info, base);
     RFPK_CHECK_LAUNCH();
     return 0;
   }
   const i64 n1 = split_point(n), n2 = n - n1;
   View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
   int rc;
-  if ((rc = trtri_lower(c, unit, A11))) return rc;
-  // A21 <- A21 W11   <=>  A21^T <- W11^T A21^T (W11^T upper in its view)
+  if ((rc = potrf_lower(c, A11, base, W))) return rc;
+  // A21 <- A21 L11^{-H}  <=>  conj(L11) A21^T = A21^T
+  if ((rc = trsm_rec(c, true, is_cplx<T>::value, A11, A21.t(), W, false))) return rc;
+  // A22 <- A22 - A21 A21^H (lower triangle)
+  if ((rc = herk_core(c, TRI_LOWER, -1.0, A21, false, 1.0, A22, true))) return rc;
+  return potrf_lower(c, A22, base + (int)n1, W + n1 * 64);
+}
+
+// A <- L^{-1} in place (lower): all 64-leaves are inverted in one launch,
+// then each recursion node forms A21 <- -W22 A21 W11 with two trmms.
+template <typename T> int trtri_rec(Ctx c, bool unit, View<T> A) {
+  const i64 n = A.m;
+  if (n <= LEAF) return 0;
+  const i64 n1 = split_point(n), n2 = n - n1;
+  View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
+  int rc;
+  if ((rc = trtri_rec(c, unit, A11))) return rc;
+  if ((rc = trtri_rec(c, unit, A22))) return rc;
+  // A21 <- A21 W11  <=>  A21^T <- W11^T A21^T (upper in its view)
   if ((rc = trmm_rec(c, false, false, unit, one<T>(), A11.t(), A21.t()))) return rc;
-  // A21 <- -L22^{-1} A21
-  if ((rc = trsm_left(c, true, false, unit, neg_one<T>(), A22, A21))) return rc;
-  return trtri_lower(c, unit, A22);
+  return trmm_rec(c, true, false, unit, neg_one<T>(), A22, A21);
+}
+
+template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
+  if (A.m == 0) return 0;
+  int rc = leaf_inverses<T>(c, A, unit, nullptr);
+  if (rc) return rc;
+  return trtri_rec(c, unit, A);
 }
 
 // A <- L^H L in place, lower triangle
@@ -464,7 +451,7 @@ int blas_gemm(Ctx c, char transa, char transb, T alpha, View<T> A, View<T> B, T 
 
 template <typename T>
 int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B,
-              bool scan) {
+              bool scan, T* W) {
   if (B.empty() || A.m == 0) return 0;
   View<T> v, b = B;
   bool lower, conj;
@@ -481,7 +468,7 @@ int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<
     int rc = diag_scan(c, v, 0, !lower);
     if (rc) return rc;
   }
-  return trsm_left(c, lower, conj, diag == 'U', alpha, v, b);
+  return trsm_left(c, lower, conj, diag == 'U', alpha, v, b, W);
 }
 
 template <typename T>
@@ -512,8 +499,17 @@ int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta
 // potrf('U', A) == potrf('L', A^T view): with V = A^T, V's lower triangle holds
 // conj(H); conj(H) = L L^H gives H = conj(L) L^T = U^H U for U = L^T, which
 // is stored exactly where the reference stores U.  Same pivots, same info.
-template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base) {
-  return potrf_lower(c, uplo == 'L' ? A : A.t(), base);
+template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W) {
+  View<T> v = uplo == 'L' ? A : A.t();
+  T* own = nullptr;
+  int rc;
+  if (!W) {
+    if ((rc = ws_alloc(&own, v.m, c.st))) return rc;
+    W = own;
+  }
+  rc = potrf_lower(c, v, base, W);
+  ws_free(own, c.st);
+  return rc;
 }
 
 template <typename T> int blas_trtri(Ctx c, char uplo, char diag, View<T> A, int base) {
@@ -532,12 +528,14 @@ template <typename T> int blas_lauum(Ctx c, char uplo, View<T> A) {
 
 #define RFPK_INST(T)                                                                           \
   template int blas_gemm<T>(Ctx, char, char, T, View<T>, View<T>, T, View<T>);                 \
-  template int blas_trsm<T>(Ctx, char, char, char, char, T, View<T>, View<T>, bool);                 \
+  template int blas_trsm<T>(Ctx, char, char, char, char, T, View<T>, View<T>, bool, T*);       \
   template int blas_trmm<T>(Ctx, char, char, char, char, T, View<T>, View<T>);                 \
   template int blas_syrk<T>(Ctx, char, char, double, View<T>, double, View<T>, bool);          \
-  template int blas_potrf<T>(Ctx, char, View<T>, int);                                         \
+  template int blas_potrf<T>(Ctx, char, View<T>, int, T*);                                     \
   template int blas_trtri<T>(Ctx, char, char, View<T>, int);                                   \
-  template int blas_lauum<T>(Ctx, char, View<T>);
+  template int blas_lauum<T>(Ctx, char, View<T>);                                              \
+  template int ws_alloc<T>(T**, i64, cudaStream_t);                                            \
+  template void ws_free<T>(T*, cudaStream_t);
 RFPK_INST(double)
 RFPK_INST(Z)
 

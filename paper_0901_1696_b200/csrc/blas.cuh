@@ -25,7 +25,9 @@ int blas_gemm(Ctx c, char transa, char transb, T alpha, View<T> A, View<T> B, T 
 //       zero diagonal -> *info = 1-based index, B untouched
 template <typename T>
 int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B,
-              bool scan = true);
+              bool scan = true, T* W = nullptr);
+// (W: optional leaf inverses of the effective triangle, as produced by
+//  blas_potrf on the same view -- pftrf reuses T1's.)
 // trmm: B <- alpha op(A) B / alpha B op(A)                     (kernels.py:307)
 template <typename T>
 int blas_trmm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B);
@@ -34,7 +36,10 @@ template <typename T>
 int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta, View<T> C,
               bool herm);
 // potrf: L L^H (uplo L) / U^H U (uplo U); *info = base + first failing pivot
-template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base);
+template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W = nullptr);
+// stream-ordered workspace for leaf inverses of an order-n triangle
+template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
+template <typename T> void ws_free(T* p, cudaStream_t st);
 // trtri: in-place inverse; zero diagonal -> *info (matrix untouched) (kernels.py:515)
 template <typename T> int blas_trtri(Ctx c, char uplo, char diag, View<T> A, int base);
 // lauum: L^H L (uplo L) / U U^H (uplo U)                        (kernels.py:575)

@@ -44,126 +44,96 @@ __device__ __forceinline__ bool tri_keep(int mode, int row, int col) {
   return mode == TRI_FULL || (mode == TRI_LOWER ? row >= col : row <= col);
 }
 
-// ------------------------------------------------------------ real kernel
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
-    dgemm_kernel(GemmArgs<double> g) {
-  constexpr int WARPS_M = BM / WM;
-  constexpr int NT = WARPS_M * (BN / WN) * 32;
-  constexpr int PA = BM + 4, PB = BN + 4;  // == 4 (mod 16): conflict-free fragment loads
-  constexpr int MI = WM / 16, NI = WN / 8;
-  extern __shared__ __align__(16) double smem_d[];
-  double* As = smem_d;
-  double* Bs = smem_d + STAGES * BK * PA;
-  if (g.skip && *g.skip) return;
-  int tm, tn;
-  if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
-  else tri_tile(MODE, g.tiles_m, tm, tn);
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int M = g.M, N = g.N, K = g.K;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-  const int gq = lane >> 2, tq = lane & 3;
-
-  double acc[MI][NI][4];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-
-  const int KT = (K + BK - 1) / BK;
-  const double* __restrict__ Ag = g.A;
-  const double* __restrict__ Bg = g.B;
-  const i64 lda = g.lda, ldb = g.ldb;
-
-  auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * BK;
-    double* as = As + stage * BK * PA;
-    double* bs = Bs + stage * BK * PB;
-#pragma unroll
-    for (int i = tid; i < BM * BK; i += NT) {
-      int m, k;
-      if (AK) { k = i % BK; m = i / BK; } else { m = i % BM; k = i / BM; }
-      const int gm = m0 + m, gk = k0 + k;
-      const bool ok = gm < M && gk < K;
-      const double* src = ok ? (AK ? Ag + (i64)gm * lda + gk : Ag + gm + (i64)gk * lda) : Ag;
-      cp_async8(as + k * PA + m, src, ok);
-    }
-#pragma unroll
-    for (int i = tid; i < BN * BK; i += NT) {
-      int n, k;
-      if (BKM) { k = i % BK; n = i / BK; } else { n = i % BN; k = i / BN; }
-      const int gn = n0 + n, gk = k0 + k;
-      const bool ok = gn < N && gk < K;
-      const double* src = ok ? (BKM ? Bg + gk + (i64)gn * ldb : Bg + (i64)gk * ldb + gn) : Bg;
-      cp_async8(bs + k * PB + n, src, ok);
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_async_commit();
+__device__ __forceinline__ bool a_keep(int a_tri, int m, int k) {
+  switch (a_tri) {
+    case A_LOWER: return m >= k;
+    case A_UPPER: return m <= k;
+    case A_SLOWER: return m > k;
+    case A_SUPPER: return m < k;
+    default: return true;
   }
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int nk = kt + STAGES - 1;
-    if (nk < KT) load_stage(nk % STAGES, nk);
-    cp_async_commit();
-    const double* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
-    const double* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[MI][2], bf[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        af[i][0] = as[(kk + tq) * PA + i * 16];
-        af[i][1] = as[(kk + tq) * PA + i * 16 + 8];
-      }
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[j] = bs[(kk + tq) * PB + j * 8];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
-    }
-  }
-  cp_async_wait<0>();
-
-  const double alpha = g.alpha, beta = g.beta;
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = m0 + wm * WM + i * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = n0 + wn * WN + j * 8 + 2 * tq + (r & 1);
-        if (row < M && col < N && tri_keep(MODE, row, col)) {
-          double* c = g.C + row + (i64)col * g.ldc;
-          double v = alpha * acc[i][j][r];
-          if (beta != 0.0) v = fma(beta, *c, v);
-          *c = v;
-        }
-      }
 }
 
-// ------------------------------------------------------------ complex kernel
-// Complex product from 4 real DMMAs per fragment pair on interleaved smem
-// tiles: Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br (conjugation = sign flip).
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
+// ------------------------------------------------------------ tile loader
+// Global -> shared copy of one operand tile (R rows along M or N, BK along K)
+// with all addressing hoisted out of the K loop: each thread owns EPT
+// elements at a fixed stride, so a stage costs one 64-bit add + one cp.async
+// per element.  The K tail and the triangular masks (a_tri / b_tri, used only
+// by the in-place triangular leaves) take a separate predicated path.
+template <typename T, int R, int BK, int NT, int P, bool KMAJOR>
+struct TileLoader {
+  static constexpr int EPT = R * BK / NT;
+  static_assert(R * BK % NT == 0, "tile must divide evenly");
+  static constexpr int RE = KMAJOR ? NT / BK : 0;   // row delta per element
+  static constexpr int KE = KMAJOR ? 0 : NT / R;    // k delta per element
+  const T* ptr;     // element 0 at the current k0
+  i64 step;         // global delta between consecutive elements
+  i64 kstep;        // global delta per stage
+  int r0, k_0;      // tile coords of element 0
+  int soff;         // smem offset of element 0
+  unsigned rowok;   // bit e: row of element e inside the matrix
+
+  __device__ __forceinline__ void init(const T* base, i64 ld, int tile0, int rows, int tid) {
+    if (KMAJOR) { k_0 = tid % BK; r0 = tid / BK; }
+    else { r0 = tid % R; k_0 = tid / R; }
+    // element (r, k) at base + r*ld + k (KMAJOR) or base + r + k*ld
+    ptr = KMAJOR ? base + (i64)(tile0 + r0) * ld + k_0 : base + (tile0 + r0) + (i64)k_0 * ld;
+    step = KMAJOR ? (i64)RE * ld : (i64)KE * ld;
+    kstep = KMAJOR ? (i64)BK : (i64)BK * ld;
+    soff = k_0 * P + r0;
+    rowok = 0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (tile0 + r0 + e * RE < rows) rowok |= 1u << e;
+  }
+  static constexpr int sstep() { return KMAJOR ? RE : KE * P; }
+
+  // fast path: full K range, no mask
+  __device__ __forceinline__ void load(T* s) const {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      if (rowok & (1u << e)) {
+        cp_async_t(s + soff + e * sstep(), ptr + e * step, true);
+      } else {
+        cp_async_t(s + soff + e * sstep(), ptr, false);
+      }
+    }
+  }
+  // tail / masked path: K bound and triangle mask (tri on (row, k) coords)
+  __device__ __forceinline__ void load_pred(T* s, int k0, int K, int tile0, int tri) const {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int r = tile0 + r0 + e * RE, k = k0 + k_0 + e * KE;
+      const bool ok = (rowok & (1u << e)) && k < K && a_keep(tri, r, k);
+      cp_async_t(s + soff + e * sstep(), ok ? ptr + e * step : ptr, ok);
+    }
+  }
+  __device__ __forceinline__ void advance() { ptr += kstep; }
+
+  __device__ __forceinline__ static void cp_async_t(T* s, const T* g, bool ok) {
+    if constexpr (sizeof(T) == 8) cp_async8(s, g, ok);
+    else cp_async16(s, g, ok);
+  }
+};
+
+// ------------------------------------------------------------ kernel
+// One CTA computes a BM x BN tile of C with (BM/WM) x (BN/WN) warps; each warp
+// a WM x WN sub-tile of m16n8k4 DMMA fragments.  Real: one DMMA per fragment
+// pair.  Complex: 4 real DMMAs (Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br),
+// conjugation by sign flips.  Padded smem rows (P = BM + 4 real / + 2 complex)
+// make the fragment loads bank-conflict free.
+template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
-    zgemm_kernel(GemmArgs<Z> g) {
+    gemm_kernel(GemmArgs<T> g) {
+  constexpr bool CPLX = is_cplx<T>::value;
   constexpr int WARPS_M = BM / WM;
   constexpr int NT = WARPS_M * (BN / WN) * 32;
-  constexpr int PA = BM + 2, PB = BN + 2;  // == 2 (mod 8) complex: conflict-free LDS.128
+  constexpr int PA = BM + (CPLX ? 2 : 4), PB = BN + (CPLX ? 2 : 4);
   constexpr int MI = WM / 16, NI = WN / 8;
+  constexpr int NACC = CPLX ? 2 : 1;
   extern __shared__ __align__(16) double smem_d[];
-  Z* As = reinterpret_cast<Z*>(smem_d);
-  Z* Bs = As + STAGES * BK * PA;
+  T* As = reinterpret_cast<T*>(smem_d);
+  T* Bs = As + STAGES * BK * PA;
   if (g.skip && *g.skip) return;
   int tm, tn;
   if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
@@ -173,43 +143,37 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int gq = lane >> 2, tq = lane & 3;
-  const double sa = g.conjA ? -1.0 : 1.0, sb = g.conjB ? -1.0 : 1.0;
 
-  double re[MI][NI][4], im[MI][NI][4];
+  TileLoader<T, BM, BK, NT, PA, AK> la;
+  TileLoader<T, BN, BK, NT, PB, BKM> lb;
+  la.init(g.A, g.lda, m0, M, tid);
+  lb.init(g.B, g.ldb, n0, N, tid);
+  const bool masked = g.a_tri != A_FULL || g.b_tri != A_FULL;
+
+  double acc[NACC][MI][NI][4];
 #pragma unroll
-  for (int i = 0; i < MI; ++i)
+  for (int c = 0; c < NACC; ++c)
 #pragma unroll
-    for (int j = 0; j < NI; ++j)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) re[i][j][r] = im[i][j][r] = 0.0;
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[c][i][j][r] = 0.0;
 
   const int KT = (K + BK - 1) / BK;
-  const Z* __restrict__ Ag = g.A;
-  const Z* __restrict__ Bg = g.B;
-  const i64 lda = g.lda, ldb = g.ldb;
-
   auto load_stage = [&](int stage, int kt) {
+    T* as = As + stage * BK * PA;
+    T* bs = Bs + stage * BK * PB;
     const int k0 = kt * BK;
-    Z* as = As + stage * BK * PA;
-    Z* bs = Bs + stage * BK * PB;
-#pragma unroll
-    for (int i = tid; i < BM * BK; i += NT) {
-      int m, k;
-      if (AK) { k = i % BK; m = i / BK; } else { m = i % BM; k = i / BM; }
-      const int gm = m0 + m, gk = k0 + k;
-      const bool ok = gm < M && gk < K;
-      const Z* src = ok ? (AK ? Ag + (i64)gm * lda + gk : Ag + gm + (i64)gk * lda) : Ag;
-      cp_async16(as + k * PA + m, src, ok);
+    if (!masked && k0 + BK <= K) {
+      la.load(as);
+      lb.load(bs);
+    } else {
+      la.load_pred(as, k0, K, m0, g.a_tri);
+      lb.load_pred(bs, k0, K, n0, g.b_tri);
     }
-#pragma unroll
-    for (int i = tid; i < BN * BK; i += NT) {
-      int n, k;
-      if (BKM) { k = i % BK; n = i / BK; } else { n = i % BN; k = i / BN; }
-      const int gn = n0 + n, gk = k0 + k;
-      const bool ok = gn < N && gk < K;
-      const Z* src = ok ? (BKM ? Bg + gk + (i64)gn * ldb : Bg + (i64)gk * ldb + gn) : Bg;
-      cp_async16(bs + k * PB + n, src, ok);
-    }
+    la.advance();
+    lb.advance();
   };
 
 #pragma unroll
@@ -217,45 +181,61 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     if (s < KT) load_stage(s, s);
     cp_async_commit();
   }
+  const double sa = (CPLX && g.conjA) ? -1.0 : 1.0, sb = (CPLX && g.conjB) ? -1.0 : 1.0;
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nk = kt + STAGES - 1;
     if (nk < KT) load_stage(nk % STAGES, nk);
     cp_async_commit();
-    const Z* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
-    const Z* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
+    const T* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
+    const T* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double ar[MI][2], ai[MI][2], nai[MI][2], br[NI], bi[NI];
+      if constexpr (!CPLX) {
+        double af[MI][2], bf[NI];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        Z v0 = as[(kk + tq) * PA + i * 16];
-        Z v1 = as[(kk + tq) * PA + i * 16 + 8];
-        ar[i][0] = v0.x; ai[i][0] = sa * v0.y;
-        ar[i][1] = v1.x; ai[i][1] = sa * v1.y;
-        nai[i][0] = -ai[i][0]; nai[i][1] = -ai[i][1];
-      }
+        for (int i = 0; i < MI; ++i) {
+          af[i][0] = as[(kk + tq) * PA + i * 16];
+          af[i][1] = as[(kk + tq) * PA + i * 16 + 8];
+        }
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        Z w = bs[(kk + tq) * PB + j * 8];
-        br[j] = w.x; bi[j] = sb * w.y;
-      }
+        for (int j = 0; j < NI; ++j) bf[j] = bs[(kk + tq) * PB + j * 8];
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma16x8x4(acc[0][i][j], af[i][0], af[i][1], bf[j]);
+      } else {
+        double ar[MI][2], ai[MI][2], nai[MI][2], br[NI], bi[NI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const Z v0 = as[(kk + tq) * PA + i * 16];
+          const Z v1 = as[(kk + tq) * PA + i * 16 + 8];
+          ar[i][0] = v0.x; ai[i][0] = sa * v0.y;
+          ar[i][1] = v1.x; ai[i][1] = sa * v1.y;
+          nai[i][0] = -ai[i][0]; nai[i][1] = -ai[i][1];
+        }
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
-          dmma16x8x4(re[i][j], ar[i][0], ar[i][1], br[j]);
-          dmma16x8x4(re[i][j], nai[i][0], nai[i][1], bi[j]);
-          dmma16x8x4(im[i][j], ar[i][0], ar[i][1], bi[j]);
-          dmma16x8x4(im[i][j], ai[i][0], ai[i][1], br[j]);
+          const Z w = bs[(kk + tq) * PB + j * 8];
+          br[j] = w.x; bi[j] = sb * w.y;
         }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) {
+            dmma16x8x4(acc[0][i][j], ar[i][0], ar[i][1], br[j]);
+            dmma16x8x4(acc[0][i][j], nai[i][0], nai[i][1], bi[j]);
+            dmma16x8x4(acc[1][i][j], ar[i][0], ar[i][1], bi[j]);
+            dmma16x8x4(acc[1][i][j], ai[i][0], ai[i][1], br[j]);
+          }
+      }
     }
   }
   cp_async_wait<0>();
 
-  const Z alpha = g.alpha, beta = g.beta;
-  const bool use_beta = !(beta.x == 0.0 && beta.y == 0.0);
+  const T alpha = g.alpha, beta = g.beta;
+  const bool use_beta = !is_zero(beta);
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -265,11 +245,17 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
         const int row = m0 + wm * WM + i * 16 + gq + ((r & 2) ? 8 : 0);
         const int col = n0 + wn * WN + j * 8 + 2 * tq + (r & 1);
         if (row < M && col < N && tri_keep(MODE, row, col)) {
-          Z* c = g.C + row + (i64)col * g.ldc;
-          Z v = alpha * Z{re[i][j][r], im[i][j][r]};
-          if (use_beta) v = v + beta * (*c);
-          if (MODE != TRI_FULL && g.herm_diag && row == col) v.y = 0.0;
-          *c = v;
+          T* c = g.C + row + (i64)col * g.ldc;
+          if constexpr (!CPLX) {
+            double v = alpha * acc[0][i][j][r];
+            if (use_beta) v = fma(beta, *c, v);
+            *c = v;
+          } else {
+            Z v = alpha * Z{acc[0][i][j][r], acc[1][i][j][r]};
+            if (use_beta) v = v + beta * (*c);
+            if (MODE != TRI_FULL && g.herm_diag && row == col) v.y = 0.0;
+            *c = v;
+          }
         }
       }
 }
@@ -331,10 +317,7 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
   constexpr int NT = (BM / WM) * (BN / WN) * 32;
   constexpr int PA = BM + (is_cplx<T>::value ? 2 : 4), PB = BN + (is_cplx<T>::value ? 2 : 4);
   constexpr size_t smem = (size_t)ST * BK * (PA + PB) * sizeof(T);
-  auto kern = [] {
-    if constexpr (is_cplx<T>::value) return zgemm_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
-    else return dgemm_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
-  }();
+  auto kern = gemm_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -377,7 +360,8 @@ int launch_mode(const GemmArgs<T>& a, int mode, bool ak, bool bk, cudaStream_t s
 
 template <typename T>
 int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T beta,
-         View<T> C, bool herm_diag, const int* skip, cudaStream_t st) {
+         View<T> C, bool herm_diag, const int* skip, cudaStream_t st, int a_tri,
+         bool inplace_leaf) {
   if (C.empty()) return 0;
   if (A.n == 0 || is_zero(alpha)) {
     bool unit_beta;
@@ -386,18 +370,24 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
     if (unit_beta && !herm_diag) return 0;
     return scale_view(C, beta, tri_mode, herm_diag, skip, st);
   }
-  if (!(C.rs == 1 || C.n == 1)) {
-    // C row-major: solve C^T = op(B)^T op(A)^T (column-major)
+  // in-place leaf: the leaf dimension (M) must fit one 64-wide tile; after the
+  // optional transpose below it becomes N, and the 64x64 config covers it
+  // either way, so each CTA reads its whole slab of B before overwriting it.
+  if (inplace_leaf && C.m > 64) return -101;
+  bool transposed = false;
+  if (!(C.rs == 1 || C.m == 1)) {
+    // C not column-major: solve C^T = op(B)^T op(A)^T (column-major)
     View<T> At = B.t(), Bt = A.t();
     A = At; B = Bt;
     bool c = conjA; conjA = conjB; conjB = c;
+    transposed = true;
     C = C.t();
     if (tri_mode == TRI_LOWER) tri_mode = TRI_UPPER;
     else if (tri_mode == TRI_UPPER) tri_mode = TRI_LOWER;
   }
   OperandLayout la = classify(A);
   OperandLayout lb = classify(B.t());  // B^T is N x K
-  if (!la.ok || !lb.ok || !(C.rs == 1 || C.n == 1)) return -100;
+  if (!la.ok || !lb.ok || !(C.rs == 1 || C.m == 1)) return -100;
   GemmArgs<T> g;
   g.M = (int)C.m; g.N = (int)C.n; g.K = (int)A.n;
   g.A = A.p; g.lda = la.ld;
@@ -408,9 +398,15 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
   g.herm_diag = herm_diag ? 1 : 0;
   g.skip = skip;
   g.tiles_m = 0;
+  g.a_tri = transposed ? A_FULL : a_tri;
+  g.b_tri = transposed ? a_tri : A_FULL;
   // operand "K-major": A contiguous along K  <=> la.kmajor; for B, B^T (N x K)
   // contiguous along K <=> lb.kmajor.
   const bool ak = la.kmajor, bk = lb.kmajor;
+  if (inplace_leaf) {
+    return launch_mode<T, 64, 64, 16 / (is_cplx<T>::value ? 2 : 1), 32, 32, 3>(g, tri_mode, ak,
+                                                                               bk, st);
+  }
   if constexpr (is_cplx<T>::value) {
     long long tiles = (long long)((g.M + 63) / 64) * ((g.N + 63) / 64);
     if (tiles >= num_sms())
@@ -425,9 +421,9 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
 }
 
 template int gemm<double>(int, double, View<double>, bool, View<double>, bool, double,
-                          View<double>, bool, const int*, cudaStream_t);
+                          View<double>, bool, const int*, cudaStream_t, int, bool);
 template int gemm<Z>(int, Z, View<Z>, bool, View<Z>, bool, Z, View<Z>, bool, const int*,
-                     cudaStream_t);
+                     cudaStream_t, int, bool);
 template int scale_view<double>(View<double>, double, int, bool, const int*, cudaStream_t);
 template int scale_view<Z>(View<Z>, Z, int, bool, const int*, cudaStream_t);
 

@@ -32,11 +32,20 @@ template <typename T> struct GemmArgs {
   int herm_diag;      // complex TRI modes: force Im(C_ii) = 0
   const int* skip;    // device flag: nonzero -> do nothing (failed factorization)
   int tiles_m;        // tiles along M (for the triangular mapping)
+  int a_tri;          // A operand mask: 0 none, 1 lower, 2 upper, 3 strict lower, 4 strict upper
+  int b_tri;          // same mask applied to B (k, n) as if it were A (n, k) (transposed problems)
 };
+
+// A-operand triangle masks (for triangular-times-matrix leaves)
+enum ATri : int { A_FULL = 0, A_LOWER = 1, A_UPPER = 2, A_SLOWER = 3, A_SUPPER = 4 };
+
 
 template <typename T>
 int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T beta,
-         View<T> C, bool herm_diag, const int* skip, cudaStream_t st);
+         View<T> C, bool herm_diag, const int* skip, cudaStream_t st, int a_tri = A_FULL,
+         bool inplace_leaf = false);
+// inplace_leaf: C aliases B and M <= 64; the launch uses one CTA row (BM >= M) so
+// every CTA reads its whole B column block before writing it back.
 
 // scale/zero a (possibly triangular) view: C <- beta*C (beta == 0 writes zeros)
 template <typename T>

@@ -47,21 +47,28 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
   const bool herm = is_cplx<T>::value;
   View<T> t1, t2, s1;
   rfp_blocks(d, arf, t1, t2, s1);
+  // one workspace for the leaf inverses: T1's are reused by the S1 solve,
+  // then the buffer is reused for T2's potrf
+  T* W = nullptr;
+  TRY(ws_alloc(&W, d.n1, c.st));
+  int rc = 0;
   if (d.lower) {
-    TRY(blas_potrf(c, 'L', t1, 0));
-    if (d.n2) {
-      TRY(blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false));
-      TRY(blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm));
-      TRY(blas_potrf(c, 'U', t2, (int)d.n1));
+    rc = blas_potrf(c, 'L', t1, 0, W);
+    if (!rc && d.n2) {
+      if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
+      if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
+      if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n1, W);
     }
-    return 0;
+  } else {
+    if (d.n2) {
+      rc = blas_potrf(c, 'L', t1, 0, W);
+      if (!rc) rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
+      if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
+    }
+    if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n2, W);
   }
-  if (d.n2) {
-    TRY(blas_potrf(c, 'L', t1, 0));
-    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false));
-    TRY(blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm));
-  }
-  return blas_potrf(c, 'U', t2, (int)d.n2);
+  ws_free(W, c.st);
+  return rc;
 }
 
 // forward/back substitution through T1/S1/T2 (rfp.py:106-136)
