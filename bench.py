@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark contract for the B200 RFPF path ("Measurement").
+
+Default workload = BASELINE config 3 (the north-star target): one real FP64
+SPD matrix, n = 16384, TRANSR='N', UPLO='L', A = B B^T / n + I; a step is
+pftrf followed by pftrs with nrhs = 1024, on an RFP buffer restored from a
+pristine device copy at the start of the step (the RFP buffer, 1.07 GB, and
+the RHS exceed the 126 MB L2, so no flush is needed).  Metric: FP64 GFLOP/s
+with the LAPACK flop model n^3/3 + 2 n^2 nrhs.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  --workload c3 (default) | c1 | c2 | c4 | c5   (other BASELINE configs)
+
+Under torchrun (N > 1) every rank factors its own replica (single matrices
+do not shard: "replicas only", weak scaling); config 4 (--workload c4) is
+sharded by matrix.  --impl reference times the CPU oracle (the NumPy
+restatement of the reference algorithm; the reference itself is pure Python
+and cannot be installed on the GPU box) on a bounded sample of the same
+workload on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 128 flop/clk x 1.965 GHz (B200_PROFILING / SURVEY 6)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- dist
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- CPU (oracle)
+def cpu_sample(n=4096, nrhs=256, reps=2, seed=3):
+    """Oracle pftrf + pftrs on the host cores (bounded sample of config 3)."""
+    from oracle import rfp_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    a = O.spd_matrix(n, seed, "1/n")
+    buf0 = O.trttf(a, "L", "N")
+    b0 = np.asfortranarray(np.random.default_rng(seed + 1).standard_normal((n, nrhs)))
+    ts = []
+    for _ in range(reps):
+        buf = buf0.copy()
+        x = b0.copy(order="F")
+        t0 = time.perf_counter()
+        assert O.pftrf(buf, n, "L", "N") == 0
+        O.pftrs(buf, n, "L", "N", x)
+        ts.append(time.perf_counter() - t0)
+    flops = n ** 3 / 3 + 2 * n * n * nrhs
+    t = float(np.median(ts))
+    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+            "sample": f"oracle pftrf+pftrs n={n} LN nrhs={nrhs} (median of {reps}, "
+                      f"{t:.2f} s each; OpenBLAS {cores} threads)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_sample(n=args.ref_n, nrhs=args.ref_nrhs, reps=1, seed=3 + i)
+        if i >= args.warmup:
+            steps.append(res["value"])
+    value = float(np.mean(steps))
+    n, nrhs = 16384, 1024
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (args.ref_n ** 3 / 3 + 2 * args.ref_n ** 2 * args.ref_nrhs) / value / 1e6,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy)",
+        "config": {"workload": f"config3 sample: n={args.ref_n} LN pftrf+pftrs nrhs={args.ref_nrhs} "
+                               f"(bounded CPU sample of n={n}, nrhs={nrhs})"},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"], "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "FP64 GFLOP/s of RFPF pftrf+pftrs (n=16384, TRANSR=N, UPLO=L, nrhs=1024)"
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args, rank, world, local):
+    import torch
+    from paper_0901_1696_b200 import _capi, convert, rfp
+    from paper_0901_1696_b200.layout import make_descriptor
+
+    lib = _capi.lib()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, nrhs, uplo, transr = args.n, args.nrhs, "L", "N"
+    desc = make_descriptor(n, uplo, transr)
+    flops = n ** 3 / 3 + 2 * n * n * nrhs
+
+    # inputs: B ~ N(0,1) seeded on the host, A = B B^T / n + I formed on the device
+    seed = 1234 + rank
+    rng = np.random.default_rng(seed)
+    bh = torch.from_numpy(rng.standard_normal((n, n)))
+    bd = bh.to(dev)
+    del bh
+    a = bd @ bd.t()
+    a /= n
+    a.diagonal().add_(1.0)
+    del bd
+    pristine = convert.trttf(a, uplo, transr).data  # our trttf kernel
+    rhs0 = torch.from_numpy(np.random.default_rng(seed + 7).standard_normal((nrhs, n))).to(dev).t()
+    work = torch.empty_like(pristine)
+    x = torch.empty((nrhs, n), dtype=torch.float64, device=dev).t()
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    sh = st.cuda_stream
+    T, U = transr.encode(), uplo.encode()
+
+    def step():
+        work.copy_(pristine)
+        x.copy_(rhs0)
+        rc = lib.rfpk_dpftrf(T, U, n, work.data_ptr(), info.data_ptr(), sh)
+        rc |= lib.rfpk_dpftrs(T, U, n, nrhs, work.data_ptr(), x.data_ptr(), n, info.data_ptr(), sh)
+        if rc:
+            raise RuntimeError(f"rfpk call failed rc={rc}")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0, "factorization failed"
+
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = lib.rfpk_launch_count()
+    with ClockSampler(local) as clk:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        for _ in range(args.steps):
+            step()
+        e.record(st)
+        torch.cuda.synchronize()
+    launches = lib.rfpk_launch_count() - l0
+    barrier(world)
+    ms = max_over_ranks(s.elapsed_time(e) / args.steps, world)
+    value = world * flops / (ms * 1e-3) / 1e9
+
+    # result check: ||A X - B|| / (||A|| ||X|| n eps) on the last step's solution
+    r = a @ x - rhs0
+    resid = float(r.norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
+
+    # dominant kernel: the SYRK/HERK T2 <- T2 - S1^T S1 of pftrf (n2 x n2, k = n1),
+    # timed alone through the C ABI on the live RFP views with CUDA events
+    off_t2, off_s1 = 0, desc.n1 + desc.shift
+    ld = desc.ldar
+    kern_flops = desc.n2 * (desc.n2 + 1) * desc.n1
+    t2p = work.data_ptr() + 8 * ((1 - desc.shift) * ld)
+    s1p = work.data_ptr() + 8 * off_s1
+
+    def dom():
+        lib.rfpk_dsyrk(b"U", b"C", -1.0, s1p, desc.n2, desc.n1, 1, ld, 1.0, t2p, desc.n2, 1, ld, sh)
+
+    dom()
+    torch.cuda.synchronize()
+    ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kreps = 3
+    ks.record(st)
+    for _ in range(kreps):
+        dom()
+    ke.record(st)
+    torch.cuda.synchronize()
+    kms = ks.elapsed_time(ke) / kreps
+    k_tflops = kern_flops / (kms * 1e-3) / 1e12
+
+    # measured DGEMM ceiling (cuBLAS via torch) for context
+    g1 = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    g2 = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    torch.matmul(g1, g2)
+    torch.cuda.synchronize()
+    gs, ge = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gs.record(st)
+    for _ in range(3):
+        torch.matmul(g1, g2)
+    ge.record(st)
+    torch.cuda.synchronize()
+    dgemm_tflops = 3 * 2 * 8192 ** 3 / (gs.elapsed_time(ge) * 1e-3) / 1e12
+    del g1, g2
+
+    # end-to-end through the public Python API with host (pinned) buffers
+    host_rfp = pristine.cpu().pin_memory()
+    host_b = rhs0.t().contiguous().cpu().pin_memory()  # nrhs x n row-major == column-major B
+    h2d = host_rfp.numel() * 8 + host_b.numel() * 8
+    d2h = host_b.numel() * 8
+    out_x = torch.empty_like(host_b).pin_memory()
+    e2e_steps = max(1, args.steps // 2)
+
+    def e2e_step():
+        r_ = convert.RfpTriangle(host_rfp.to(dev, non_blocking=True), desc)
+        xb = host_b.to(dev, non_blocking=True).t()
+        assert rfp.pftrf(r_) == 0
+        rfp.pftrs(r_, xb)
+        out_x.copy_(xb.t(), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    e2e_step()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record(st)
+    for _ in range(e2e_steps):
+        e2e_step()
+    ee.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(es.elapsed_time(ee) / e2e_steps, world)
+    e2e_value = world * flops / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        return
+    cpu = cpu_sample() if (world == 1 and not args.no_cpu) else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: B~N(0,1) seeded numpy, A=B B^T/n+I (formed on device), RHS~N(0,1)",
+        "config": {"workload": "BASELINE config 3: pftrf+pftrs, n=16384, TRANSR=N, UPLO=L, nrhs=1024",
+                   "n": n, "nrhs": nrhs, "transr": transr, "uplo": uplo,
+                   "l2": "no flush: RFP buffer 1.07 GB + RHS 134 MB exceed the 126 MB L2",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "fraction_of_fp64_nominal": value / 1e3 / NOMINAL_FP64_TFLOPS,
+        "fraction_of_fp64_measured_dgemm": value / 1e3 / dgemm_tflops,
+        "roofline": {"bound": "tensor", "kernel": "gemm_kernel TRI (SYRK T2 -= S1^T S1, 8192x8192, k=8192)",
+                     "achieved": k_tflops, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
+                     "frac": k_tflops / NOMINAL_FP64_TFLOPS, "traffic": None,
+                     "peak_source": "nominal FP64 DMMA (MEASURED_PEAKS.json has no FP64 figure); "
+                                    f"measured cuBLAS DGEMM here: {dgemm_tflops:.2f} TFLOP/s"},
+        "residual_scaled": resid,
+        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "path": "rfp.pftrf/rfp.pftrs (public API) on pinned host buffers"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--nrhs", type=int, default=1024)
+    ap.add_argument("--ref-n", type=int, default=4096)
+    ap.add_argument("--ref-nrhs", type=int, default=256)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

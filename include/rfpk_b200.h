@@ -45,6 +45,8 @@ typedef struct CUstream_st* rfpk_stream_t; /* == cudaStream_t */
 const char* rfpk_version(void);
 /* number of SMs of the current device, or a negative CUDA error */
 int rfpk_device_sms(void);
+/* total kernels this library has launched in the process (monotonic) */
+long long rfpk_launch_count(void);
 
 /* conversions: verbatim copies, bit-exact (convert.py:156-275) ----------- */
 /* replaces convert.trttf(a, uplo, transr)   convert.py:156-186 */

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   T* Ws = S + 64 * LD64;
+  T* scratch = Ws + 64 * LD64;  // 64 entries: column broadcast / reciprocals
   __shared__ int fail;
   if (*info) return;
   const int n = (int)A.m;
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   leaf_load_lower(S, A, n);
   __syncthreads();
   if (warp == 0) {
-    const int f = chol32_warp(S, 0);
+    const int f = chol32_warp(S, 0, scratch);
     if (lane == 0 && f) fail = f;
   }
   __syncthreads();
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
     if (threadIdx.x == 0) *info = base + fail;
     return;
   }
-  if (warp == 0) inv32_warp(S, 0, Ws, 0, false);
+  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
   __syncthreads();
   const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
   T acc[8];
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
     if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
   __syncthreads();
   if (warp == 0) {
-    const int f = chol32_warp(S, 32);
+    const int f = chol32_warp(S, 32, scratch);
     if (lane == 0 && f) fail = 32 + f;
   }
   __syncthreads();
@@ -115,9 +116,9 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
     if (threadIdx.x == 0) *info = base + fail;
     return;
   }
-  if (warp == 1) inv32_warp(S, 32, Ws, 32, false);
+  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
   __syncthreads();
-  if (W) inv64_block(S, Ws, false, true);
+  if (W) inv64_block(S, Ws, false, true, scratch);
   __syncthreads();
   leaf_store_lower(S, A, n, false);
   if (W)
@@ -132,13 +133,14 @@ __global__ void __launch_bounds__(128) trtri_leaves_kernel(View<T> A, T* W, int 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   T* Ws = S + 64 * LD64;
+  T* scratch = Ws + 64 * LD64;
   if (skip && *skip) return;
   const i64 r0 = (i64)blockIdx.x * 64;
   const int len = (int)((A.m - r0) < 64 ? (A.m - r0) : 64);
   View<T> blk = A.sub(r0, r0, len, len);
   leaf_load_lower(S, blk, len);
   __syncthreads();
-  inv64_block(S, Ws, unit != 0, false);
+  inv64_block(S, Ws, unit != 0, false, scratch);
   __syncthreads();
   if (W) {
     T* dst = W + r0 * 64;
@@ -196,7 +198,7 @@ __global__ void diag_scan_kernel(View<T> A, int* info, int base, int highest) {
 namespace {
 
 template <typename T> size_t leaf_smem(int tiles) {
-  return (size_t)tiles * (LEAF + 1) * LEAF * sizeof(T);
+  return ((size_t)tiles * (LEAF + 1) * LEAF + 64) * sizeof(T);
 }
 
 template <typename K> void allow_smem(K kern, size_t bytes) {
@@ -227,9 +229,24 @@ template <typename T> bool is_one(T v) {
 // workspace for the leaf inverses of an order-n triangle (64 x 64 per leaf)
 template <typename T> size_t leaf_ws_elems(i64 n) { return (size_t)((n + 63) / 64) * 64 * 64; }
 
+// The device's default memory pool keeps freed blocks (release threshold =
+// max), so the per-call workspace is a cheap stream-ordered suballocation.
+static void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st) {
   *p = nullptr;
   if (n <= 0) return 0;
+  keep_pool_memory();
   cudaError_t e = cudaMallocAsync((void**)p, leaf_ws_elems<T>(n) * sizeof(T), st);
   return e == cudaSuccess ? 0 : (int)e;
 }

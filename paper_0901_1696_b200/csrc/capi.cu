@@ -145,9 +145,15 @@ Z zc(double re, double im) { return Z{re, im}; }
 
 }  // namespace
 
+namespace rfpk {
+std::atomic<long long> g_launch_count{0};
+}
+
 extern "C" {
 
 const char* rfpk_version(void) { return "rfpk_b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+long long rfpk_launch_count(void) { return g_launch_count.load(); }
 
 int rfpk_device_sms(void) {
   int dev = 0, sms = 0;

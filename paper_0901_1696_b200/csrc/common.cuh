@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 
@@ -80,8 +81,13 @@ template <typename T> struct View {
 };
 
 // ---------------------------------------------------------------- errors
+// Every kernel launch site ends with RFPK_CHECK_LAUNCH, which also counts the
+// launch (exported as rfpk_launch_count() so benchmarks can report how many
+// of the library's kernels ran).
+extern std::atomic<long long> g_launch_count;
 #define RFPK_CHECK_LAUNCH()                                                   \
   do {                                                                        \
+    g_launch_count.fetch_add(1, std::memory_order_relaxed);                   \
     cudaError_t e_ = cudaGetLastError();                                      \
     if (e_ != cudaSuccess) {                                                  \
       fprintf(stderr, "rfpk: launch failed %s at %s:%d\n",                    \

@@ -236,8 +236,22 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
   const T alpha = g.alpha, beta = g.beta;
   const bool use_beta = !is_zero(beta);
+  // Epilogue, one MI row-block at a time: all C loads of the block are issued
+  // before any store (so their latencies overlap), then alpha/beta are
+  // applied and the triangle-masked stores issued.
 #pragma unroll
-  for (int i = 0; i < MI; ++i)
+  for (int i = 0; i < MI; ++i) {
+    T cv[NI][4];
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm * WM + i * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * WN + j * 8 + 2 * tq + (r & 1);
+        cv[j][r] = (use_beta && row < M && col < N && tri_keep(MODE, row, col))
+                       ? g.C[row + (i64)col * g.ldc]
+                       : sc_from<T>(0.0);
+      }
 #pragma unroll
     for (int j = 0; j < NI; ++j)
 #pragma unroll
@@ -248,16 +262,17 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
           T* c = g.C + row + (i64)col * g.ldc;
           if constexpr (!CPLX) {
             double v = alpha * acc[0][i][j][r];
-            if (use_beta) v = fma(beta, *c, v);
+            if (use_beta) v = fma(beta, cv[j][r], v);
             *c = v;
           } else {
             Z v = alpha * Z{acc[0][i][j][r], acc[1][i][j][r]};
-            if (use_beta) v = v + beta * (*c);
+            if (use_beta) v = v + beta * cv[j][r];
             if (MODE != TRI_FULL && g.herm_diag && row == col) v.y = 0.0;
             *c = v;
           }
         }
       }
+  }
 }
 
 // ------------------------------------------------------------ scale kernel

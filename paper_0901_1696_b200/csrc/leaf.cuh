@@ -1,13 +1,14 @@
 // Shared-memory / register building blocks for the 64 x 64 diagonal leaves.
 //
 // A leaf is split 2 x 2 into 32 x 32 blocks.  The 32 x 32 Cholesky and the
-// 32 x 32 triangular inverse each run on ONE warp over shared memory (lane i
-// owns row i for the Cholesky, column i for the inverse; only __syncwarp, no
-// CTA barriers); the 32 x 32 off-diagonal products use all four warps.
-// Leaves are stored column-major in shared memory with a 65-element stride
-// (conflict-free columns).  Loops are kept rolled on purpose: a fully
-// unrolled register version compiled to ~36k SASS instructions and ran
-// 10x slower from instruction-cache misses.
+// 32 x 32 triangular inverse each run on ONE warp with the block in registers
+// (lane i owns row i for the Cholesky, column i for the inverse; shuffles and
+// shared-memory broadcasts, no CTA barriers); the 32 x 32 off-diagonal
+// products use all four warps.  Leaves are stored column-major in shared
+// memory with a 65-element stride (conflict-free columns).  The unrolled
+// 32-blocks are __noinline__ so each kernel holds ONE copy: inlining every
+// call site (and per-element divisions) produced ~36k SASS instructions per
+// kernel and a 10x slowdown from instruction-cache misses.
 #pragma once
 #include "common.cuh"
 
@@ -63,56 +64,73 @@ __device__ void leaf_store_lower(const T* S, View<T> A, int n, bool skip_diag) {
   }
 }
 
+// 1/sqrt(x) for x > 0: MUFU seed + Newton steps (relative error ~1 ulp).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y = rsqrt(x);
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
 // One warp: in-place Cholesky (A = L L^H) of the 32 x 32 lower block of S at
-// (off, off), right-looking, lane i owning row i.  Loops stay rolled (the
-// leaf kernels must fit the instruction cache).  Returns 0 or the 1-based
+// (off, off), right-looking, lane i holding row i in registers.  Column k is
+// broadcast through a 32-entry shared-memory vector (one LDS per update, no
+// shuffles); the trailing update runs unpredicated on every lane -- values
+// that land above the diagonal are never read back or stored, so lower
+// entries only ever combine valid factor entries.  Not inlined: one copy of
+// the unrolled body serves both diagonal blocks.  Returns 0 or the 1-based
 // failing pivot (warp-uniform); `not d > 0` catches NaN (kernels.py:441).
 template <typename T>
-__device__ int chol32_warp(T* S, int off) {
-  const int i = threadIdx.x & 31;
-  T* B = S + off + off * LD64;
+__device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
+  const int lane = threadIdx.x & 31;
+  T r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) r[j] = S[(off + lane) + (off + j) * LD64];
+  int fail = 0;
+#pragma unroll
   for (int k = 0; k < 32; ++k) {
-    const double dkk = sc_re(B[k + k * LD64]);
-    if (!(dkk > 0.0)) return k + 1;
-    const double d = sqrt(dkk);
-    T lik = zero_<T>();
-    if (i > k) {
-      lik = B[i + k * LD64] / d;
-      B[i + k * LD64] = lik;
-    }
+    const double dkk = shfl(sc_re(r[k]), k);
+    if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
+    const double rd = rsqrt_nr(dkk);
+    const T lk = (lane == k) ? sc_from<T>(dkk * rd) : rd * r[k];
+    r[k] = lk;
+    colk[lane] = conj_(lk);
     __syncwarp();
-    if (i == k) B[k + k * LD64] = sc_from<T>(d);
-    if (i > k) {
-#pragma unroll 4
-      for (int j = k + 1; j <= i; ++j) B[i + j * LD64] = fnmac(lik, conj_(B[j + k * LD64]), B[i + j * LD64]);
-    }
+#pragma unroll
+    for (int j = k + 1; j < 32; ++j) r[j] = fnmac(lk, colk[j], r[j]);
     __syncwarp();
   }
+  if (fail) return fail;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j <= lane) S[(off + lane) + (off + j) * LD64] = r[j];
   return 0;
 }
 
 // One warp: W(offw.., offw..) = inverse of the 32 x 32 lower block of S at
-// (off, off); lane j computes column j (zeros above the diagonal).
+// (off, off); lane j holds column j of W in registers (rows above j are 0).
+// Row i of L is read with shared-memory broadcasts; reciprocals of the
+// diagonal are computed once per lane into `rdiag`.
 template <typename T>
-__device__ void inv32_warp(const T* S, int off, T* W, int offw, bool unit) {
+__device__ __noinline__ void inv32_warp(const T* S, int off, T* W, int offw, bool unit, T* rdiag) {
   const int j = threadIdx.x & 31;
   const T* L = S + off + off * LD64;
-  T* w = W + offw + (offw + j) * LD64;
+  rdiag[j] = unit ? one_<T>() : one_<T>() / L[j + j * LD64];
+  __syncwarp();
+  T w[32];
+#pragma unroll
   for (int i = 0; i < 32; ++i) {
-    if (i < j) {
-      w[i] = zero_<T>();
-      continue;
-    }
     T s0 = (i == j) ? one_<T>() : zero_<T>(), s1 = zero_<T>();
-    int k = j;
-    for (; k + 1 < i; k += 2) {
-      s0 = fnmac(L[i + k * LD64], w[k], s0);
-      s1 = fnmac(L[i + (k + 1) * LD64], w[k + 1], s1);
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      if (k & 1) s1 = fnmac(L[i + k * LD64], w[k], s1);
+      else s0 = fnmac(L[i + k * LD64], w[k], s0);
     }
-    if (k < i) s0 = fnmac(L[i + k * LD64], w[k], s0);
-    const T s = s0 + s1;
-    w[i] = unit ? s : s / L[i + i * LD64];
+    w[i] = (s0 + s1) * rdiag[i];
   }
+  T* wc = W + offw + (offw + j) * LD64;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) wc[i] = (i >= j) ? w[i] : zero_<T>();
   __syncwarp();
 }
 
@@ -143,11 +161,11 @@ __device__ __forceinline__ void mm32(const T* X, int xr, int xc, const T* Y, int
 // diagonal).  Needs 128 threads; S's upper-right 32 x 32 block is used as
 // scratch.  Caller syncs before (S ready) and after.
 template <typename T>
-__device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done) {
+__device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scratch) {
   const int warp = threadIdx.x >> 5;
   if (!both_diag_done) {
-    if (warp == 0) inv32_warp(S, 0, W, 0, unit);
-    if (warp == 1) inv32_warp(S, 32, W, 32, unit);
+    if (warp == 0) inv32_warp(S, 0, W, 0, unit, scratch);
+    if (warp == 1) inv32_warp(S, 32, W, 32, unit, scratch + 32);
     __syncthreads();
   }
   // Y = L21 * W11  (scratch: S rows 0..31, cols 32..63)
