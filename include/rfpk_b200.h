@@ -45,8 +45,13 @@ typedef struct CUstream_st* rfpk_stream_t; /* == cudaStream_t */
 const char* rfpk_version(void);
 /* number of SMs of the current device, or a negative CUDA error */
 int rfpk_device_sms(void);
-/* total kernels this library has launched in the process (monotonic) */
+/* total kernels this library has launched in the process (monotonic;
+   kernels replayed from a cached CUDA graph are counted per replay) */
 long long rfpk_launch_count(void);
+/* pftrf/pftrs/tftri/pftri calls are captured into CUDA graphs keyed by their
+   full argument tuple (pointers included) and replayed on repeat calls;
+   RFPK_GRAPHS=0 disables.  This drops every cached graph. */
+int rfpk_graph_cache_clear(void);
 
 /* conversions: verbatim copies, bit-exact (convert.py:156-275) ----------- */
 /* replaces convert.trttf(a, uplo, transr)   convert.py:156-186 */

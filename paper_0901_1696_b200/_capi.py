@@ -27,6 +27,7 @@ SIGNATURES = {
     "rfpk_version": ([], ctypes.c_char_p),
     "rfpk_device_sms": ([], _int),
     "rfpk_launch_count": ([], ctypes.c_longlong),
+    "rfpk_graph_cache_clear": ([], _int),
     "rfpk_dtrttf": ([_c, _c, _i64, _p, _i64, _p, _p], _int),
     "rfpk_ztrttf": ([_c, _c, _i64, _p, _i64, _p, _p], _int),
     "rfpk_dtfttr": ([_c, _c, _i64, _p, _p, _i64, _p], _int),

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   T* Ws = S + 64 * LD64;
-  T* scratch = Ws + 64 * LD64;  // 64 entries: column broadcast / reciprocals
+  T* scratch = Ws + 64 * LD64;  // 64 entries: column broadcast (2 x 32) / reciprocals
   __shared__ int fail;
   if (*info) return;
   const int n = (int)A.m;

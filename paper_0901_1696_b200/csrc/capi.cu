@@ -1,6 +1,7 @@
 // extern "C" boundary (include/rfpk_b200.h): argument checking, info reset,
 // and dispatch into the templated drivers.  No allocations, no host syncs.
 #include "../../include/rfpk_b200.h"
+#include "graph_cache.cuh"
 #include "rfp.cuh"
 
 using namespace rfpk;
@@ -14,6 +15,7 @@ bool one_of(char c, const char* set) {
   return false;
 }
 cudaStream_t S(rfpk_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+int cur_device();
 
 int reset_info(int* info, cudaStream_t st) {
   if (!info) return 0;
@@ -102,8 +104,12 @@ int pftrf_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_
   if (!one_of(uplo, "LU")) return -2;
   if (n < 0) return -3;
   if (!info) return -5;
-  if (int rc = reset_info(info, st)) return rc;
-  return pftrf<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (T*)arf);
+  GraphKey key{1, is_cplx<T>::value ? 'z' : 'd', transr, uplo, 'N', n, 0, 0, 0, arf, nullptr, info,
+               cur_device()};
+  return GraphCache::get().run(key, st, [&](cudaStream_t s) {
+    if (int rc = reset_info(info, s)) return rc;
+    return pftrf<T>(Ctx{s, info}, rfp_desc(n, uplo, transr), (T*)arf);
+  });
 }
 template <typename T>
 int pftrs_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* arf, void* b,
@@ -115,9 +121,13 @@ int pftrs_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* arf, vo
   if (nrhs < 0) return -4;
   if (!unit_stride(n, nrhs, rsb, csb)) return -7;
   if (!info) return -8;
-  if (int rc = reset_info(info, st)) return rc;
-  return pftrs<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (const T*)arf,
-                  V<T>(b, n, nrhs, rsb, csb));
+  GraphKey key{2, is_cplx<T>::value ? 'z' : 'd', transr, uplo, 'N', n, nrhs, rsb, csb, arf, b, info,
+               cur_device()};
+  return GraphCache::get().run(key, st, [&](cudaStream_t s) {
+    if (int rc = reset_info(info, s)) return rc;
+    return pftrs<T>(Ctx{s, info}, rfp_desc(n, uplo, transr), (const T*)arf,
+                    V<T>(b, n, nrhs, rsb, csb));
+  });
 }
 template <typename T>
 int tftri_t(char transr, char uplo, char diag, int64_t n, void* arf, int* info, cudaStream_t st) {
@@ -127,8 +137,12 @@ int tftri_t(char transr, char uplo, char diag, int64_t n, void* arf, int* info, 
   if (!one_of(diag, "NU")) return -3;
   if (n < 0) return -4;
   if (!info) return -6;
-  if (int rc = reset_info(info, st)) return rc;
-  return tftri<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), diag, (T*)arf);
+  GraphKey key{3, is_cplx<T>::value ? 'z' : 'd', transr, uplo, diag, n, 0, 0, 0, arf, nullptr, info,
+               cur_device()};
+  return GraphCache::get().run(key, st, [&](cudaStream_t s) {
+    if (int rc = reset_info(info, s)) return rc;
+    return tftri<T>(Ctx{s, info}, rfp_desc(n, uplo, transr), diag, (T*)arf);
+  });
 }
 template <typename T>
 int pftri_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_t st) {
@@ -137,11 +151,21 @@ int pftri_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_
   if (!one_of(uplo, "LU")) return -2;
   if (n < 0) return -3;
   if (!info) return -5;
-  if (int rc = reset_info(info, st)) return rc;
-  return pftri<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (T*)arf);
+  GraphKey key{4, is_cplx<T>::value ? 'z' : 'd', transr, uplo, 'N', n, 0, 0, 0, arf, nullptr, info,
+               cur_device()};
+  return GraphCache::get().run(key, st, [&](cudaStream_t s) {
+    if (int rc = reset_info(info, s)) return rc;
+    return pftri<T>(Ctx{s, info}, rfp_desc(n, uplo, transr), (T*)arf);
+  });
 }
 
 Z zc(double re, double im) { return Z{re, im}; }
+
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 
 }  // namespace
 
@@ -154,6 +178,11 @@ extern "C" {
 const char* rfpk_version(void) { return "rfpk_b200 0.1 (sm_100a, FP64 DMMA)"; }
 
 long long rfpk_launch_count(void) { return g_launch_count.load(); }
+
+int rfpk_graph_cache_clear(void) {
+  GraphCache::get().clear();
+  return 0;
+}
 
 int rfpk_device_sms(void) {
   int dev = 0, sms = 0;

@@ -87,18 +87,24 @@ __device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) r[j] = S[(off + lane) + (off + j) * LD64];
   int fail = 0;
+  double dkk = shfl(sc_re(r[0]), 0);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
-    const double dkk = shfl(sc_re(r[k]), k);
     if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
     const double rd = rsqrt_nr(dkk);
     const T lk = (lane == k) ? sc_from<T>(dkk * rd) : rd * r[k];
     r[k] = lk;
-    colk[lane] = conj_(lk);
+    T* cb = colk + (k & 1) * 32;  // double-buffered column broadcast
+    cb[lane] = conj_(lk);
     __syncwarp();
+    if (k + 1 < 32) {
+      // look-ahead: the next pivot's row first, so its broadcast overlaps
+      // the rest of this step's update
+      r[k + 1] = fnmac(lk, cb[k + 1], r[k + 1]);
+      dkk = shfl(sc_re(r[k + 1]), k + 1);
+    }
 #pragma unroll
-    for (int j = k + 1; j < 32; ++j) r[j] = fnmac(lk, colk[j], r[j]);
-    __syncwarp();
+    for (int j = k + 2; j < 32; ++j) r[j] = fnmac(lk, cb[j], r[j]);
   }
   if (fail) return fail;
 #pragma unroll

@@ -13,6 +13,8 @@ Extensions for BASELINE config 4: ``pftrf_batched`` / ``pftrs_batched`` /
 
 from __future__ import annotations
 
+import threading
+
 import torch
 
 from . import _capi
@@ -38,8 +40,21 @@ def _run(name: str, *args) -> None:
     _capi.check(_fn(name)(*args), name)
 
 
+_TLS = threading.local()
+
+
 def _info(device) -> torch.Tensor:
-    return torch.empty(1, dtype=torch.int32, device=device)
+    """A persistent per-thread, per-device info int: stable pointers let the
+    C ABI's CUDA-graph cache replay repeated calls on the same buffers."""
+    cache = getattr(_TLS, "info", None)
+    if cache is None:
+        cache = _TLS.info = {}
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    t = cache.get(idx)
+    if t is None:
+        t = cache[idx] = torch.zeros(1, dtype=torch.int32, device=torch.device("cuda", idx))
+    return t
 
 
 def pftrf(r: RfpTriangle) -> int:

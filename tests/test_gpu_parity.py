@@ -218,3 +218,32 @@ def test_batched_failure_info(P):
     arf = torch.from_numpy(np.stack(bufs)).cuda()
     info = rfp.pftrf_batched(arf, n, "U", "N")
     assert info.cpu().tolist() == want
+
+
+def test_graph_replay_matches_direct(P):
+    """Repeated calls on the same buffers are replayed from a cached CUDA
+    graph (2nd call captures, 3rd+ replay); results must equal the first,
+    directly launched, call bit for bit."""
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    from paper_0901_1696_b200 import _capi
+    lib = _capi.lib()
+    n = 700
+    a = O.spd_matrix(n, 77, "n")
+    src = conv.trttf(a, "U", "T")
+    work = conv.RfpTriangle(src.data.clone(), src.desc)
+    b0 = torch.from_numpy(np.asfortranarray(np.random.default_rng(5).standard_normal((n, 9)))).cuda()
+    outs = []
+    for rep in range(4):
+        work.data.copy_(src.data)
+        work.state = conv.FactorState.UNFACTORED
+        assert rfp.pftrf(work) == 0
+        x = b0.clone() if rep == 0 else x.copy_(b0)
+        rfp.pftrs(work, x)
+        outs.append((work.data.clone(), x.clone()))
+    c0 = lib.rfpk_launch_count()
+    work.data.copy_(src.data)
+    work.state = conv.FactorState.UNFACTORED
+    assert rfp.pftrf(work) == 0
+    assert lib.rfpk_launch_count() > c0  # replayed kernels are counted
+    for f, x in outs[1:]:
+        assert torch.equal(f, outs[0][0]) and torch.equal(x, outs[0][1])
