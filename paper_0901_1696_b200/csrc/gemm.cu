@@ -1,6 +1,8 @@
 // FP64 / complex128 DMMA GEMM for sm_100a (see gemm.cuh for the contract).
 #include "gemm.cuh"
 
+#include <cstdlib>
+
 namespace rfpk {
 
 // ------------------------------------------------------------ PTX helpers
@@ -60,12 +62,26 @@ __device__ __forceinline__ bool a_keep(int a_tri, int m, int k) {
 // elements at a fixed stride, so a stage costs one 64-bit add + one cp.async
 // per element.  The K tail and the triangular masks (a_tri / b_tri, used only
 // by the in-place triangular leaves) take a separate predicated path.
-template <typename T, int R, int BK, int NT, int P, bool KMAJOR>
+// Shared-memory layout of one operand stage.  MN-major operands are stored
+// [k][r] with pitch R + 4 (complex R + 2), K-major ones [r][k] with pitch
+// BK + 4, so both the cp.async stores (contiguous along the global fast
+// dimension) and the m16n8k4 fragment loads are bank-conflict free.
+template <typename T, int R, int BK, bool KM>
+struct SmemLayout {
+  static constexpr int P = KM ? BK + 4 : R + (is_cplx<T>::value ? 2 : 4);
+  static constexpr int SIZE = KM ? R * P : BK * P;  // elements per stage
+  static constexpr int RS = KM ? P : 1;             // stride between rows r
+  static constexpr int KS = KM ? 1 : P;             // stride between k
+};
+
+template <typename T, int R, int BK, int NT, bool KMAJOR>
 struct TileLoader {
+  using L = SmemLayout<T, R, BK, KMAJOR>;
   static constexpr int EPT = R * BK / NT;
   static_assert(R * BK % NT == 0, "tile must divide evenly");
   static constexpr int RE = KMAJOR ? NT / BK : 0;   // row delta per element
   static constexpr int KE = KMAJOR ? 0 : NT / R;    // k delta per element
+  static constexpr int SSTEP = RE * L::RS + KE * L::KS;
   const T* ptr;     // element 0 at the current k0
   i64 step;         // global delta between consecutive elements
   i64 kstep;        // global delta per stage
@@ -80,22 +96,21 @@ struct TileLoader {
     ptr = KMAJOR ? base + (i64)(tile0 + r0) * ld + k_0 : base + (tile0 + r0) + (i64)k_0 * ld;
     step = KMAJOR ? (i64)RE * ld : (i64)KE * ld;
     kstep = KMAJOR ? (i64)BK : (i64)BK * ld;
-    soff = k_0 * P + r0;
+    soff = r0 * L::RS + k_0 * L::KS;
     rowok = 0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e)
       if (tile0 + r0 + e * RE < rows) rowok |= 1u << e;
   }
-  static constexpr int sstep() { return KMAJOR ? RE : KE * P; }
 
   // fast path: full K range, no mask
   __device__ __forceinline__ void load(T* s) const {
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       if (rowok & (1u << e)) {
-        cp_async_t(s + soff + e * sstep(), ptr + e * step, true);
+        cp_async_t(s + soff + e * SSTEP, ptr + e * step, true);
       } else {
-        cp_async_t(s + soff + e * sstep(), ptr, false);
+        cp_async_t(s + soff + e * SSTEP, ptr, false);
       }
     }
   }
@@ -105,7 +120,7 @@ struct TileLoader {
     for (int e = 0; e < EPT; ++e) {
       const int r = tile0 + r0 + e * RE, k = k0 + k_0 + e * KE;
       const bool ok = (rowok & (1u << e)) && k < K && a_keep(tri, r, k);
-      cp_async_t(s + soff + e * sstep(), ok ? ptr + e * step : ptr, ok);
+      cp_async_t(s + soff + e * SSTEP, ok ? ptr + e * step : ptr, ok);
     }
   }
   __device__ __forceinline__ void advance() { ptr += kstep; }
@@ -123,17 +138,19 @@ struct TileLoader {
 // conjugation by sign flips.  Padded smem rows (P = BM + 4 real / + 2 complex)
 // make the fragment loads bank-conflict free.
 template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
+                                  (BM * BN <= 64 * 64) ? (is_cplx<T>::value ? 2 : (STAGES <= 3 ? 4 : 3)) : 1)
     gemm_kernel(GemmArgs<T> g) {
   constexpr bool CPLX = is_cplx<T>::value;
   constexpr int WARPS_M = BM / WM;
   constexpr int NT = WARPS_M * (BN / WN) * 32;
-  constexpr int PA = BM + (CPLX ? 2 : 4), PB = BN + (CPLX ? 2 : 4);
+  using LA = SmemLayout<T, BM, BK, AK>;
+  using LB = SmemLayout<T, BN, BK, BKM>;
   constexpr int MI = WM / 16, NI = WN / 8;
   constexpr int NACC = CPLX ? 2 : 1;
   extern __shared__ __align__(16) double smem_d[];
   T* As = reinterpret_cast<T*>(smem_d);
-  T* Bs = As + STAGES * BK * PA;
+  T* Bs = As + STAGES * LA::SIZE;
   if (g.skip && *g.skip) return;
   int tm, tn;
   if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
@@ -144,8 +161,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int gq = lane >> 2, tq = lane & 3;
 
-  TileLoader<T, BM, BK, NT, PA, AK> la;
-  TileLoader<T, BN, BK, NT, PB, BKM> lb;
+  TileLoader<T, BM, BK, NT, AK> la;
+  TileLoader<T, BN, BK, NT, BKM> lb;
   la.init(g.A, g.lda, m0, M, tid);
   lb.init(g.B, g.ldb, n0, N, tid);
   const bool masked = g.a_tri != A_FULL || g.b_tri != A_FULL;
@@ -162,10 +179,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
   const int KT = (K + BK - 1) / BK;
   auto load_stage = [&](int stage, int kt) {
-    T* as = As + stage * BK * PA;
-    T* bs = Bs + stage * BK * PB;
+    T* as = As + stage * LA::SIZE;
+    T* bs = Bs + stage * LB::SIZE;
     const int k0 = kt * BK;
-    if (!masked && k0 + BK <= K) {
+    if (!masked && k0 + BK <= K) {  // uniform
       la.load(as);
       lb.load(bs);
     } else {
@@ -188,19 +205,19 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     const int nk = kt + STAGES - 1;
     if (nk < KT) load_stage(nk % STAGES, nk);
     cp_async_commit();
-    const T* as = As + (kt % STAGES) * BK * PA + wm * WM + gq;
-    const T* bs = Bs + (kt % STAGES) * BK * PB + wn * WN + gq;
+    const T* as = As + (kt % STAGES) * LA::SIZE + (wm * WM + gq) * LA::RS + tq * LA::KS;
+    const T* bs = Bs + (kt % STAGES) * LB::SIZE + (wn * WN + gq) * LB::RS + tq * LB::KS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       if constexpr (!CPLX) {
         double af[MI][2], bf[NI];
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
-          af[i][0] = as[(kk + tq) * PA + i * 16];
-          af[i][1] = as[(kk + tq) * PA + i * 16 + 8];
+          af[i][0] = as[kk * LA::KS + (i * 16) * LA::RS];
+          af[i][1] = as[kk * LA::KS + (i * 16 + 8) * LA::RS];
         }
 #pragma unroll
-        for (int j = 0; j < NI; ++j) bf[j] = bs[(kk + tq) * PB + j * 8];
+        for (int j = 0; j < NI; ++j) bf[j] = bs[kk * LB::KS + (j * 8) * LB::RS];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -209,15 +226,15 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
         double ar[MI][2], ai[MI][2], nai[MI][2], br[NI], bi[NI];
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
-          const Z v0 = as[(kk + tq) * PA + i * 16];
-          const Z v1 = as[(kk + tq) * PA + i * 16 + 8];
+          const Z v0 = as[kk * LA::KS + (i * 16) * LA::RS];
+          const Z v1 = as[kk * LA::KS + (i * 16 + 8) * LA::RS];
           ar[i][0] = v0.x; ai[i][0] = sa * v0.y;
           ar[i][1] = v1.x; ai[i][1] = sa * v1.y;
           nai[i][0] = -ai[i][0]; nai[i][1] = -ai[i][1];
         }
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
-          const Z w = bs[(kk + tq) * PB + j * 8];
+          const Z w = bs[kk * LB::KS + (j * 8) * LB::RS];
           br[j] = w.x; bi[j] = sb * w.y;
         }
 #pragma unroll
@@ -330,8 +347,9 @@ template <typename T> OperandLayout classify(const View<T>& v) {
 template <typename T, int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int MODE>
 int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
   constexpr int NT = (BM / WM) * (BN / WN) * 32;
-  constexpr int PA = BM + (is_cplx<T>::value ? 2 : 4), PB = BN + (is_cplx<T>::value ? 2 : 4);
-  constexpr size_t smem = (size_t)ST * BK * (PA + PB) * sizeof(T);
+  constexpr size_t smem = (size_t)ST *
+                          (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
+                          sizeof(T);
   auto kern = gemm_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
   static bool configured = false;
   if (!configured) {
@@ -428,9 +446,14 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
       return launch_mode<T, 64, 64, 8, 32, 32, 3>(g, tri_mode, ak, bk, st);
     return launch_mode<T, 32, 32, 8, 16, 16, 3>(g, tri_mode, ak, bk, st);
   } else {
-    long long tiles = (long long)((g.M + 127) / 128) * ((g.N + 127) / 128);
-    if (tiles >= (num_sms() * 3) / 4)
-      return launch_mode<T, 128, 128, 16, 64, 32, 3>(g, tri_mode, ak, bk, st);
+    // 64 x 64 tiles, 4 warps of 32 x 32, 3 stages, 4 CTAs per SM: the
+    // measured best FP64 config (33 TFLOP/s at 8192^3 vs 31 for a 1-CTA/SM
+    // 128 x 128 tile: more resident CTAs hide the per-stage barrier).
+    static const int force = [] {
+      const char* v = std::getenv("RFPK_TILE");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (force == 128) return launch_mode<T, 128, 128, 16, 64, 32, 4>(g, tri_mode, ak, bk, st);
     return launch_mode<T, 64, 64, 16, 32, 32, 3>(g, tri_mode, ak, bk, st);
   }
 }
