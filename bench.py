@@ -13,10 +13,10 @@ with the LAPACK flop model n^3/3 + 2 n^2 nrhs.
 
 Under torchrun (N > 1) every rank factors its own replica (single matrices
 do not shard: "replicas only", weak scaling); config 4 (--workload c4) is
-sharded by matrix.  --impl reference times the CPU oracle (the NumPy
-restatement of the reference algorithm; the reference itself is pure Python
-and cannot be installed on the GPU box) on a bounded sample of the same
-workload on the host cores.
+sharded by matrix.  --impl reference times the reference's own CPU path
+(the unmodified `rfpk` package installed into baseline/_ref from
+/root/reference/pkg; falls back to the NumPy oracle port if absent) on a
+bounded sample of the same workload on the host cores.
 """
 
 from __future__ import annotations
@@ -133,31 +133,64 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-# ---------------------------------------------------------------- CPU (oracle)
-def cpu_sample(n=4096, nrhs=256, reps=2, seed=3):
-    """Oracle pftrf + pftrs on the host cores (bounded sample of config 3)."""
-    from oracle import rfp_oracle as O
+# ---------------------------------------------------------------- CPU baselines
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_module():
+    """The UNMODIFIED reference package installed by `pip install --target
+    baseline/_ref /root/reference/pkg` (git-ignored; travels with gpurun), or
+    None when absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "rfpk")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import rfpk.convert
+        import rfpk.rfp
+        return rfpk
+    except Exception:
+        return None
+
+
+def _threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+        return max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
+        return os.cpu_count()
+
+
+def cpu_sample(n=4096, nrhs=256, reps=2, seed=3):
+    """pftrf + pftrs on the host cores on a bounded sample of config 3: the
+    reference itself (baseline/_ref, kind "reference") when installed, else
+    the oracle port (kind "port")."""
+    from oracle import rfp_oracle as O
+    ref = _reference_module()
     a = O.spd_matrix(n, seed, "1/n")
-    buf0 = O.trttf(a, "L", "N")
     b0 = np.asfortranarray(np.random.default_rng(seed + 1).standard_normal((n, nrhs)))
     ts = []
     for _ in range(reps):
-        buf = buf0.copy()
         x = b0.copy(order="F")
-        t0 = time.perf_counter()
-        assert O.pftrf(buf, n, "L", "N") == 0
-        O.pftrs(buf, n, "L", "N", x)
+        if ref is not None:
+            r = ref.convert.trttf(a, "L", "N")
+            t0 = time.perf_counter()
+            assert ref.rfp.pftrf(r) == 0
+            ref.rfp.pftrs(r, x)
+        else:
+            buf = O.trttf(a, "L", "N")
+            t0 = time.perf_counter()
+            assert O.pftrf(buf, n, "L", "N") == 0
+            O.pftrs(buf, n, "L", "N", x)
         ts.append(time.perf_counter() - t0)
+    cores = _threads()
     flops = n ** 3 / 3 + 2 * n * n * nrhs
     t = float(np.median(ts))
-    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-            "sample": f"oracle pftrf+pftrs n={n} LN nrhs={nrhs} (median of {reps}, "
-                      f"{t:.2f} s each; OpenBLAS {cores} threads)"}
+    who = "reference rfpk (baseline/_ref)" if ref is not None else "oracle port"
+    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": cores,
+            "kind": "reference" if ref is not None else "port",
+            "sample": f"{who} pftrf+pftrs n={n} LN nrhs={nrhs} (median of {reps}, "
+                      f"{t:.2f} s each; numpy/OpenBLAS {cores} threads)"}
 
 
 def run_reference(args, rank, world):
@@ -179,8 +212,8 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded numpy)",
         "config": {"workload": f"config3 sample: n={args.ref_n} LN pftrf+pftrs nrhs={args.ref_nrhs} "
                                f"(bounded CPU sample of n={n}, nrhs={nrhs})"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"], "kind": "port",
-                         "sample": res["sample"]},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
