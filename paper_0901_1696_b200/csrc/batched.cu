@@ -11,6 +11,10 @@
 // map of SURVEY Appendix B (layout.py:127-163).
 #include "../../include/rfpk_b200.h"
 #include "rfp.cuh"
+#include "batched64.cuh"
+
+#include <cstdint>
+#include <cstdlib>
 
 namespace rfpk {
 
@@ -122,12 +126,158 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
                    factor != 0, solve != 0);
 }
 
+
+// ---------------------------------------------------------------- n == 64
+// One warp per matrix; see batched64.cuh for the algorithm.  Shared memory:
+// RFP buffer (2080) + W1, W2 (32 x 33 each) + RHS chunk / scratch (64 x 8).
+constexpr int B64_SMEM_DOUBLES = b64::NT + 2 * 32 * b64::WLD + 64 * 8;
+
+template <bool FACTOR, bool SOLVE>
+__global__ void __launch_bounds__(32) batched64_kernel(int lower, int trans, double* arf,
+                                                       i64 stride_arf, int nrhs, double* b,
+                                                       i64 ldb, i64 stride_b, int* info) {
+  using namespace b64;
+  extern __shared__ __align__(16) double sm[];
+  double* R = sm;
+  double* W1 = R + NT;
+  double* W2 = W1 + 32 * WLD;
+  double* X = W2 + 32 * WLD;   // RHS chunk, ld 64; scratch during the factorization
+  double* colk = X;            // 64 entries
+  double* rdiag = X + 64;      // 32 entries
+  const int lane = threadIdx.x;
+  const i64 k = blockIdx.x;
+  double* g = arf + k * stride_arf;
+  const bool al16 = ((reinterpret_cast<uintptr_t>(g) & 15) == 0);
+  if (al16) {
+    for (int c = lane; c < NT / 2; c += 32) {
+      unsigned s = (unsigned)__cvta_generic_to_shared(R + 2 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g + 2 * c));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  } else {
+    for (int c = lane; c < NT; c += 32) R[c] = g[c];
+  }
+  __syncwarp();
+  const int rs = trans ? 32 : 1, cs = trans ? 1 : 65;
+  SV T1, T2, S1;
+  if (lower) {
+    T1 = SV{R + 1 * rs, rs, cs};
+    T2 = SV{R, rs, cs};          // rect[0:32, 0:32] (d = 1 for even n)
+    S1 = SV{R + 33 * rs, rs, cs};
+  } else {
+    T1 = SV{R + 33 * rs, rs, cs};
+    T2 = SV{R + 32 * rs, rs, cs};
+    S1 = SV{R, rs, cs};
+  }
+  const SV V1 = T1, V2 = T2.t();
+  const SV w1{W1, 1, WLD}, w2{W2, 1, WLD};
+  if (FACTOR) {
+    int f = chol32(V1, colk);
+    if (f) {
+      if (lane == 0) info[k] = f;
+      return;
+    }
+    inv32(V1, W1, rdiag);
+    double acc[2][4][4];
+    zero_acc<32>(acc);
+    if (lower) mm32<32>(S1, w1.t(), acc);   // S1 <- S1 W1^T
+    else mm32<32>(w1, S1, acc);             // S1 <- W1 S1
+    __syncwarp();
+    store_acc<32>(S1, acc, 1.0, 0.0, 0);
+    __syncwarp();
+    zero_acc<32>(acc);
+    if (lower) mm32<32>(S1, S1.t(), acc);   // T2 -= S1 S1^T
+    else mm32<32>(S1.t(), S1, acc);         // T2 -= S1^T S1
+    store_acc<32>(T2, acc, -1.0, 1.0, 2);
+    __syncwarp();
+    f = chol32(V2, colk);
+    if (lane == 0) info[k] = f ? 32 + f : 0;
+    if (f) return;
+    if (SOLVE) inv32(V2, W2, rdiag);
+    if (al16) {
+      for (int c = lane; c < NT / 2; c += 32)
+        reinterpret_cast<double2*>(g)[c] = reinterpret_cast<const double2*>(R)[c];
+    } else {
+      for (int c = lane; c < NT; c += 32) g[c] = R[c];
+    }
+  } else {
+    inv32(V1, W1, rdiag);
+    inv32(V2, W2, rdiag);
+  }
+  if (!SOLVE) return;
+  double* bk = b + k * stride_b;
+  const SV x1{X, 1, 64}, x2{X + 32, 1, 64};
+  for (int c0 = 0; c0 < nrhs; c0 += 8) {
+    const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
+    __syncwarp();
+    for (int e = lane; e < 64 * 8; e += 32) {
+      const int i = e & 63, c = e >> 6;
+      X[e] = c < cw ? bk[i + (i64)(c0 + c) * ldb] : 0.0;
+    }
+    __syncwarp();
+    double a8[2][1][4];
+    zero_acc<8>(a8);
+    mm32<8>(w1, x1, a8);                      // b1 = W1 b1
+    __syncwarp();
+    store_acc<8>(x1, a8, 1.0, 0.0, 0);
+    __syncwarp();
+    zero_acc<8>(a8);
+    if (lower) mm32<8>(S1, x1, a8);           // b2 -= S1 b1
+    else mm32<8>(S1.t(), x1, a8);             // b2 -= S1^T b1
+    store_acc<8>(x2, a8, -1.0, 1.0, 0);
+    __syncwarp();
+    zero_acc<8>(a8);
+    mm32<8>(w2, x2, a8);                      // b2 = W2 b2
+    __syncwarp();
+    store_acc<8>(x2, a8, 1.0, 0.0, 0);
+    __syncwarp();
+    zero_acc<8>(a8);
+    mm32<8>(w2.t(), x2, a8);                  // b2 = W2^T b2
+    __syncwarp();
+    store_acc<8>(x2, a8, 1.0, 0.0, 0);
+    __syncwarp();
+    zero_acc<8>(a8);
+    if (lower) mm32<8>(S1.t(), x2, a8);       // b1 -= S1^T b2
+    else mm32<8>(S1, x2, a8);                 // b1 -= S1 b2
+    store_acc<8>(x1, a8, -1.0, 1.0, 0);
+    __syncwarp();
+    zero_acc<8>(a8);
+    mm32<8>(w1.t(), x1, a8);                  // b1 = W1^T b1
+    __syncwarp();
+    store_acc<8>(x1, a8, 1.0, 0.0, 0);
+    __syncwarp();
+    for (int e = lane; e < 64 * cw; e += 32) {
+      const int i = e & 63, c = e >> 6;
+      bk[i + (i64)(c0 + c) * ldb] = X[e];
+    }
+  }
+}
+
+int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, int nrhs,
+                     double* b, i64 ldb, i64 stride_b, int* info, bool factor, bool solve,
+                     cudaStream_t st) {
+  const size_t sm = B64_SMEM_DOUBLES * sizeof(double);
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<(unsigned)batch, 32, sm, st>>>(r.lower ? 1 : 0, r.trans ? 1 : 0, arf, stride_arf, nrhs,
+                                          b, ldb, stride_b, info);
+  };
+  if (factor && solve) launch(batched64_kernel<true, true>);
+  else if (factor) launch(batched64_kernel<true, false>);
+  else launch(batched64_kernel<false, true>);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
 int batched_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, int nrhs, double* b,
                    i64 ldb, i64 stride_b, int* info, bool factor, bool solve, cudaStream_t st) {
   if (batch == 0) return 0;
   cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int) * batch, st);
   if (e != cudaSuccess) return (int)e;
   if (r.n == 0) return 0;
+  if (r.n == 64 && !(std::getenv("RFPK_BATCHED_GENERIC")))
+    return batched64_launch(r, arf, stride_arf, batch, nrhs, b, ldb, stride_b, info, factor, solve,
+                            st);
   batched_kernel<128><<<(unsigned)batch, 128, 0, st>>>(r, arf, stride_arf, nrhs, b, ldb, stride_b,
                                                        info, factor, solve);
   RFPK_CHECK_LAUNCH();

@@ -1,0 +1,156 @@
+// Batched n = 64 RFP Cholesky factor + solve, ONE WARP PER MATRIX
+// (BASELINE config 4: 65,536 x n = 64, TRANSR='N', UPLO='U', nrhs = 8).
+//
+// The matrix never leaves the RFP layout: the 16,640-byte RFP buffer is
+// copied into shared memory with 16-byte cp.async, and the reference's SRPA
+// composition (rfp.py:55-136) runs on the T1 / T2 / S1 views *inside shared
+// memory* (ld 65 for TRANSR='N', 32 for 'T'):
+//
+//   chol(T1) -> W1 = L1^-1 -> S1 <- S1 W1^T (L) | W1 S1 (U)
+//   -> T2 -= S1 S1^T (L) | S1^T S1 (U)  (upper part)  -> chol(T2^T) -> W2
+//   solve:  b1 = W1 b1; b2 -= S1 b1 | S1^T b1; b2 = W2 b2;          (forward)
+//           b2 = W2^T b2; b1 -= S1^T b2 | S1 b2; b1 = W1^T b1       (back)
+//
+// with the 32x32 Cholesky and inverse on the warp's registers and every
+// product (S1 update, T2 update, all six solve steps) on FP64 DMMA
+// (mma.m16n8k4) fragments read from shared memory.  Only __syncwarp is
+// needed, so up to six matrices (warps) are resident per SM and their
+// loads/compute overlap.  The factor is written back in the RFP layout,
+// coalesced; HBM traffic is the algorithmic 2*nt*8 (+ 2*n*nrhs*8) bytes.
+#pragma once
+#include "common.cuh"
+
+namespace rfpk {
+namespace b64 {
+
+constexpr int N = 64, H = 32, NT = N * (N + 1) / 2;  // 2080
+constexpr int WLD = 33;                              // smem pitch of W1/W2
+
+__device__ __forceinline__ double shfl(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+__device__ __forceinline__ void mma(double* c, double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+// strided smem view: element (i, j) at p[i*rs + j*cs]
+struct SV {
+  double* p;
+  int rs, cs;
+  __device__ __forceinline__ double& operator()(int i, int j) const { return p[i * rs + j * cs]; }
+  __device__ __forceinline__ SV t() const { return SV{p, cs, rs}; }
+};
+
+// 32x32 lower Cholesky of view V by one warp (lane i holds row i).
+// Returns 0 or the 1-based failing pivot (warp-uniform).
+__device__ __noinline__ int chol32(SV V, double* colk) {
+  const int lane = threadIdx.x & 31;
+  double r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) r[j] = (j <= lane) ? V(lane, j) : 0.0;
+  int fail = 0;
+  double dkk = shfl(r[0], 0);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
+    const double rd = rsqrt(dkk);
+    const double lk = (lane == k) ? dkk * rd : rd * r[k];
+    r[k] = lk;
+    double* cb = colk + (k & 1) * 32;
+    cb[lane] = lk;
+    __syncwarp();
+    if (k + 1 < 32) {
+      r[k + 1] = fma(-lk, cb[k + 1], r[k + 1]);
+      dkk = shfl(r[k + 1], k + 1);
+    }
+#pragma unroll
+    for (int j = k + 2; j < 32; ++j) r[j] = fma(-lk, cb[j], r[j]);
+  }
+  if (fail) return fail;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j <= lane) V(lane, j) = r[j];
+  __syncwarp();
+  return 0;
+}
+
+// W (pitch WLD, zeros above the diagonal) = inverse of the lower 32x32 view L;
+// lane j computes column j.
+__device__ __noinline__ void inv32(SV L, double* W, double* rdiag) {
+  const int j = threadIdx.x & 31;
+  rdiag[j] = 1.0 / L(j, j);
+  __syncwarp();
+  double w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      if (k & 1) s1 = fma(-L(i, k), w[k], s1);
+      else s0 = fma(-L(i, k), w[k], s0);
+    }
+    w[i] = (s0 + s1) * rdiag[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) W[i + j * WLD] = (i >= j) ? w[i] : 0.0;
+  __syncwarp();
+}
+
+// acc(32 x NC) += A(32x32) * B(32 x NC), A and B smem views; fragment layout of
+// m16n8k4 (g = lane/4, t = lane%4).  acc[mi][ni][4].
+template <int NC>
+__device__ __forceinline__ void mm32(SV A, SV B, double acc[2][NC / 8][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    double a[2][2], b[NC / 8];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      a[mi][0] = A(mi * 16 + g, k0 + t);
+      a[mi][1] = A(mi * 16 + g + 8, k0 + t);
+    }
+#pragma unroll
+    for (int ni = 0; ni < NC / 8; ++ni) b[ni] = B(k0 + t, ni * 8 + g);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NC / 8; ++ni) mma(acc[mi][ni], a[mi][0], a[mi][1], b[ni]);
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void zero_acc(double acc[2][NC / 8][4]) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NC / 8; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[mi][ni][r] = 0.0;
+}
+
+// C = alpha*acc + beta*C on a 32 x NC view (mask: 0 all, 2 upper incl diag)
+template <int NC>
+__device__ __forceinline__ void store_acc(SV C, double acc[2][NC / 8][4], double alpha,
+                                          double beta, int mask) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NC / 8; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = mi * 16 + g + ((r & 2) ? 8 : 0), j = ni * 8 + 2 * t + (r & 1);
+        if (mask == 2 && i > j) continue;
+        double v = alpha * acc[mi][ni][r];
+        if (beta != 0.0) v = fma(beta, C(i, j), v);
+        C(i, j) = v;
+      }
+}
+
+}  // namespace b64
+}  // namespace rfpk

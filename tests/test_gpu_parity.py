@@ -168,7 +168,9 @@ def test_recursive_sizes_vs_oracle(P, n, uplo, transr, cplx):
 def test_batched_vs_oracle(P):
     rfp = P.rfp
     for n, uplo, transr, nrhs in [(64, "U", "N", 8), (64, "L", "T", 3), (33, "L", "N", 1),
-                                  (1, "U", "T", 2), (17, "U", "C", 8), (64, "L", "N", 0)]:
+                                  (1, "U", "T", 2), (17, "U", "C", 8), (64, "L", "N", 0),
+                                  (64, "L", "N", 13), (64, "U", "T", 8), (64, "U", "C", 1),
+                                  (63, "U", "N", 8)]:
         batch = 37
         bufs, facs, xs, bs = [], [], [], []
         for k in range(batch):
@@ -201,7 +203,8 @@ def test_batched_vs_oracle(P):
             assert rel(b2, np.stack(xs)[:, :, :nrhs]) <= TOL
 
 
-def test_batched_failure_info(P):
+@pytest.mark.parametrize("uplo,transr", [("U", "N"), ("L", "N"), ("U", "T"), ("L", "T")])
+def test_batched_failure_info(P, uplo, transr):
     rfp = P.rfp
     n, batch = 64, 8
     bufs, want = [], []
@@ -212,11 +215,11 @@ def test_batched_failure_info(P):
             a[:, k + 5] = 0.0
             a[k + 5, :] = 0.0
             a[k + 5, k + 5] = -1.0
-        buf = O.trttf(a, "U", "N")
-        want.append(O.pftrf(buf.copy(), n, "U", "N"))
+        buf = O.trttf(a, uplo, transr)
+        want.append(O.pftrf(buf.copy(), n, uplo, transr))
         bufs.append(buf)
     arf = torch.from_numpy(np.stack(bufs)).cuda()
-    info = rfp.pftrf_batched(arf, n, "U", "N")
+    info = rfp.pftrf_batched(arf, n, uplo, transr)
     assert info.cpu().tolist() == want
 
 
