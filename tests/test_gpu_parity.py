@@ -250,3 +250,113 @@ def test_graph_replay_matches_direct(P):
     assert lib.rfpk_launch_count() > c0  # replayed kernels are counted
     for f, x in outs[1:]:
         assert torch.equal(f, outs[0][0]) and torch.equal(x, outs[0][1])
+
+
+# ---------------------------------------------------------------- BASELINE configs
+
+
+def _backward_error(P, buf_factor, a, n, uplo, transr):
+    """||A - L L^H||_F / (n eps ||A||_F) with eps = 2^-53 (BASELINE.json)."""
+    t = P.convert.tfttr(P.convert.RfpTriangle(buf_factor, P.layout.make_descriptor(n, uplo, transr)))
+    f = t if uplo == "L" else t.mH
+    r = a - f @ f.mH
+    return float(torch.linalg.norm(r) / (n * 2.0 ** -53 * torch.linalg.norm(a)))
+
+
+def test_config1_n1000_vs_oracle(P):
+    """Config 1: n=1000 LN, A = B B^T + n I; pftrf, pftrs(100), pftri vs the oracle."""
+    conv, rfp = P.convert, P.rfp
+    n = 1000
+    a = O.spd_matrix(n, 2024, "n")
+    buf = O.trttf(a, "L", "N")
+    r = conv.trttf(a, "L", "N")
+    assert bits(r.data) == buf.tobytes()
+    f = buf.copy()
+    assert O.pftrf(f, n, "L", "N") == 0
+    assert rfp.pftrf(r) == 0
+    assert rel(r.data, f) <= TOL
+    assert _backward_error(P, r.data, torch.from_numpy(a).cuda(), n, "L", "N") <= 10
+    b = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 100)))
+    xo = b.copy(order="F")
+    O.pftrs(f, n, "L", "N", xo)
+    x = torch.from_numpy(b).cuda()
+    rfp.pftrs(r, x)
+    assert rel(x, xo) <= TOL
+    O.pftri(f, n, "L", "N")
+    assert rfp.pftri(r) == 0
+    assert rel(r.data, f) <= TOL
+
+
+@pytest.mark.parametrize("n", [4000, 4001])
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+def test_config2_layout_sweep(P, n, uplo, transr):
+    """Config 2: bit-exact trttf/tfttr and pack/tpttf/tfttp round trips at
+    n = 4000/4001 in all 8 layouts (against the oracle's index maps), then
+    pftrf (backward error <= 10) and pftrs(64) (scaled residual)."""
+    conv, packed, rfp = P.convert, P.packed, P.rfp
+    g = torch.Generator(device="cuda").manual_seed(n)
+    bm = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    a = bm @ bm.t()
+    a.diagonal().add_(float(n))
+    a = a.t().contiguous().t()
+    r = conv.trttf(a, uplo, transr)
+    ah = a.cpu().numpy()
+    assert bits(r.data) == O.trttf(ah, uplo, transr).tobytes()
+    full = conv.tfttr(r)
+    want = torch.tril(a) if uplo == "L" else torch.triu(a)
+    assert torch.equal(full, want)
+    p = packed.pack(a, uplo)
+    assert bits(p.data) == O.pack(ah, uplo).tobytes()
+    r2 = conv.tpttf(p, transr)
+    assert torch.equal(r2.data, r.data)
+    assert torch.equal(conv.tfttp(r).data, p.data)
+    assert rfp.pftrf(r) == 0
+    assert _backward_error(P, r.data, a, n, uplo, transr) <= 10
+    b = torch.randn(64, n, dtype=torch.float64, device="cuda", generator=g).t()
+    x = b.clone()
+    rfp.pftrs(r, x)
+    res = float((a @ x - b).norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
+    assert res <= 10
+
+
+def test_config3_n16384_properties(P):
+    """Config 3 at full size: pftrf backward error <= 10 and pftrs(1024) residual."""
+    conv, rfp = P.convert, P.rfp
+    n, nrhs = 16384, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    bm = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    a = bm @ bm.t()
+    del bm
+    a /= n
+    a.diagonal().add_(1.0)
+    r = conv.trttf(a, "L", "N")
+    assert rfp.pftrf(r) == 0
+    assert _backward_error(P, r.data, a, n, "L", "N") <= 10
+    b = torch.randn(nrhs, n, dtype=torch.float64, device="cuda", generator=g).t()
+    x = b.clone()
+    rfp.pftrs(r, x)
+    res = float((a @ x - b).norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
+    assert res <= 10
+
+
+@pytest.mark.parametrize("n", [1500, 3001])
+def test_config5_complex_inverse_columns(P, n):
+    """Config 5 shape at reduced n: complex Hermitian, TRANSR='C', UPLO='L',
+    A = B B^H / n + I, pftrf -> pftri, ||A Y - I[:, J]|| on 256 columns."""
+    conv, rfp = P.convert, P.rfp
+    g = torch.Generator(device="cuda").manual_seed(n)
+    s = 0.5 ** 0.5
+    bm = torch.complex(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g) * s,
+                       torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g) * s)
+    a = bm @ bm.mH / n
+    a.diagonal().add_(1.0)
+    r = conv.trttf(a, "L", "C")
+    assert rfp.pftrf(r) == 0
+    assert rfp.pftri(r) == 0
+    full = conv.tfttr(r)
+    inv = torch.tril(full) + torch.tril(full, -1).mH
+    J = torch.randperm(n, generator=torch.Generator().manual_seed(1))[:256].cuda()
+    E = a @ inv[:, J]
+    E[J, torch.arange(256, device="cuda")] -= 1.0
+    assert float(E.abs().max()) <= 1e-12
