@@ -175,54 +175,94 @@ __device__ __forceinline__ i64 storage_addr(const Storage& s, i64 i, i64 j, bool
   return row * r.n1 + col;
 }
 
-// One 32x32 tile of the logical (i, j) space per CTA (256 threads).  Loads
-// are issued with an i-fast or j-fast thread mapping according to the
-// source's contiguity at each element, staged through shared memory, and
-// stored with the destination's contiguity -- so both sides are coalesced
-// even where RFP stores a block transposed.
+// Contiguity of a storage over a whole column range [j0, j0 + 64): 1 = i-fast,
+// 2 = j-fast, 3 = mixed (the tile straddles the RFP block boundary at column
+// n1 (L) / n2 (U), where the transposed block starts).
+__device__ __forceinline__ int tile_mode(const Storage& s, i64 j0) {
+  if (s.kind != ST_RFP) return 1;
+  const RfpDesc& r = s.r;
+  const i64 split = r.lower ? r.n1 : r.n2;
+  const bool lo_rowvar = r.lower;             // columns j < split are "row-varying" for L
+  const i64 j1 = j0 + 63;
+  auto mode_of = [&](bool left) {
+    const bool rowvar = left ? lo_rowvar : !lo_rowvar;
+    return (rowvar != r.trans) ? 1 : 2;
+  };
+  if (j1 < split) return mode_of(true);
+  if (j0 >= split) return mode_of(false);
+  return 3;
+}
+
+// One 64x64 tile of the logical (i, j) space per CTA (256 threads, 16
+// elements per thread per pass, all loads of a pass issued before the shared
+// stores).  Loads use an i-fast or j-fast thread mapping according to the
+// source's contiguity, stores according to the destination's, so both sides
+// are coalesced even where RFP stores a block transposed; tiles that lie in
+// one block run a single pass each way.
 template <typename T>
 __global__ void __launch_bounds__(256) convert_kernel(Storage src, const T* __restrict__ sp,
                                                       Storage dst, T* __restrict__ dp, i64 n,
                                                       i64 rows_total, int lower, int zero_fill) {
-  __shared__ T tile[32][33];
-  const i64 i0 = (i64)blockIdx.x * 32, j0 = (i64)blockIdx.y * 32;
-  if (!zero_fill && (lower ? (i0 + 31 < j0) : (i0 > j0 + 31))) return;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);  // tile[jj * 65 + ii]
+  constexpr int TL = 65;
+  const i64 i0 = (i64)blockIdx.x * 64, j0 = (i64)blockIdx.y * 64;
+  if (!zero_fill && (lower ? (i0 + 63 < j0) : (i0 > j0 + 63))) return;
+  const int tid = threadIdx.x;
+  const int smode = tile_mode(src, j0);
+  const int dmode = zero_fill ? 1 : tile_mode(dst, j0);
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool want_ifast = pass == 0;
+  for (int pass = 1; pass <= 2; ++pass) {
+    if (!(smode & pass)) continue;
+    T v[16];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int a = tx, b = ty + 8 * r;
-      const int ii = want_ifast ? a : b, jj = want_ifast ? b : a;
+    for (int r = 0; r < 16; ++r) {
+      const int a = tid & 63, b = (tid >> 6) + 4 * r;
+      const int ii = pass == 1 ? a : b, jj = pass == 1 ? b : a;
       const i64 i = i0 + ii, j = j0 + jj;
       const bool in = i < n && j < n && (lower ? i >= j : i <= j);
+      v[r] = sc_from<T>(0.0);
       if (in) {
         bool f;
-        i64 off = storage_addr(src, i, j, f);
-        if (f == want_ifast) tile[jj][ii] = sp[off];
-      } else if (want_ifast) {
-        tile[jj][ii] = sc_from<T>(0.0);
+        const i64 off = storage_addr(src, i, j, f);
+        if (smode != 3 || f == (pass == 1)) v[r] = sp[off];
       }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int a = tid & 63, b = (tid >> 6) + 4 * r;
+      const int ii = pass == 1 ? a : b, jj = pass == 1 ? b : a;
+      const i64 i = i0 + ii, j = j0 + jj;
+      const bool in = i < n && j < n && (lower ? i >= j : i <= j);
+      bool mine = true;
+      if (smode == 3 && in) {
+        bool f;
+        storage_addr(src, i, j, f);
+        mine = f == (pass == 1);
+      }
+      // out-of-triangle elements are written (as zero) by the i-fast pass only
+      if (in ? mine : pass == 1 || smode == 2) tile[jj * TL + ii] = v[r];
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool want_ifast = pass == 0;
+  for (int pass = 1; pass <= 2; ++pass) {
+    if (!(dmode & pass)) continue;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int a = tx, b = ty + 8 * r;
-      const int ii = want_ifast ? a : b, jj = want_ifast ? b : a;
+    for (int r = 0; r < 16; ++r) {
+      const int a = tid & 63, b = (tid >> 6) + 4 * r;
+      const int ii = pass == 1 ? a : b, jj = pass == 1 ? b : a;
       const i64 i = i0 + ii, j = j0 + jj;
-      const bool in = i < n && j < n && (lower ? i >= j : i <= j);
       if (zero_fill) {
         // full destination, i-fast: every element of the ld x n array
-        if (want_ifast && i < rows_total && j < n) dp[i + j * dst.ld] = tile[jj][ii];
-      } else if (in) {
+        if (i < rows_total && j < n) dp[i + j * dst.ld] = tile[jj * TL + ii];
+        continue;
+      }
+      const bool in = i < n && j < n && (lower ? i >= j : i <= j);
+      if (in) {
         bool f;
-        i64 off = storage_addr(dst, i, j, f);
-        if (f == want_ifast) dp[off] = tile[jj][ii];
+        const i64 off = storage_addr(dst, i, j, f);
+        if (dmode != 3 || f == (pass == 1)) dp[off] = tile[jj * TL + ii];
       }
     }
   }
@@ -235,9 +275,15 @@ int convert(const Storage& src, const T* s, const Storage& dst, T* dptr, bool ze
   if (n == 0 && !(zero_fill && dst.kind == ST_FULL)) return 0;
   const i64 rows = (zero_fill && dst.kind == ST_FULL) ? dst.ld : n;
   if (rows == 0 || n == 0) return 0;
-  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((n + 31) / 32));
-  convert_kernel<T><<<grid, 256, 0, st>>>(src, s, dst, dptr, n, rows, src.r.lower ? 1 : 0,
-                                          zero_fill ? 1 : 0);
+  dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((n + 63) / 64));
+  const size_t sm = 64 * 65 * sizeof(T);
+  auto k = convert_kernel<T>;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  k<<<grid, 256, sm, st>>>(src, s, dst, dptr, n, rows, src.r.lower ? 1 : 0, zero_fill ? 1 : 0);
   RFPK_CHECK_LAUNCH();
   return 0;
 }
