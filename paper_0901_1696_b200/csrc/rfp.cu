@@ -207,8 +207,18 @@ __global__ void __launch_bounds__(256) convert_kernel(Storage src, const T* __re
   T* tile = reinterpret_cast<T*>(smem_raw);  // tile[jj * 65 + ii]
   constexpr int TL = 65;
   const i64 i0 = (i64)blockIdx.x * 64, j0 = (i64)blockIdx.y * 64;
-  if (!zero_fill && (lower ? (i0 + 63 < j0) : (i0 > j0 + 63))) return;
+  const bool outside = lower ? (i0 + 63 < j0) : (i0 > j0 + 63);
   const int tid = threadIdx.x;
+  if (outside) {
+    if (!zero_fill) return;
+    // zero-only tile of the full destination: stream zeros, no smem round trip
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const i64 i = i0 + (tid & 63), j = j0 + (tid >> 6) + 4 * r;
+      if (i < rows_total && j < n) dp[i + j * dst.ld] = sc_from<T>(0.0);
+    }
+    return;
+  }
   const int smode = tile_mode(src, j0);
   const int dmode = zero_fill ? 1 : tile_mode(dst, j0);
 #pragma unroll
