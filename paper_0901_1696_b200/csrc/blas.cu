@@ -17,6 +17,8 @@
 #include "blas.cuh"
 #include "leaf.cuh"
 
+#include <cstdlib>
+
 namespace rfpk {
 
 // ============================================================ leaf kernels
@@ -365,10 +367,84 @@ int trmm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
   return trmm_rec(c, lower, conj, unit, alpha, Tm, B);
 }
 
+// ---------------------------------------------------------------- look-ahead
+// Library-owned streams for the recursive look-ahead: the critical path of a
+// factorization runs on a high-priority stream, and the bulk trailing update
+// of each level is forked to a low-priority side stream (one per nesting
+// depth) so it overlaps the latency-bound factorization of the next diagonal
+// block.  Fork/join are event record/wait, which also work under CUDA-graph
+// stream capture (the forked streams join the capture).
+struct LaStreams {
+  cudaStream_t hi = nullptr;
+  cudaStream_t side[24] = {};
+  cudaEvent_t ev[128] = {};
+  int next = 0;
+  bool ok = false;
+};
+
+static LaStreams& la_streams() {
+  static LaStreams s[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LaStreams& L = s[dev & 15];
+  if (!L.ok) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, greatest);
+    for (auto& x : L.side) cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, least);
+    for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    L.ok = true;
+  }
+  return L;
+}
+
+// make `to` wait for everything issued so far on `from`
+static int la_link(cudaStream_t from, cudaStream_t to) {
+  LaStreams& L = la_streams();
+  cudaEvent_t e = L.ev[L.next++ % 128];
+  cudaError_t r = cudaEventRecord(e, from);
+  if (r == cudaSuccess) r = cudaStreamWaitEvent(to, e, 0);
+  return r == cudaSuccess ? 0 : (int)r;
+}
+
+// levels whose trailing block is at least this large use the look-ahead
+constexpr i64 LA_MIN = 512;
+
+template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth);
+
+// A22 <- A22 - G G^H, then factor A22 (lower).  With look-ahead the update is
+// split: B11 (the first diagonal child of A22) is updated on the critical
+// stream and factored right away, while B21/B22 are updated on a side stream.
+template <typename T>
+int update_and_factor(Ctx c, View<T> A22, View<T> G, int base, T* W, int depth) {
+  const i64 n2 = A22.m, k = G.n;
+  int rc;
+  if (n2 < LA_MIN || depth >= 24) {
+    if ((rc = herk_core(c, TRI_LOWER, -1.0, G, false, 1.0, A22, true))) return rc;
+    return potrf_node(c, A22, base, W, depth);
+  }
+  const i64 m1 = split_point(n2), m2 = n2 - m1;
+  View<T> G1 = G.sub(0, 0, m1, k), G2 = G.sub(m1, 0, m2, k);
+  View<T> B11 = A22.sub(0, 0, m1, m1), B21 = A22.sub(m1, 0, m2, m1), B22 = A22.sub(m1, m1, m2, m2);
+  if ((rc = herk_core(c, TRI_LOWER, -1.0, G1, false, 1.0, B11, true))) return rc;
+  cudaStream_t side = la_streams().side[depth];
+  if ((rc = la_link(c.st, side))) return rc;
+  Ctx cs{side, c.info};
+  const bool cplx = is_cplx<T>::value;
+  if ((rc = gemm<T>(TRI_FULL, sc_from<T>(-1.0), G2, false, G1.t(), cplx, sc_from<T>(1.0), B21,
+                    false, c.info, side)))
+    return rc;
+  if ((rc = herk_core(cs, TRI_LOWER, -1.0, G2, false, 1.0, B22, true))) return rc;
+  if ((rc = potrf_node(c, B11, base, W, depth + 1))) return rc;
+  if ((rc = la_link(side, c.st))) return rc;
+  if ((rc = trsm_rec(c, true, cplx, B11, B21.t(), W, false))) return rc;
+  return update_and_factor(c, B22, B21, base + (int)m1, W + m1 * 64, depth);
+}
+
 // A = L L^H, lower triangle of the view; W receives the leaf inverses (slab
 // b <-> rows 64b..), reused by the trsm steps of this recursion and by the
 // caller (pftrf's S1 solve).
-template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
+template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth) {
   const i64 n = A.m;
   if (n == 0) return 0;
   if (n <= LEAF) {
@@ -382,12 +458,80 @@ template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
   const i64 n1 = split_point(n), n2 = n - n1;
   View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
   int rc;
-  if ((rc = potrf_lower(c, A11, base, W))) return rc;
+  if ((rc = potrf_node(c, A11, base, W, depth))) return rc;
   // A21 <- A21 L11^{-H}  <=>  conj(L11) A21^T = A21^T
   if ((rc = trsm_rec(c, true, is_cplx<T>::value, A11, A21.t(), W, false))) return rc;
-  // A22 <- A22 - A21 A21^H (lower triangle)
-  if ((rc = herk_core(c, TRI_LOWER, -1.0, A21, false, 1.0, A22, true))) return rc;
-  return potrf_lower(c, A22, base + (int)n1, W + n1 * 64);
+  // A22 <- A22 - A21 A21^H, then factor (with look-ahead)
+  return update_and_factor(c, A22, A21, base + (int)n1, W + n1 * 64, depth);
+}
+
+// run `body` on the high-priority library stream, ordered after / before the
+// caller's stream
+template <typename F> int on_hi_stream(Ctx c, F&& body) {
+  cudaStream_t hi = la_streams().hi;
+  int rc = la_link(c.st, hi);
+  if (rc) return rc;
+  rc = body(Ctx{hi, c.info});
+  int rc2 = la_link(hi, c.st);
+  return rc ? rc : rc2;
+}
+
+// Right-looking blocked Cholesky with look-ahead for large n (nb = 256).
+// Iteration k: factor the diagonal block and solve the panel below it on the
+// critical (high-priority) stream; update the NEXT panel's columns there too;
+// fork the rest of the rank-nb trailing update to a low-priority side stream,
+// where it overlaps the next iteration's panel factorization.  Every 64-leaf
+// is still factored by potf2_inv64 at a 64-aligned offset, so the W slabs are
+// exactly those the recursive trsm (pftrf's S1 solve) expects.
+constexpr i64 RL_NB = 256;
+constexpr i64 RL_MIN = 1024;
+
+template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
+  const i64 n = A.m;
+  const bool cplx = is_cplx<T>::value;
+  cudaStream_t side = la_streams().side[23];
+  Ctx cs{side, c.info};
+  int rc;
+  bool side_busy = false;
+  for (i64 o = 0; o < n; o += RL_NB) {
+    const i64 s = (n - o) < RL_NB ? (n - o) : RL_NB;
+    const i64 rest = n - o - s;
+    View<T> Akk = A.sub(o, o, s, s);
+    // panel factorization (its columns are fully updated already)
+    if ((rc = potrf_node(c, Akk, base + (int)o, W + o * 64, 0))) return rc;
+    if (rest == 0) break;
+    View<T> P = A.sub(o + s, o, rest, s);
+    if ((rc = trsm_rec(c, true, cplx, Akk, P.t(), W + o * 64, false))) return rc;
+    // the side stream's previous trailing update also wrote the next panel
+    if (side_busy && (rc = la_link(side, c.st))) return rc;
+    const i64 s2 = rest < RL_NB ? rest : RL_NB;
+    View<T> P1 = P.sub(0, 0, s2, s);
+    if ((rc = herk_core(c, TRI_LOWER, -1.0, P1, false, 1.0, A.sub(o + s, o + s, s2, s2), true)))
+      return rc;
+    if (rest > s2) {
+      const i64 r2 = rest - s2;
+      View<T> P2 = P.sub(s2, 0, r2, s);
+      if ((rc = gemm<T>(TRI_FULL, sc_from<T>(-1.0), P2, false, P1.t(), cplx, sc_from<T>(1.0),
+                        A.sub(o + s + s2, o + s, r2, s2), false, c.info, c.st)))
+        return rc;
+      // trailing update of the columns after the next panel, off the critical path
+      if ((rc = la_link(c.st, side))) return rc;
+      if ((rc = herk_core(cs, TRI_LOWER, -1.0, P2, false, 1.0, A.sub(o + s + s2, o + s + s2, r2, r2),
+                          true)))
+        return rc;
+      side_busy = true;
+    }
+  }
+  if (side_busy && (rc = la_link(side, c.st))) return rc;
+  return 0;
+}
+
+template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
+  if (A.m < LA_MIN) return potrf_node(c, A, base, W, 0);
+  return on_hi_stream(c, [&](Ctx h) {
+    if (A.m >= RL_MIN && !std::getenv("RFPK_NO_RL")) return potrf_rl(h, A, base, W);
+    return potrf_node(h, A, base, W, 0);
+  });
 }
 
 // A <- L^{-1} in place (lower): all 64-leaves are inverted in one launch,
