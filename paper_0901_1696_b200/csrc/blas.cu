@@ -281,92 +281,6 @@ template <typename T> int leaf_inverses(Ctx c, View<T> L, bool unit, T* W) {
   return 0;
 }
 
-// Solve conj?(T) X = B (T lower or upper in its view) with the leaf inverses
-// W: W slab b holds inv(leaf b) of T (wtrans == false) or of T^T (wtrans).
-// Leaves are in-place 64-row GEMMs X_b = W_b B_b; updates are GEMMs.
-template <typename T>
-int trsm_rec(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
-  const i64 n = Tm.m;
-  if (n == 0 || B.n == 0) return 0;
-  if (n <= LEAF) {
-    View<T> Wv{W, n, n, 1, 64};
-    if (wtrans) Wv = Wv.t();
-    return gemm<T>(TRI_FULL, one<T>(), Wv, conj, B, false, sc_from<T>(0.0), B, false, c.info,
-                   c.st, A_FULL, true);
-  }
-  const i64 n1 = split_point(n), n2 = n - n1;
-  View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
-  T* W2 = W + n1 * 64;
-  int rc;
-  if (lower) {
-    if ((rc = trsm_rec(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans))) return rc;
-    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(n1, 0, n2, n1), conj, B1, false, one<T>(), B2,
-                      false, c.info, c.st)))
-      return rc;
-    return trsm_rec(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans);
-  }
-  if ((rc = trsm_rec(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans))) return rc;
-  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(0, n1, n1, n2), conj, B2, false, one<T>(), B1,
-                    false, c.info, c.st)))
-    return rc;
-  return trsm_rec(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans);
-}
-
-// conj?(T) X = alpha B.  If W is null the leaf inverses are computed here.
-template <typename T>
-int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B, T* W) {
-  if (B.empty() || Tm.m == 0) return 0;
-  if (!is_one(alpha)) {
-    int rc = scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
-    if (rc || is_zero(alpha)) return rc;
-  }
-  T* own = nullptr;
-  int rc;
-  if (!W) {
-    if ((rc = ws_alloc(&own, Tm.m, c.st))) return rc;
-    if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
-    W = own;
-  }
-  rc = trsm_rec(c, lower, conj, Tm, B, W, !lower);
-  ws_free(own, c.st);
-  return rc;
-}
-
-// B <- alpha conj?(T) B; leaves are in-place 64-row GEMMs with a masked
-// (triangular) A operand; unit diagonal = strict mask + beta = alpha.
-template <typename T>
-int trmm_rec(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
-  const i64 n = Tm.m;
-  if (n == 0 || B.n == 0) return 0;
-  if (n <= LEAF) {
-    const int mask = lower ? (unit ? A_SLOWER : A_LOWER) : (unit ? A_SUPPER : A_UPPER);
-    return gemm<T>(TRI_FULL, alpha, Tm, conj, B, false, unit ? alpha : sc_from<T>(0.0), B, false,
-                   c.info, c.st, mask, true);
-  }
-  const i64 n1 = split_point(n), n2 = n - n1;
-  View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
-  int rc;
-  if (lower) {
-    if ((rc = trmm_rec(c, lower, conj, unit, alpha, Tm.sub(n1, n1, n2, n2), B2))) return rc;
-    if ((rc = gemm<T>(TRI_FULL, alpha, Tm.sub(n1, 0, n2, n1), conj, B1, false, one<T>(), B2,
-                      false, c.info, c.st)))
-      return rc;
-    return trmm_rec(c, lower, conj, unit, alpha, Tm.sub(0, 0, n1, n1), B1);
-  }
-  if ((rc = trmm_rec(c, lower, conj, unit, alpha, Tm.sub(0, 0, n1, n1), B1))) return rc;
-  if ((rc = gemm<T>(TRI_FULL, alpha, Tm.sub(0, n1, n1, n2), conj, B2, false, one<T>(), B1, false,
-                    c.info, c.st)))
-    return rc;
-  return trmm_rec(c, lower, conj, unit, alpha, Tm.sub(n1, n1, n2, n2), B2);
-}
-
-template <typename T>
-int trmm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
-  if (B.empty()) return 0;
-  if (is_zero(alpha)) return scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
-  return trmm_rec(c, lower, conj, unit, alpha, Tm, B);
-}
-
 // ---------------------------------------------------------------- look-ahead
 // Library-owned streams for the recursive look-ahead: the critical path of a
 // factorization runs on a high-priority stream, and the bulk trailing update
@@ -407,8 +321,195 @@ static int la_link(cudaStream_t from, cudaStream_t to) {
   return r == cudaSuccess ? 0 : (int)r;
 }
 
+// run `body` on the high-priority library stream, ordered after / before the
+// caller's stream
+template <typename F> int on_hi_stream(Ctx c, F&& body) {
+  cudaStream_t hi = la_streams().hi;
+  int rc = la_link(c.st, hi);
+  if (rc) return rc;
+  rc = body(Ctx{hi, c.info});
+  int rc2 = la_link(hi, c.st);
+  return rc ? rc : rc2;
+}
+
 // levels whose trailing block is at least this large use the look-ahead
 constexpr i64 LA_MIN = 512;
+
+// Solve conj?(T) X = B (T lower or upper in its view) with the leaf inverses
+// W: W slab b holds inv(leaf b) of T (wtrans == false) or of T^T (wtrans).
+// Leaves are in-place 64-row GEMMs X_b = W_b B_b; updates are GEMMs.
+template <typename T>
+int trsm_plain(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
+  const i64 n = Tm.m;
+  if (n == 0 || B.n == 0) return 0;
+  if (n <= LEAF) {
+    View<T> Wv{W, n, n, 1, 64};
+    if (wtrans) Wv = Wv.t();
+    return gemm<T>(TRI_FULL, one<T>(), Wv, conj, B, false, sc_from<T>(0.0), B, false, c.info,
+                   c.st, A_FULL, true);
+  }
+  const i64 n1 = split_point(n), n2 = n - n1;
+  View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
+  T* W2 = W + n1 * 64;
+  int rc;
+  if (lower) {
+    if ((rc = trsm_plain(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans))) return rc;
+    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(n1, 0, n2, n1), conj, B1, false, one<T>(), B2,
+                      false, c.info, c.st)))
+      return rc;
+    return trsm_plain(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans);
+  }
+  if ((rc = trsm_plain(c, lower, conj, Tm.sub(n1, n1, n2, n2), B2, W2, wtrans))) return rc;
+  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(0, n1, n1, n2), conj, B2, false, one<T>(), B1,
+                    false, c.info, c.st)))
+    return rc;
+  return trsm_plain(c, lower, conj, Tm.sub(0, 0, n1, n1), B1, W, wtrans);
+}
+
+
+// Look-ahead trsm (SURVEY 7 "hard part": small solves on the critical path).
+// After a block of rows is solved, the update of the remaining rows is split:
+// the rows of the next diagonal child are updated on the critical stream and
+// solved immediately, while the update of the other rows runs on a side
+// stream.  Same splits and leaf inverses as trsm_plain.
+template <typename T>
+int trsm_rest_lower(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool wtrans, int depth);
+template <typename T>
+int trsm_rest_upper(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool wtrans, int depth);
+
+template <typename T>
+int trsm_rec(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans,
+             int depth = 0) {
+  const i64 n = Tm.m;
+  if (n < LA_MIN || depth >= 8 || B.n == 0) return trsm_plain(c, lower, conj, Tm, B, W, wtrans);
+  const i64 n1 = split_point(n), n2 = n - n1;
+  int rc;
+  if (lower) {
+    if ((rc = trsm_rec(c, true, conj, Tm.sub(0, 0, n1, n1), B.sub(0, 0, n1, B.n), W, wtrans,
+                       depth)))
+      return rc;
+    return trsm_rest_lower(c, conj, Tm, B, n1, W, wtrans, depth);
+  }
+  if ((rc = trsm_rec(c, false, conj, Tm.sub(n1, n1, n2, n2), B.sub(n1, 0, n2, B.n), W + n1 * 64,
+                     wtrans, depth)))
+    return rc;
+  return trsm_rest_upper(c, conj, Tm, B, n1, W, wtrans, depth);
+}
+
+// rows [0, n1) of B solved; finish rows [n1, n): T22^{-1} (B2 - T21 X1)
+template <typename T>
+int trsm_rest_lower(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool wtrans, int depth) {
+  const i64 n = Tm.m, n2 = n - n1, N = B.n;
+  View<T> T21 = Tm.sub(n1, 0, n2, n1), T22 = Tm.sub(n1, n1, n2, n2);
+  View<T> X1 = B.sub(0, 0, n1, N), B2 = B.sub(n1, 0, n2, N);
+  T* W2 = W + n1 * 64;
+  int rc;
+  if (n2 < LA_MIN || depth >= 8) {
+    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T21, conj, X1, false, one<T>(), B2, false, c.info,
+                      c.st)))
+      return rc;
+    return trsm_plain(c, true, conj, T22, B2, W2, wtrans);
+  }
+  const i64 m1 = split_point(n2), m2 = n2 - m1;
+  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T21.sub(0, 0, m1, n1), conj, X1, false, one<T>(),
+                    B2.sub(0, 0, m1, N), false, c.info, c.st)))
+    return rc;
+  cudaStream_t side = la_streams().side[12 + depth];
+  if ((rc = la_link(c.st, side))) return rc;
+  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T21.sub(m1, 0, m2, n1), conj, X1, false, one<T>(),
+                    B2.sub(m1, 0, m2, N), false, c.info, side)))
+    return rc;
+  if ((rc = trsm_rec(c, true, conj, T22.sub(0, 0, m1, m1), B2.sub(0, 0, m1, N), W2, wtrans,
+                     depth + 1)))
+    return rc;
+  if ((rc = la_link(side, c.st))) return rc;
+  return trsm_rest_lower(c, conj, T22, B2, m1, W2, wtrans, depth);
+}
+
+// rows [n1, n) of B solved; finish rows [0, n1): T11^{-1} (B1 - T12 X2), T upper
+template <typename T>
+int trsm_rest_upper(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool wtrans, int depth) {
+  const i64 n = Tm.m, n2 = n - n1, N = B.n;
+  View<T> T12 = Tm.sub(0, n1, n1, n2), T11 = Tm.sub(0, 0, n1, n1);
+  View<T> X2 = B.sub(n1, 0, n2, N), B1 = B.sub(0, 0, n1, N);
+  int rc;
+  if (n1 < LA_MIN || depth >= 8) {
+    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T12, conj, X2, false, one<T>(), B1, false, c.info,
+                      c.st)))
+      return rc;
+    return trsm_plain(c, false, conj, T11, B1, W, wtrans);
+  }
+  const i64 m1 = split_point(n1), m2 = n1 - m1;  // T11's children [0,m1), [m1,n1)
+  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T12.sub(m1, 0, m2, n2), conj, X2, false, one<T>(),
+                    B1.sub(m1, 0, m2, N), false, c.info, c.st)))
+    return rc;
+  cudaStream_t side = la_streams().side[12 + depth];
+  if ((rc = la_link(c.st, side))) return rc;
+  if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), T12.sub(0, 0, m1, n2), conj, X2, false, one<T>(),
+                    B1.sub(0, 0, m1, N), false, c.info, side)))
+    return rc;
+  if ((rc = trsm_rec(c, false, conj, T11.sub(m1, m1, m2, m2), B1.sub(m1, 0, m2, N), W + m1 * 64,
+                     wtrans, depth + 1)))
+    return rc;
+  if ((rc = la_link(side, c.st))) return rc;
+  return trsm_rest_upper(c, conj, T11, B1, m1, W, wtrans, depth);
+}
+
+// conj?(T) X = alpha B.  If W is null the leaf inverses are computed here.
+template <typename T>
+int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B, T* W) {
+  if (B.empty() || Tm.m == 0) return 0;
+  if (!is_one(alpha)) {
+    int rc = scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
+    if (rc || is_zero(alpha)) return rc;
+  }
+  T* own = nullptr;
+  int rc;
+  if (!W) {
+    if ((rc = ws_alloc(&own, Tm.m, c.st))) return rc;
+    if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
+    W = own;
+  }
+  if (Tm.m >= LA_MIN) rc = on_hi_stream(c, [&](Ctx h) { return trsm_rec(h, lower, conj, Tm, B, W, !lower); });
+  else rc = trsm_rec(c, lower, conj, Tm, B, W, !lower);
+  ws_free(own, c.st);
+  return rc;
+}
+
+// B <- alpha conj?(T) B; leaves are in-place 64-row GEMMs with a masked
+// (triangular) A operand; unit diagonal = strict mask + beta = alpha.
+template <typename T>
+int trmm_rec(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
+  const i64 n = Tm.m;
+  if (n == 0 || B.n == 0) return 0;
+  if (n <= LEAF) {
+    const int mask = lower ? (unit ? A_SLOWER : A_LOWER) : (unit ? A_SUPPER : A_UPPER);
+    return gemm<T>(TRI_FULL, alpha, Tm, conj, B, false, unit ? alpha : sc_from<T>(0.0), B, false,
+                   c.info, c.st, mask, true);
+  }
+  const i64 n1 = split_point(n), n2 = n - n1;
+  View<T> B1 = B.sub(0, 0, n1, B.n), B2 = B.sub(n1, 0, n2, B.n);
+  int rc;
+  if (lower) {
+    if ((rc = trmm_rec(c, lower, conj, unit, alpha, Tm.sub(n1, n1, n2, n2), B2))) return rc;
+    if ((rc = gemm<T>(TRI_FULL, alpha, Tm.sub(n1, 0, n2, n1), conj, B1, false, one<T>(), B2,
+                      false, c.info, c.st)))
+      return rc;
+    return trmm_rec(c, lower, conj, unit, alpha, Tm.sub(0, 0, n1, n1), B1);
+  }
+  if ((rc = trmm_rec(c, lower, conj, unit, alpha, Tm.sub(0, 0, n1, n1), B1))) return rc;
+  if ((rc = gemm<T>(TRI_FULL, alpha, Tm.sub(0, n1, n1, n2), conj, B2, false, one<T>(), B1, false,
+                    c.info, c.st)))
+    return rc;
+  return trmm_rec(c, lower, conj, unit, alpha, Tm.sub(n1, n1, n2, n2), B2);
+}
+
+template <typename T>
+int trmm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
+  if (B.empty()) return 0;
+  if (is_zero(alpha)) return scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
+  return trmm_rec(c, lower, conj, unit, alpha, Tm, B);
+}
 
 template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth);
 
@@ -465,16 +566,6 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
   return update_and_factor(c, A22, A21, base + (int)n1, W + n1 * 64, depth);
 }
 
-// run `body` on the high-priority library stream, ordered after / before the
-// caller's stream
-template <typename F> int on_hi_stream(Ctx c, F&& body) {
-  cudaStream_t hi = la_streams().hi;
-  int rc = la_link(c.st, hi);
-  if (rc) return rc;
-  rc = body(Ctx{hi, c.info});
-  int rc2 = la_link(hi, c.st);
-  return rc ? rc : rc2;
-}
 
 // Right-looking blocked Cholesky with look-ahead for large n (nb = 256).
 // Iteration k: factor the diagonal block and solve the panel below it on the
