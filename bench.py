@@ -37,6 +37,16 @@ sys.path.insert(0, ROOT)
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 128 flop/clk x 1.965 GHz (B200_PROFILING / SURVEY 6)
 
 
+def ncu_traffic(key):
+    """DRAM bytes per launch of a kernel from a committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[key]["bytes"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -375,7 +385,9 @@ def run_b200(args, rank, world, local):
         "fraction_of_fp64_measured_dgemm": value / 1e3 / dgemm_tflops,
         "roofline": {"bound": "tensor", "kernel": "gemm_kernel TRI (SYRK T2 -= S1^T S1, 8192x8192, k=8192)",
                      "achieved": k_tflops, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
-                     "frac": k_tflops / NOMINAL_FP64_TFLOPS, "traffic": None,
+                     "frac": k_tflops / NOMINAL_FP64_TFLOPS,
+                     "traffic": ncu_traffic("syrk_T2_n16384_LN"),
+                     "algorithmic_bytes": 8 * (desc.n2 * desc.n1 + desc.n2 * (desc.n2 + 1)),
                      "peak_source": "nominal FP64 DMMA (MEASURED_PEAKS.json has no FP64 figure); "
                                     f"measured cuBLAS DGEMM here: {dgemm_tflops:.2f} TFLOP/s"},
         "residual_scaled": resid,
@@ -528,7 +540,8 @@ def run_c4(args, rank, world, local):
                    "l2": "no flush: every step factors its own fresh 1.6 GB copy"},
         "roofline": {"bound": "hbm", "kernel": "batched64_kernel (fused pftrf+pftrs)",
                      "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm_peak, "traffic": None,
+                     "frac": achieved_gbs / hbm_peak,
+                     "traffic": ncu_traffic("batched64_fused_65536") if count == 65536 else None,
                      "bytes_per_matrix": per_matrix_bytes},
         "max_residual_scaled": float(gr.max()), "failed_matrices": int((gi != 0).sum()),
         "gather_ms": gather_ms,
