@@ -132,8 +132,8 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 // RFP buffer (2080) + W1, W2 (32 x 33 each) + RHS chunk / scratch (64 x 8).
 constexpr int B64_SMEM_DOUBLES = b64::NT + 2 * 32 * b64::WLD + 64 * 8;
 
-template <bool FACTOR, bool SOLVE>
-__global__ void __launch_bounds__(32) batched64_kernel(int lower, int trans, double* arf,
+template <bool FACTOR, bool SOLVE, int TRANS>
+__global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
                                                        i64 stride_arf, int nrhs, double* b,
                                                        i64 ldb, i64 stride_b, int* info) {
   using namespace b64;
@@ -158,19 +158,16 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, int trans, dou
     for (int c = lane; c < NT; c += 32) R[c] = g[c];
   }
   __syncwarp();
-  const int rs = trans ? 32 : 1, cs = trans ? 1 : 65;
-  SV T1, T2, S1;
-  if (lower) {
-    T1 = SV{R + 1 * rs, rs, cs};
-    T2 = SV{R, rs, cs};          // rect[0:32, 0:32] (d = 1 for even n)
-    S1 = SV{R + 33 * rs, rs, cs};
-  } else {
-    T1 = SV{R + 33 * rs, rs, cs};
-    T2 = SV{R + 32 * rs, rs, cs};
-    S1 = SV{R, rs, cs};
-  }
-  const SV V1 = T1, V2 = T2.t();
-  const SV w1{W1, 1, WLD}, w2{W2, 1, WLD};
+  constexpr int rs = TRANS ? 32 : 1, cs = TRANS ? 1 : 65;
+  using V = SV<rs, cs>;
+  // T1 / T2 / S1 of the normal 65 x 32 rectangle (convert.py:142-153, d = 1)
+  const V T1{R + (lower ? 1 : 33) * rs};
+  const V T2{R + (lower ? 0 : 32) * rs};
+  const V S1{R + (lower ? 33 : 0) * rs};
+  const V V1 = T1;
+  const auto V2 = T2.t();
+  const SV<1, WLD> w1{W1}, w2{W2};
+  const SV<1, 64> x1{X}, x2{X + 32};
   if (FACTOR) {
     int f = chol32(V1, colk);
     if (f) {
@@ -206,7 +203,6 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, int trans, dou
   }
   if (!SOLVE) return;
   double* bk = b + k * stride_b;
-  const SV x1{X, 1, 64}, x2{X + 32, 1, 64};
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
     __syncwarp();
@@ -259,12 +255,18 @@ int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, i
   const size_t sm = B64_SMEM_DOUBLES * sizeof(double);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<(unsigned)batch, 32, sm, st>>>(r.lower ? 1 : 0, r.trans ? 1 : 0, arf, stride_arf, nrhs,
-                                          b, ldb, stride_b, info);
+    kern<<<(unsigned)batch, 32, sm, st>>>(r.lower ? 1 : 0, arf, stride_arf, nrhs, b, ldb,
+                                          stride_b, info);
   };
-  if (factor && solve) launch(batched64_kernel<true, true>);
-  else if (factor) launch(batched64_kernel<true, false>);
-  else launch(batched64_kernel<false, true>);
+  if (r.trans) {
+    if (factor && solve) launch(batched64_kernel<true, true, 1>);
+    else if (factor) launch(batched64_kernel<true, false, 1>);
+    else launch(batched64_kernel<false, true, 1>);
+  } else {
+    if (factor && solve) launch(batched64_kernel<true, true, 0>);
+    else if (factor) launch(batched64_kernel<true, false, 0>);
+    else launch(batched64_kernel<false, true, 0>);
+  }
   RFPK_CHECK_LAUNCH();
   return 0;
 }

@@ -38,17 +38,19 @@ __device__ __forceinline__ void mma(double* c, double a0, double a1, double b) {
       : "d"(a0), "d"(a1), "d"(b));
 }
 
-// strided smem view: element (i, j) at p[i*rs + j*cs]
-struct SV {
+// shared-memory view with compile-time strides: element (i, j) at p[i*RS + j*CS]
+template <int RS, int CS> struct SV {
   double* p;
-  int rs, cs;
-  __device__ __forceinline__ double& operator()(int i, int j) const { return p[i * rs + j * cs]; }
-  __device__ __forceinline__ SV t() const { return SV{p, cs, rs}; }
+  __device__ __forceinline__ double& operator()(int i, int j) const { return p[i * RS + j * CS]; }
+  __device__ __forceinline__ SV<CS, RS> t() const { return SV<CS, RS>{p}; }
 };
 
 // 32x32 lower Cholesky of view V by one warp (lane i holds row i).
 // Returns 0 or the 1-based failing pivot (warp-uniform).
-__device__ __noinline__ int chol32(SV V, double* colk) {
+template <int RS, int CS>
+__device__ __noinline__ int chol32(SV<RS, CS> V, double* colk) {
+  __builtin_assume(__isShared(V.p));
+  __builtin_assume(__isShared(colk));
   const int lane = threadIdx.x & 31;
   double r[32];
 #pragma unroll
@@ -61,15 +63,14 @@ __device__ __noinline__ int chol32(SV V, double* colk) {
     const double rd = rsqrt(dkk);
     const double lk = (lane == k) ? dkk * rd : rd * r[k];
     r[k] = lk;
+    double dnext = 0.0;
+    if (k + 1 < 32) dnext = shfl(fma(-lk, lk, r[k + 1]), k + 1);  // lane k+1's new pivot
     double* cb = colk + (k & 1) * 32;
     cb[lane] = lk;
     __syncwarp();
-    if (k + 1 < 32) {
-      r[k + 1] = fma(-lk, cb[k + 1], r[k + 1]);
-      dkk = shfl(r[k + 1], k + 1);
-    }
 #pragma unroll
-    for (int j = k + 2; j < 32; ++j) r[j] = fma(-lk, cb[j], r[j]);
+    for (int j = k + 1; j < 32; ++j) r[j] = fma(-lk, cb[j], r[j]);
+    dkk = dnext;
   }
   if (fail) return fail;
 #pragma unroll
@@ -81,20 +82,27 @@ __device__ __noinline__ int chol32(SV V, double* colk) {
 
 // W (pitch WLD, zeros above the diagonal) = inverse of the lower 32x32 view L;
 // lane j computes column j.
-__device__ __noinline__ void inv32(SV L, double* W, double* rdiag) {
+template <int RS, int CS>
+__device__ __noinline__ void inv32(SV<RS, CS> L, double* W, double* rdiag) {
+  __builtin_assume(__isShared(L.p));
+  __builtin_assume(__isShared(W));
+  __builtin_assume(__isShared(rdiag));
   const int j = threadIdx.x & 31;
   rdiag[j] = 1.0 / L(j, j);
   __syncwarp();
   double w[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0;
+    double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int k = 0; k < i; ++k) {
-      if (k & 1) s1 = fma(-L(i, k), w[k], s1);
-      else s0 = fma(-L(i, k), w[k], s0);
+      const double l = L(i, k);
+      if ((k & 3) == 0) s0 = fma(-l, w[k], s0);
+      else if ((k & 3) == 1) s1 = fma(-l, w[k], s1);
+      else if ((k & 3) == 2) s2 = fma(-l, w[k], s2);
+      else s3 = fma(-l, w[k], s3);
     }
-    w[i] = (s0 + s1) * rdiag[i];
+    w[i] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i) W[i + j * WLD] = (i >= j) ? w[i] : 0.0;
@@ -103,8 +111,8 @@ __device__ __noinline__ void inv32(SV L, double* W, double* rdiag) {
 
 // acc(32 x NC) += A(32x32) * B(32 x NC), A and B smem views; fragment layout of
 // m16n8k4 (g = lane/4, t = lane%4).  acc[mi][ni][4].
-template <int NC>
-__device__ __forceinline__ void mm32(SV A, SV B, double acc[2][NC / 8][4]) {
+template <int NC, class VA, class VB>
+__device__ __forceinline__ void mm32(VA A, VB B, double acc[2][NC / 8][4]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int k0 = 0; k0 < 32; k0 += 4) {
@@ -134,8 +142,8 @@ __device__ __forceinline__ void zero_acc(double acc[2][NC / 8][4]) {
 }
 
 // C = alpha*acc + beta*C on a 32 x NC view (mask: 0 all, 2 upper incl diag)
-template <int NC>
-__device__ __forceinline__ void store_acc(SV C, double acc[2][NC / 8][4], double alpha,
+template <int NC, class VC>
+__device__ __forceinline__ void store_acc(VC C, double acc[2][NC / 8][4], double alpha,
                                           double beta, int mask) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   T* Ws = S + 64 * LD64;
-  T* scratch = Ws + 64 * LD64;  // 64 entries: column broadcast (2 x 32) / reciprocals
+  T* scratch = Ws + 64 * LD64;  // 128 entries: column broadcast (2 x 64) / reciprocals
   __shared__ int fail;
   if (*info) return;
   const int n = (int)A.m;
@@ -200,7 +200,7 @@ __global__ void diag_scan_kernel(View<T> A, int* info, int base, int highest) {
 namespace {
 
 template <typename T> size_t leaf_smem(int tiles) {
-  return ((size_t)tiles * (LEAF + 1) * LEAF + 64) * sizeof(T);
+  return ((size_t)tiles * (LEAF + 1) * LEAF + 128) * sizeof(T);
 }
 
 template <typename K> void allow_smem(K kern, size_t bytes) {

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) leaf_phases(T* A, long long* tick) {
 }
 
 extern "C" int run_leaf_phases(int cplx, void* A, long long* tick) {
-  size_t sm = (2 * 64 * 65 + 64) * (cplx ? 16 : 8);
+  size_t sm = (2 * 64 * 65 + 128) * (cplx ? 16 : 8);
   if (cplx) {
     cudaFuncSetAttribute(leaf_phases<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     leaf_phases<Z><<<1, 128, sm>>>((Z*)A, tick);
