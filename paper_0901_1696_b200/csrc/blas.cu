@@ -567,15 +567,20 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
 }
 
 
-// Right-looking blocked Cholesky with look-ahead for large n (nb = 256).
+// Right-looking blocked Cholesky with look-ahead for large n (nb = 128 while
+// more than 4096 columns remain, then 64; measured best on B200 for 2048-8192).
 // Iteration k: factor the diagonal block and solve the panel below it on the
 // critical (high-priority) stream; update the NEXT panel's columns there too;
 // fork the rest of the rank-nb trailing update to a low-priority side stream,
 // where it overlaps the next iteration's panel factorization.  Every 64-leaf
 // is still factored by potf2_inv64 at a 64-aligned offset, so the W slabs are
 // exactly those the recursive trsm (pftrf's S1 solve) expects.
-constexpr i64 RL_NB = 256;
-constexpr i64 RL_MIN = 1024;
+static i64 env_int(const char* name, i64 dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+static const i64 RL_NB = env_int("RFPK_RL_NB", 0);  // 0: adaptive 128 / 64
+static const i64 RL_MIN = env_int("RFPK_RL_MIN", 1024);
 
 template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
   const i64 n = A.m;
@@ -584,8 +589,14 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
   Ctx cs{side, c.info};
   int rc;
   bool side_busy = false;
-  for (i64 o = 0; o < n; o += RL_NB) {
-    const i64 s = (n - o) < RL_NB ? (n - o) : RL_NB;
+  // panel width: wider while the trailing matrix is large (rank-nb updates stay
+  // GEMM-efficient), 64 (one leaf) near the end where the critical path rules
+  auto width = [&](i64 o) {
+    const i64 nb = RL_NB > 0 ? RL_NB : ((n - o) > 4096 ? 128 : 64);
+    return (n - o) < nb ? (n - o) : nb;
+  };
+  for (i64 o = 0, s = 0; o < n; o += s) {
+    s = width(o);
     const i64 rest = n - o - s;
     View<T> Akk = A.sub(o, o, s, s);
     // panel factorization (its columns are fully updated already)
@@ -595,7 +606,7 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
     if ((rc = trsm_rec(c, true, cplx, Akk, P.t(), W + o * 64, false))) return rc;
     // the side stream's previous trailing update also wrote the next panel
     if (side_busy && (rc = la_link(side, c.st))) return rc;
-    const i64 s2 = rest < RL_NB ? rest : RL_NB;
+    const i64 s2 = width(o + s);
     View<T> P1 = P.sub(0, 0, s2, s);
     if ((rc = herk_core(c, TRI_LOWER, -1.0, P1, false, 1.0, A.sub(o + s, o + s, s2, s2), true)))
       return rc;
