@@ -1,6 +1,9 @@
 // RFP drivers (rfp.py) and full/packed/RFP conversion kernels (convert.py).
 #include "rfp.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace rfpk {
 
 RfpDesc rfp_desc(i64 n, char uplo, char transr) {
@@ -35,6 +38,40 @@ void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2, View<T>& s1)
 template <typename T> static T one() { return sc_from<T>(1.0); }
 template <typename T> static T m_one() { return sc_from<T>(-1.0); }
 
+// RFPK_TRACE=1: per-phase GPU times of the SRPA steps (direct, non-captured
+// calls only), printed to stderr -- a poor man's timeline without nsys.
+struct PhaseTrace {
+  cudaStream_t st;
+  const char* name;
+  bool on = false;
+  cudaEvent_t ev[8];
+  const char* lab[8];
+  int k = 0;
+  PhaseTrace(cudaStream_t s, const char* nm) : st(s), name(nm) {
+    const char* v = std::getenv("RFPK_TRACE");
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    on = v && v[0] == '1' && cs == cudaStreamCaptureStatusNone;
+    if (on) mark("start");
+  }
+  void mark(const char* l) {
+    if (!on || k >= 8) return;
+    cudaEventCreate(&ev[k]);
+    cudaEventRecord(ev[k], st);
+    lab[k++] = l;
+  }
+  ~PhaseTrace() {
+    if (!on) return;
+    cudaEventSynchronize(ev[k - 1]);
+    for (int i = 1; i < k; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[rfpk trace] %s %-10s %9.3f ms\n", name, lab[i], ms);
+    }
+    for (int i = 0; i < k; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+
 #define TRY(x)              \
   do {                      \
     int rc_ = (x);          \
@@ -52,20 +89,29 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
   T* W = nullptr;
   TRY(ws_alloc(&W, d.n1, c.st));
   int rc = 0;
+  PhaseTrace tr(c.st, "pftrf");
   if (d.lower) {
     rc = blas_potrf(c, 'L', t1, 0, W);
+    tr.mark("potrf(T1)");
     if (!rc && d.n2) {
       if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
+      tr.mark("trsm(S1)");
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
+      tr.mark("syrk(T2)");
       if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n1, W);
+      tr.mark("potrf(T2)");
     }
   } else {
     if (d.n2) {
       rc = blas_potrf(c, 'L', t1, 0, W);
+      tr.mark("potrf(T1)");
       if (!rc) rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
+      tr.mark("trsm(S1)");
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
+      tr.mark("syrk(T2)");
     }
     if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n2, W);
+    tr.mark("potrf(T2)");
   }
   ws_free(W, c.st);
   return rc;
