@@ -613,6 +613,132 @@ def pftri(buf, n, uplo, transr):
 
 
 # ---------------------------------------------------------------------------
+# SURVEY 8(f) "next" rows: tfsm, sfrk_hfrk, lansf (rfp.py:139-417)
+
+
+def _tfsm_left(buf, ds, uplo, trans, diag, alpha, b):
+    """Left RFP triangular solve through T1/S1/T2 (rfp.py:139-178); singular
+    indices re-based to the global row (rfp.py:46-52)."""
+    n1, n2 = ds.n1, ds.n2
+    t1, t2, s1 = blocks(buf, ds)
+
+    def solve(base, *args):
+        try:
+            trsm(*args)
+        except OracleSingular as exc:
+            raise OracleSingular(base + exc.index) from None
+
+    if uplo == "L":
+        b1, b2 = b[:n1], b[n1:]
+        if trans == "N":
+            solve(0, "L", "L", "N", diag, alpha, t1, b1)
+            if n2:
+                gemm("N", "N", -1.0, s1, b1, alpha, b2)
+                solve(n1, "L", "U", "T", diag, 1.0, t2, b2)
+        elif trans == "T":
+            if n2:
+                solve(n1, "L", "U", "N", diag, alpha, t2, b2)
+                gemm("T", "N", -1.0, s1, b2, alpha, b1)
+                solve(0, "L", "L", "T", diag, 1.0, t1, b1)
+            else:
+                solve(0, "L", "L", "T", diag, alpha, t1, b1)
+        else:
+            if n2:
+                solve(n1, "L", "L", "C", diag, alpha, t2.T, b2)
+                gemm("C", "N", -1.0, s1, b2, alpha, b1)
+                solve(0, "L", "L", "C", diag, 1.0, t1, b1)
+            else:
+                solve(0, "L", "L", "C", diag, alpha, t1, b1)
+    else:
+        b1, b2 = b[:n2], b[n2:]
+        if trans == "N":
+            solve(n2, "L", "U", "N", diag, alpha, t2, b2)
+            if n2:
+                gemm("N", "N", -1.0, s1, b2, alpha, b1)
+                solve(0, "L", "L", "T", diag, 1.0, t1, b1)
+        elif trans == "T":
+            if n2:
+                solve(0, "L", "L", "N", diag, alpha, t1, b1)
+                gemm("T", "N", -1.0, s1, b1, alpha, b2)
+                solve(n2, "L", "U", "T", diag, 1.0, t2, b2)
+            else:
+                solve(n2, "L", "U", "T", diag, alpha, t2, b2)
+        else:
+            if n2:
+                solve(0, "L", "U", "C", diag, alpha, t1.T, b1)
+                gemm("C", "N", -1.0, s1, b1, alpha, b2)
+                solve(n2, "L", "U", "C", diag, 1.0, t2, b2)
+            else:
+                solve(n2, "L", "U", "C", diag, alpha, t2, b2)
+
+
+def tfsm(buf, nord, uplo, transr, side, trans, diag, alpha, b):
+    """op(A) X = alpha B (side L) / X op(A) = alpha B (side R) with an
+    RFP-stored triangle of order ``nord`` (rfp.py:181-224); in place on b."""
+    ds = desc(nord, uplo, transr)
+    m, n = b.shape
+    if m == 0 or n == 0:
+        return
+    if alpha == 0:
+        b[...] = 0
+        return
+    if not np.iscomplexobj(buf) and trans == "C":
+        trans = "T"
+    if side == "L":
+        _tfsm_left(buf, ds, uplo, trans, diag, alpha, b)
+    elif trans == "C":
+        np.conjugate(b, out=b)
+        _tfsm_left(buf, ds, uplo, "N", diag, np.conj(alpha), b.T)
+        np.conjugate(b, out=b)
+    else:
+        _tfsm_left(buf, ds, uplo, "T" if trans == "N" else "N", diag, alpha, b.T)
+
+
+def sfrk_hfrk(buf, n, uplo, transr, trans, k, alpha, a, beta, herm):
+    """C <- alpha G G^(T|H) + beta C on an RFP triangle (rfp.py:227-283)."""
+    ds = desc(n, uplo, transr)
+    if n == 0:
+        return
+    if alpha == 0 or k == 0:
+        if beta == 0:
+            buf[...] = 0
+        elif beta != 1:
+            buf *= beta
+        return
+    n1, n2 = ds.n1, ds.n2
+    t1, t2, s1 = blocks(buf, ds)
+    rows = trans == "N"
+    if ds.uplo == "L":
+        a1 = a[:n1, :] if rows else a[:, :n1]
+        a2 = a[n1:, :] if rows else a[:, n1:]
+        syrk_herk("L", trans, alpha, a1, beta, t1, herm)
+        if n2:
+            gemm("N", "C", alpha, a2, a1, beta, s1) if rows else gemm("C", "N", alpha, a2, a1, beta, s1)
+            syrk_herk("U", "C" if rows else "N", alpha, a2.T, beta, t2, herm)
+    else:
+        a1 = a[:n2, :] if rows else a[:, :n2]
+        a2 = a[n2:, :] if rows else a[:, n2:]
+        if n2:
+            syrk_herk("L", "C" if rows else "N", alpha, a1.T, beta, t1, herm)
+            gemm("N", "C", alpha, a1, a2, beta, s1) if rows else gemm("C", "N", alpha, a1, a2, beta, s1)
+        syrk_herk("U", trans, alpha, a2, beta, t2, herm)
+
+
+def lansf(norm, buf, n, uplo, transr):
+    """Norm of the implied full symmetric/Hermitian matrix (rfp.py:363-417):
+    'M' max |a|, '1'/'O'/'I' max column |.|-sum, 'F'/'E' Frobenius."""
+    norm = str(norm).upper()[:1]
+    if n == 0:
+        return 0.0
+    if norm == "M":
+        return float(np.abs(buf).max())
+    full = expand_hermitian(buf, n, uplo, transr)
+    if norm in ("1", "O", "I"):
+        return float(np.abs(full).sum(axis=0).max())
+    return float(np.sqrt((np.abs(full) ** 2).sum()))
+
+
+# ---------------------------------------------------------------------------
 # seeded inputs (BASELINE.json configs; RNG convention of packed.py:166)
 
 

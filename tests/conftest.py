@@ -26,8 +26,19 @@ def golden_cases(g):
     """(key, dtype, uplo, transr, n) for every golden SPD case."""
     out = []
     for k in g:
-        if k.endswith("_rfp") and not k.startswith(("fail_", "spec_")):
+        if k.endswith("_rfp") and not k.startswith(("fail_", "spec_", "lansf_", "tfsm_", "sfrk_")):
             base = k[:-4]
+            dt, ut, nn = base.split("_")
+            out.append((base, dt, ut[0], ut[1], int(nn[1:])))
+    return sorted(out)
+
+
+def next_row_cases(g):
+    """(key, dtype, uplo, transr, n) for the SURVEY 8(f) golden cases."""
+    out = []
+    for k in g:
+        if k.startswith("lansf_") and k.endswith("_rfp"):
+            base = k[len("lansf_"):-4]
             dt, ut, nn = base.split("_")
             out.append((base, dt, ut[0], ut[1], int(nn[1:])))
     return sorted(out)

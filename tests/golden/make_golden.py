@@ -69,6 +69,40 @@ def case(out, n, uplo, transr, cplx, nrhs=3, seed=None):
     out[key + "_pftri"] = inv.data.copy()
 
 
+def next_rows(out, n, uplo, transr, cplx):
+    """tfsm (all side/trans/diag), sfrk_hfrk, lansf."""
+    key = f"{'c128' if cplx else 'f64'}_{uplo}{transr}_n{n}"
+    a = spd(n, 4321 + n, cplx)
+    r = convert.trttf(a, uplo, transr)
+    f = r.copy()
+    assert rfp.pftrf(f) == 0
+    rng = np.random.default_rng(77 + n)
+    for side in "LR":
+        for trans in "NTC":
+            for diag in "NU":
+                shape = (n, 3) if side == "L" else (3, n)
+                b = rng.standard_normal(shape) + (1j * rng.standard_normal(shape) if cplx else 0)
+                b = np.asfortranarray(b)
+                x = b.copy(order="F")
+                alpha = (1.5 - 0.5j) if cplx else 1.5
+                rfp.tfsm(transr, side, uplo, trans, diag, x.shape[0], x.shape[1], alpha, f, x)
+                out[f"tfsm_{key}_{side}{trans}{diag}_B"] = b
+                out[f"tfsm_{key}_{side}{trans}{diag}_X"] = x
+    out[f"tfsm_{key}_factor"] = f.data.copy()
+    for trans in "NC":
+        kk = 5
+        g = rng.standard_normal((n, kk) if trans == "N" else (kk, n))
+        if cplx:
+            g = g + 1j * rng.standard_normal(g.shape)
+        c = r.copy()
+        rfp.sfrk_hfrk(transr, uplo, trans, n, kk, -0.75, g, 1.25, c)
+        out[f"sfrk_{key}_{trans}_A"] = g
+        out[f"sfrk_{key}_{trans}_C0"] = r.data.copy()
+        out[f"sfrk_{key}_{trans}_C"] = c.data.copy()
+    out[f"lansf_{key}"] = np.array([rfp.lansf(nm, r) for nm in "M1IF"])
+    out[f"lansf_{key}_rfp"] = r.data.copy()
+
+
 def failing(out, n, uplo, transr, cplx, k, nan=False):
     """A = I + small symmetric noise with pivot k (0-based) made negative."""
     a = np.eye(n, dtype=np.complex128 if cplx else np.float64)
@@ -95,6 +129,11 @@ def main():
                                   (130, "U", "N", False), (129, "L", "T", False),
                                   (130, "L", "T", True), (129, "U", "N", True)]:
         case(out, n, uplo, transr, cplx, nrhs=5)
+    for cplx in (False, True):
+        for uplo in "LU":
+            for transr in "NT":
+                for n in (1, 6, 7, 40, 41):
+                    next_rows(out, n, uplo, transr, cplx)
     for cplx in (False, True):
         for uplo in "LU":
             for transr in "NT":

@@ -152,3 +152,30 @@ def test_scipy_lapack_second_oracle(n, uplo, transr):
     O.pftri(inv, n, uplo, transr)
     li, info = lapack.dpftri(n, lf, transr=transr, uplo=uplo)
     assert rel(inv, li) <= 1e-12
+
+
+# ---------------------------------------------------------------- SURVEY 8(f) rows
+from tests.conftest import next_row_cases  # noqa: E402
+
+with np.load(__import__("tests.conftest", fromlist=["GOLDEN"]).GOLDEN) as _z:
+    NEXT = next_row_cases({k: None for k in _z.files})
+
+
+@pytest.mark.parametrize("key,dt,uplo,transr,n", NEXT, ids=[c[0] for c in NEXT])
+def test_next_rows_match_reference(golden, key, dt, uplo, transr, n):
+    f = golden[f"tfsm_{key}_factor"]
+    cplx = dt == "c128"
+    for side in "LR":
+        for trans in "NTC":
+            for diag in "NU":
+                b = golden[f"tfsm_{key}_{side}{trans}{diag}_B"].copy(order="F")
+                alpha = (1.5 - 0.5j) if cplx else 1.5
+                O.tfsm(f, n, uplo, transr, side, trans, diag, alpha, b)
+                assert rel(b, golden[f"tfsm_{key}_{side}{trans}{diag}_X"]) <= 1e-12, (side, trans, diag)
+    for trans in "NC":
+        c = golden[f"sfrk_{key}_{trans}_C0"].copy()
+        O.sfrk_hfrk(c, n, uplo, transr, trans, 5, -0.75, golden[f"sfrk_{key}_{trans}_A"], 1.25, cplx)
+        assert rel(c, golden[f"sfrk_{key}_{trans}_C"]) <= 1e-13
+    want = golden[f"lansf_{key}"]
+    got = [O.lansf(nm, golden[f"lansf_{key}_rfp"], n, uplo, transr) for nm in "M1IF"]
+    assert np.allclose(got, want, rtol=1e-13, atol=0)
