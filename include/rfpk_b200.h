@@ -111,6 +111,33 @@ int rfpk_ztftri(char transr, char uplo, char diag, int64_t n, void* arf, int* in
 int rfpk_dpftri(char transr, char uplo, int64_t n, double* arf, int* info, rfpk_stream_t stream);
 int rfpk_zpftri(char transr, char uplo, int64_t n, void* arf, int* info, rfpk_stream_t stream);
 
+/* SURVEY 8(f) rows ------------------------------------------------------- */
+/* replaces rfp.tfsm(transr, side, uplo, trans, diag, m, n, alpha, a, b)
+   rfp.py:181-224; a holds the order-m (side L) / order-n (side R) triangle;
+   b is m x n with element (i, j) at b[i*rsb + j*csb]; info (device) receives
+   the 1-based global index of a zero diagonal (SingularMatrixError) */
+int rfpk_dtfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n,
+               double alpha, const double* arf, double* b, int64_t rsb, int64_t csb, int* info,
+               rfpk_stream_t stream);
+int rfpk_ztfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n,
+               double alpha_re, double alpha_im, const void* arf, void* b, int64_t rsb,
+               int64_t csb, int* info, rfpk_stream_t stream);
+/* replaces rfp.sfrk_hfrk(transr, uplo, trans, n, k, alpha, a, beta, c)
+   rfp.py:227-283: C <- alpha G G^(T|H) + beta C; a is n x k (trans 'N') or
+   k x n, element (i, j) at a[i*rsa + j*csa] */
+int rfpk_dsfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha,
+               const double* a, int64_t rsa, int64_t csa, double beta, double* arf,
+               rfpk_stream_t stream);
+int rfpk_zhfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha,
+               const void* a, int64_t rsa, int64_t csa, double beta, void* arf, int hermitian,
+               rfpk_stream_t stream);
+/* replaces rfp.lansf(norm, r)   rfp.py:363-417: 'M', '1'/'O', 'I', 'F'/'E' norm
+   of the implied full matrix, written to the device double *result */
+int rfpk_dlansf(char norm, char transr, char uplo, int64_t n, const double* arf, double* result,
+                rfpk_stream_t stream);
+int rfpk_zlansf(char norm, char transr, char uplo, int64_t n, const void* arf, double* result,
+                rfpk_stream_t stream);
+
 /* batched small-n (BASELINE config 4; no reference counterpart beyond a loop
    over rfp.pftrf / rfp.pftrs per matrix) --------------------------------- */
 /* batch independent RFP buffers at arf + k*stride_arf; info[k] per matrix */

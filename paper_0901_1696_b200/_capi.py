@@ -50,6 +50,12 @@ SIGNATURES = {
     "rfpk_ztftri": ([_c, _c, _c, _i64, _p, _p, _p], _int),
     "rfpk_dpftri": ([_c, _c, _i64, _p, _p, _p], _int),
     "rfpk_zpftri": ([_c, _c, _i64, _p, _p, _p], _int),
+    "rfpk_dtfsm": ([_c, _c, _c, _c, _c, _i64, _i64, _d, _p, _p, _i64, _i64, _p, _p], _int),
+    "rfpk_ztfsm": ([_c, _c, _c, _c, _c, _i64, _i64, _d, _d, _p, _p, _i64, _i64, _p, _p], _int),
+    "rfpk_dsfrk": ([_c, _c, _c, _i64, _i64, _d, _p, _i64, _i64, _d, _p, _p], _int),
+    "rfpk_zhfrk": ([_c, _c, _c, _i64, _i64, _d, _p, _i64, _i64, _d, _p, _int, _p], _int),
+    "rfpk_dlansf": ([_c, _c, _c, _i64, _p, _p, _p], _int),
+    "rfpk_zlansf": ([_c, _c, _c, _i64, _p, _p, _p], _int),
     "rfpk_dpftrf_batched": ([_c, _c, _i64, _p, _i64, _i64, _p, _p], _int),
     "rfpk_dpftrs_batched": ([_c, _c, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _p], _int),
     "rfpk_dpftrf_pftrs_batched": ([_c, _c, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _p],

@@ -714,7 +714,7 @@ int blas_gemm(Ctx c, char transa, char transb, T alpha, View<T> A, View<T> B, T 
 
 template <typename T>
 int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B,
-              bool scan, T* W) {
+              bool scan, T* W, int base) {
   if (B.empty() || A.m == 0) return 0;
   View<T> v, b = B;
   bool lower, conj;
@@ -728,7 +728,7 @@ int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<
   }
   if (diag == 'N' && scan) {
     // the reference raises at the first zero pivot in its solve order
-    int rc = diag_scan(c, v, 0, !lower);
+    int rc = diag_scan(c, v, base, !lower);
     if (rc) return rc;
   }
   return trsm_left(c, lower, conj, diag == 'U', alpha, v, b, W);
@@ -791,7 +791,7 @@ template <typename T> int blas_lauum(Ctx c, char uplo, View<T> A) {
 
 #define RFPK_INST(T)                                                                           \
   template int blas_gemm<T>(Ctx, char, char, T, View<T>, View<T>, T, View<T>);                 \
-  template int blas_trsm<T>(Ctx, char, char, char, char, T, View<T>, View<T>, bool, T*);       \
+  template int blas_trsm<T>(Ctx, char, char, char, char, T, View<T>, View<T>, bool, T*, int);       \
   template int blas_trmm<T>(Ctx, char, char, char, char, T, View<T>, View<T>);                 \
   template int blas_syrk<T>(Ctx, char, char, double, View<T>, double, View<T>, bool);          \
   template int blas_potrf<T>(Ctx, char, View<T>, int, T*);                                     \

@@ -25,7 +25,7 @@ int blas_gemm(Ctx c, char transa, char transb, T alpha, View<T> A, View<T> B, T 
 //       zero diagonal -> *info = 1-based index, B untouched
 template <typename T>
 int blas_trsm(Ctx c, char side, char uplo, char trans, char diag, T alpha, View<T> A, View<T> B,
-              bool scan = true, T* W = nullptr);
+              bool scan = true, T* W = nullptr, int base = 0);
 // (W: optional leaf inverses of the effective triangle, as produced by
 //  blas_potrf on the same view -- pftrf reuses T1's.)
 // trmm: B <- alpha op(A) B / alpha B op(A)                     (kernels.py:307)

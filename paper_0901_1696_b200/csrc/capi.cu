@@ -222,6 +222,82 @@ int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_st
 int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftri_t<double>(t, u, n, arf, info, S(s)); }
 int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftri_t<Z>(t, u, n, arf, info, S(s)); }
 
+// ---------------------------------------------------------------- SURVEY 8(f) rows
+static int tfsm_check(char& transr, char& side, char& uplo, char& trans, char& diag, int64_t m,
+                      int64_t n, int64_t rsb, int64_t csb, int* info) {
+  transr = up(transr); side = up(side); uplo = up(uplo); trans = up(trans); diag = up(diag);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(side, "LR")) return -2;
+  if (!one_of(uplo, "LU")) return -3;
+  if (!one_of(trans, "NTC")) return -4;
+  if (!one_of(diag, "NU")) return -5;
+  if (m < 0) return -6;
+  if (n < 0) return -7;
+  if (!unit_stride(m, n, rsb, csb)) return -10;
+  if (!info) return -13;
+  return 0;
+}
+int rfpk_dtfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n, double alpha,
+               const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) {
+  if (int rc = tfsm_check(transr, side, uplo, trans, diag, m, n, rsb, csb, info)) return rc;
+  if (int rc = reset_info(info, S(s))) return rc;
+  const int64_t order = side == 'L' ? m : n;
+  return tfsm<double>(Ctx{S(s), info}, rfp_desc(order, uplo, transr), side, trans, diag, alpha, arf,
+                      V<double>(b, m, n, rsb, csb));
+}
+int rfpk_ztfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n, double are,
+               double aim, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) {
+  if (int rc = tfsm_check(transr, side, uplo, trans, diag, m, n, rsb, csb, info)) return rc;
+  if (int rc = reset_info(info, S(s))) return rc;
+  const int64_t order = side == 'L' ? m : n;
+  return tfsm<Z>(Ctx{S(s), info}, rfp_desc(order, uplo, transr), side, trans, diag, zc(are, aim),
+                 (const Z*)arf, V<Z>(b, m, n, rsb, csb));
+}
+static int sfrk_check(char& transr, char& uplo, char& trans, int64_t n, int64_t k, int64_t rsa, int64_t csa) {
+  transr = up(transr); uplo = up(uplo); trans = up(trans);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (!one_of(trans, "NTC")) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  const int64_t r = trans == 'N' ? n : k, c = trans == 'N' ? k : n;
+  if (!unit_stride(r, c, rsa, csa)) return -8;
+  return 0;
+}
+int rfpk_dsfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
+               int64_t rsa, int64_t csa, double beta, double* arf, rfpk_stream_t s) {
+  if (int rc = sfrk_check(transr, uplo, trans, n, k, rsa, csa)) return rc;
+  const int64_t r = trans == 'N' ? n : k, c = trans == 'N' ? k : n;
+  return sfrk<double>(Ctx{S(s), nullptr}, rfp_desc(n, uplo, transr), trans, k, alpha,
+                      V<double>(a, r, c, rsa, csa), beta, arf, false);
+}
+int rfpk_zhfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha, const void* a,
+               int64_t rsa, int64_t csa, double beta, void* arf, int hermitian, rfpk_stream_t s) {
+  if (int rc = sfrk_check(transr, uplo, trans, n, k, rsa, csa)) return rc;
+  const int64_t r = trans == 'N' ? n : k, c = trans == 'N' ? k : n;
+  return sfrk<Z>(Ctx{S(s), nullptr}, rfp_desc(n, uplo, transr), trans, k, alpha,
+                 V<Z>(a, r, c, rsa, csa), beta, (Z*)arf, hermitian != 0);
+}
+static int lansf_check(char& norm, char& transr, char& uplo, int64_t n, const double* out) {
+  norm = up(norm); transr = up(transr); uplo = up(uplo);
+  if (norm == 'O') norm = '1';
+  if (norm == 'E') norm = 'F';
+  if (!one_of(norm, "M1IF")) return -1;
+  if (!one_of(transr, "NTC")) return -2;
+  if (!one_of(uplo, "LU")) return -3;
+  if (n < 0) return -4;
+  if (!out) return -6;
+  return 0;
+}
+int rfpk_dlansf(char norm, char transr, char uplo, int64_t n, const double* arf, double* out, rfpk_stream_t s) {
+  if (int rc = lansf_check(norm, transr, uplo, n, out)) return rc;
+  return lansf<double>(S(s), rfp_desc(n, uplo, transr), norm, arf, out);
+}
+int rfpk_zlansf(char norm, char transr, char uplo, int64_t n, const void* arf, double* out, rfpk_stream_t s) {
+  if (int rc = lansf_check(norm, transr, uplo, n, out)) return rc;
+  return lansf<Z>(S(s), rfp_desc(n, uplo, transr), norm, (const Z*)arf, out);
+}
+
 // ---------------------------------------------------------------- dense kernels
 int rfpk_dgemm(char ta, char tb, double alpha, const double* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
                const double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, double beta,

@@ -321,6 +321,27 @@ int scale_view(View<T> C, T beta, int tri_mode, bool herm_diag, const int* skip,
   return 0;
 }
 
+// elementwise conjugation of a complex view (no-op launch for real)
+template <typename T> __global__ void conj_kernel(View<T> C, const int* skip) {
+  if (skip && *skip) return;
+  const i64 total = C.m * C.n;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    T* c = C.at(e % C.m, e / C.m);
+    *c = conj_(*c);
+  }
+}
+
+template <typename T> int conj_view(View<T> C, const int* skip, cudaStream_t st) {
+  if (!is_cplx<T>::value || C.empty()) return 0;
+  i64 total = C.m * C.n;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  conj_kernel<T><<<blocks, 256, 0, st>>>(C, skip);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
 // ------------------------------------------------------------ dispatch
 namespace {
 
@@ -462,6 +483,8 @@ template int gemm<double>(int, double, View<double>, bool, View<double>, bool, d
                           View<double>, bool, const int*, cudaStream_t, int, bool);
 template int gemm<Z>(int, Z, View<Z>, bool, View<Z>, bool, Z, View<Z>, bool, const int*,
                      cudaStream_t, int, bool);
+template int conj_view<double>(View<double>, const int*, cudaStream_t);
+template int conj_view<Z>(View<Z>, const int*, cudaStream_t);
 template int scale_view<double>(View<double>, double, int, bool, const int*, cudaStream_t);
 template int scale_view<Z>(View<Z>, Z, int, bool, const int*, cudaStream_t);
 

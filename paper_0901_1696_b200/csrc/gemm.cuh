@@ -47,6 +47,9 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
 // inplace_leaf: C aliases B and M <= 64; the launch uses one CTA row (BM >= M) so
 // every CTA reads its whole B column block before writing it back.
 
+// in-place complex conjugation of a view (no-op for real)
+template <typename T> int conj_view(View<T> C, const int* skip, cudaStream_t st);
+
 // scale/zero a (possibly triangular) view: C <- beta*C (beta == 0 writes zeros)
 template <typename T>
 int scale_view(View<T> C, T beta, int tri_mode, bool herm_diag, const int* skip, cudaStream_t st);

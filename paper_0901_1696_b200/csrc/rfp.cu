@@ -344,13 +344,228 @@ int convert(const Storage& src, const T* s, const Storage& dst, T* dptr, bool ze
   return 0;
 }
 
+
+// ============================================================ SURVEY 8(f) rows
+// tfsm: RFP triangular solve through T1/S1/T2 (rfp.py:139-224); singular
+// indices re-based to the global row via the scan base (rfp.py:46-52).
+template <typename T>
+static int tfsm_left(Ctx c, const RfpDesc& d, char trans, char diag, T alpha, View<T> t1,
+                     View<T> t2, View<T> s1, View<T> b) {
+  const i64 n1 = d.n1, n2 = d.n2, N = b.n;
+  const int in1 = (int)n1, in2 = (int)n2;
+  const T one_ = one<T>(), mone = m_one<T>();
+  if (d.lower) {
+    View<T> b1 = b.sub(0, 0, n1, N), b2 = b.sub(n1, 0, n2, N);
+    if (trans == 'N') {
+      TRY(blas_trsm(c, 'L', 'L', 'N', diag, alpha, t1, b1, true, (T*)nullptr, 0));
+      if (n2) {
+        TRY(blas_gemm(c, 'N', 'N', mone, s1, b1, alpha, b2));
+        TRY(blas_trsm(c, 'L', 'U', 'T', diag, one_, t2, b2, true, (T*)nullptr, in1));
+      }
+    } else if (trans == 'T') {
+      if (n2) {
+        TRY(blas_trsm(c, 'L', 'U', 'N', diag, alpha, t2, b2, true, (T*)nullptr, in1));
+        TRY(blas_gemm(c, 'T', 'N', mone, s1, b2, alpha, b1));
+        TRY(blas_trsm(c, 'L', 'L', 'T', diag, one_, t1, b1, true, (T*)nullptr, 0));
+      } else {
+        TRY(blas_trsm(c, 'L', 'L', 'T', diag, alpha, t1, b1, true, (T*)nullptr, 0));
+      }
+    } else {
+      if (n2) {
+        TRY(blas_trsm(c, 'L', 'L', 'C', diag, alpha, t2.t(), b2, true, (T*)nullptr, in1));
+        TRY(blas_gemm(c, 'C', 'N', mone, s1, b2, alpha, b1));
+        TRY(blas_trsm(c, 'L', 'L', 'C', diag, one_, t1, b1, true, (T*)nullptr, 0));
+      } else {
+        TRY(blas_trsm(c, 'L', 'L', 'C', diag, alpha, t1, b1, true, (T*)nullptr, 0));
+      }
+    }
+    return 0;
+  }
+  View<T> b1 = b.sub(0, 0, n2, N), b2 = b.sub(n2, 0, n1, N);
+  if (trans == 'N') {
+    TRY(blas_trsm(c, 'L', 'U', 'N', diag, alpha, t2, b2, true, (T*)nullptr, in2));
+    if (n2) {
+      TRY(blas_gemm(c, 'N', 'N', mone, s1, b2, alpha, b1));
+      TRY(blas_trsm(c, 'L', 'L', 'T', diag, one_, t1, b1, true, (T*)nullptr, 0));
+    }
+  } else if (trans == 'T') {
+    if (n2) {
+      TRY(blas_trsm(c, 'L', 'L', 'N', diag, alpha, t1, b1, true, (T*)nullptr, 0));
+      TRY(blas_gemm(c, 'T', 'N', mone, s1, b1, alpha, b2));
+      TRY(blas_trsm(c, 'L', 'U', 'T', diag, one_, t2, b2, true, (T*)nullptr, in2));
+    } else {
+      TRY(blas_trsm(c, 'L', 'U', 'T', diag, alpha, t2, b2, true, (T*)nullptr, in2));
+    }
+  } else {
+    if (n2) {
+      TRY(blas_trsm(c, 'L', 'U', 'C', diag, alpha, t1.t(), b1, true, (T*)nullptr, 0));
+      TRY(blas_gemm(c, 'C', 'N', mone, s1, b1, alpha, b2));
+      TRY(blas_trsm(c, 'L', 'U', 'C', diag, one_, t2, b2, true, (T*)nullptr, in2));
+    } else {
+      TRY(blas_trsm(c, 'L', 'U', 'C', diag, alpha, t2, b2, true, (T*)nullptr, in2));
+    }
+  }
+  return 0;
+}
+
+template <typename T>
+int tfsm(Ctx c, const RfpDesc& d, char side, char trans, char diag, T alpha, const T* arf,
+         View<T> b) {
+  if (b.empty()) return 0;
+  if (is_zero(alpha)) return scale_view<T>(b, alpha, TRI_FULL, false, c.info, c.st);
+  if (!is_cplx<T>::value && trans == 'C') trans = 'T';
+  View<T> t1, t2, s1;
+  rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
+  if (side == 'L') return tfsm_left(c, d, trans, diag, alpha, t1, t2, s1, b);
+  if (trans == 'C') {
+    // X A^H = alpha B  <=>  A conj(X)^T = conj(alpha) conj(B)^T  (rfp.py:218-222)
+    TRY(conj_view<T>(b, c.info, c.st));
+    TRY(tfsm_left(c, d, 'N', diag, conj_(alpha), t1, t2, s1, b.t()));
+    return conj_view<T>(b, c.info, c.st);
+  }
+  return tfsm_left(c, d, trans == 'N' ? 'T' : 'N', diag, alpha, t1, t2, s1, b.t());
+}
+
+// sfrk/hfrk: C <- alpha G G^(T|H) + beta C on the RFP blocks (rfp.py:227-283)
+template <typename T>
+int sfrk(Ctx c, const RfpDesc& d, char trans, i64 k, double alpha, View<T> a, double beta, T* arf,
+         bool herm) {
+  if (d.n == 0) return 0;
+  if (alpha == 0.0 || k == 0) {
+    if (beta == 1.0) return 0;
+    return scale_view<T>(View<T>{arf, d.nt, 1, 1, d.nt}, sc_from<T>(beta), TRI_FULL, false,
+                         c.info, c.st);
+  }
+  View<T> t1, t2, s1;
+  rfp_blocks(d, arf, t1, t2, s1);
+  const bool rows = trans == 'N';
+  const i64 n1 = d.n1, n2 = d.n2;
+  const T al = sc_from<T>(alpha), be = sc_from<T>(beta);
+  auto part = [&](i64 r0, i64 cnt) { return rows ? a.sub(r0, 0, cnt, k) : a.sub(0, r0, k, cnt); };
+  const char tc = rows ? 'C' : 'N';
+  if (d.lower) {
+    View<T> a1 = part(0, n1), a2 = part(n1, n2);
+    TRY(blas_syrk(c, 'L', trans, alpha, a1, beta, t1, herm));
+    if (n2) {
+      if (rows) TRY(blas_gemm(c, 'N', 'C', al, a2, a1, be, s1));
+      else TRY(blas_gemm(c, 'C', 'N', al, a2, a1, be, s1));
+      TRY(blas_syrk(c, 'U', tc, alpha, a2.t(), beta, t2, herm));
+    }
+    return 0;
+  }
+  View<T> a1 = part(0, n2), a2 = part(n2, n1);
+  if (n2) {
+    TRY(blas_syrk(c, 'L', tc, alpha, a1.t(), beta, t1, herm));
+    if (rows) TRY(blas_gemm(c, 'N', 'C', al, a1, a2, be, s1));
+    else TRY(blas_gemm(c, 'C', 'N', al, a1, a2, be, s1));
+  }
+  return blas_syrk(c, 'U', trans, alpha, a2, beta, t2, herm);
+}
+
+// lansf: one pass over the RFP buffer (rfp.py:363-417).  Each stored element
+// (i, j) of the triangle stands for |A(i,j)| = |A(j,i)|: 'M' takes the max,
+// 'F' sums |a|^2 twice off the diagonal, '1'/'I' add |a| to the column sums
+// of columns j and i (the implied full matrix is symmetric in magnitude).
+__device__ __forceinline__ void rfp_slot_cell(const RfpDesc& d, i64 p, i64& i, i64& j) {
+  i64 r, c;
+  if (!d.trans) { c = p / d.ldar; r = p - c * d.ldar; }
+  else { r = p / d.n1; c = p - r * d.n1; }
+  if (d.lower) {
+    if (r >= c + d.d) { i = r - d.d; j = c; }
+    else { j = r + d.n1; i = c + d.n1 - 1 + d.d; }
+  } else {
+    if (r <= c + d.n2) { i = r; j = c + d.n2; }
+    else { j = r - d.n2 - 1; i = c; }
+  }
+}
+
+__device__ __forceinline__ double mag(double v) { return fabs(v); }
+__device__ __forceinline__ double mag(Z v) { return hypot(v.x, v.y); }
+
+__device__ __forceinline__ void atomic_max_pos(double* a, double v) {
+  // v >= 0: the IEEE bit pattern of non-negative doubles orders like the value
+  atomicMax(reinterpret_cast<unsigned long long*>(a), __double_as_longlong(v));
+}
+
+template <typename T>
+__global__ void lansf_kernel(RfpDesc d, const T* __restrict__ arf, int mode, double* acc,
+                             double* colsum) {
+  double local = 0.0;
+  for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < d.nt;
+       p += (i64)gridDim.x * blockDim.x) {
+    const double m = mag(arf[p]);
+    if (mode == 0) {
+      local = fmax(local, m);
+    } else if (mode == 2) {
+      i64 i, j;
+      rfp_slot_cell(d, p, i, j);
+      local += (i == j ? 1.0 : 2.0) * m * m;
+    } else {
+      i64 i, j;
+      rfp_slot_cell(d, p, i, j);
+      atomicAdd(colsum + j, m);
+      if (i != j) atomicAdd(colsum + i, m);
+    }
+  }
+  if (mode == 1) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v = __shfl_down_sync(0xffffffffu, local, o);
+    local = mode == 0 ? fmax(local, v) : local + v;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mode == 0) atomic_max_pos(acc, local);
+    else atomicAdd(acc, local);
+  }
+}
+
+__global__ void colmax_kernel(const double* colsum, i64 n, double* acc) {
+  double local = 0.0;
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x)
+    local = fmax(local, colsum[j]);
+  for (int o = 16; o > 0; o >>= 1) local = fmax(local, __shfl_down_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(acc, local);
+}
+
+__global__ void sqrt_kernel(double* acc) { *acc = sqrt(*acc); }
+
+template <typename T>
+int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* out) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return (int)e;
+  if (d.n == 0) return 0;
+  const int mode = norm == 'M' ? 0 : (norm == 'F' || norm == 'E') ? 2 : 1;
+  int blocks = (int)((d.nt + 255) / 256);
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+  double* colsum = nullptr;
+  if (mode == 1) {
+    if ((e = cudaMallocAsync((void**)&colsum, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(colsum, 0, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
+  }
+  lansf_kernel<T><<<blocks, 256, 0, st>>>(d, arf, mode, out, colsum);
+  RFPK_CHECK_LAUNCH();
+  if (mode == 1) {
+    int cb = (int)((d.n + 255) / 256);
+    if (cb > 4 * num_sms()) cb = 4 * num_sms();
+    colmax_kernel<<<cb, 256, 0, st>>>(colsum, d.n, out);
+    RFPK_CHECK_LAUNCH();
+    cudaFreeAsync(colsum, st);
+  } else if (mode == 2) {
+    sqrt_kernel<<<1, 1, 0, st>>>(out);
+    RFPK_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
 #define RFPK_RFP_INST(T)                                                                     \
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
   template int pftrf<T>(Ctx, const RfpDesc&, T*);                                            \
   template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>);                             \
   template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
   template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \
-  template int convert<T>(const Storage&, const T*, const Storage&, T*, bool, cudaStream_t);
+  template int convert<T>(const Storage&, const T*, const Storage&, T*, bool, cudaStream_t);  \
+  template int tfsm<T>(Ctx, const RfpDesc&, char, char, char, T, const T*, View<T>);         \
+  template int sfrk<T>(Ctx, const RfpDesc&, char, i64, double, View<T>, double, T*, bool);   \
+  template int lansf<T>(cudaStream_t, const RfpDesc&, char, const T*, double*);
 RFPK_RFP_INST(double)
 RFPK_RFP_INST(Z)
 

@@ -24,6 +24,17 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
 template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf);
 template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf);
 
+// SURVEY 8(f) rows
+template <typename T>
+int tfsm(Ctx c, const RfpDesc& d, char side, char trans, char diag, T alpha, const T* arf,
+         View<T> b);
+template <typename T>
+int sfrk(Ctx c, const RfpDesc& d, char trans, i64 k, double alpha, View<T> a, double beta, T* arf,
+         bool herm);
+// norm of the implied full matrix into *out (device double): 'M', '1', 'I', 'F'
+template <typename T> int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf,
+                                double* out);
+
 // Storage descriptors for the conversion kernel.
 enum StorageKind : int { ST_FULL = 0, ST_PACKED = 1, ST_RFP = 2 };
 struct Storage {

@@ -24,8 +24,11 @@ from .layout import make_descriptor, normalize_flag
 __all__ = [
     "pftrf",
     "pftrs",
+    "tfsm",
+    "sfrk_hfrk",
     "tftri",
     "pftri",
+    "lansf",
     "pftrf_batched",
     "pftrs_batched",
     "pftrf_pftrs_batched",
@@ -156,6 +159,149 @@ def pftri(r: RfpTriangle) -> int:
     if v == 0:
         r.state = FactorState.FULL_INVERSE
     return v
+
+
+# ---------------------------------------------------------------- SURVEY 8(f) rows
+
+
+def _flag(value, allowed, what):
+    f = str(value).upper()[:1]
+    if f not in allowed:
+        raise ValueError(f"{what} must be one of {tuple(allowed)}, got {value!r}")
+    return f
+
+
+def _canon_transr(t):
+    return "T" if t == "C" else t
+
+
+def _check_desc(desc, n, uplo, transr):
+    if (desc.n, desc.uplo, desc.transr) != (int(n), uplo, _canon_transr(transr)):
+        raise ValueError(
+            f"descriptor (n={desc.n}, uplo={desc.uplo}, transr={desc.transr}) "
+            f"does not match (n={n}, uplo={uplo}, transr={transr})")
+
+
+def _device_inplace(b):
+    """(working CUDA tensor with a unit stride, foreign original or None)."""
+    foreign = None
+    if not isinstance(b, torch.Tensor) or not b.is_cuda:
+        foreign = b
+        bt = as_device(b)
+    else:
+        bt = b
+    work = bt
+    if bt.dtype not in (torch.float64, torch.complex128) or (bt.dim() == 2 and bt.stride(0) != 1
+                                                            and bt.stride(1) != 1):
+        work = bt.to(torch.complex128 if bt.is_complex() else torch.float64).t().contiguous().t()
+    return bt, work, foreign
+
+
+def _writeback(bt, work, foreign):
+    if work is not bt:
+        bt.copy_(work)
+    if foreign is not None:
+        host = bt.cpu()
+        if isinstance(foreign, torch.Tensor):
+            foreign.copy_(host)
+        else:
+            foreign[...] = host.numpy()
+
+
+def tfsm(transr: str, side: str, uplo: str, trans: str, diag: str, m: int, n: int, alpha,
+         a: RfpTriangle, b) -> None:
+    """Triangular solve with an RFP-stored triangle (rfp.py:181-224):
+    ``op(A) X = alpha B`` (side 'L') or ``X op(A) = alpha B`` (side 'R'),
+    in place on the ``m x n`` array ``b``.  A zero diagonal (diag 'N') raises
+    ``kernels.SingularMatrixError`` with the 1-based global index."""
+    from .kernels import SingularMatrixError
+    transr = _flag(transr, "NTC", "transr")
+    side = _flag(side, "LR", "side")
+    uplo = _flag(uplo, "LU", "uplo")
+    trans = _flag(trans, "NTC", "trans")
+    diag = _flag(diag, "NU", "diag")
+    order = m if side == "L" else n
+    _check_desc(a.desc, order, uplo, transr)
+    bt, work, foreign = _device_inplace(b)
+    if tuple(bt.shape) != (m, n):
+        raise ValueError(f"b must be {(m, n)}, got {tuple(bt.shape)}")
+    if m == 0 or n == 0:
+        return
+    data = a.data
+    if work.is_complex() and not data.is_complex():
+        data = data.to(torch.complex128)
+    if data.is_complex() and not work.is_complex():
+        raise ValueError("complex triangle needs a complex right-hand side")
+    info = _info(work.device)
+    st = _capi.stream_handle(work.device)
+    flags = [_capi.flag(x) for x in (a.desc.transr, side, uplo, trans, diag)]
+    if data.is_complex():
+        al = complex(alpha)
+        _run("rfpk_ztfsm", *flags, m, n, al.real, al.imag, data.data_ptr(), work.data_ptr(),
+             work.stride(0), work.stride(1), info.data_ptr(), st)
+    else:
+        _run("rfpk_dtfsm", *flags, m, n, float(alpha), data.data_ptr(), work.data_ptr(),
+             work.stride(0), work.stride(1), info.data_ptr(), st)
+    v = int(info.item())
+    if v:
+        raise SingularMatrixError(v)
+    _writeback(bt, work, foreign)
+
+
+def sfrk_hfrk(transr: str, uplo: str, trans: str, n: int, k: int, alpha: float, a, beta: float,
+              c: RfpTriangle, hermitian=None) -> None:
+    """RFP rank-k update ``C <- alpha G G^(T|H) + beta C`` (rfp.py:227-283),
+    G = A (n x k) for trans 'N', A^(T|H) (A k x n) otherwise; real alpha, beta."""
+    transr = _flag(transr, "NTC", "transr")
+    uplo = _flag(uplo, "LU", "uplo")
+    trans = _flag(trans, "NTC", "trans")
+    _check_desc(c.desc, n, uplo, transr)
+    alpha, beta = float(alpha), float(beta)
+    herm = c.data.is_complex() if hermitian is None else bool(hermitian)
+    if c.data.is_complex() and not herm:
+        raise ValueError("complex symmetric (non-conjugated) updates are not supported")
+    if n == 0:
+        return
+    st = _capi.stream_handle(c.data.device)
+    flags = [_capi.flag(x) for x in (c.desc.transr, uplo, trans)]
+    if alpha == 0 or k == 0:
+        if c.data.is_complex():
+            _run("rfpk_zhfrk", *flags, n, 0, 0.0, 0, 1, 1, beta, c.data.data_ptr(), 1, st)
+        else:
+            _run("rfpk_dsfrk", *flags, n, 0, 0.0, 0, 1, 1, beta, c.data.data_ptr(), st)
+        return
+    at = as_device(a)
+    want = (n, k) if trans == "N" else (k, n)
+    if tuple(at.shape) != want:
+        raise ValueError(f"a must be {want} for trans={trans!r}, got {tuple(at.shape)}")
+    if at.stride(0) != 1 and at.stride(1) != 1:
+        at = at.t().contiguous().t()
+    if c.data.is_complex():
+        at = at.to(torch.complex128)
+        _run("rfpk_zhfrk", *flags, n, k, alpha, at.data_ptr(), at.stride(0), at.stride(1), beta,
+             c.data.data_ptr(), 1, st)
+    else:
+        if at.is_complex():
+            raise ValueError("real triangle needs a real update matrix")
+        _run("rfpk_dsfrk", *flags, n, k, alpha, at.data_ptr(), at.stride(0), at.stride(1), beta,
+             c.data.data_ptr(), st)
+
+
+def lansf(norm: str, r: RfpTriangle, hermitian: bool = True) -> float:
+    """Norm of the full symmetric/Hermitian matrix implied by an RFP triangle
+    (rfp.py:363-417): 'M' max |a|, '1'/'O' and 'I' (equal for symmetric),
+    'F'/'E' Frobenius.  One device pass over the RFP buffer."""
+    nm = str(norm).upper()[:1]
+    if nm not in ("M", "1", "O", "I", "F", "E"):
+        raise ValueError(f"unknown norm selector {nm!r}")
+    d = r.desc
+    if d.n == 0:
+        return 0.0
+    out = torch.zeros(1, dtype=torch.float64, device=r.data.device)
+    fn = "rfpk_zlansf" if r.data.is_complex() else "rfpk_dlansf"
+    _run(fn, _capi.flag(nm), _capi.flag(d.transr), _capi.flag(d.uplo), d.n, r.data.data_ptr(),
+         out.data_ptr(), _capi.stream_handle(r.data.device))
+    return float(out.item())
 
 
 # ---------------------------------------------------------------- batched

@@ -360,3 +360,77 @@ def test_config5_complex_inverse_columns(P, n):
     E = a @ inv[:, J]
     E[J, torch.arange(256, device="cuda")] -= 1.0
     assert float(E.abs().max()) <= 1e-12
+
+
+# ---------------------------------------------------------------- SURVEY 8(f) rows
+from tests.conftest import next_row_cases  # noqa: E402
+
+with np.load(GOLDEN) as _z2:
+    NEXT = next_row_cases({k: None for k in _z2.files})
+
+
+@pytest.mark.parametrize("key,dt,uplo,transr,n", NEXT, ids=[c[0] for c in NEXT])
+def test_next_rows_match_reference(P, golden, key, dt, uplo, transr, n):
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    cplx = dt == "c128"
+    d = layout.make_descriptor(n, uplo, transr)
+    f = conv.RfpTriangle(golden[f"tfsm_{key}_factor"], d)
+    for side in "LR":
+        for trans in "NTC":
+            for diag in "NU":
+                b = torch.from_numpy(golden[f"tfsm_{key}_{side}{trans}{diag}_B"]).cuda()
+                alpha = (1.5 - 0.5j) if cplx else 1.5
+                rfp.tfsm(transr, side, uplo, trans, diag, b.shape[0], b.shape[1], alpha, f, b)
+                assert rel(b, golden[f"tfsm_{key}_{side}{trans}{diag}_X"]) <= TOL, (side, trans, diag)
+    for trans in "NC":
+        c = conv.RfpTriangle(golden[f"sfrk_{key}_{trans}_C0"], d)
+        rfp.sfrk_hfrk(transr, uplo, trans, n, 5, -0.75, golden[f"sfrk_{key}_{trans}_A"], 1.25, c)
+        assert rel(c.data, golden[f"sfrk_{key}_{trans}_C"]) <= TOL
+    r = conv.RfpTriangle(golden[f"lansf_{key}_rfp"], d)
+    got = [rfp.lansf(nm, r) for nm in "M1IF"]
+    assert np.allclose(got, golden[f"lansf_{key}"], rtol=1e-12, atol=0)
+
+
+def test_next_rows_large_vs_oracle(P):
+    """Recursive sizes for tfsm / sfrk_hfrk / lansf against the oracle, plus
+    the singular-index re-basing of tfsm (rfp.py:46-52)."""
+    conv, rfp, kernels = P.convert, P.rfp, P.kernels
+    for n, uplo, transr, cplx in [(700, "L", "N", False), (513, "U", "T", True), (1100, "U", "N", False)]:
+        a = O.spd_matrix(n, n, "n", complex_=cplx)
+        buf = O.trttf(a, uplo, transr)
+        f = buf.copy()
+        assert O.pftrf(f, n, uplo, transr) == 0
+        fr = conv.RfpTriangle(f, P.layout.make_descriptor(n, uplo, transr))
+        g = np.random.default_rng(n)
+        for side, trans in [("L", "N"), ("R", "C"), ("L", "T"), ("R", "N")]:
+            shape = (n, 9) if side == "L" else (9, n)
+            b = np.asfortranarray(g.standard_normal(shape) + (1j * g.standard_normal(shape) if cplx else 0))
+            xo = b.copy(order="F")
+            O.tfsm(f, n, uplo, transr, side, trans, "N", 0.5, xo)
+            x = torch.from_numpy(b).cuda()
+            rfp.tfsm(transr, side, uplo, trans, "N", shape[0], shape[1], 0.5, fr, x)
+            assert rel(x, xo) <= TOL
+        k = 37
+        ga = np.asfortranarray(g.standard_normal((n, k)) + (1j * g.standard_normal((n, k)) if cplx else 0))
+        co = buf.copy()
+        O.sfrk_hfrk(co, n, uplo, transr, "N", k, 2.0, ga, -0.5, cplx)
+        c = conv.RfpTriangle(buf.copy(), P.layout.make_descriptor(n, uplo, transr))
+        rfp.sfrk_hfrk(transr, uplo, "N", n, k, 2.0, ga, -0.5, c)
+        assert rel(c.data, co) <= TOL
+        for nm in "M1IF":
+            assert rfp.lansf(nm, c) == pytest.approx(O.lansf(nm, co, n, uplo, transr), rel=1e-12)
+    # singular triangle: global index of the zero diagonal (T2 block, L layout)
+    n = 150
+    a = O.spd_matrix(n, 3, "n")
+    f = O.trttf(a, "L", "N")
+    assert O.pftrf(f, n, "L", "N") == 0
+    ds = O.desc(n, "L", "N")
+    t1, t2, s1 = O.blocks(f, ds)
+    t2[10, 10] = 0.0
+    fr = conv.RfpTriangle(f, P.layout.make_descriptor(n, "L", "N"))
+    b = torch.ones(n, 2, dtype=torch.float64, device="cuda")
+    with pytest.raises(kernels.SingularMatrixError) as e:
+        rfp.tfsm("N", "L", "L", "N", "N", n, 2, 1.0, fr, b)
+    with pytest.raises(O.OracleSingular) as eo:
+        O.tfsm(f, n, "L", "N", "L", "N", "N", 1.0, np.ones((n, 2), order="F"))
+    assert e.value.index == eo.value.index == ds.n1 + 11
