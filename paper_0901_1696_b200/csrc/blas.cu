@@ -455,6 +455,48 @@ int trsm_rest_upper(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool 
   return trsm_rest_upper(c, conj, T11, B1, m1, W, wtrans, depth);
 }
 
+// Blocked right-looking trsm with look-ahead for a narrow right-hand side
+// (B.n <= 2048, e.g. pftrs with nrhs = 1024): the recursive form leaves its
+// bottom levels as 64 x N x 64 GEMMs of ~16 CTAs; here the critical path is
+// 256-row block solves (trsm_plain over the same 64-leaf inverses) plus the
+// update of the next block, and the rank-256 update of the remaining rows
+// runs on a side stream.  Same W slab layout as trsm_rec.
+constexpr i64 TRL_NB = 256;
+
+template <typename T>
+int trsm_rl(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
+  const i64 n = Tm.m, N = B.n;
+  cudaStream_t side = la_streams().side[22];
+  int rc;
+  bool side_busy = false;
+  const i64 nblk = (n + TRL_NB - 1) / TRL_NB;
+  auto sz = [&](i64 k) { return (n - k * TRL_NB) < TRL_NB ? (n - k * TRL_NB) : TRL_NB; };
+  for (i64 step = 0; step < nblk; ++step) {
+    const i64 k = lower ? step : nblk - 1 - step;
+    const i64 o = k * TRL_NB, s = sz(k);
+    View<T> Xk = B.sub(o, 0, s, N);
+    if ((rc = trsm_plain(c, lower, conj, Tm.sub(o, o, s, s), Xk, W + o * 64, wtrans))) return rc;
+    if (step + 1 == nblk) break;
+    if (side_busy && (rc = la_link(side, c.st))) return rc;
+    // next block to be solved, and the rows beyond it
+    const i64 kn = lower ? k + 1 : k - 1;
+    const i64 on = kn * TRL_NB, sn = sz(kn);
+    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(on, o, sn, s), conj, Xk, false, one<T>(),
+                      B.sub(on, 0, sn, N), false, c.info, c.st)))
+      return rc;
+    const i64 r0 = lower ? on + sn : 0, rn = lower ? n - (on + sn) : on;
+    if (rn > 0) {
+      if ((rc = la_link(c.st, side))) return rc;
+      if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(r0, o, rn, s), conj, Xk, false, one<T>(),
+                        B.sub(r0, 0, rn, N), false, c.info, side)))
+        return rc;
+      side_busy = true;
+    }
+  }
+  if (side_busy && (rc = la_link(side, c.st))) return rc;
+  return 0;
+}
+
 // conj?(T) X = alpha B.  If W is null the leaf inverses are computed here.
 template <typename T>
 int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B, T* W) {
@@ -470,7 +512,10 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
     if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
     W = own;
   }
-  if (Tm.m >= LA_MIN) rc = on_hi_stream(c, [&](Ctx h) { return trsm_rec(h, lower, conj, Tm, B, W, !lower); });
+  if (Tm.m >= 1024 && B.n <= 2048 && !std::getenv("RFPK_NO_TRSM_RL"))
+    rc = on_hi_stream(c, [&](Ctx h) { return trsm_rl(h, lower, conj, Tm, B, W, !lower); });
+  else if (Tm.m >= LA_MIN)
+    rc = on_hi_stream(c, [&](Ctx h) { return trsm_rec(h, lower, conj, Tm, B, W, !lower); });
   else rc = trsm_rec(c, lower, conj, Tm, B, W, !lower);
   ws_free(own, c.st);
   return rc;

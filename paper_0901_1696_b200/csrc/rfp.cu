@@ -123,16 +123,24 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
   View<T> t1, t2, s1;
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
   const i64 n1 = d.n1, n2 = d.n2, r = b.n;
+  PhaseTrace tr(c.st, "pftrs");
   if (d.lower) {
     View<T> b1 = b.sub(0, 0, n1, r), b2 = b.sub(n1, 0, n2, r);
     TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false));
+    tr.mark("trsm1");
     if (n2) {
       TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+      tr.mark("gemm1");
       TRY(blas_trsm(c, 'L', 'U', 'T', 'N', one<T>(), t2, b2, false));
+      tr.mark("trsm2");
       TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false));
+      tr.mark("trsm3");
       TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+      tr.mark("gemm2");
     }
-    return blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false);
+    TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false));
+    tr.mark("trsm4");
+    return 0;
   }
   View<T> b1 = b.sub(0, 0, n2, r), b2 = b.sub(n2, 0, n1, r);
   if (n2) {
