@@ -129,8 +129,28 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 
 // ---------------------------------------------------------------- n == 64
 // One warp per matrix; see batched64.cuh for the algorithm.  Shared memory:
-// RFP buffer (2080) + W1, W2 (32 x 33 each) + RHS chunk / scratch (64 x 8).
-constexpr int B64_SMEM_DOUBLES = b64::NT + 2 * 32 * b64::WLD + 64 * 8;
+// RFP buffer (2080) + RHS chunk (64 x 8) + scratch (96) = 21 KB, so ten
+// matrices (warps) are resident per SM.  W1 = L1^-1 and W2 = L2^-1 are formed
+// IN PLACE of the factor blocks T1 / T2 once those are safely in HBM.
+constexpr int B64_SMEM_DOUBLES = b64::NT + 64 * 8 + 96;
+
+// X (64 x 8, ld 64) <- columns [c0, c0 + cw) of the n x nrhs RHS, zero-padded;
+// 8-byte cp.async so the global latency overlaps the factorization.
+__device__ __forceinline__ void b64_fetch_rhs(double* X, const double* bk, i64 ldb, int c0,
+                                              int cw) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < 64 * 8; e += 32) {
+    const int i = e & 63, c = e >> 6;
+    if (c < cw) {
+      unsigned s = (unsigned)__cvta_generic_to_shared(X + e);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s),
+                   "l"(bk + i + (i64)(c0 + c) * ldb));
+    } else {
+      X[e] = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
 
 template <bool FACTOR, bool SOLVE, int TRANS>
 __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
@@ -139,23 +159,28 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   using namespace b64;
   extern __shared__ __align__(16) double sm[];
   double* R = sm;
-  double* W1 = R + NT;
-  double* W2 = W1 + 32 * WLD;
-  double* X = W2 + 32 * WLD;   // RHS chunk, ld 64; scratch during the factorization
-  double* colk = X;            // 64 entries
-  double* rdiag = X + 64;      // 32 entries
+  double* X = R + NT;      // RHS chunk, ld 64
+  double* colk = X + 512;  // 64 entries (chol32)
+  double* rdiag = colk + 64;  // 32 entries (inv32)
   const int lane = threadIdx.x;
   const i64 k = blockIdx.x;
   double* g = arf + k * stride_arf;
+  double* bk = SOLVE ? b + k * stride_b : nullptr;
   const bool al16 = ((reinterpret_cast<uintptr_t>(g) & 15) == 0);
   if (al16) {
     for (int c = lane; c < NT / 2; c += 32) {
       unsigned s = (unsigned)__cvta_generic_to_shared(R + 2 * c);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g + 2 * c));
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   } else {
     for (int c = lane; c < NT; c += 32) R[c] = g[c];
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (SOLVE) {
+    b64_fetch_rhs(X, bk, ldb, 0, nrhs < 8 ? nrhs : 8);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::);
   }
   __syncwarp();
   constexpr int rs = TRANS ? 32 : 1, cs = TRANS ? 1 : 65;
@@ -164,9 +189,8 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   const V T1{R + (lower ? 1 : 33) * rs};
   const V T2{R + (lower ? 0 : 32) * rs};
   const V S1{R + (lower ? 33 : 0) * rs};
-  const V V1 = T1;
-  const auto V2 = T2.t();
-  const SV<1, WLD> w1{W1}, w2{W2};
+  const V V1 = T1;            // L1 (lower), later W1
+  const auto V2 = T2.t();     // L2 (lower), later W2
   const SV<1, 64> x1{X}, x2{X + 32};
   if (FACTOR) {
     int f = chol32(V1, colk);
@@ -174,71 +198,67 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
       if (lane == 0) info[k] = f;
       return;
     }
-    inv32(V1, W1, rdiag);
+    put_view<1>(V1, R, g);  // L1 is final: store it before W1 overwrites it
+    inv32(V1, rdiag);
     double acc[2][4][4];
     zero_acc<32>(acc);
-    if (lower) mm32<32>(S1, w1.t(), acc);   // S1 <- S1 W1^T
-    else mm32<32>(w1, S1, acc);             // S1 <- W1 S1
+    if (lower) mm32<32, 0, 2>(S1, V1.t(), acc);   // S1 <- S1 W1^T
+    else mm32<32, 1, 0>(V1, S1, acc);             // S1 <- W1 S1
     __syncwarp();
     store_acc<32>(S1, acc, 1.0, 0.0, 0);
     __syncwarp();
     zero_acc<32>(acc);
-    if (lower) mm32<32>(S1, S1.t(), acc);   // T2 -= S1 S1^T
-    else mm32<32>(S1.t(), S1, acc);         // T2 -= S1^T S1
+    if (lower) mm32<32, 0, 0>(S1, S1.t(), acc);   // T2 -= S1 S1^T
+    else mm32<32, 0, 0>(S1.t(), S1, acc);         // T2 -= S1^T S1
     store_acc<32>(T2, acc, -1.0, 1.0, 2);
     __syncwarp();
     f = chol32(V2, colk);
     if (lane == 0) info[k] = f ? 32 + f : 0;
     if (f) return;
-    if (SOLVE) inv32(V2, W2, rdiag);
-    if (al16) {
-      for (int c = lane; c < NT / 2; c += 32)
-        reinterpret_cast<double2*>(g)[c] = reinterpret_cast<const double2*>(R)[c];
-    } else {
-      for (int c = lane; c < NT; c += 32) g[c] = R[c];
-    }
+    put_view<1>(V2, R, g);
+    put_view<0>(S1, R, g);
+    if (SOLVE) inv32(V2, rdiag);
   } else {
-    inv32(V1, W1, rdiag);
-    inv32(V2, W2, rdiag);
+    inv32(V1, rdiag);
+    inv32(V2, rdiag);
   }
   if (!SOLVE) return;
-  double* bk = b + k * stride_b;
+  const auto w1 = V1;
+  const auto w2 = V2;
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
     __syncwarp();
-    for (int e = lane; e < 64 * 8; e += 32) {
-      const int i = e & 63, c = e >> 6;
-      X[e] = c < cw ? bk[i + (i64)(c0 + c) * ldb] : 0.0;
-    }
+    if (c0) b64_fetch_rhs(X, bk, ldb, c0, cw);
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncwarp();
     double a8[2][1][4];
     zero_acc<8>(a8);
-    mm32<8>(w1, x1, a8);                      // b1 = W1 b1
+    mm32<8, 1, 0>(w1, x1, a8);                 // b1 = W1 b1
     __syncwarp();
     store_acc<8>(x1, a8, 1.0, 0.0, 0);
     __syncwarp();
     zero_acc<8>(a8);
-    if (lower) mm32<8>(S1, x1, a8);           // b2 -= S1 b1
-    else mm32<8>(S1.t(), x1, a8);             // b2 -= S1^T b1
+    if (lower) mm32<8, 0, 0>(S1, x1, a8);      // b2 -= S1 b1
+    else mm32<8, 0, 0>(S1.t(), x1, a8);        // b2 -= S1^T b1
     store_acc<8>(x2, a8, -1.0, 1.0, 0);
     __syncwarp();
     zero_acc<8>(a8);
-    mm32<8>(w2, x2, a8);                      // b2 = W2 b2
+    mm32<8, 1, 0>(w2, x2, a8);                 // b2 = W2 b2
     __syncwarp();
     store_acc<8>(x2, a8, 1.0, 0.0, 0);
     __syncwarp();
     zero_acc<8>(a8);
-    mm32<8>(w2.t(), x2, a8);                  // b2 = W2^T b2
+    mm32<8, 2, 0>(w2.t(), x2, a8);             // b2 = W2^T b2
     __syncwarp();
     store_acc<8>(x2, a8, 1.0, 0.0, 0);
     __syncwarp();
     zero_acc<8>(a8);
-    if (lower) mm32<8>(S1.t(), x2, a8);       // b1 -= S1^T b2
-    else mm32<8>(S1, x2, a8);                 // b1 -= S1 b2
+    if (lower) mm32<8, 0, 0>(S1.t(), x2, a8);  // b1 -= S1^T b2
+    else mm32<8, 0, 0>(S1, x2, a8);            // b1 -= S1 b2
     store_acc<8>(x1, a8, -1.0, 1.0, 0);
     __syncwarp();
     zero_acc<8>(a8);
-    mm32<8>(w1.t(), x1, a8);                  // b1 = W1^T b1
+    mm32<8, 2, 0>(w1.t(), x1, a8);             // b1 = W1^T b1
     __syncwarp();
     store_acc<8>(x1, a8, 1.0, 0.0, 0);
     __syncwarp();

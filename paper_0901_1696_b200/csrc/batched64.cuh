@@ -24,7 +24,6 @@ namespace rfpk {
 namespace b64 {
 
 constexpr int N = 64, H = 32, NT = N * (N + 1) / 2;  // 2080
-constexpr int WLD = 33;                              // smem pitch of W1/W2
 
 __device__ __forceinline__ double shfl(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
@@ -80,12 +79,12 @@ __device__ __noinline__ int chol32(SV<RS, CS> V, double* colk) {
   return 0;
 }
 
-// W (pitch WLD, zeros above the diagonal) = inverse of the lower 32x32 view L;
-// lane j computes column j.
+// In-place inverse of the lower 32x32 view L (only the lower triangle is read
+// or written: the slots above it belong to the other RFP block).  Lane j
+// computes column j; rdiag is a 32-entry scratch.
 template <int RS, int CS>
-__device__ __noinline__ void inv32(SV<RS, CS> L, double* W, double* rdiag) {
+__device__ __noinline__ void inv32(SV<RS, CS> L, double* rdiag) {
   __builtin_assume(__isShared(L.p));
-  __builtin_assume(__isShared(W));
   __builtin_assume(__isShared(rdiag));
   const int j = threadIdx.x & 31;
   rdiag[j] = 1.0 / L(j, j);
@@ -104,30 +103,64 @@ __device__ __noinline__ void inv32(SV<RS, CS> L, double* W, double* rdiag) {
     }
     w[i] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
   }
+  __syncwarp();  // every lane has finished reading L
 #pragma unroll
-  for (int i = 0; i < 32; ++i) W[i + j * WLD] = (i >= j) ? w[i] : 0.0;
+  for (int i = 0; i < 32; ++i)
+    if (i >= j) L(i, j) = w[i];
   __syncwarp();
 }
 
 // acc(32 x NC) += A(32x32) * B(32 x NC), A and B smem views; fragment layout of
-// m16n8k4 (g = lane/4, t = lane%4).  acc[mi][ni][4].
-template <int NC, class VA, class VB>
+// m16n8k4 (g = lane/4, t = lane%4).  acc[mi][ni][4].  TA / TB select a
+// triangular operand whose other triangle holds unrelated data and reads as
+// zero: TA 1 = A lower (k <= i), 2 = A upper (k >= i); TB 2 = B upper (k <= n).
+template <int NC, int TA, int TB, class VA, class VB>
 __device__ __forceinline__ void mm32(VA A, VB B, double acc[2][NC / 8][4]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int k0 = 0; k0 < 32; k0 += 4) {
+    const int kk = k0 + t;
     double a[2][2], b[NC / 8];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
-      a[mi][0] = A(mi * 16 + g, k0 + t);
-      a[mi][1] = A(mi * 16 + g + 8, k0 + t);
+      const int r0 = mi * 16 + g, r1 = r0 + 8;
+      a[mi][0] = (TA == 1 && kk > r0) || (TA == 2 && kk < r0) ? 0.0 : A(r0, kk);
+      a[mi][1] = (TA == 1 && kk > r1) || (TA == 2 && kk < r1) ? 0.0 : A(r1, kk);
     }
 #pragma unroll
-    for (int ni = 0; ni < NC / 8; ++ni) b[ni] = B(k0 + t, ni * 8 + g);
+    for (int ni = 0; ni < NC / 8; ++ni) {
+      const int nn = ni * 8 + g;
+      b[ni] = (TB == 2 && kk > nn) ? 0.0 : B(kk, nn);
+    }
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < 2; ++mi) {
+      // whole 16-row strips that the triangle zeroes are skipped
+      if (TA == 1 && mi == 0 && k0 >= 16) continue;
+      if (TA == 2 && mi == 1 && k0 < 16) continue;
 #pragma unroll
-      for (int ni = 0; ni < NC / 8; ++ni) mma(acc[mi][ni], a[mi][0], a[mi][1], b[ni]);
+      for (int ni = 0; ni < NC / 8; ++ni) {
+        if (TB == 2 && k0 >= (ni + 1) * 8) continue;
+        mma(acc[mi][ni], a[mi][0], a[mi][1], b[ni]);
+      }
+    }
+  }
+}
+
+// global <- smem for the part of view V selected by MASK (0 all, 1 lower incl.
+// diagonal); g is the global image of the smem buffer R.  Lanes run along
+// the unit-stride dimension so every store instruction is coalesced.
+template <int MASK, int RS, int CS>
+__device__ __forceinline__ void put_view(SV<RS, CS> V, const double* R, double* g) {
+  const int lane = threadIdx.x & 31;
+  double* gv = g + (V.p - R);
+  if (RS == 1) {
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j)
+      if (MASK == 0 || lane >= j) gv[lane + j * CS] = V(lane, j);
+  } else {
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i)
+      if (MASK == 0 || i >= lane) gv[i * RS + lane] = V(i, lane);
   }
 }
 
