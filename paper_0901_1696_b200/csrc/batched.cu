@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 
 // ---------------------------------------------------------------- n == 64
 // One warp per matrix; see batched64.cuh for the algorithm.  Shared memory:
-// RFP buffer (2080) + RHS chunk (64 x 8) + scratch (96) = 21 KB, so ten
+// RFP buffer (2080) + RHS chunk (64 x 8) + scratch (64) = 21 KB, so ten
 // matrices (warps) are resident per SM.  W1 = L1^-1 and W2 = L2^-1 are formed
 // IN PLACE of the factor blocks T1 / T2 once those are safely in HBM.
 constexpr int B64_SMEM_DOUBLES = b64::NT + 64 * 8 + 96;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   extern __shared__ __align__(16) double sm[];
   double* R = sm;
   double* X = R + NT;      // RHS chunk, ld 64
-  double* colk = X + 512;  // 64 entries (chol32)
+  double* colk = X + 512;  // 64 entries (factor_inv32)
   double* rdiag = colk + 64;  // 32 entries (inv32)
   const int lane = threadIdx.x;
   const i64 k = blockIdx.x;
@@ -192,13 +192,14 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   const V V1 = T1;            // L1 (lower), later W1
   const auto V2 = T2.t();     // L2 (lower), later W2
   const SV<1, 64> x1{X}, x2{X + 32};
+  const i64 off1 = V1.p - R, off2 = V2.p - R;
   if (FACTOR) {
-    int f = chol32(V1, colk);
+    // L1 goes to HBM inside factor_inv32 before W1 overwrites it
+    int f = factor_inv32(V1.p, rs, cs, colk, g + off1, F32_FACTOR);
     if (f) {
       if (lane == 0) info[k] = f;
       return;
     }
-    put_view<1>(V1, R, g);  // L1 is final: store it before W1 overwrites it
     inv32(V1, rdiag);
     double acc[2][4][4];
     zero_acc<32>(acc);
@@ -212,11 +213,10 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
     else mm32<32, 0, 0>(S1.t(), S1, acc);         // T2 -= S1^T S1
     store_acc<32>(T2, acc, -1.0, 1.0, 2);
     __syncwarp();
-    f = chol32(V2, colk);
+    put_view<0>(S1, R, g);
+    f = factor_inv32(V2.p, cs, rs, colk, g + off2, F32_FACTOR);
     if (lane == 0) info[k] = f ? 32 + f : 0;
     if (f) return;
-    put_view<1>(V2, R, g);
-    put_view<0>(S1, R, g);
     if (SOLVE) inv32(V2, rdiag);
   } else {
     inv32(V1, rdiag);

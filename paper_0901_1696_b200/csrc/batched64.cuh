@@ -44,37 +44,94 @@ template <int RS, int CS> struct SV {
   __device__ __forceinline__ SV<CS, RS> t() const { return SV<CS, RS>{p}; }
 };
 
-// 32x32 lower Cholesky of view V by one warp (lane i holds row i).
+// 32x32 lower Cholesky and/or in-place inverse of the smem view
+// p[i*rs + j*cs] (lower triangle only; the slots above it belong to the other
+// RFP block) by one warp.  One non-inlined body serves every view and layout
+// (strides are runtime values touched only at load / store), which keeps the
+// per-SM instruction footprint small with ten matrices in flight.
+//   FACTOR: lane i holds row i in registers; 32 right-looking steps, the
+//           pivot column broadcast through colk (64 entries, double-buffered).
+//           The factor is written back, and to gout (the global image of p)
+//           when given, with lanes along the unit-stride dimension.
+//   INVERT: lane j forms column j of L^-1 by forward substitution, reading
+//           L(i, k) from lane i's registers with shuffles; written in place.
 // Returns 0 or the 1-based failing pivot (warp-uniform).
-template <int RS, int CS>
-__device__ __noinline__ int chol32(SV<RS, CS> V, double* colk) {
-  __builtin_assume(__isShared(V.p));
+enum { F32_FACTOR = 1, F32_INVERT = 2 };
+__device__ __noinline__ int factor_inv32(double* p, int rs, int cs, double* colk, double* gout,
+                                         int mode) {
+  __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(colk));
   const int lane = threadIdx.x & 31;
+  double* prow = p + lane * rs;
   double r[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) r[j] = (j <= lane) ? V(lane, j) : 0.0;
-  int fail = 0;
-  double dkk = shfl(r[0], 0);
+  for (int j = 0; j < 32; ++j) r[j] = (j <= lane) ? prow[j * cs] : 0.0;
+  double myrd;  // 1 / L(lane, lane)
+  if (mode & F32_FACTOR) {
+    int fail = 0;
+    double dkk = shfl(r[0], 0);
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
-    const double rd = rsqrt(dkk);
-    const double lk = (lane == k) ? dkk * rd : rd * r[k];
-    r[k] = lk;
-    double dnext = 0.0;
-    if (k + 1 < 32) dnext = shfl(fma(-lk, lk, r[k + 1]), k + 1);  // lane k+1's new pivot
-    double* cb = colk + (k & 1) * 32;
-    cb[lane] = lk;
-    __syncwarp();
+    for (int k = 0; k < 32; ++k) {
+      if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
+      const double rd = rsqrt(dkk);
+      const double lk = (lane == k) ? dkk * rd : rd * r[k];
+      if (lane == k) myrd = rd;
+      r[k] = lk;
+      double dnext = 0.0;
+      if (k + 1 < 32) dnext = shfl(fma(-lk, lk, r[k + 1]), k + 1);  // lane k+1's new pivot
+      double* cb = colk + (k & 1) * 32;
+      cb[lane] = lk;
+      __syncwarp();
 #pragma unroll
-    for (int j = k + 1; j < 32; ++j) r[j] = fma(-lk, cb[j], r[j]);
-    dkk = dnext;
+      for (int jj = (k + 1) & ~1; jj < 32; jj += 2) {
+        const double2 c = *reinterpret_cast<const double2*>(cb + jj);
+        if (jj >= k + 1) r[jj] = fma(-lk, c.x, r[jj]);
+        r[jj + 1] = fma(-lk, c.y, r[jj + 1]);
+      }
+      dkk = dnext;
+    }
+    if (fail) return fail;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j <= lane) prow[j * cs] = r[j];
+    if (gout) {
+      if (rs == 1) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j <= lane) gout[lane + j * cs] = r[j];
+      } else {
+        __syncwarp();
+        // cs == 1: lane j stores column j
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i)
+          if (i >= lane) gout[i * rs + lane] = p[i * rs + lane];
+      }
+    }
+  } else {
+    myrd = 1.0 / prow[lane * cs];
   }
-  if (fail) return fail;
+  if (mode & F32_INVERT) {
+    const int j = lane;
+    double w[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j <= lane) V(lane, j) = r[j];
+    for (int i = 0; i < 32; ++i) {
+      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        const double l = shfl(r[k], i);
+        if ((k & 3) == 0) s0 = fma(-l, w[k], s0);
+        else if ((k & 3) == 1) s1 = fma(-l, w[k], s1);
+        else if ((k & 3) == 2) s2 = fma(-l, w[k], s2);
+        else s3 = fma(-l, w[k], s3);
+      }
+      w[i] = ((s0 + s1) + (s2 + s3)) * shfl(myrd, i);
+    }
+    __syncwarp();  // every lane is done reading p
+    double* pcol = p + j * cs;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i >= j) pcol[i * rs] = w[i];
+  }
   __syncwarp();
   return 0;
 }
