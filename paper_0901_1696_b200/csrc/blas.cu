@@ -82,45 +82,13 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   __shared__ int fail;
   if (*info) return;
   const int n = (int)A.m;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) fail = 0;
   leaf_load_lower(S, A, n);
   __syncthreads();
-  if (warp == 0) {
-    const int f = chol32_warp(S, 0, scratch);
-    if (lane == 0 && f) fail = f;
-  }
-  __syncthreads();
-  if (fail) {
-    if (threadIdx.x == 0) *info = base + fail;
+  const int f = leaf_factor_inv64(S, Ws, scratch, &fail);
+  if (f) {
+    if (threadIdx.x == 0) *info = base + f;
     return;
   }
-  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
-  __syncthreads();
-  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
-  T acc[8];
-  mm32<T, true, true>(S, 32, 0, Ws, 0, 0, acc);  // L21 = A21 W11^H
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 8; ++q) S[(32 + i) + (jg + q) * LD64] = acc[q];
-  __syncthreads();
-  mm32<T, true, true>(S, 32, 0, S, 32, 0, acc);  // L21 L21^H
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
-  __syncthreads();
-  if (warp == 0) {
-    const int f = chol32_warp(S, 32, scratch);
-    if (lane == 0 && f) fail = 32 + f;
-  }
-  __syncthreads();
-  if (fail) {
-    if (threadIdx.x == 0) *info = base + fail;
-    return;
-  }
-  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
-  __syncthreads();
-  if (W) inv64_block(S, Ws, false, true, scratch);
   __syncthreads();
   leaf_store_lower(S, A, n, false);
   if (W)
@@ -463,9 +431,21 @@ int trsm_rest_upper(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool 
 // runs on a side stream.  Same W slab layout as trsm_rec.
 constexpr i64 TRL_NB = 256;
 
+// SMs' worth of CTAs granted to an off-critical-path update (GemmCap); the
+// rest stay free for the critical path.  RFPK_SIDE_RESERVE = SMs kept free.
+int side_cap() {
+  static const int cap = [] {
+    const char* v = std::getenv("RFPK_SIDE_RESERVE");
+    const int r = v ? std::atoi(v) : 0;
+    return r > 0 ? num_sms() - r : 0;
+  }();
+  return cap;
+}
+
 template <typename T>
 int trsm_rl(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
   const i64 n = Tm.m, N = B.n;
+  const int cap = side_cap();
   cudaStream_t side = la_streams().side[22];
   int rc;
   bool side_busy = false;
@@ -487,6 +467,7 @@ int trsm_rl(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtra
     const i64 r0 = lower ? on + sn : 0, rn = lower ? n - (on + sn) : on;
     if (rn > 0) {
       if ((rc = la_link(c.st, side))) return rc;
+      GemmCap capped(cap);
       if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(r0, o, rn, s), conj, Xk, false, one<T>(),
                         B.sub(r0, 0, rn, N), false, c.info, side)))
         return rc;
@@ -663,6 +644,7 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
         return rc;
       // trailing update of the columns after the next panel, off the critical path
       if ((rc = la_link(c.st, side))) return rc;
+      GemmCap capped(side_cap());
       if ((rc = herk_core(cs, TRI_LOWER, -1.0, P2, false, 1.0, A.sub(o + s + s2, o + s + s2, r2, r2),
                           true)))
         return rc;
@@ -673,7 +655,12 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
   return 0;
 }
 
+static const i64 TILE_MAX = env_int("RFPK_TILE_MAX", 4096);
+
 template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
+  // the dataflow tile kernel (tile_potrf.cu) wherever the critical path rules
+  if (A.m > LEAF && A.m <= TILE_MAX && W && !std::getenv("RFPK_NO_TILE"))
+    return potrf_tiles(c, A, base, W);
   if (A.m < LA_MIN) return potrf_node(c, A, base, W, 0);
   return on_hi_stream(c, [&](Ctx h) {
     if (A.m >= RL_MIN && !std::getenv("RFPK_NO_RL")) return potrf_rl(h, A, base, W);

@@ -37,6 +37,8 @@ int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta
               bool herm);
 // potrf: L L^H (uplo L) / U^H U (uplo U); *info = base + first failing pivot
 template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W = nullptr);
+// dataflow tile Cholesky of a lower view (tile_potrf.cu); W required
+template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
 // stream-ordered workspace for leaf inverses of an order-n triangle
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
 template <typename T> void ws_free(T* p, cudaStream_t st);

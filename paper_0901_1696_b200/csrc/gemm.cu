@@ -1,135 +1,23 @@
 // FP64 / complex128 DMMA GEMM for sm_100a (see gemm.cuh for the contract).
 #include "gemm.cuh"
+#include "dmma.cuh"
 
 #include <cstdlib>
 
 namespace rfpk {
 
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-// D += A(16x4, row) * B(4x8, col); fragments per the PTX m16n8k4 f64 layout
-// (verified on the B200 by tools/probe_mma.cu): a0=(g,t) a1=(g+8,t), b=(t,g),
-// c0..c3 = (g,2t) (g,2t+1) (g+8,2t) (g+8,2t+1) with g = lane/4, t = lane%4.
-__device__ __forceinline__ void dmma16x8x4(double* c, double a0, double a1, double b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
-      "{%0,%1,%2,%3};\n"
-      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a0), "d"(a1), "d"(b));
-}
-
-__device__ __forceinline__ void tri_tile(int mode, int tiles, int& tm, int& tn) {
-  // blockIdx.x enumerates the tiles (ti >= tj) of a lower-triangular tile grid
-  long long b = blockIdx.x;
+__device__ __forceinline__ void tri_tile(int mode, long long b, int& tm, int& tn) {
+  // b enumerates the tiles (ti >= tj) of a lower-triangular tile grid
   int ti = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
   while ((long long)(ti + 1) * (ti + 2) / 2 <= b) ++ti;
   while ((long long)ti * (ti + 1) / 2 > b) --ti;
   int tj = (int)(b - (long long)ti * (ti + 1) / 2);
   if (mode == TRI_LOWER) { tm = ti; tn = tj; } else { tm = tj; tn = ti; }
-  (void)tiles;
 }
 
 __device__ __forceinline__ bool tri_keep(int mode, int row, int col) {
   return mode == TRI_FULL || (mode == TRI_LOWER ? row >= col : row <= col);
 }
-
-__device__ __forceinline__ bool a_keep(int a_tri, int m, int k) {
-  switch (a_tri) {
-    case A_LOWER: return m >= k;
-    case A_UPPER: return m <= k;
-    case A_SLOWER: return m > k;
-    case A_SUPPER: return m < k;
-    default: return true;
-  }
-}
-
-// ------------------------------------------------------------ tile loader
-// Global -> shared copy of one operand tile (R rows along M or N, BK along K)
-// with all addressing hoisted out of the K loop: each thread owns EPT
-// elements at a fixed stride, so a stage costs one 64-bit add + one cp.async
-// per element.  The K tail and the triangular masks (a_tri / b_tri, used only
-// by the in-place triangular leaves) take a separate predicated path.
-// Shared-memory layout of one operand stage.  MN-major operands are stored
-// [k][r] with pitch R + 4 (complex R + 2), K-major ones [r][k] with pitch
-// BK + 4, so both the cp.async stores (contiguous along the global fast
-// dimension) and the m16n8k4 fragment loads are bank-conflict free.
-template <typename T, int R, int BK, bool KM>
-struct SmemLayout {
-  static constexpr int P = KM ? BK + 4 : R + (is_cplx<T>::value ? 2 : 4);
-  static constexpr int SIZE = KM ? R * P : BK * P;  // elements per stage
-  static constexpr int RS = KM ? P : 1;             // stride between rows r
-  static constexpr int KS = KM ? 1 : P;             // stride between k
-};
-
-template <typename T, int R, int BK, int NT, bool KMAJOR>
-struct TileLoader {
-  using L = SmemLayout<T, R, BK, KMAJOR>;
-  static constexpr int EPT = R * BK / NT;
-  static_assert(R * BK % NT == 0, "tile must divide evenly");
-  static constexpr int RE = KMAJOR ? NT / BK : 0;   // row delta per element
-  static constexpr int KE = KMAJOR ? 0 : NT / R;    // k delta per element
-  static constexpr int SSTEP = RE * L::RS + KE * L::KS;
-  const T* ptr;     // element 0 at the current k0
-  i64 step;         // global delta between consecutive elements
-  i64 kstep;        // global delta per stage
-  int r0, k_0;      // tile coords of element 0
-  int soff;         // smem offset of element 0
-  unsigned rowok;   // bit e: row of element e inside the matrix
-
-  __device__ __forceinline__ void init(const T* base, i64 ld, int tile0, int rows, int tid) {
-    if (KMAJOR) { k_0 = tid % BK; r0 = tid / BK; }
-    else { r0 = tid % R; k_0 = tid / R; }
-    // element (r, k) at base + r*ld + k (KMAJOR) or base + r + k*ld
-    ptr = KMAJOR ? base + (i64)(tile0 + r0) * ld + k_0 : base + (tile0 + r0) + (i64)k_0 * ld;
-    step = KMAJOR ? (i64)RE * ld : (i64)KE * ld;
-    kstep = KMAJOR ? (i64)BK : (i64)BK * ld;
-    soff = r0 * L::RS + k_0 * L::KS;
-    rowok = 0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e)
-      if (tile0 + r0 + e * RE < rows) rowok |= 1u << e;
-  }
-
-  // fast path: full K range, no mask
-  __device__ __forceinline__ void load(T* s) const {
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      if (rowok & (1u << e)) {
-        cp_async_t(s + soff + e * SSTEP, ptr + e * step, true);
-      } else {
-        cp_async_t(s + soff + e * SSTEP, ptr, false);
-      }
-    }
-  }
-  // tail / masked path: K bound and triangle mask (tri on (row, k) coords)
-  __device__ __forceinline__ void load_pred(T* s, int k0, int K, int tile0, int tri) const {
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int r = tile0 + r0 + e * RE, k = k0 + k_0 + e * KE;
-      const bool ok = (rowok & (1u << e)) && k < K && a_keep(tri, r, k);
-      cp_async_t(s + soff + e * SSTEP, ok ? ptr + e * step : ptr, ok);
-    }
-  }
-  __device__ __forceinline__ void advance() { ptr += kstep; }
-
-  __device__ __forceinline__ static void cp_async_t(T* s, const T* g, bool ok) {
-    if constexpr (sizeof(T) == 8) cp_async8(s, g, ok);
-    else cp_async16(s, g, ok);
-  }
-};
 
 // ------------------------------------------------------------ kernel
 // One CTA computes a BM x BN tile of C with (BM/WM) x (BN/WN) warps; each warp
@@ -138,9 +26,7 @@ struct TileLoader {
 // conjugation by sign flips.  Padded smem rows (P = BM + 4 real / + 2 complex)
 // make the fragment loads bank-conflict free.
 template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
-                                  (BM * BN <= 64 * 64) ? (is_cplx<T>::value ? 2 : (STAGES <= 3 ? 4 : 3)) : 1)
-    gemm_kernel(GemmArgs<T> g) {
+__device__ __forceinline__ void gemm_tile(const GemmArgs<T>& g, int tm, int tn, T* As, T* Bs) {
   constexpr bool CPLX = is_cplx<T>::value;
   constexpr int WARPS_M = BM / WM;
   constexpr int NT = WARPS_M * (BN / WN) * 32;
@@ -148,13 +34,6 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   using LB = SmemLayout<T, BN, BK, BKM>;
   constexpr int MI = WM / 16, NI = WN / 8;
   constexpr int NACC = CPLX ? 2 : 1;
-  extern __shared__ __align__(16) double smem_d[];
-  T* As = reinterpret_cast<T*>(smem_d);
-  T* Bs = As + STAGES * LA::SIZE;
-  if (g.skip && *g.skip) return;
-  int tm, tn;
-  if (MODE == TRI_FULL) { tm = blockIdx.x; tn = blockIdx.y; }
-  else tri_tile(MODE, g.tiles_m, tm, tn);
   const int m0 = tm * BM, n0 = tn * BN;
   const int M = g.M, N = g.N, K = g.K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -292,6 +171,24 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   }
 }
 
+template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
+                                  (BM * BN <= 64 * 64) ? (is_cplx<T>::value ? 2 : (STAGES <= 3 ? 4 : 3)) : 1)
+    gemm_kernel(GemmArgs<T> g) {
+  using LA = SmemLayout<T, BM, BK, AK>;
+  extern __shared__ __align__(16) double smem_d[];
+  T* As = reinterpret_cast<T*>(smem_d);
+  T* Bs = As + STAGES * LA::SIZE;
+  if (g.skip && *g.skip) return;
+  for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    int tm, tn;
+    if (MODE == TRI_FULL) { tm = (int)(t % g.tiles_m); tn = (int)(t / g.tiles_m); }
+    else tri_tile(MODE, t, tm, tn);
+    gemm_tile<T, BM, BN, BK, WM, WN, STAGES, AK, BKM, MODE>(g, tm, tn, As, Bs);
+    if (t + gridDim.x < g.ntiles) __syncthreads();  // smem stages are reused
+  }
+}
+
 // ------------------------------------------------------------ scale kernel
 template <typename T>
 __global__ void scale_kernel(View<T> C, T beta, int mode, int herm_diag, const int* skip) {
@@ -372,21 +269,19 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
                           (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
                           sizeof(T);
   auto kern = gemm_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
-  static bool configured = false;
-  if (!configured) {
+  static int per_sm = [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, smem);
+    return nb > 0 ? nb : 1;
+  }();
   const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   GemmArgs<T> g = a;
   g.tiles_m = tm;
-  if (MODE == TRI_FULL) {
-    dim3 grid(tm, tn);
-    kern<<<grid, NT, smem, st>>>(g);
-  } else {
-    long long nb = (long long)tm * (tm + 1) / 2;
-    kern<<<(unsigned)nb, NT, smem, st>>>(g);
-  }
+  g.ntiles = MODE == TRI_FULL ? (long long)tm * tn : (long long)tm * (tm + 1) / 2;
+  long long grid = g.ntiles;
+  if (a.ntiles > 0 && grid > a.ntiles * per_sm) grid = a.ntiles * per_sm;  // GemmCap (SMs)
+  kern<<<(unsigned)grid, NT, smem, st>>>(g);
   RFPK_CHECK_LAUNCH();
   return 0;
 }
@@ -411,6 +306,13 @@ int launch_mode(const GemmArgs<T>& a, int mode, bool ak, bool bk, cudaStream_t s
 }
 
 }  // namespace
+
+namespace {
+thread_local int tl_cta_cap = 0;
+}
+int gemm_cta_cap() { return tl_cta_cap; }
+GemmCap::GemmCap(int n) : prev(tl_cta_cap) { tl_cta_cap = n; }
+GemmCap::~GemmCap() { tl_cta_cap = prev; }
 
 template <typename T>
 int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T beta,
@@ -452,6 +354,7 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
   g.herm_diag = herm_diag ? 1 : 0;
   g.skip = skip;
   g.tiles_m = 0;
+  g.ntiles = gemm_cta_cap();  // launch_one turns this into the tile count
   g.a_tri = transposed ? A_FULL : a_tri;
   g.b_tri = transposed ? a_tri : A_FULL;
   // operand "K-major": A contiguous along K  <=> la.kmajor; for B, B^T (N x K)

@@ -88,23 +88,26 @@ __device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
   for (int j = 0; j < 32; ++j) r[j] = S[(off + lane) + (off + j) * LD64];
   int fail = 0;
   double dkk = shfl(sc_re(r[0]), 0);
+  double rd = rsqrt(dkk);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
-    const double rd = rsqrt_nr(dkk);
     const T lk = (lane == k) ? sc_from<T>(dkk * rd) : rd * r[k];
     r[k] = lk;
+    // the next pivot straight from lane k+1's own registers (its update with
+    // its own lk); its rsqrt is issued before this step's trailing update so
+    // the two overlap -- the serial chain per step is mul -> fma -> shfl ->
+    // rsqrt, everything else runs beside it
+    double dnext = 1.0;
+    if (k + 1 < 32) dnext = shfl(sc_re(fnmac(lk, conj_(lk), r[k + 1])), k + 1);
     T* cb = colk + (k & 1) * 32;  // double-buffered column broadcast
     cb[lane] = conj_(lk);
     __syncwarp();
-    if (k + 1 < 32) {
-      // look-ahead: the next pivot's row first, so its broadcast overlaps
-      // the rest of this step's update
-      r[k + 1] = fnmac(lk, cb[k + 1], r[k + 1]);
-      dkk = shfl(sc_re(r[k + 1]), k + 1);
-    }
+    const double rd_next = rsqrt(dnext);
 #pragma unroll
-    for (int j = k + 2; j < 32; ++j) r[j] = fnmac(lk, cb[j], r[j]);
+    for (int j = k + 1; j < 32; ++j) r[j] = fnmac(lk, cb[j], r[j]);
+    dkk = dnext;
+    rd = rd_next;
   }
   if (fail) return fail;
 #pragma unroll
@@ -188,6 +191,113 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
     W[(32 + i) + (jg + q) * LD64] = zero_<T>() - acc[q];
     W[i + (32 + jg + q) * LD64] = zero_<T>();
   }
+}
+
+// The whole 64-leaf on 128 threads: S (lower, LD64, identity-padded) is
+// factored in place (S = L, upper part scratch) and, when Ws is given, its
+// inverse formed in Ws (zeros above the diagonal).  Returns 0 or the 1-based
+// failing pivot, uniform over the CTA (s_fail: a __shared__ int).  Callers
+// sync before (S ready) and after.
+__device__ inline int leaf_factor_inv64_rows(double* S, double* Ws, double* scratch, int* s_fail);
+
+template <typename T>
+__device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
+  if constexpr (!is_cplx<T>::value) return leaf_factor_inv64_rows(S, Ws, scratch, s_fail);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) *s_fail = 0;
+  __syncthreads();
+  if (warp == 0) {
+    const int f = chol32_warp(S, 0, scratch);
+    if (lane == 0 && f) *s_fail = f;
+  }
+  __syncthreads();
+  if (*s_fail) return *s_fail;
+  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
+  __syncthreads();
+  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
+  T acc[8];
+  mm32<T, true, true>(S, 32, 0, Ws, 0, 0, acc);  // L21 = A21 W11^H
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) S[(32 + i) + (jg + q) * LD64] = acc[q];
+  __syncthreads();
+  mm32<T, true, true>(S, 32, 0, S, 32, 0, acc);  // L21 L21^H
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
+  __syncthreads();
+  if (warp == 0) {
+    const int f = chol32_warp(S, 32, scratch);
+    if (lane == 0 && f) *s_fail = 32 + f;
+  }
+  __syncthreads();
+  if (*s_fail) return *s_fail;
+  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
+  __syncthreads();
+  inv64_block(S, Ws, false, true, scratch);
+  return 0;
+}
+
+// Real 64 x 64 Cholesky on TWO warps (64 threads): thread r holds row r in
+// registers for all 64 steps, so no 2 x 2 blocking (no inverse / product /
+// second factorization on the critical path).  One named barrier per step:
+// before it, every row publishes its new column entry and row k+1 its next
+// pivot (from its own registers); after it, everyone starts the next rsqrt
+// and applies the rank-1 update.  colk: 128 doubles (double-buffered column);
+// the two pivot slots live in S's unused upper corner.  Returns 0 or the
+// 1-based failing pivot (uniform over the 64 threads).
+__device__ __noinline__ int chol64_rows(double* S, double* colk) {
+  const int r = threadIdx.x & 63;
+  double* dsl = S + 62 * LD64;  // (0, 62) and (0, 63): strictly upper, unused
+  double a[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) a[j] = (j <= r) ? S[r + j * LD64] : 0.0;
+  double d = S[0];
+  double rd = rsqrt(d);
+  int fail = 0;
+#pragma unroll
+  for (int k = 0; k < 64; ++k) {
+    if (!(d > 0.0)) fail = fail ? fail : k + 1;
+    const double lk = (r == k) ? d * rd : rd * a[k];
+    a[k] = lk;
+    double* cb = colk + (k & 1) * 64;
+    cb[r] = lk;
+    if (k + 1 < 64 && r == k + 1) dsl[(k & 1) * LD64] = fma(-lk, lk, a[k + 1]);
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    if (k + 1 < 64) {
+      const double dn = dsl[(k & 1) * LD64];
+      const double rdn = rsqrt(dn);
+#pragma unroll
+      for (int j = k + 1; j < 64; ++j) a[j] = fma(-lk, cb[j], a[j]);
+      d = dn;
+      rd = rdn;
+    }
+  }
+  if (fail) return fail;
+#pragma unroll
+  for (int j = 0; j < 64; ++j)
+    if (j <= r) S[r + j * LD64] = a[j];
+  return 0;
+}
+
+// Real leaf: chol64_rows on warps 0-1, then both 32-inverses at once (warps 0
+// and 1) and W21 = -W22 L21 W11 on all four.  Same contract as
+// leaf_factor_inv64.
+__device__ inline int leaf_factor_inv64_rows(double* S, double* Ws, double* scratch, int* s_fail) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) *s_fail = 0;
+  __syncthreads();
+  if (warp < 2) {
+    const int f = chol64_rows(S, scratch);
+    if (threadIdx.x == 0 && f) *s_fail = f;
+  }
+  __syncthreads();
+  if (*s_fail) return *s_fail;
+  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
+  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
+  __syncthreads();
+  inv64_block(S, Ws, false, true, scratch);
+  return 0;
 }
 
 }  // namespace rfpk

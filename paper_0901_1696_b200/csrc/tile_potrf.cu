@@ -1,0 +1,453 @@
+// Dataflow tile Cholesky: ONE persistent kernel factors a lower view
+// A = L L^H tile by tile (64 x 64 tiles = the 64-leaves of the recursive
+// drivers), with the dependencies tracked on the device instead of by host
+// streams and events.
+//
+// Task (i, j), i >= j, owns tile (i, j).  Tasks are handed out in column-major
+// order (j, then i) by an atomic counter to whichever CTA is free, and each
+// task is left-looking:
+//
+//   acc = sum_{k < j} L(i, k) L(j, k)^H         64-wide chunks, DMMA, 3-stage
+//                                               cp.async pipeline; chunk k is
+//                                               loaded only once done(i, k)
+//                                               and done(j, k) are published
+//   i == j:  L(j, j), W_j = L(j, j)^-1  <- leaf(A(j, j) - acc)     (one CTA)
+//   i >  j:  wait done(j, j);  L(i, j) = (A(i, j) - acc) W_j^H     (DMMA)
+//   publish done(i, j)
+//
+// A task only ever waits on tasks handed out before it, and those are held
+// by running CTAs, so progress never depends on co-residency (no deadlock
+// whatever the grid size or other work on the GPU).  Publication: the CTA's
+// stores, __syncthreads, then one thread's __threadfence + st.release.gpu of
+// the flag; consumption: one thread's ld.acquire.gpu spin, __syncthreads,
+// then the tile reads (cp.async / ld.global.cg from L2).
+//
+// Compared with the stream-scheduled right-looking driver, the critical path
+// per column shrinks to one 64-chunk update + the leaf + one 64x64x64
+// product (no kernel launches, no event round trips), and all other tiles'
+// updates overlap it.  The W_j slabs are those every other driver produces
+// (slab j at W + 64*64*j), so the trsm that follows in pftrf reuses them.
+// Failure: the failing diagonal task writes info = base + pivot and raises
+// an abort flag that every waiting CTA checks (kernels.py:441-442 semantics:
+// the first failing pivot; later tiles are never factored).
+#include "blas.cuh"
+#include "dmma.cuh"
+#include "leaf.cuh"
+
+#include <cstdlib>
+
+namespace rfpk {
+namespace {
+
+constexpr int TP = 64;    // tile order (== LEAF)
+constexpr int TPT = 128;  // threads per CTA (4 warps, 2 x 2 of 32 x 32)
+constexpr int STAGES = 3;
+constexpr int SYNC_HDR = 32;  // ints before the flag array: [0] counter, [1] abort
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// one thread: wait for *f != 0 (true) or an abort (false)
+__device__ bool spin_wait(const int* f, const int* abort) {
+  unsigned ns = 32;
+  for (;;) {
+    if (ld_acquire(f)) return true;
+    if (ld_acquire(abort)) return false;
+    __nanosleep(ns);
+    if (ns < 256) ns *= 2;
+  }
+}
+
+template <typename T> struct TileCfg {
+  static constexpr bool CPLX = is_cplx<T>::value;
+  static constexpr int BK = CPLX ? 8 : 16;
+  static constexpr int SPC = TP / BK;  // k-slices per 64-chunk
+  static constexpr int NACC = CPLX ? 2 : 1;
+};
+
+template <typename T, bool KM> size_t tile_smem_bytes() {
+  using C = TileCfg<T>;
+  using L = SmemLayout<T, TP, C::BK, KM>;
+  const size_t pipe = (size_t)STAGES * 2 * L::SIZE;
+  const size_t leaf = (size_t)2 * TP * LD64 + 128;
+  return (pipe > leaf ? pipe : leaf) * sizeof(T);
+}
+
+template <typename T>
+__device__ __forceinline__ T frag(const double (&acc)[TileCfg<T>::NACC][2][4][4], int mi, int ni,
+                                  int r) {
+  if constexpr (is_cplx<T>::value) return Z{acc[0][mi][ni][r], acc[1][mi][ni][r]};
+  else return acc[0][mi][ni][r];
+}
+
+// acc += X Y^H for 64-wide K from two LD64 shared tiles (rows of X and of Y
+// along M / N): the off-diagonal solve L(i, j) = C W_j^H.
+template <typename T>
+__device__ __forceinline__ void smem_mm_yh(const T* X, const T* Y,
+                                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+  for (int k = 0; k < TP; k += 4) {
+    if constexpr (!is_cplx<T>::value) {
+      double a[2][2], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a[mi][0] = X[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
+        a[mi][1] = X[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = Y[(wn * 32 + ni * 8 + g) + (k + t) * LD64];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], a[mi][0], a[mi][1], b[ni]);
+    } else {
+      double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const Z v0 = X[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
+        const Z v1 = X[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+        ar[mi][0] = v0.x; ai[mi][0] = v0.y; nai[mi][0] = -v0.y;
+        ar[mi][1] = v1.x; ai[mi][1] = v1.y; nai[mi][1] = -v1.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const Z w = Y[(wn * 32 + ni * 8 + g) + (k + t) * LD64];
+        br[ni] = w.x; bi[ni] = -w.y;  // conj
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
+          dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
+          dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
+          dmma16x8x4(acc[1][mi][ni], ai[mi][0], ai[mi][1], br[ni]);
+        }
+    }
+  }
+}
+
+// One task; false = aborted (a factorization failed somewhere).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <typename T, bool KM>
+__device__ bool tile_task(const View<T>& A, T* W, int* info, int base, int* done, int* abort,
+                          int nt, int i, int j, T* sm, int* s_ok, unsigned long long* tr) {
+  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | j); tr[5] = blockIdx.x; }
+  using C = TileCfg<T>;
+  using LA = SmemLayout<T, TP, C::BK, KM>;
+  constexpr int NACC = C::NACC, BK = C::BK, SPC = C::SPC;
+  const int n = (int)A.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
+  T* As = sm;
+  T* Bs = sm + STAGES * LA::SIZE;
+  const i64 ld = KM ? A.rs : A.cs;
+
+  TileLoader<T, TP, BK, TPT, KM> la, lb;
+  la.init(A.p, ld, i * TP, n, tid);
+  lb.init(A.p, ld, j * TP, n, tid);
+  double acc[NACC][2][4][4];
+#pragma unroll
+  for (int c = 0; c < NACC; ++c)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[c][mi][ni][r] = 0.0;
+
+  // chunk kc of both operand panels is final
+  auto ready = [&](int kc) -> bool {
+    if (tid == 0) {
+      bool ok = spin_wait(done + (i64)i * nt + kc, abort);
+      if (ok && i != j) ok = spin_wait(done + (i64)j * nt + kc, abort);
+      *s_ok = ok;
+    }
+    __syncthreads();
+    return *s_ok != 0;
+  };
+  auto load_stage = [&](int stage) {
+    la.load(As + stage * LA::SIZE);
+    lb.load(Bs + stage * LA::SIZE);
+    la.advance();
+    lb.advance();
+  };
+
+  const int KT = j * SPC;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      if (s % SPC == 0 && !ready(s / SPC)) {
+        cp_async_wait<0>();
+        return false;
+      }
+      load_stage(s);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) {
+      if (nk % SPC == 0 && !ready(nk / SPC)) {
+        cp_async_wait<0>();
+        return false;
+      }
+      load_stage(nk % STAGES);
+    }
+    cp_async_commit();
+    const T* as = As + (kt % STAGES) * LA::SIZE + (wm * 32 + gq) * LA::RS + tq * LA::KS;
+    const T* bs = Bs + (kt % STAGES) * LA::SIZE + (wn * 32 + gq) * LA::RS + tq * LA::KS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if constexpr (!C::CPLX) {
+        double af[2][2], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          af[mi][0] = as[kk * LA::KS + (mi * 16) * LA::RS];
+          af[mi][1] = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[kk * LA::KS + (ni * 8) * LA::RS];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], af[mi][0], af[mi][1], bf[ni]);
+      } else {
+        double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const Z v0 = as[kk * LA::KS + (mi * 16) * LA::RS];
+          const Z v1 = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
+          ar[mi][0] = v0.x; ai[mi][0] = v0.y; nai[mi][0] = -v0.y;
+          ar[mi][1] = v1.x; ai[mi][1] = v1.y; nai[mi][1] = -v1.y;
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const Z w = bs[kk * LA::KS + (ni * 8) * LA::RS];
+          br[ni] = w.x; bi[ni] = -w.y;  // L(j, k)^H
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
+            dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
+            dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
+            dmma16x8x4(acc[1][mi][ni], ai[mi][0], ai[mi][1], br[ni]);
+          }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // pipeline buffers are reused below
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
+
+  T* S = sm;
+  T* Ws = S + TP * LD64;
+  T* scr = Ws + TP * LD64;
+  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
+  const int mrows = n - (int)i0 < TP ? n - (int)i0 : TP;
+  if (i == j) {
+    for (int e = tid; e < TP * TP; e += TPT) {
+      const int r = e & 63, c = e >> 6;
+      S[r + c * LD64] = (r == c) ? one_<T>() : zero_<T>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+          if (row < mrows && col <= row)
+            S[row + col * LD64] = *A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r);
+        }
+    __syncthreads();
+    const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
+    if (f) {
+      if (tid == 0) {
+        *info = base + (int)j0 + f;
+        __threadfence();
+        st_release(abort, 1);
+      }
+      return false;
+    }
+    __syncthreads();
+    for (int e = tid; e < TP * TP; e += TPT) {
+      int r, c;
+      if (KM) { c = e & 63; r = e >> 6; }  // lanes along the unit-stride dimension
+      else { r = e & 63; c = e >> 6; }
+      if (r < mrows && c <= r) *A.at(i0 + r, j0 + c) = S[r + c * LD64];
+    }
+    T* w = W + (i64)j * TP * TP;
+    for (int e = tid; e < TP * TP; e += TPT) w[e] = Ws[(e & 63) + (e >> 6) * LD64];
+  } else {
+    if (tid == 0) *s_ok = spin_wait(done + (i64)j * nt + j, abort);
+    __syncthreads();
+    if (!*s_ok) return false;
+    if (tr && threadIdx.x == 0) tr[2] = gtimer();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+          S[row + col * LD64] =
+              row < mrows ? *A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r) : zero_<T>();
+        }
+    const T* w = W + (i64)j * TP * TP;
+    for (int e = tid; e < TP * TP; e += TPT) {
+      if constexpr (is_cplx<T>::value) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(w + e));
+        Ws[(e & 63) + (e >> 6) * LD64] = Z{v.x, v.y};
+      } else {
+        Ws[(e & 63) + (e >> 6) * LD64] = __ldcg(w + e);
+      }
+    }
+    __syncthreads();
+    double x[NACC][2][4][4];
+#pragma unroll
+    for (int c = 0; c < NACC; ++c)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) x[c][mi][ni][r] = 0.0;
+    smem_mm_yh<T>(S, Ws, x);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+          if (row < mrows) *A.at(i0 + row, j0 + col) = frag<T>(x, mi, ni, r);
+        }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(done + (i64)i * nt + j, 1);
+    if (tr) tr[3] = gtimer();
+  }
+  return true;
+}
+
+template <typename T, bool KM>
+__global__ void __launch_bounds__(TPT) tile_potrf_kernel(View<T> A, T* W, int* info, int base,
+                                                         int* sync, int nt,
+                                                         unsigned long long* trace) {
+  extern __shared__ __align__(16) double smem_d[];
+  T* sm = reinterpret_cast<T*>(smem_d);
+  __shared__ int s_task, s_ok;
+  if (*info) return;  // an earlier step of the chain failed
+  int* counter = sync;
+  int* abort = sync + 1;
+  int* done = sync + SYNC_HDR;
+  const long long total = (long long)nt * (nt + 1) / 2;
+  int j = 0;
+  long long cbase = 0;  // index of task (j, j)
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long t = s_task;
+    __syncthreads();
+    if (t >= total) return;
+    while (t >= cbase + (nt - j)) {
+      cbase += nt - j;
+      ++j;
+    }
+    const int i = j + (int)(t - cbase);
+    if (!tile_task<T, KM>(A, W, info, base, done, abort, nt, i, j, sm, &s_ok,
+                          trace ? trace + 8 * t : nullptr))
+      return;
+  }
+}
+
+template <typename T, bool KM>
+int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
+  // RFPK_TILE_TRACE=file: per-task globaltimer stamps (start, acc done, diag
+  // ready, published), tile and CTA -> CSV (debug only; synchronises)
+  static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
+  unsigned long long* trace = nullptr;
+  const long long ntask = (long long)nt * (nt + 1) / 2;
+  if (trace_file) {
+    cudaMallocManaged(&trace, ntask * 8 * sizeof(unsigned long long));
+    cudaMemset(trace, 0, ntask * 8 * sizeof(unsigned long long));
+  }
+  auto kern = tile_potrf_kernel<T, KM>;
+  const size_t smem = tile_smem_bytes<T, KM>();
+  static const int per_sm = [&] {  // one per (T, KM) instantiation
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
+    return nb > 0 ? nb : 1;
+  }();
+  const long long tasks = (long long)nt * (nt + 1) / 2;
+  long long grid = (long long)per_sm * num_sms();
+  if (grid > tasks) grid = tasks;
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, W, c.info, base, sync, nt, trace);
+  RFPK_CHECK_LAUNCH();
+  if (trace) {
+    cudaStreamSynchronize(c.st);
+    FILE* f = fopen(trace_file, "a");
+    if (f) {
+      fprintf(f, "# n=%lld nt=%d grid=%lld\n", (long long)A.m, nt, grid);
+      for (long long t = 0; t < ntask; ++t) {
+        const unsigned long long* r = trace + 8 * t;
+        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 16, r[4] & 0xffff, r[5], r[0],
+                r[1], r[2], r[3]);
+      }
+      fclose(f);
+    }
+    cudaFree(trace);
+  }
+  return 0;
+}
+
+}  // namespace
+
+// Factor the lower view A (col- or row-major) with the dataflow kernel.
+// W (leaf-inverse slabs for ceil(n/64) tiles) is required.
+template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
+  const i64 n = A.m;
+  if (n == 0) return 0;
+  if (!W) return -100;
+  const bool km = !(A.rs == 1);
+  if (km && A.cs != 1) return -100;
+  const int nt = (int)((n + TP - 1) / TP);
+  const size_t ints = SYNC_HDR + (size_t)nt * nt;
+  int* sync = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
+  if (e != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  int rc = km ? tile_launch<T, true>(A, W, c, base, sync, nt)
+              : tile_launch<T, false>(A, W, c, base, sync, nt);
+  cudaFreeAsync(sync, c.st);
+  return rc;
+}
+
+template int potrf_tiles<double>(Ctx, View<double>, int, double*);
+template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
+
+}  // namespace rfpk

@@ -64,3 +64,55 @@ extern "C" int run_leaf_phases(int cplx, void* A, long long* tick) {
   }
   return (int)cudaDeviceSynchronize();
 }
+
+// whole leaf (leaf_factor_inv64) timed, and its result written back for checking
+template <typename T>
+__global__ void __launch_bounds__(128) leaf_full(T* A, T* Wout, long long* tick) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  T* Ws = S + 64 * LD64;
+  T* scr = Ws + 64 * LD64;
+  __shared__ int fail;
+  View<T> v{A, 64, 64, 1, 64};
+  leaf_load_lower(S, v, 64);
+  __syncthreads();
+  long long t0 = clock64();
+  int f = leaf_factor_inv64(S, Ws, scr, &fail);
+  __syncthreads();
+  long long t1 = clock64();
+  leaf_store_lower(S, v, 64, false);
+  for (int e = threadIdx.x; e < 4096; e += 128) Wout[e] = Ws[(e & 63) + (e >> 6) * LD64];
+  if (threadIdx.x == 0) { tick[0] = t1 - t0; tick[1] = f; }
+}
+
+extern "C" int run_leaf_full(int cplx, void* A, void* W, long long* tick) {
+  size_t sm = (2 * 64 * 65 + 128) * (cplx ? 16 : 8);
+  if (cplx) {
+    cudaFuncSetAttribute(leaf_full<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    leaf_full<Z><<<1, 128, sm>>>((Z*)A, (Z*)W, tick);
+  } else {
+    cudaFuncSetAttribute(leaf_full<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    leaf_full<double><<<1, 128, sm>>>((double*)A, (double*)W, tick);
+  }
+  return (int)cudaDeviceSynchronize();
+}
+
+__global__ void __launch_bounds__(128) chol64_only(double* A, long long* tick) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);
+  double* scr = S + 2 * 64 * LD64;
+  View<double> v{A, 64, 64, 1, 64};
+  leaf_load_lower(S, v, 64);
+  __syncthreads();
+  long long t0 = clock64();
+  if (threadIdx.x < 64) chol64_rows(S, scr);
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) tick[0] = t1 - t0;
+}
+extern "C" int run_chol64(void* A, long long* tick) {
+  size_t sm = (2 * 64 * 65 + 128) * 8;
+  cudaFuncSetAttribute(chol64_only, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  chol64_only<<<1, 128, sm>>>((double*)A, tick);
+  return (int)cudaDeviceSynchronize();
+}

@@ -188,6 +188,9 @@ if __name__ == "__main__":
                 for t in "NT":
                     rfp_bench(n, u, t, 64)
         rfp_bench(16384, "L", "N", 1024, reps=3)
+    if w == "big":
+        rfp_bench(16384, "L", "N", 1024, reps=3)
+        rfp_bench(4000, "L", "N", 64)
     if w in ("all", "cplx"):
         rfp_bench(6000, "L", "T", 0, do_pftri=True, cplx=True, reps=2)
     if w in ("all", "conv"):
