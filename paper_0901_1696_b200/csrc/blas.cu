@@ -607,6 +607,7 @@ static i64 env_int(const char* name, i64 dflt) {
 }
 static const i64 RL_NB = env_int("RFPK_RL_NB", 0);  // 0: adaptive 128 / 64
 static const i64 RL_MIN = env_int("RFPK_RL_MIN", 1024);
+static const i64 RL_TAIL = env_int("RFPK_RL_TAIL", 4096);  // tile kernel for the last columns
 
 template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
   const i64 n = A.m;
@@ -622,6 +623,12 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
     return (n - o) < nb ? (n - o) : nb;
   };
   for (i64 o = 0, s = 0; o < n; o += s) {
+    // the latency-bound tail goes to the dataflow tile kernel once its
+    // columns have received every trailing update
+    if (n - o <= RL_TAIL && !std::getenv("RFPK_NO_TILE")) {
+      if (side_busy && (rc = la_link(side, c.st))) return rc;
+      return potrf_tiles(c, A.sub(o, o, n - o, n - o), base + (int)o, W + o * 64);
+    }
     s = width(o);
     const i64 rest = n - o - s;
     View<T> Akk = A.sub(o, o, s, s);
@@ -655,7 +662,7 @@ template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
   return 0;
 }
 
-static const i64 TILE_MAX = env_int("RFPK_TILE_MAX", 4096);
+static const i64 TILE_MAX = env_int("RFPK_TILE_MAX", (i64)1 << 40);  // measured: the tile kernel wins at every n
 
 template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
   // the dataflow tile kernel (tile_potrf.cu) wherever the critical path rules

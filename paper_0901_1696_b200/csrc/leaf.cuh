@@ -198,11 +198,8 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
 // inverse formed in Ws (zeros above the diagonal).  Returns 0 or the 1-based
 // failing pivot, uniform over the CTA (s_fail: a __shared__ int).  Callers
 // sync before (S ready) and after.
-__device__ inline int leaf_factor_inv64_rows(double* S, double* Ws, double* scratch, int* s_fail);
-
 template <typename T>
 __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
-  if constexpr (!is_cplx<T>::value) return leaf_factor_inv64_rows(S, Ws, scratch, s_fail);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) *s_fail = 0;
   __syncthreads();
@@ -232,68 +229,6 @@ __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
   }
   __syncthreads();
   if (*s_fail) return *s_fail;
-  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
-  __syncthreads();
-  inv64_block(S, Ws, false, true, scratch);
-  return 0;
-}
-
-// Real 64 x 64 Cholesky on TWO warps (64 threads): thread r holds row r in
-// registers for all 64 steps, so no 2 x 2 blocking (no inverse / product /
-// second factorization on the critical path).  One named barrier per step:
-// before it, every row publishes its new column entry and row k+1 its next
-// pivot (from its own registers); after it, everyone starts the next rsqrt
-// and applies the rank-1 update.  colk: 128 doubles (double-buffered column);
-// the two pivot slots live in S's unused upper corner.  Returns 0 or the
-// 1-based failing pivot (uniform over the 64 threads).
-__device__ __noinline__ int chol64_rows(double* S, double* colk) {
-  const int r = threadIdx.x & 63;
-  double* dsl = S + 62 * LD64;  // (0, 62) and (0, 63): strictly upper, unused
-  double a[64];
-#pragma unroll
-  for (int j = 0; j < 64; ++j) a[j] = (j <= r) ? S[r + j * LD64] : 0.0;
-  double d = S[0];
-  double rd = rsqrt(d);
-  int fail = 0;
-#pragma unroll
-  for (int k = 0; k < 64; ++k) {
-    if (!(d > 0.0)) fail = fail ? fail : k + 1;
-    const double lk = (r == k) ? d * rd : rd * a[k];
-    a[k] = lk;
-    double* cb = colk + (k & 1) * 64;
-    cb[r] = lk;
-    if (k + 1 < 64 && r == k + 1) dsl[(k & 1) * LD64] = fma(-lk, lk, a[k + 1]);
-    asm volatile("bar.sync 1, 64;" ::: "memory");
-    if (k + 1 < 64) {
-      const double dn = dsl[(k & 1) * LD64];
-      const double rdn = rsqrt(dn);
-#pragma unroll
-      for (int j = k + 1; j < 64; ++j) a[j] = fma(-lk, cb[j], a[j]);
-      d = dn;
-      rd = rdn;
-    }
-  }
-  if (fail) return fail;
-#pragma unroll
-  for (int j = 0; j < 64; ++j)
-    if (j <= r) S[r + j * LD64] = a[j];
-  return 0;
-}
-
-// Real leaf: chol64_rows on warps 0-1, then both 32-inverses at once (warps 0
-// and 1) and W21 = -W22 L21 W11 on all four.  Same contract as
-// leaf_factor_inv64.
-__device__ inline int leaf_factor_inv64_rows(double* S, double* Ws, double* scratch, int* s_fail) {
-  const int warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) *s_fail = 0;
-  __syncthreads();
-  if (warp < 2) {
-    const int f = chol64_rows(S, scratch);
-    if (threadIdx.x == 0 && f) *s_fail = f;
-  }
-  __syncthreads();
-  if (*s_fail) return *s_fail;
-  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
   if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
   __syncthreads();
   inv64_block(S, Ws, false, true, scratch);

@@ -97,22 +97,3 @@ extern "C" int run_leaf_full(int cplx, void* A, void* W, long long* tick) {
   return (int)cudaDeviceSynchronize();
 }
 
-__global__ void __launch_bounds__(128) chol64_only(double* A, long long* tick) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* S = reinterpret_cast<double*>(smem_raw);
-  double* scr = S + 2 * 64 * LD64;
-  View<double> v{A, 64, 64, 1, 64};
-  leaf_load_lower(S, v, 64);
-  __syncthreads();
-  long long t0 = clock64();
-  if (threadIdx.x < 64) chol64_rows(S, scr);
-  __syncthreads();
-  long long t1 = clock64();
-  if (threadIdx.x == 0) tick[0] = t1 - t0;
-}
-extern "C" int run_chol64(void* A, long long* tick) {
-  size_t sm = (2 * 64 * 65 + 128) * 8;
-  cudaFuncSetAttribute(chol64_only, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  chol64_only<<<1, 128, sm>>>((double*)A, tick);
-  return (int)cudaDeviceSynchronize();
-}

@@ -22,9 +22,3 @@ for cplx in (0, 1):
     ref = torch.linalg.cholesky(a)
     e1 = float((L - ref).abs().max()); e2 = float((Wm @ L - torch.eye(64, dtype=dt, device="cuda")).abs().max())
     print("full", "cplx" if cplx else "real", "cycles", int(tick[0]), "fail", int(tick[1]), "errL", e1, "errW", e2)
-g = torch.randn(64, 64, dtype=torch.float64, device="cuda"); a = g @ g.t() + 64 * torch.eye(64, dtype=torch.float64, device="cuda")
-tick = torch.zeros(2, dtype=torch.int64, device="cuda")
-for rep in range(3):
-    b = a.clone()
-    lib.run_chol64(ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(tick.data_ptr()))
-print("chol64_rows cycles", int(tick[0]))
