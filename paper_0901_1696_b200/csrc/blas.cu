@@ -21,6 +21,11 @@
 
 namespace rfpk {
 
+static i64 env_int(const char* name, i64 dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+
 // ============================================================ leaf kernels
 
 // Load an m x n view into column-major shared memory s[i + j*ld].
@@ -493,6 +498,12 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
     if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
     W = own;
   }
+  static const i64 tile_min = env_int("RFPK_TILE_TRSM_MIN", 512);
+  if (Tm.m >= tile_min && !std::getenv("RFPK_NO_TILE_TRSM") &&
+      (rc = trsm_tiles(c, lower, conj, Tm, B, (const T*)W, !lower)) != -100) {
+    ws_free(own, c.st);
+    return rc;
+  }
   if (Tm.m >= 1024 && B.n <= 2048 && !std::getenv("RFPK_NO_TRSM_RL"))
     rc = on_hi_stream(c, [&](Ctx h) { return trsm_rl(h, lower, conj, Tm, B, W, !lower); });
   else if (Tm.m >= LA_MIN)
@@ -601,10 +612,6 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
 // where it overlaps the next iteration's panel factorization.  Every 64-leaf
 // is still factored by potf2_inv64 at a 64-aligned offset, so the W slabs are
 // exactly those the recursive trsm (pftrf's S1 solve) expects.
-static i64 env_int(const char* name, i64 dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoll(v) : dflt;
-}
 static const i64 RL_NB = env_int("RFPK_RL_NB", 0);  // 0: adaptive 128 / 64
 static const i64 RL_MIN = env_int("RFPK_RL_MIN", 1024);
 static const i64 RL_TAIL = env_int("RFPK_RL_TAIL", 4096);  // tile kernel for the last columns

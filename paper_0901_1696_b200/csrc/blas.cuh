@@ -39,6 +39,10 @@ int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta
 template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W = nullptr);
 // dataflow tile Cholesky of a lower view (tile_potrf.cu); W required
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
+// dataflow tile trsm: conj?(Tm) X = B in place (tile_potrf.cu); W = lower-form
+// 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
+template <typename T>
+int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans);
 // stream-ordered workspace for leaf inverses of an order-n triangle
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
 template <typename T> void ws_free(T* p, cudaStream_t st);

@@ -52,12 +52,12 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// one thread: wait for *f != 0 (true) or an abort (false)
+// one thread: wait for *f != 0 (true) or an abort (false; abort may be null)
 __device__ bool spin_wait(const int* f, const int* abort) {
   unsigned ns = 32;
   for (;;) {
     if (ld_acquire(f)) return true;
-    if (ld_acquire(abort)) return false;
+    if (abort && ld_acquire(abort)) return false;
     __nanosleep(ns);
     if (ns < 256) ns *= 2;
   }
@@ -425,7 +425,360 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
   return 0;
 }
 
+// ============================================================ tile trsm
+// conj?(Tm) X = B in place, Tm lower (forward) or upper (backward) in its
+// view, with the 64-block inverses W (lower form; wtrans: the diagonal block
+// of Tm is the TRANSPOSE of slab i, i.e. Tm upper).  Same dataflow scheme:
+// task (i, c) owns the 64 x 64 block X(i, c) (c: 64-column block of B);
+//   acc = sum_{k solved before i} Tm(i, k) X(k, c)   (waits done(k, c))
+//   X(i, c) = W'_i (B(i, c) - acc)                    (DMMA from smem)
+// Tasks go out step-major (forward: i ascending; backward: descending), so
+// every column block's chain of row blocks advances in parallel and all
+// off-chain accumulation overlaps it.
+
+// acc += A B for 64 x 64 LD64 shared tiles (A(r, k) = A[r + k*LD64],
+// B(k, n) = B[k + n*LD64]).
+template <typename T>
+__device__ __forceinline__ void smem_mm_ab(const T* As, const T* Bs,
+                                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+  for (int k = 0; k < TP; k += 4) {
+    if constexpr (!is_cplx<T>::value) {
+      double a[2][2], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a[mi][0] = As[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
+        a[mi][1] = As[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k + t) + (wn * 32 + ni * 8 + g) * LD64];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], a[mi][0], a[mi][1], b[ni]);
+    } else {
+      double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const Z v0 = As[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
+        const Z v1 = As[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+        ar[mi][0] = v0.x; ai[mi][0] = v0.y; nai[mi][0] = -v0.y;
+        ar[mi][1] = v1.x; ai[mi][1] = v1.y; nai[mi][1] = -v1.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const Z w = Bs[(k + t) + (wn * 32 + ni * 8 + g) * LD64];
+        br[ni] = w.x; bi[ni] = w.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
+          dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
+          dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
+          dmma16x8x4(acc[1][mi][ni], ai[mi][0], ai[mi][1], br[ni]);
+        }
+    }
+  }
+}
+
+struct TrsmArgs {
+  int n, nrhs, nb, nc;
+  int lower, conj, wtrans;
+};
+
+template <typename T, bool AK, bool BKM>
+__device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const TrsmArgs& a,
+                          int* done, int i, int c, T* sm, int* s_ok, unsigned long long* tr) {
+  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | c); tr[5] = blockIdx.x; }
+  using C = TileCfg<T>;
+  using LA = SmemLayout<T, TP, C::BK, AK>;
+  using LB = SmemLayout<T, TP, C::BK, BKM>;
+  constexpr int NACC = C::NACC, BK = C::BK, SPC = C::SPC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
+  T* As = sm;
+  T* Bs = sm + STAGES * LA::SIZE;
+  const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
+  const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
+  auto chunk = [&](int q) { return a.lower ? q : a.nb - 1 - q; };
+
+  TileLoader<T, TP, BK, TPT, AK> la;
+  TileLoader<T, TP, BK, TPT, BKM> lb;
+  double acc[NACC][2][4][4];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[q][mi][ni][r] = 0.0;
+
+  int kvalid = TP;  // valid k of the chunk being loaded
+  // wait for X(kk, c) and point the loaders at chunk kk
+  auto open_chunk = [&](int kk) -> bool {
+    if (tid == 0) *s_ok = spin_wait(done + (i64)kk * a.nc + c, nullptr);
+    __syncthreads();
+    const T* ta = AK ? Tm.p + (i64)kk * TP : Tm.p + (i64)kk * TP * Tm.cs;
+    la.init(ta, lda, i * TP, a.n, tid);
+    const T* tb = BKM ? B.p + (i64)kk * TP : B.p + (i64)kk * TP * B.rs;
+    lb.init(tb, ldb, c * TP, a.nrhs, tid);
+    kvalid = a.n - kk * TP < TP ? a.n - kk * TP : TP;
+    return *s_ok != 0;
+  };
+  auto load_stage = [&](int stage, int q) {
+    const int k0 = (q % SPC) * BK;
+    if (kvalid == TP) {
+      la.load(As + stage * LA::SIZE);
+      lb.load(Bs + stage * LB::SIZE);
+    } else {
+      la.load_pred(As + stage * LA::SIZE, k0, kvalid, 0, A_FULL);
+      lb.load_pred(Bs + stage * LB::SIZE, k0, kvalid, 0, A_FULL);
+    }
+    la.advance();
+    lb.advance();
+  };
+
+  const int KT = nprev * SPC;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      if (s % SPC == 0) open_chunk(chunk(s / SPC));
+      load_stage(s, s);
+    }
+    cp_async_commit();
+  }
+  const double sa = (C::CPLX && a.conj) ? -1.0 : 1.0;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) {
+      if (nk % SPC == 0) open_chunk(chunk(nk / SPC));
+      load_stage(nk % STAGES, nk);
+    }
+    cp_async_commit();
+    const T* as = As + (kt % STAGES) * LA::SIZE + (wm * 32 + gq) * LA::RS + tq * LA::KS;
+    const T* bs = Bs + (kt % STAGES) * LB::SIZE + (wn * 32 + gq) * LB::RS + tq * LB::KS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if constexpr (!C::CPLX) {
+        double af[2][2], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          af[mi][0] = as[kk * LA::KS + (mi * 16) * LA::RS];
+          af[mi][1] = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[kk * LB::KS + (ni * 8) * LB::RS];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], af[mi][0], af[mi][1], bf[ni]);
+      } else {
+        double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const Z v0 = as[kk * LA::KS + (mi * 16) * LA::RS];
+          const Z v1 = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
+          ar[mi][0] = v0.x; ai[mi][0] = sa * v0.y; nai[mi][0] = -ai[mi][0];
+          ar[mi][1] = v1.x; ai[mi][1] = sa * v1.y; nai[mi][1] = -ai[mi][1];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const Z w = bs[kk * LB::KS + (ni * 8) * LB::RS];
+          br[ni] = w.x; bi[ni] = w.y;
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
+            dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
+            dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
+            dmma16x8x4(acc[1][mi][ni], ai[mi][0], ai[mi][1], br[ni]);
+          }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (nprev > 0 && !*s_ok) return false;
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
+
+  // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
+  T* S = sm;
+  T* Ws = S + TP * LD64;
+  const i64 i0 = (i64)i * TP, c0 = (i64)c * TP;
+  const int mrows = a.n - (int)i0 < TP ? a.n - (int)i0 : TP;
+  const int ncols = a.nrhs - (int)c0 < TP ? a.nrhs - (int)c0 : TP;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+        S[row + col * LD64] = (row < mrows && col < ncols)
+                                  ? *B.at(i0 + row, c0 + col) - frag<T>(acc, mi, ni, r)
+                                  : zero_<T>();
+      }
+  const T* w = W + (i64)i * TP * TP;
+  for (int e = tid; e < TP * TP; e += TPT) {
+    const int r = e & 63, k = e >> 6;
+    T v;
+    if constexpr (is_cplx<T>::value) {
+      const double2 d = __ldcg(reinterpret_cast<const double2*>(w + e));
+      v = Z{d.x, d.y};
+    } else {
+      v = __ldcg(w + e);
+    }
+    if (a.conj) v = conj_(v);
+    if (a.wtrans) Ws[k + r * LD64] = v;  // W'(k, r) = W(r, k)
+    else Ws[r + k * LD64] = v;
+  }
+  __syncthreads();
+  double x[NACC][2][4][4];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) x[q][mi][ni][r] = 0.0;
+  smem_mm_ab<T>(Ws, S, x);
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+        if (row < mrows && col < ncols) *B.at(i0 + row, c0 + col) = frag<T>(x, mi, ni, r);
+      }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(done + (i64)i * a.nc + c, 1);
+    if (tr) tr[3] = gtimer();
+  }
+  return true;
+}
+
+template <typename T, bool AK, bool BKM>
+__global__ void __launch_bounds__(TPT) tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
+                                                        TrsmArgs a, int* sync, const int* info,
+                                                        unsigned long long* trace) {
+  extern __shared__ __align__(16) double smem_d[];
+  T* sm = reinterpret_cast<T*>(smem_d);
+  __shared__ int s_task, s_ok;
+  if (info && *info) return;
+  int* counter = sync;
+  int* done = sync + SYNC_HDR;
+  const long long total = (long long)a.nb * a.nc;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long t = s_task;
+    __syncthreads();
+    if (t >= total) return;
+    const int step = (int)(t / a.nc), c = (int)(t % a.nc);
+    const int i = a.lower ? step : a.nb - 1 - step;
+    if (!trsm_task<T, AK, BKM>(Tm, B, W, a, done, i, c, sm, &s_ok, trace ? trace + 8 * t : nullptr))
+      return;
+  }
+}
+
+template <typename T, bool AK, bool BKM> size_t trsm_smem_bytes() {
+  using C = TileCfg<T>;
+  const size_t pipe = (size_t)STAGES * (SmemLayout<T, TP, C::BK, AK>::SIZE +
+                                        SmemLayout<T, TP, C::BK, BKM>::SIZE);
+  const size_t tiles = (size_t)2 * TP * LD64;
+  return (pipe > tiles ? pipe : tiles) * sizeof(T);
+}
+
+template <typename T, bool AK, bool BKM>
+int trsm_launch(View<T> Tm, View<T> B, const T* W, const TrsmArgs& a, int* sync, Ctx c) {
+  auto kern = tile_trsm_kernel<T, AK, BKM>;
+  const size_t smem = trsm_smem_bytes<T, AK, BKM>();
+  static const int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
+    return nb > 0 ? nb : 1;
+  }();
+  const long long tasks = (long long)a.nb * a.nc;
+  long long grid = (long long)per_sm * num_sms();
+  if (grid > tasks) grid = tasks;
+  static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
+  unsigned long long* trace = nullptr;
+  if (trace_file) {
+    cudaMallocManaged(&trace, tasks * 8 * sizeof(unsigned long long));
+    cudaMemset(trace, 0, tasks * 8 * sizeof(unsigned long long));
+  }
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(Tm, B, W, a, sync, c.info, trace);
+  RFPK_CHECK_LAUNCH();
+  if (trace) {
+    cudaStreamSynchronize(c.st);
+    FILE* f = fopen(trace_file, "a");
+    if (f) {
+      fprintf(f, "# trsm n=%d nrhs=%d grid=%lld\n", a.n, a.nrhs, grid);
+      for (long long t = 0; t < tasks; ++t) {
+        const unsigned long long* r = trace + 8 * t;
+        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 16, r[4] & 0xffff, r[5], r[0],
+                r[1], r[2], r[3]);
+      }
+      fclose(f);
+    }
+    cudaFree(trace);
+  }
+  return 0;
+}
+
 }  // namespace
+
+// conj?(Tm) X = B in place with the dataflow kernel (W: lower-form 64-block
+// inverses; wtrans for Tm upper).  Returns -100 for unsupported strides.
+template <typename T>
+int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans) {
+  const i64 n = Tm.m;
+  if (n == 0 || B.n == 0) return 0;
+  const bool ak = !(Tm.rs == 1);
+  if (ak && Tm.cs != 1) return -100;
+  if (!(B.rs == 1 || B.cs == 1 || B.n == 1)) return -100;
+  TrsmArgs a;
+  a.n = (int)n;
+  a.nrhs = (int)B.n;
+  a.nb = (int)((n + TP - 1) / TP);
+  a.nc = (int)((B.n + TP - 1) / TP);
+  a.lower = lower ? 1 : 0;
+  a.conj = conj ? 1 : 0;
+  a.wtrans = wtrans ? 1 : 0;
+  const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
+  int* sync = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
+  if (e != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  // B operand = X^T (nrhs x K): K-major when B is column-major
+  const bool bkm = B.rs == 1;
+  int rc;
+  if (ak) rc = bkm ? trsm_launch<T, true, true>(Tm, B, W, a, sync, c)
+                   : trsm_launch<T, true, false>(Tm, B, W, a, sync, c);
+  else rc = bkm ? trsm_launch<T, false, true>(Tm, B, W, a, sync, c)
+                : trsm_launch<T, false, false>(Tm, B, W, a, sync, c);
+  cudaFreeAsync(sync, c.st);
+  return rc;
+}
+
+template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, const double*, bool);
+template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool);
 
 // Factor the lower view A (col- or row-major) with the dataflow kernel.
 // W (leaf-inverse slabs for ceil(n/64) tiles) is required.
