@@ -303,16 +303,18 @@ def run_b200(args, rank, world, local):
     r = a @ x - rhs0
     resid = float(r.norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
 
-    # dominant kernel: the SYRK/HERK T2 <- T2 - S1^T S1 of pftrf (n2 x n2, k = n1),
-    # timed alone through the C ABI on the live RFP views with CUDA events
-    off_t2, off_s1 = 0, desc.n1 + desc.shift
+    # dominant kernel: tile_trsm_kernel (the dataflow trsm).  Its largest launch
+    # is pftrf's S1 <- S1 T1^-H (conj(T1) X = S1^T, 8192 x 8192 triangle, 8192
+    # right-hand sides); it also runs the four pftrs solves.  Timed alone through
+    # the C ABI on the live factored RFP views, CUDA events on the launch stream.
     ld = desc.ldar
-    kern_flops = desc.n2 * (desc.n2 + 1) * desc.n1
-    t2p = work.data_ptr() + 8 * ((1 - desc.shift) * ld)
-    s1p = work.data_ptr() + 8 * off_s1
+    kern_flops = desc.n1 * desc.n1 * desc.n2  # m^2 n for a triangular solve
+    t1p = work.data_ptr() + 8 * desc.shift
+    s1p = work.data_ptr() + 8 * (desc.n1 + desc.shift)
 
     def dom():
-        lib.rfpk_dsyrk(b"U", b"C", -1.0, s1p, desc.n2, desc.n1, 1, ld, 1.0, t2p, desc.n2, 1, ld, sh)
+        lib.rfpk_dtrsm(b"R", b"L", b"C", b"N", 1.0, t1p, desc.n1, 1, ld, s1p, desc.n2, desc.n1,
+                       1, ld, info.data_ptr(), sh)
 
     dom()
     torch.cuda.synchronize()
@@ -383,11 +385,13 @@ def run_b200(args, rank, world, local):
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "fraction_of_fp64_nominal": value / 1e3 / NOMINAL_FP64_TFLOPS,
         "fraction_of_fp64_measured_dgemm": value / 1e3 / dgemm_tflops,
-        "roofline": {"bound": "tensor", "kernel": "gemm_kernel TRI (SYRK T2 -= S1^T S1, 8192x8192, k=8192)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "tile_trsm_kernel (pftrf S1 <- S1 T1^-H: 8192x8192 triangle, 8192 RHS)",
                      "achieved": k_tflops, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
                      "frac": k_tflops / NOMINAL_FP64_TFLOPS,
-                     "traffic": ncu_traffic("syrk_T2_n16384_LN"),
-                     "algorithmic_bytes": 8 * (desc.n2 * desc.n1 + desc.n2 * (desc.n2 + 1)),
+                     "algorithmic_flops": kern_flops, "ms_per_launch": kms,
+                     "traffic": ncu_traffic("trsm_S1_n16384_LN"),
+                     "algorithmic_bytes": 8 * (desc.n1 * (desc.n1 + 1) // 2 + 2 * desc.n1 * desc.n2),
                      "peak_source": "nominal FP64 DMMA (MEASURED_PEAKS.json has no FP64 figure); "
                                     f"measured cuBLAS DGEMM here: {dgemm_tflops:.2f} TFLOP/s"},
         "residual_scaled": resid,

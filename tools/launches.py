@@ -10,8 +10,8 @@ for r in rows:
     v = float(r[vi].replace(",", "")); u = r[ui]
     us = v / 1000 if u in ("nsecond", "ns") else (v if u == "usecond" else v * 1000)
     name = r[ki]
-    m = re.match(r"(void )?(rfpk::)?([\w]+)", name)
-    key = m.group(3) if m else name[:40]
+    base = re.sub(r"^void ", "", name).replace("<unnamed>::", "").split("(")[0].split("<")[0]
+    key = base.split("::")[-1] or name[:40]
     if "gemm" in key:
         t = re.search(r"<(\d+), (\d+), (\d+),", name)
         key += f"<{t.group(1)}x{t.group(2)}>" if t else ""
