@@ -134,45 +134,84 @@ __device__ __forceinline__ void smem_mm_yh(const T* X, const T* Y,
   }
 }
 
-// One task; false = aborted (a factorization failed somewhere).
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
-template <typename T, bool KM>
-__device__ bool tile_task(const View<T>& A, T* W, int* info, int base, int* done, int* abort,
-                          int nt, int i, int j, T* sm, int* s_ok, unsigned long long* tr) {
-  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | j); tr[5] = blockIdx.x; }
-  using C = TileCfg<T>;
-  using LA = SmemLayout<T, TP, C::BK, KM>;
-  constexpr int NACC = C::NACC, BK = C::BK, SPC = C::SPC;
-  const int n = (int)A.m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
-  T* As = sm;
-  T* Bs = sm + STAGES * LA::SIZE;
-  const i64 ld = KM ? A.rs : A.cs;
+// ---------------------------------------------------------- task helpers
+// Task kinds of the Cholesky DAG (see potrf_tiles): the chain of diagonal
+// tiles is carried by "super" tasks -- ST(j) finishes tile (j+1, j) AND
+// factors diagonal tile j+1 straight from its own result, so the critical
+// path per column is one 64^3 solve + one 64^3 rank-64 update + the leaf,
+// with no flag round trip between the sub-diagonal tile and the next leaf.
+enum TaskKind : int { TK_DIAG0 = 0, TK_SUPER = 1, TK_NORMAL = 2, TK_PARTIAL = 3 };
 
-  TileLoader<T, TP, BK, TPT, KM> la, lb;
-  la.init(A.p, ld, i * TP, n, tid);
-  lb.init(A.p, ld, j * TP, n, tid);
-  double acc[NACC][2][4][4];
+template <typename T> struct CholCtx {
+  View<T> A;
+  T* W;
+  int* info;
+  int* done;    // nt x nt tile flags
+  int* pready;  // nt flags: diagonal partial sums written
+  int* abort;
+  int base, n, nt;
+};
+
+template <typename T>
+__device__ __forceinline__ void zero_acc(double (&acc)[TileCfg<T>::NACC][2][4][4]) {
 #pragma unroll
-  for (int c = 0; c < NACC; ++c)
+  for (int c = 0; c < TileCfg<T>::NACC; ++c)
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[c][mi][ni][r] = 0.0;
+}
 
-  // chunk kc of both operand panels is final
+// fragment (mi, ni, r) -> tile coordinates
+__device__ __forceinline__ void frag_rc(int mi, int ni, int r, int& row, int& col) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  row = (warp & 1) * 32 + mi * 16 + (lane >> 2) + ((r & 2) ? 8 : 0);
+  col = (warp >> 1) * 32 + ni * 8 + 2 * (lane & 3) + (r & 1);
+}
+
+// one thread publishes a flag after the whole CTA's stores
+__device__ __forceinline__ void publish(int* f) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(f, 1);
+  }
+}
+__device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok) {
+  if (threadIdx.x == 0) *s_ok = spin_wait(f, abort);
+  __syncthreads();
+  return *s_ok != 0;
+}
+
+// acc += sum_{k < kend} L(i, k) L(j, k)^H, chunk k loaded only once tiles
+// (i, k) and (j, k) are published.  3-stage cp.async pipeline; returns false
+// on abort.  Leaves the pipeline drained and the CTA synchronised.
+template <typename T, bool KM>
+__device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, int* s_ok,
+                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+  using C = TileCfg<T>;
+  using LA = SmemLayout<T, TP, C::BK, KM>;
+  constexpr int BK = C::BK, SPC = C::SPC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
+  T* As = sm;
+  T* Bs = sm + STAGES * LA::SIZE;
+  const i64 ld = KM ? X.A.rs : X.A.cs;
+  TileLoader<T, TP, BK, TPT, KM> la, lb;
+  la.init(X.A.p, ld, i * TP, X.n, tid);
+  lb.init(X.A.p, ld, j * TP, X.n, tid);
   auto ready = [&](int kc) -> bool {
     if (tid == 0) {
-      bool ok = spin_wait(done + (i64)i * nt + kc, abort);
-      if (ok && i != j) ok = spin_wait(done + (i64)j * nt + kc, abort);
+      bool ok = spin_wait(X.done + (i64)i * X.nt + kc, X.abort);
+      if (ok && i != j) ok = spin_wait(X.done + (i64)j * X.nt + kc, X.abort);
       *s_ok = ok;
     }
     __syncthreads();
@@ -184,8 +223,7 @@ __device__ bool tile_task(const View<T>& A, T* W, int* info, int base, int* done
     la.advance();
     lb.advance();
   };
-
-  const int KT = j * SPC;
+  const int KT = kend * SPC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
@@ -253,134 +291,249 @@ __device__ bool tile_task(const View<T>& A, T* W, int* info, int base, int* done
     }
   }
   cp_async_wait<0>();
-  __syncthreads();  // pipeline buffers are reused below
-  if (tr && threadIdx.x == 0) tr[1] = gtimer();
-
-  T* S = sm;
-  T* Ws = S + TP * LD64;
-  T* scr = Ws + TP * LD64;
-  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
-  const int mrows = n - (int)i0 < TP ? n - (int)i0 : TP;
-  if (i == j) {
-    for (int e = tid; e < TP * TP; e += TPT) {
-      const int r = e & 63, c = e >> 6;
-      S[r + c * LD64] = (r == c) ? one_<T>() : zero_<T>();
-    }
-    __syncthreads();
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
-          if (row < mrows && col <= row)
-            S[row + col * LD64] = *A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r);
-        }
-    __syncthreads();
-    const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
-    if (f) {
-      if (tid == 0) {
-        *info = base + (int)j0 + f;
-        __threadfence();
-        st_release(abort, 1);
-      }
-      return false;
-    }
-    __syncthreads();
-    for (int e = tid; e < TP * TP; e += TPT) {
-      int r, c;
-      if (KM) { c = e & 63; r = e >> 6; }  // lanes along the unit-stride dimension
-      else { r = e & 63; c = e >> 6; }
-      if (r < mrows && c <= r) *A.at(i0 + r, j0 + c) = S[r + c * LD64];
-    }
-    T* w = W + (i64)j * TP * TP;
-    for (int e = tid; e < TP * TP; e += TPT) w[e] = Ws[(e & 63) + (e >> 6) * LD64];
-  } else {
-    if (tid == 0) *s_ok = spin_wait(done + (i64)j * nt + j, abort);
-    __syncthreads();
-    if (!*s_ok) return false;
-    if (tr && threadIdx.x == 0) tr[2] = gtimer();
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
-          S[row + col * LD64] =
-              row < mrows ? *A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r) : zero_<T>();
-        }
-    const T* w = W + (i64)j * TP * TP;
-    for (int e = tid; e < TP * TP; e += TPT) {
-      if constexpr (is_cplx<T>::value) {
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(w + e));
-        Ws[(e & 63) + (e >> 6) * LD64] = Z{v.x, v.y};
-      } else {
-        Ws[(e & 63) + (e >> 6) * LD64] = __ldcg(w + e);
-      }
-    }
-    __syncthreads();
-    double x[NACC][2][4][4];
-#pragma unroll
-    for (int c = 0; c < NACC; ++c)
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) x[c][mi][ni][r] = 0.0;
-    smem_mm_yh<T>(S, Ws, x);
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
-          if (row < mrows) *A.at(i0 + row, j0 + col) = frag<T>(x, mi, ni, r);
-        }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release(done + (i64)i * nt + j, 1);
-    if (tr) tr[3] = gtimer();
-  }
+  __syncthreads();  // pipeline buffers are reused by the caller
   return true;
 }
 
+// Off-diagonal tile (i, j): X = (A(i, j) - acc) W_j^H into x (registers) and
+// A(i, j); W_j must be published.  Leaves X in smem tile S.
+template <typename T>
+__device__ void solve_tile(const CholCtx<T>& X, int i, int j,
+                           const double (&acc)[TileCfg<T>::NACC][2][4][4], T* S, T* Ws,
+                           double (&x)[TileCfg<T>::NACC][2][4][4]) {
+  const int tid = threadIdx.x;
+  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
+  const int mrows = X.n - (int)i0 < TP ? X.n - (int)i0 : TP;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int row, col;
+        frag_rc(mi, ni, r, row, col);
+        S[row + col * LD64] =
+            row < mrows ? *X.A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r) : zero_<T>();
+      }
+  const T* w = X.W + (i64)j * TP * TP;
+  for (int e = tid; e < TP * TP; e += TPT) {
+    if constexpr (is_cplx<T>::value) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(w + e));
+      Ws[(e & 63) + (e >> 6) * LD64] = Z{v.x, v.y};
+    } else {
+      Ws[(e & 63) + (e >> 6) * LD64] = __ldcg(w + e);
+    }
+  }
+  __syncthreads();
+  zero_acc<T>(x);
+  smem_mm_yh<T>(S, Ws, x);
+  __syncthreads();  // S and Ws fully read
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int row, col;
+        frag_rc(mi, ni, r, row, col);
+        const T v = frag<T>(x, mi, ni, r);
+        S[row + col * LD64] = row < mrows ? v : zero_<T>();
+        if (row < mrows) *X.A.at(i0 + row, j0 + col) = v;
+      }
+}
+
+// Diagonal tile d from S (lower, identity-padded, ready): leaf -> L(d, d)
+// into A and W_d into its slab, then publish done(d, d).  false = failure.
+template <typename T>
+__device__ bool finish_diag(const CholCtx<T>& X, int d, T* S, T* Ws, T* scr, int* s_ok) {
+  const int tid = threadIdx.x;
+  const i64 d0 = (i64)d * TP;
+  const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+  const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
+  if (f) {
+    if (tid == 0) {
+      *X.info = X.base + (int)d0 + f;
+      __threadfence();
+      st_release(X.abort, 1);
+    }
+    return false;
+  }
+  __syncthreads();
+  const bool km = X.A.rs != 1;
+  for (int e = tid; e < TP * TP; e += TPT) {
+    int r, c;
+    if (km) { c = e & 63; r = e >> 6; }  // lanes along the unit-stride dimension
+    else { r = e & 63; c = e >> 6; }
+    if (r < m && c <= r) *X.A.at(d0 + r, d0 + c) = S[r + c * LD64];
+  }
+  T* w = X.W + (i64)d * TP * TP;
+  for (int e = tid; e < TP * TP; e += TPT) w[e] = Ws[(e & 63) + (e >> 6) * LD64];
+  publish(X.done + (i64)d * X.nt + d);
+  return true;
+}
+
+// S <- identity-padded lower part of A(d, d) (read from L2: it may have been
+// written by another CTA)
+template <typename T> __device__ void load_diag(const CholCtx<T>& X, int d, T* S) {
+  const i64 d0 = (i64)d * TP;
+  const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+  for (int e = threadIdx.x; e < TP * TP; e += TPT) {
+    int r, c;
+    if (X.A.rs != 1) { c = e & 63; r = e >> 6; }
+    else { r = e & 63; c = e >> 6; }
+    T v = (r == c) ? one_<T>() : zero_<T>();
+    if (r < m && c < m && c <= r) {
+      const T* src = X.A.at(d0 + r, d0 + c);
+      if constexpr (is_cplx<T>::value) {
+        const double2 q = __ldcg(reinterpret_cast<const double2*>(src));
+        v = Z{q.x, q.y};
+      } else {
+        v = __ldcg(src);
+      }
+    }
+    S[r + c * LD64] = v;
+  }
+}
+
 template <typename T, bool KM>
-__global__ void __launch_bounds__(TPT) tile_potrf_kernel(View<T> A, T* W, int* info, int base,
+__device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int* s_ok,
+                         unsigned long long* tr) {
+  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((kind << 28) | (a << 14) | b); tr[5] = blockIdx.x; }
+  using C = TileCfg<T>;
+  T* S = sm;
+  T* Ws = S + TP * LD64;
+  T* scr = Ws + TP * LD64;
+  double acc[C::NACC][2][4][4];
+  zero_acc<T>(acc);
+  if (kind == TK_DIAG0) {
+    load_diag(X, 0, S);
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+    const bool ok = finish_diag(X, 0, S, Ws, scr, s_ok);
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
+    return ok;
+  }
+  if (kind == TK_PARTIAL) {
+    // A(d, d) <- A(d, d) - sum_{k < d-1} L(d, k) L(d, k)^H  (lower part)
+    const int d = a;
+    if (!accumulate<T, KM>(X, d, d, d - 1, sm, s_ok, acc)) return false;
+    const i64 d0 = (i64)d * TP;
+    const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          int row, col;
+          frag_rc(mi, ni, r, row, col);
+          if (row < m && col <= row) {
+            T* p = X.A.at(d0 + row, d0 + col);
+            *p = *p - frag<T>(acc, mi, ni, r);
+          }
+        }
+    publish(X.pready + d);
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
+    return true;
+  }
+  // TK_NORMAL (i, j) and TK_SUPER (j + 1, j)
+  const int i = a, j = b;
+  if (!accumulate<T, KM>(X, i, j, j, sm, s_ok, acc)) return false;
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
+  if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok)) return false;
+  if (tr && threadIdx.x == 0) tr[2] = gtimer();
+  double x[C::NACC][2][4][4];
+  solve_tile(X, i, j, acc, S, Ws, x);
+  publish(X.done + (i64)i * X.nt + j);
+  if (kind == TK_NORMAL) {
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
+    return true;
+  }
+  // super: factor diagonal tile d = j + 1 from the partial sum and L(d, j)
+  const int d = i;
+  // X (= L(d, j)) stays in S; bring it to Ws so S can take the diagonal
+  for (int e = threadIdx.x; e < TP * TP; e += TPT) {
+    const int r = e & 63, c = e >> 6;
+    Ws[r + c * LD64] = S[r + c * LD64];
+  }
+  __syncthreads();
+  if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
+  load_diag(X, d, S);
+  __syncthreads();
+  zero_acc<T>(x);
+  smem_mm_yh<T>(Ws, Ws, x);  // L(d, j) L(d, j)^H
+  const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int row, col;
+        frag_rc(mi, ni, r, row, col);
+        if (row < m && col <= row) S[row + col * LD64] = S[row + col * LD64] - frag<T>(x, mi, ni, r);
+      }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();  // (overwrites: diag start)
+  const bool ok = finish_diag(X, d, S, Ws, scr, s_ok);
+  if (tr && threadIdx.x == 0) tr[3] = gtimer();
+  return ok;
+}
+
+// Task list: DIAG0, then for g = 0 .. nt-2 the group
+//   [ SUPER(g) = tile (g+1, g) + diag g+1,  NORMAL (i, g) for i = g+2 .. nt-1,
+//     PARTIAL(g+2) (diag g+2 over chunks k <= g) ]
+// Every task depends only on tasks listed before it.
+__host__ __device__ inline long long chol_task_count(int nt) {
+  long long t = nt > 0 ? 1 : 0;
+  for (int g = 0; g + 1 < nt; ++g) t += (g + 2 < nt) ? nt - g : 1;
+  return t;
+}
+
+template <typename T, bool KM>
+__global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
+    tile_potrf_kernel(View<T> A, T* W, int* info, int base,
                                                          int* sync, int nt,
                                                          unsigned long long* trace) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
   if (*info) return;  // an earlier step of the chain failed
-  int* counter = sync;
-  int* abort = sync + 1;
-  int* done = sync + SYNC_HDR;
-  const long long total = (long long)nt * (nt + 1) / 2;
-  int j = 0;
-  long long cbase = 0;  // index of task (j, j)
+  CholCtx<T> X;
+  X.A = A;
+  X.W = W;
+  X.info = info;
+  X.abort = sync + 1;
+  X.done = sync + SYNC_HDR;
+  X.pready = X.done + (i64)nt * nt;
+  X.base = base;
+  X.n = (int)A.m;
+  X.nt = nt;
+  const long long total = chol_task_count(nt);
+  int g = 0;
+  long long gbase = 1;  // task index of SUPER(g)
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    if (threadIdx.x == 0) s_task = atomicAdd(sync, 1);
     __syncthreads();
     const long long t = s_task;
     __syncthreads();
     if (t >= total) return;
-    while (t >= cbase + (nt - j)) {
-      cbase += nt - j;
-      ++j;
+    int kind, a, b;
+    if (t == 0) {
+      kind = TK_DIAG0; a = 0; b = 0;
+    } else {
+      for (;;) {
+        const long long gs = (g + 2 < nt) ? nt - g : 1;
+        if (t < gbase + gs) break;
+        gbase += gs;
+        ++g;
+      }
+      const int o = (int)(t - gbase);
+      if (o == 0) { kind = TK_SUPER; a = g + 1; b = g; }
+      else if (o <= nt - g - 2) { kind = TK_NORMAL; a = g + 1 + o; b = g; }
+      else { kind = TK_PARTIAL; a = g + 2; b = 0; }
     }
-    const int i = j + (int)(t - cbase);
-    if (!tile_task<T, KM>(A, W, info, base, done, abort, nt, i, j, sm, &s_ok,
-                          trace ? trace + 8 * t : nullptr))
-      return;
+    if (!run_task<T, KM>(X, kind, a, b, sm, &s_ok, trace ? trace + 8 * t : nullptr)) return;
   }
 }
 
@@ -390,7 +543,7 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
   // ready, published), tile and CTA -> CSV (debug only; synchronises)
   static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
   unsigned long long* trace = nullptr;
-  const long long ntask = (long long)nt * (nt + 1) / 2;
+  const long long ntask = chol_task_count(nt);
   if (trace_file) {
     cudaMallocManaged(&trace, ntask * 8 * sizeof(unsigned long long));
     cudaMemset(trace, 0, ntask * 8 * sizeof(unsigned long long));
@@ -403,7 +556,7 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
     return nb > 0 ? nb : 1;
   }();
-  const long long tasks = (long long)nt * (nt + 1) / 2;
+  const long long tasks = ntask;
   long long grid = (long long)per_sm * num_sms();
   if (grid > tasks) grid = tasks;
   kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, W, c.info, base, sync, nt, trace);
@@ -415,8 +568,8 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
       fprintf(f, "# n=%lld nt=%d grid=%lld\n", (long long)A.m, nt, grid);
       for (long long t = 0; t < ntask; ++t) {
         const unsigned long long* r = trace + 8 * t;
-        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 16, r[4] & 0xffff, r[5], r[0],
-                r[1], r[2], r[3]);
+        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 28, (r[4] >> 14) & 0x3fff,
+                r[4] & 0x3fff, r[5], r[0], r[1], r[2], r[3]);
       }
       fclose(f);
     }
@@ -789,7 +942,7 @@ template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
   const bool km = !(A.rs == 1);
   if (km && A.cs != 1) return -100;
   const int nt = (int)((n + TP - 1) / TP);
-  const size_t ints = SYNC_HDR + (size_t)nt * nt;
+  const size_t ints = SYNC_HDR + (size_t)nt * nt + nt;  // + the partial-ready flags
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
   if (e != cudaSuccess) return (int)e;
