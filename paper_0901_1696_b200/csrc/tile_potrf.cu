@@ -445,6 +445,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   double x[C::NACC][2][4][4];
   solve_tile(X, i, j, acc, S, Ws, x);
   publish(X.done + (i64)i * X.nt + j);
+  if (tr && threadIdx.x == 0) tr[6] = gtimer();
   if (kind == TK_NORMAL) {
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return true;
@@ -460,6 +461,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
   load_diag(X, d, S);
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[7] = gtimer();
   zero_acc<T>(x);
   smem_mm_yh<T>(Ws, Ws, x);  // L(d, j) L(d, j)^H
   const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
@@ -557,7 +559,11 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
     return nb > 0 ? nb : 1;
   }();
   const long long tasks = ntask;
-  long long grid = (long long)per_sm * num_sms();
+  static const int cap = [] {
+    const char* v = std::getenv("RFPK_TILE_PER_SM");
+    return v ? std::atoi(v) : 0;
+  }();
+  long long grid = (long long)(cap > 0 && cap < per_sm ? cap : per_sm) * num_sms();
   if (grid > tasks) grid = tasks;
   kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, W, c.info, base, sync, nt, trace);
   RFPK_CHECK_LAUNCH();
@@ -568,8 +574,8 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
       fprintf(f, "# n=%lld nt=%d grid=%lld\n", (long long)A.m, nt, grid);
       for (long long t = 0; t < ntask; ++t) {
         const unsigned long long* r = trace + 8 * t;
-        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 28, (r[4] >> 14) & 0x3fff,
-                r[4] & 0x3fff, r[5], r[0], r[1], r[2], r[3]);
+        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 28,
+                (r[4] >> 14) & 0x3fff, r[4] & 0x3fff, r[5], r[0], r[1], r[2], r[3], r[6], r[7]);
       }
       fclose(f);
     }
