@@ -111,6 +111,21 @@ int rfpk_ztftri(char transr, char uplo, char diag, int64_t n, void* arf, int* in
 int rfpk_dpftri(char transr, char uplo, int64_t n, double* arf, int* info, rfpk_stream_t stream);
 int rfpk_zpftri(char transr, char uplo, int64_t n, void* arf, int* info, rfpk_stream_t stream);
 
+/* packed Cholesky ------------------------------------ */
+/* replaces packed.pptrf_ref(p)   packed.py:70-108 -- in place on the
+   column-packed triangle ap (n(n+1)/2 elements, LAPACK 'L'/'U' packing);
+   info (device) = 0 or the 1-based order of the first non-positive leading
+   minor.  Computed through RFP (tpttf -> pftrf -> tfttp) in a workspace. */
+int rfpk_dpptrf(char uplo, int64_t n, double* ap, int* info, rfpk_stream_t stream);
+int rfpk_zpptrf(char uplo, int64_t n, void* ap, int* info, rfpk_stream_t stream);
+/* replaces packed.pptrs_ref(p, b)   packed.py:111-146 -- solve A X = B in
+   place from a packed factor; b is n x nrhs with element (i, j) at
+   b[i*rsb + j*csb] (one of the strides 1) */
+int rfpk_dpptrs(char uplo, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb,
+                int64_t csb, int* info, rfpk_stream_t stream);
+int rfpk_zpptrs(char uplo, int64_t n, int64_t nrhs, const void* ap, void* b, int64_t rsb,
+                int64_t csb, int* info, rfpk_stream_t stream);
+
 /* SURVEY 8(f) rows ------------------------------------------------------- */
 /* replaces rfp.tfsm(transr, side, uplo, trans, diag, m, n, alpha, a, b)
    rfp.py:181-224; a holds the order-m (side L) / order-n (side R) triangle;

@@ -175,6 +175,66 @@ def tfttp(buf, n, uplo, transr):
 # full-format kernels (kernels.py)
 
 
+def pptrf(p, n, uplo):
+    """Unblocked packed Cholesky in place (packed.py:70-108): right-looking
+    rank-1 updates of the packed trailing columns for 'L', left-looking
+    dot-product columns for 'U'.  Returns 0 or the first failing order."""
+    herm = np.iscomplexobj(p)
+    st = list(packed_offsets(n, uplo)) + [n * (n + 1) // 2]
+    if uplo == "L":
+        for j in range(n):
+            d = p[st[j]].real if herm else p[st[j]]
+            if not d > 0:
+                return j + 1
+            d = np.sqrt(d)
+            p[st[j]] = d
+            x = p[st[j] + 1:st[j + 1]]
+            x /= d
+            for c in range(j + 1, n):
+                t = c - j - 1
+                p[st[c]:st[c + 1]] -= (np.conj(x[t]) if herm else x[t]) * x[t:]
+        return 0
+    for j in range(n):
+        col = p[st[j]:st[j + 1]]  # rows 0..j of column j
+        for t in range(j):
+            pc = p[st[t]:st[t + 1]]
+            col[t] = (col[t] - np.vdot(pc[:t], col[:t])) / pc[t]
+        d = col[j].real if herm else col[j]
+        if j:
+            d = d - (np.vdot(col[:j], col[:j]).real if herm else col[:j] @ col[:j])
+        if not d > 0:
+            return j + 1
+        col[j] = np.sqrt(d)
+    return 0
+
+
+def pptrs(p, n, uplo, b):
+    """Forward/backward substitution from a packed factor, in place on b
+    (packed.py:111-146)."""
+    bv = b.reshape(-1, 1) if b.ndim == 1 else b
+    herm = np.iscomplexobj(p)
+    st = list(packed_offsets(n, uplo)) + [n * (n + 1) // 2]
+    cj = (lambda v: np.conj(v)) if herm else (lambda v: v)
+    if uplo == "L":
+        for j in range(n):
+            col = p[st[j]:st[j + 1]]
+            bv[j] /= col[0]
+            bv[j + 1:] -= col[1:, None] * bv[j:j + 1]
+        for j in range(n - 1, -1, -1):
+            col = p[st[j]:st[j + 1]]
+            bv[j] -= cj(col[1:]) @ bv[j + 1:]
+            bv[j] /= cj(col[0])
+        return
+    for j in range(n):
+        col = p[st[j]:st[j + 1]]
+        bv[j] -= cj(col[:j]) @ bv[:j]
+        bv[j] /= cj(col[j])
+    for j in range(n - 1, -1, -1):
+        col = p[st[j]:st[j + 1]]
+        bv[j] /= col[j]
+        bv[:j] -= col[:j, None] * bv[j:j + 1]
+
+
 def _opview(a, trans):
     """op(A) as (view, conjugate?) (kernels.py:78-84 semantics)."""
     if trans == "N":

@@ -50,6 +50,10 @@ SIGNATURES = {
     "rfpk_ztftri": ([_c, _c, _c, _i64, _p, _p, _p], _int),
     "rfpk_dpftri": ([_c, _c, _i64, _p, _p, _p], _int),
     "rfpk_zpftri": ([_c, _c, _i64, _p, _p, _p], _int),
+    "rfpk_dpptrf": ([_c, _i64, _p, _p, _p], _int),
+    "rfpk_zpptrf": ([_c, _i64, _p, _p, _p], _int),
+    "rfpk_dpptrs": ([_c, _i64, _i64, _p, _p, _i64, _i64, _p, _p], _int),
+    "rfpk_zpptrs": ([_c, _i64, _i64, _p, _p, _i64, _i64, _p, _p], _int),
     "rfpk_dtfsm": ([_c, _c, _c, _c, _c, _i64, _i64, _d, _p, _p, _i64, _i64, _p, _p], _int),
     "rfpk_ztfsm": ([_c, _c, _c, _c, _c, _i64, _i64, _d, _d, _p, _p, _i64, _i64, _p, _p], _int),
     "rfpk_dsfrk": ([_c, _c, _c, _i64, _i64, _d, _p, _i64, _i64, _d, _p, _p], _int),

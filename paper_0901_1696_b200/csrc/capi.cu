@@ -173,6 +173,55 @@ namespace rfpk {
 std::atomic<long long> g_launch_count{0};
 }
 
+// ---------------------------------------------------------------- packed Cholesky
+// the reference's Level-2 packed comparator
+// (packed.py:70-146 pptrf_ref / pptrs_ref).  B200 design: the column-packed
+// triangle is converted to RFP (TRANSR='N', the tiled copy kernel) in a
+// stream-ordered workspace, factored / solved there with the RFP drivers,
+// and (pptrf) converted back -- the conversions move 2*nt elements each,
+// negligible next to the n^3/3 factorization.  info = first non-positive
+// leading minor, as pptrf_ref.
+template <typename T>
+int pptrf_t(char uplo, int64_t n, void* ap, int* info, cudaStream_t st) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (n < 0) return -2;
+  if (!info) return -4;
+  if (int rc = reset_info(info, st)) return rc;
+  if (n == 0) return 0;
+  const RfpDesc d = rfp_desc(n, uplo, 'N');
+  T* w = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&w, (size_t)d.nt * sizeof(T), st);
+  if (e != cudaSuccess) return (int)e;
+  const Storage pk{ST_PACKED, 0, d}, rf{ST_RFP, 0, d};
+  int rc = convert<T>(pk, (const T*)ap, rf, w, false, st);
+  if (!rc) rc = pftrf<T>(Ctx{st, info}, d, w);
+  if (!rc) rc = convert<T>(rf, w, pk, (T*)ap, false, st);
+  cudaFreeAsync(w, st);
+  return rc;
+}
+template <typename T>
+int pptrs_t(char uplo, int64_t n, int64_t nrhs, const void* ap, void* b, int64_t rsb,
+            int64_t csb, int* info, cudaStream_t st) {
+  uplo = up(uplo);
+  if (!one_of(uplo, "LU")) return -1;
+  if (n < 0) return -2;
+  if (nrhs < 0) return -3;
+  if (!unit_stride(n, nrhs, rsb, csb)) return -6;
+  if (!info) return -8;
+  if (int rc = reset_info(info, st)) return rc;
+  if (n == 0 || nrhs == 0) return 0;
+  const RfpDesc d = rfp_desc(n, uplo, 'N');
+  T* w = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&w, (size_t)d.nt * sizeof(T), st);
+  if (e != cudaSuccess) return (int)e;
+  const Storage pk{ST_PACKED, 0, d}, rf{ST_RFP, 0, d};
+  int rc = convert<T>(pk, (const T*)ap, rf, w, false, st);
+  if (!rc) rc = pftrs<T>(Ctx{st, info}, d, w, V<T>(b, n, nrhs, rsb, csb));
+  cudaFreeAsync(w, st);
+  return rc;
+}
+
 extern "C" {
 
 const char* rfpk_version(void) { return "rfpk_b200 0.1 (sm_100a, FP64 DMMA)"; }
@@ -221,6 +270,11 @@ int rfpk_dtftri(char t, char u, char d, int64_t n, double* arf, int* info, rfpk_
 int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_stream_t s) { return tftri_t<Z>(t, u, d, n, arf, info, S(s)); }
 int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftri_t<double>(t, u, n, arf, info, S(s)); }
 int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftri_t<Z>(t, u, n, arf, info, S(s)); }
+
+int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }
+int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { return pptrf_t<Z>(u, n, ap, info, S(s)); }
+int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
+int rfpk_zpptrs(char u, int64_t n, int64_t nrhs, const void* ap, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<Z>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
 
 // ---------------------------------------------------------------- SURVEY 8(f) rows
 static int tfsm_check(char& transr, char& side, char& uplo, char& trans, char& diag, int64_t m,

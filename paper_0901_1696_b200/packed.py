@@ -3,9 +3,12 @@ reference).  ``pack``/``unpack`` are the plumbing that produces the packed
 input of BASELINE config 2's packed round trip; each is one launch of the
 tiled copy kernel (C ABI ``rfpk_?trttp`` / ``rfpk_?tpttr``).
 
-The reference's Level-2 packed Cholesky (``pptrf_ref``/``pptrs_ref``) and
-SPD generator are comparators outside the RFPF hot path (SURVEY 2, rows
-5b/5c) and are not rebuilt here.
+``pptrf_ref``/``pptrs_ref`` are the reference's Level-2 packed Cholesky
+comparator (packed.py:70-146).  Here they keep the
+reference's names, arguments, return values and errors, but compute through
+RFP on the device (C ABI ``rfpk_?pptrf`` / ``rfpk_?pptrs``: packed -> RFP ->
+pftrf/pftrs -> packed), so the packed path runs on the same tensor-core
+kernels.  The SPD generator (``spd_generate``) stays out of scope.
 """
 
 from __future__ import annotations
@@ -14,8 +17,9 @@ import torch
 
 from . import _capi
 from .convert import PackedTriangle, _call, _colmajor, _ld, _prefix, as_device
+from .rfp import _info, _rhs_view
 
-__all__ = ["pack", "unpack"]
+__all__ = ["pack", "unpack", "pptrf_ref", "pptrs_ref"]
 
 
 def pack(a, uplo: str) -> PackedTriangle:
@@ -50,3 +54,48 @@ def unpack(p: PackedTriangle, ld=None) -> torch.Tensor:
     _call(f"rfpk_{_prefix(p.dtype)}tpttr", _capi.flag(p.uplo), n, p.data.data_ptr(),
           out.data_ptr(), max(ld, 1), _capi.stream_handle(p.data.device))
     return out
+
+
+def pptrf_ref(p: PackedTriangle) -> int:
+    """Packed Cholesky factorization, in place (packed.py:70-108).  Returns 0
+    or the 1-based order of the first non-positive leading minor."""
+    if p.n == 0:
+        return 0
+    info = _info(p.data.device)
+    _call(f"rfpk_{_prefix(p.dtype)}pptrf", _capi.flag(p.uplo), p.n, p.data.data_ptr(),
+          info.data_ptr(), _capi.stream_handle(p.data.device))
+    return int(info.item())
+
+
+class _PackedOrder:
+    """The two attributes of an RfpTriangle that ``rfp._rhs_view`` reads."""
+
+    def __init__(self, p: PackedTriangle):
+        self.desc = type("D", (), {"n": p.n})()
+        self.dtype = p.dtype
+
+
+def pptrs_ref(p: PackedTriangle, b) -> None:
+    """Solve ``A @ X = B`` in place from a packed Cholesky factor
+    (packed.py:111-146); ``b`` is (n,) or (n, nrhs), device or host."""
+    bv, foreign = _rhs_view(_PackedOrder(p), b)
+    if p.n == 0 or bv.shape[1] == 0:
+        return
+    work = bv
+    data = p.data
+    if bv.dtype not in (torch.float64, torch.complex128) or (bv.stride(0) != 1 and bv.stride(1) != 1):
+        work = bv.to(torch.complex128 if bv.is_complex() else torch.float64).t().contiguous().t()
+    if work.is_complex() and not data.is_complex():
+        data = data.to(torch.complex128)
+    info = _info(work.device)
+    _call(f"rfpk_{_prefix(data.dtype)}pptrs", _capi.flag(p.uplo), p.n, work.shape[1],
+          data.data_ptr(), work.data_ptr(), work.stride(0), work.stride(1), info.data_ptr(),
+          _capi.stream_handle(work.device))
+    if work is not bv:
+        bv.copy_(work)
+    if foreign is not None:
+        host = bv.reshape(tuple(foreign.shape)).cpu()
+        if isinstance(foreign, torch.Tensor):
+            foreign.copy_(host)
+        else:
+            foreign[...] = host.numpy()

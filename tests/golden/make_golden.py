@@ -103,6 +103,25 @@ def next_rows(out, n, uplo, transr, cplx):
     out[f"lansf_{key}_rfp"] = r.data.copy()
 
 
+def packed_chol(out, n, uplo, cplx, fail_k=None):
+    """pptrf_ref / pptrs_ref (packed.py:70-146)."""
+    key = f"pp_{'c128' if cplx else 'f64'}_{uplo}_n{n}" + (f"_k{fail_k}" if fail_k is not None else "")
+    a = spd(n, 555 + n, cplx)
+    if fail_k is not None:
+        a[fail_k, fail_k] = -1.0
+    p = packed.pack(a, uplo)
+    out[key + "_P"] = p.data.copy()
+    f = p.copy()
+    out[key + "_info"] = np.array(packed.pptrf_ref(f))
+    out[key + "_F"] = f.data.copy()
+    if fail_k is None:
+        b = rhs(n, 4, 555 + n, cplx)
+        x = b.copy(order="F")
+        packed.pptrs_ref(f, x)
+        out[key + "_B"] = b
+        out[key + "_X"] = x
+
+
 def failing(out, n, uplo, transr, cplx, k, nan=False):
     """A = I + small symmetric noise with pivot k (0-based) made negative."""
     a = np.eye(n, dtype=np.complex128 if cplx else np.float64)
@@ -140,6 +159,11 @@ def main():
                 for n, k in [(7, 2), (7, 5), (40, 3), (40, 33), (41, 20), (41, 21)]:
                     failing(out, n, uplo, transr, cplx, k)
                 failing(out, 40, uplo, transr, cplx, 25, nan=True)
+    for cplx in (False, True):
+        for uplo in "LU":
+            for n in (0, 1, 2, 5, 17, 40, 41, 130):
+                packed_chol(out, n, uplo, cplx)
+            packed_chol(out, 41, uplo, cplx, fail_k=20)
     # SPEC.md:269-271 / :310 known answers
     two = convert.trttf(np.array([[4.0, 0.0], [2.0, 5.0]]), "L", "N")
     out["spec_n2_rfp"] = two.data.copy()

@@ -434,3 +434,48 @@ def test_next_rows_large_vs_oracle(P):
     with pytest.raises(O.OracleSingular) as eo:
         O.tfsm(f, n, "L", "N", "L", "N", "N", 1.0, np.ones((n, 2), order="F"))
     assert e.value.index == eo.value.index == ds.n1 + 11
+
+
+# ---------------------------------------------------------------- SURVEY 8(f) row 4
+def test_packed_cholesky_vs_reference(P, golden):
+    """pptrf_ref / pptrs_ref (packed.py:70-146) through the C ABI against the
+    reference's own outputs: factors and solutions within 1e-10, failure
+    index identical; host RHS solved in place."""
+    conv, packed = P.convert, P.packed
+    keys = sorted(k[:-5] for k in golden if k.startswith("pp_") and k.endswith("_info"))
+    assert len(keys) >= 30
+    for key in keys:
+        _, dt, uplo, nn, *rest = key.split("_")
+        n = int(nn[1:])
+        p = conv.PackedTriangle(golden[key + "_P"].copy(), n, uplo)
+        assert packed.pptrf_ref(p) == int(golden[key + "_info"]), key
+        if rest:
+            continue
+        assert rel(p.data, golden[key + "_F"]) <= TOL, key
+        x = golden[key + "_B"].copy(order="F")
+        packed.pptrs_ref(p, x)  # host array, written back
+        assert rel(x, golden[key + "_X"]) <= TOL, key
+        xd = torch.from_numpy(golden[key + "_B"].copy()).cuda()
+        packed.pptrs_ref(p, xd[:, 0])  # 1-D device RHS
+        assert rel(xd[:, 0], golden[key + "_X"][:, 0]) <= TOL, key
+    with pytest.raises(ValueError):
+        packed.pptrs_ref(conv.PackedTriangle(golden[keys[-1] + "_P"], int(keys[-1].split("_")[3][1:]),
+                                             keys[-1].split("_")[2]), torch.ones(3, 2, device="cuda"))
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("cplx", [False, True])
+def test_packed_cholesky_large_vs_oracle(P, uplo, cplx):
+    conv, packed = P.convert, P.packed
+    n = 700
+    a = O.spd_matrix(n, 11, "n", complex_=cplx)
+    po = O.pack(a, uplo)
+    pg = conv.PackedTriangle(po.copy(), n, uplo)
+    assert O.pptrf(po, n, uplo) == 0 == packed.pptrf_ref(pg)
+    assert rel(pg.data, po) <= TOL
+    b = np.asfortranarray(np.random.default_rng(2).standard_normal((n, 5)) + (1j if cplx else 0))
+    xo = b.copy(order="F")
+    O.pptrs(po, n, uplo, xo)
+    xg = torch.from_numpy(b.copy()).cuda()
+    packed.pptrs_ref(pg, xg)
+    assert rel(xg, xo) <= TOL

@@ -179,3 +179,24 @@ def test_next_rows_match_reference(golden, key, dt, uplo, transr, n):
     want = golden[f"lansf_{key}"]
     got = [O.lansf(nm, golden[f"lansf_{key}_rfp"], n, uplo, transr) for nm in "M1IF"]
     assert np.allclose(got, want, rtol=1e-13, atol=0)
+
+
+# ---------------------------------------------------------------- SURVEY 8(f) row 4
+def _pp_keys(g):
+    return sorted(k[:-len("_info")] for k in g if k.startswith("pp_") and k.endswith("_info"))
+
+
+def test_packed_cholesky_matches_reference(golden):
+    keys = _pp_keys(golden)
+    assert len(keys) >= 30
+    for key in keys:
+        _, dt, uplo, nn, *rest = key.split("_")
+        n = int(nn[1:])
+        p = golden[key + "_P"].copy()
+        assert O.pptrf(p, n, uplo) == int(golden[key + "_info"]), key
+        if rest:  # failing case: only the index is specified
+            continue
+        assert rel(p, golden[key + "_F"]) <= 1e-13, key
+        x = golden[key + "_B"].copy(order="F")
+        O.pptrs(golden[key + "_F"], n, uplo, x)
+        assert rel(x, golden[key + "_X"]) <= 1e-13, key
