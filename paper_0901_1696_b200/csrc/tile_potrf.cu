@@ -295,13 +295,13 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
   return true;
 }
 
-// Off-diagonal tile (i, j): X = (A(i, j) - acc) W_j^H into x (registers) and
-// A(i, j); W_j must be published.  Leaves X in smem tile S.
+// Off-diagonal tile (i, j) in two halves so that everything not needing W_j
+// happens before the wait for it:
+//   build_c: S = A(i, j) - acc (rows past the matrix zeroed)
+//   apply_w: Ws = W_j, x = S W_j^H; X written to A(i, j) and to smem tile Xs
 template <typename T>
-__device__ void solve_tile(const CholCtx<T>& X, int i, int j,
-                           const double (&acc)[TileCfg<T>::NACC][2][4][4], T* S, T* Ws,
-                           double (&x)[TileCfg<T>::NACC][2][4][4]) {
-  const int tid = threadIdx.x;
+__device__ void build_c(const CholCtx<T>& X, int i, int j,
+                        const double (&acc)[TileCfg<T>::NACC][2][4][4], T* S) {
   const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
   const int mrows = X.n - (int)i0 < TP ? X.n - (int)i0 : TP;
 #pragma unroll
@@ -315,7 +315,15 @@ __device__ void solve_tile(const CholCtx<T>& X, int i, int j,
         S[row + col * LD64] =
             row < mrows ? *X.A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r) : zero_<T>();
       }
+}
+template <typename T>
+__device__ void apply_w(const CholCtx<T>& X, int i, int j, T* S, T* Ws,
+                        double (&x)[TileCfg<T>::NACC][2][4][4], T* Xs) {
+  const int tid = threadIdx.x;
+  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
+  const int mrows = X.n - (int)i0 < TP ? X.n - (int)i0 : TP;
   const T* w = X.W + (i64)j * TP * TP;
+#pragma unroll 8
   for (int e = tid; e < TP * TP; e += TPT) {
     if constexpr (is_cplx<T>::value) {
       const double2 v = __ldcg(reinterpret_cast<const double2*>(w + e));
@@ -337,7 +345,7 @@ __device__ void solve_tile(const CholCtx<T>& X, int i, int j,
         int row, col;
         frag_rc(mi, ni, r, row, col);
         const T v = frag<T>(x, mi, ni, r);
-        S[row + col * LD64] = row < mrows ? v : zero_<T>();
+        Xs[row + col * LD64] = row < mrows ? v : zero_<T>();
         if (row < mrows) *X.A.at(i0 + row, j0 + col) = v;
       }
 }
@@ -440,31 +448,55 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   const int i = a, j = b;
   if (!accumulate<T, KM>(X, i, j, j, sm, s_ok, acc)) return false;
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
+  build_c(X, i, j, acc, S);
+  const int d = i;  // super: the diagonal tile factored next
+  const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
+  // real: prefetch the diagonal partial sum into acc (fragment layout, lower
+  // part, identity padding) while W_j is still being produced; complex (no
+  // spare registers) reloads it after the solve instead
+  if (kind == TK_SUPER && !C::CPLX) {
+    if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
+    const i64 d0 = (i64)d * TP;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          int row, col;
+          frag_rc(mi, ni, r, row, col);
+          T v = (row == col) ? one_<T>() : zero_<T>();
+          if (row < m && col < m && col <= row) {
+            const T* src = X.A.at(d0 + row, d0 + col);
+            if constexpr (is_cplx<T>::value) {
+              const double2 q = __ldcg(reinterpret_cast<const double2*>(src));
+              v = Z{q.x, q.y};
+            } else {
+              v = __ldcg(src);
+            }
+          }
+          if constexpr (is_cplx<T>::value) { acc[0][mi][ni][r] = v.x; acc[1][mi][ni][r] = v.y; }
+          else acc[0][mi][ni][r] = v;
+        }
+  }
   if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok)) return false;
   if (tr && threadIdx.x == 0) tr[2] = gtimer();
   double x[C::NACC][2][4][4];
-  solve_tile(X, i, j, acc, S, Ws, x);
+  apply_w(X, i, j, S, Ws, x, kind == TK_SUPER ? Ws : S);
   publish(X.done + (i64)i * X.nt + j);
   if (tr && threadIdx.x == 0) tr[6] = gtimer();
   if (kind == TK_NORMAL) {
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return true;
   }
-  // super: factor diagonal tile d = j + 1 from the partial sum and L(d, j)
-  const int d = i;
-  // X (= L(d, j)) stays in S; bring it to Ws so S can take the diagonal
-  for (int e = threadIdx.x; e < TP * TP; e += TPT) {
-    const int r = e & 63, c = e >> 6;
-    Ws[r + c * LD64] = S[r + c * LD64];
+  // super: diag d = partial - L(d, j) L(d, j)^H, then the leaf (X is in Ws)
+  if constexpr (C::CPLX) {
+    if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
+    load_diag(X, d, S);
+    __syncthreads();
   }
-  __syncthreads();
-  if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
-  load_diag(X, d, S);
-  __syncthreads();
-  if (tr && threadIdx.x == 0) tr[7] = gtimer();
   zero_acc<T>(x);
-  smem_mm_yh<T>(Ws, Ws, x);  // L(d, j) L(d, j)^H
-  const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
+  smem_mm_yh<T>(Ws, Ws, x);
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -473,10 +505,16 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
       for (int r = 0; r < 4; ++r) {
         int row, col;
         frag_rc(mi, ni, r, row, col);
-        if (row < m && col <= row) S[row + col * LD64] = S[row + col * LD64] - frag<T>(x, mi, ni, r);
+        if constexpr (C::CPLX) {
+          if (row < m && col <= row) S[row + col * LD64] = S[row + col * LD64] - frag<T>(x, mi, ni, r);
+        } else {
+          T v = (row == col) ? one_<T>() : zero_<T>();
+          if (row < m && col < m && col <= row) v = frag<T>(acc, mi, ni, r) - frag<T>(x, mi, ni, r);
+          S[row + col * LD64] = v;
+        }
       }
   __syncthreads();
-  if (tr && threadIdx.x == 0) tr[1] = gtimer();  // (overwrites: diag start)
+  if (tr && threadIdx.x == 0) tr[7] = gtimer();
   const bool ok = finish_diag(X, d, S, Ws, scr, s_ok);
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
   return ok;
