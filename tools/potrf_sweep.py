@@ -13,7 +13,8 @@ for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "500,1000,2000,
         s.record(); lib.rfpk_dpotrf(b"L", w.data_ptr(), n, 1, n, info.data_ptr(), st); e.record(); torch.cuda.synchronize()
         if rep >= 2: ts.append(s.elapsed_time(e))
     ms = sorted(ts)[len(ts) // 2]
-    ref = torch.linalg.cholesky(a); err = float((torch.tril(w) - ref).abs().max() / ref.abs().max())
+    ref = torch.linalg.cholesky(a)  # w holds L column-major = L^T in torch row-major
+    err = float((torch.triu(w).t() - ref).abs().max() / ref.abs().max())
     print(f"potrf n={n} {ms:.3f} ms {n**3/3/ms/1e9:.2f} TF info={int(info.item())} relerr={err:.1e}", flush=True)
     # cuSOLVER (torch) for reference
     ts = []
