@@ -70,10 +70,22 @@ template <typename T> struct TileCfg {
   static constexpr int NACC = CPLX ? 2 : 1;
 };
 
+// Cholesky K-loop pipeline per operand orientation.  Row-major (K-major)
+// operands from RFP blocks have an odd leading dimension, so a 16-wide k
+// slice of a row (128 B real) straddles 5 sectors instead of 4; 32-wide
+// slices (256 B: 9 instead of 8) with two stages keep three CTAs per SM and
+// measured 9.1 -> ~7.8 ms on potrf(8192) with ld 8193.
+template <typename T, bool KM> struct PipeCfg {
+  static constexpr bool CPLX = is_cplx<T>::value;
+  static constexpr int BK = KM ? (CPLX ? 16 : 32) : (CPLX ? 8 : 16);
+  static constexpr int ST = (KM && !CPLX) ? 2 : 3;
+  static constexpr int SPC = TP / BK;
+};
+
 template <typename T, bool KM> size_t tile_smem_bytes() {
-  using C = TileCfg<T>;
-  using L = SmemLayout<T, TP, C::BK, KM>;
-  const size_t pipe = (size_t)STAGES * 2 * L::SIZE;
+  using P = PipeCfg<T, KM>;
+  using L = SmemLayout<T, TP, P::BK, KM>;
+  const size_t pipe = (size_t)P::ST * 2 * L::SIZE;
   const size_t leaf = (size_t)2 * TP * LD64 + 128;
   return (pipe > leaf ? pipe : leaf) * sizeof(T);
 }
@@ -198,8 +210,9 @@ template <typename T, bool KM>
 __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, int* s_ok,
                            double (&acc)[TileCfg<T>::NACC][2][4][4]) {
   using C = TileCfg<T>;
-  using LA = SmemLayout<T, TP, C::BK, KM>;
-  constexpr int BK = C::BK, SPC = C::SPC;
+  using P = PipeCfg<T, KM>;
+  using LA = SmemLayout<T, TP, P::BK, KM>;
+  constexpr int BK = P::BK, SPC = P::SPC, STAGES = P::ST;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
   T* As = sm;
