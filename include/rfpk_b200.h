@@ -102,6 +102,14 @@ int rfpk_dpftrs_ex(char transr, char uplo, int64_t n, int64_t nrhs, const double
                    int64_t rsb, int64_t csb, int* info, rfpk_stream_t stream);
 int rfpk_zpftrs_ex(char transr, char uplo, int64_t n, int64_t nrhs, const void* arf, void* b,
                    int64_t rsb, int64_t csb, int* info, rfpk_stream_t stream);
+/* rfp.pftrf(r) on a buffer that still sits in pinned HOST memory h_arf:
+   the host->device copy into d_arf is streamed (T1/T2 rows first on `stream`,
+   S1 rows on an internal side stream) and overlapped with potrf(T1);
+   factor and info as rfpk_?pftrf.  rfp.py:55-91 + the caller's H2D copy. */
+int rfpk_dpftrf_host(char transr, char uplo, int64_t n, const double* h_arf, double* d_arf,
+                     int* info, rfpk_stream_t stream);
+int rfpk_zpftrf_host(char transr, char uplo, int64_t n, const void* h_arf, void* d_arf, int* info,
+                     rfpk_stream_t stream);
 /* replaces rfp.tftri(r, diag)   rfp.py:286-325 */
 int rfpk_dtftri(char transr, char uplo, char diag, int64_t n, double* arf, int* info,
                 rfpk_stream_t stream);

@@ -173,6 +173,47 @@ namespace rfpk {
 std::atomic<long long> g_launch_count{0};
 }
 
+// ---------------------------------------------------------------- pftrf from host
+// The factorization of a pinned HOST RFP buffer with the transfer streamed:
+// the rows holding T1/T2 are copied on `st` and potrf(T1) starts as soon as
+// they land, while the S1 rows come over on a side stream; the S1 solve
+// waits for them.  The PCIe/C2C copy of S1 (about half the buffer) thus
+// hides under potrf(T1).  Result and info as rfpk_?pftrf, in d_arf.
+template <typename T>
+int pftrf_host_t(char transr, char uplo, int64_t n, const void* h_arf, void* d_arf, int* info,
+                 cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (!info) return -6;
+  if (int rc = reset_info(info, st)) return rc;
+  if (n == 0) return 0;
+  const RfpDesc d = rfp_desc(n, uplo, transr);
+  static thread_local cudaStream_t side = [] {
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    return s;
+  }();
+  static thread_local cudaEvent_t fork = [] {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  }();
+  static thread_local cudaEvent_t s1_done = [] {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  }();
+  // the side copy must not overtake earlier work on `st` that uses d_arf
+  cudaError_t e = cudaEventRecord(fork, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+  if (e != cudaSuccess) return (int)e;
+  if (int rc = rfp_h2d_split<T>(d, (const T*)h_arf, (T*)d_arf, st, side)) return rc;
+  if ((e = cudaEventRecord(s1_done, side)) != cudaSuccess) return (int)e;
+  return pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done);
+}
+
 // ---------------------------------------------------------------- packed Cholesky
 // the reference's Level-2 packed comparator
 // (packed.py:70-146 pptrf_ref / pptrs_ref).  B200 design: the column-packed
@@ -271,6 +312,8 @@ int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_st
 int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftri_t<double>(t, u, n, arf, info, S(s)); }
 int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftri_t<Z>(t, u, n, arf, info, S(s)); }
 
+int rfpk_dpftrf_host(char t, char u, int64_t n, const double* h, double* d, int* info, rfpk_stream_t s) { return pftrf_host_t<double>(t, u, n, h, d, info, S(s)); }
+int rfpk_zpftrf_host(char t, char u, int64_t n, const void* h, void* d, int* info, rfpk_stream_t s) { return pftrf_host_t<Z>(t, u, n, h, d, info, S(s)); }
 int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }
 int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { return pptrf_t<Z>(u, n, ap, info, S(s)); }
 int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }

@@ -79,7 +79,7 @@ struct PhaseTrace {
   } while (0)
 
 // SRPA factorization (rfp.py:55-91)
-template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
+template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready) {
   if (d.n == 0) return 0;
   const bool herm = is_cplx<T>::value;
   View<T> t1, t2, s1;
@@ -93,6 +93,7 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
   if (d.lower) {
     rc = blas_potrf(c, 'L', t1, 0, W);
     tr.mark("potrf(T1)");
+    if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
     if (!rc && d.n2) {
       if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
       tr.mark("trsm(S1)");
@@ -105,6 +106,7 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
     if (d.n2) {
       rc = blas_potrf(c, 'L', t1, 0, W);
       tr.mark("potrf(T1)");
+      if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
       if (!rc) rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
       tr.mark("trsm(S1)");
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
@@ -113,8 +115,36 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf) {
     if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n2, W);
     tr.mark("potrf(T2)");
   }
+  // (the S1 copy must also be complete on every early-exit path)
+  if (s1_ready) cudaStreamWaitEvent(c.st, s1_ready, 0);
   ws_free(W, c.st);
   return rc;
+}
+
+// Rows [a, b) of the normal ldar x n1 rectangle as one copy: a 2-D strided
+// copy for TRANSR='N' (column-major rectangle), a contiguous block for 'T'.
+template <typename T>
+static cudaError_t copy_rows(const RfpDesc& d, const T* host, T* dev, i64 a, i64 b,
+                             cudaStream_t st) {
+  if (b <= a) return cudaSuccess;
+  if (d.trans)  // row r of the normal rectangle = n1 contiguous elements at r * n1
+    return cudaMemcpyAsync(dev + a * d.n1, host + a * d.n1, (size_t)(b - a) * d.n1 * sizeof(T),
+                           cudaMemcpyHostToDevice, st);
+  return cudaMemcpy2DAsync(dev + a, (size_t)d.ldar * sizeof(T), host + a,
+                           (size_t)d.ldar * sizeof(T), (size_t)(b - a) * sizeof(T), (size_t)d.n1,
+                           cudaMemcpyHostToDevice, st);
+}
+
+template <typename T>
+int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first,
+                  cudaStream_t second) {
+  // T1 and T2 live in the rows [0, n1 + d) (lower) / [n2, ldar) (upper) of the
+  // normal rectangle, S1 in the rest (rfp_blocks)
+  const i64 t0 = d.lower ? 0 : d.n2, t1 = d.lower ? d.n1 + d.d : d.ldar;
+  const i64 s0 = d.lower ? d.n1 + d.d : 0, s1 = d.lower ? d.ldar : d.n2;
+  cudaError_t e = copy_rows(d, host, dev, t0, t1, first);
+  if (e == cudaSuccess) e = copy_rows(d, host, dev, s0, s1, second);
+  return (int)e;
 }
 
 // forward/back substitution through T1/S1/T2 (rfp.py:106-136)
@@ -566,7 +596,8 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
 
 #define RFPK_RFP_INST(T)                                                                     \
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
-  template int pftrf<T>(Ctx, const RfpDesc&, T*);                                            \
+  template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t);                               \
+  template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);                                            \
   template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>);                             \
   template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
   template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \

@@ -19,7 +19,12 @@ RfpDesc rfp_desc(i64 n, char uplo, char transr);
 template <typename T> void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2,
                                       View<T>& s1);
 
-template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf);
+template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr);
+// host -> device streaming helper for pftrf: the rows of the normal rectangle
+// holding T1 and T2 (first needed) and those holding S1 (needed from the S1
+// solve on) as two copies; see rfpk_?pftrf_host
+template <typename T>
+int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first, cudaStream_t second);
 template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b);
 template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf);
 template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf);

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import threading
 
+import numpy as np
 import torch
 
 from . import _capi
@@ -23,6 +24,7 @@ from .layout import make_descriptor, normalize_flag
 
 __all__ = [
     "pftrf",
+    "pftrf_from_host",
     "pftrs",
     "tfsm",
     "sfrk_hfrk",
@@ -76,6 +78,37 @@ def pftrf(r: RfpTriangle) -> int:
     if v == 0:
         r.state = FactorState.CHOLESKY
     return v
+
+
+def pftrf_from_host(data, n: int, uplo: str, transr: str):
+    """:func:`pftrf` of an RFP buffer that still sits in host memory, with
+    the host->device transfer streamed under the factorization (the rows of
+    T1/T2 first, S1's on a side stream, hidden by potrf(T1); C ABI
+    ``rfpk_?pftrf_host``).  ``data``: CPU tensor (pinned for a truly
+    asynchronous copy) or NumPy array of ``n(n+1)/2`` scalars.  Returns
+    ``(RfpTriangle on the device, info)`` like ``pftrf``."""
+    desc = make_descriptor(n, uplo, transr)
+    host = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+    if host.is_cuda:
+        raise ValueError("pftrf_from_host expects host memory; use pftrf for device buffers")
+    if host.dtype not in (torch.float64, torch.complex128):
+        host = host.to(torch.complex128 if host.is_complex() else torch.float64)
+    host = host.reshape(-1).contiguous()
+    if host.shape[0] != desc.nt:
+        raise ValueError(f"buffer length {host.shape[0]} != nt={desc.nt} for n={desc.n}")
+    _capi.lib()
+    dev = torch.empty(desc.nt, dtype=host.dtype, device=torch.device("cuda", torch.cuda.current_device()))
+    r = RfpTriangle(dev, desc)
+    if desc.n == 0:
+        r.state = FactorState.CHOLESKY
+        return r, 0
+    info = _info(dev.device)
+    _run(f"rfpk_{_prefix(host.dtype)}pftrf_host", _capi.flag(desc.transr), _capi.flag(desc.uplo),
+         desc.n, host.data_ptr(), dev.data_ptr(), info.data_ptr(), _capi.stream_handle(dev.device))
+    v = int(info.item())
+    if v == 0:
+        r.state = FactorState.CHOLESKY
+    return r, v
 
 
 def _rhs_view(r: RfpTriangle, b):

@@ -479,3 +479,24 @@ def test_packed_cholesky_large_vs_oracle(P, uplo, cplx):
     xg = torch.from_numpy(b.copy()).cuda()
     packed.pptrs_ref(pg, xg)
     assert rel(xg, xo) <= TOL
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n", [7, 130, 601])
+def test_pftrf_from_host_streamed(P, uplo, transr, n):
+    """The streamed host->device pftrf gives the same factor (bit-identical)
+    as a device pftrf of the same buffer, and the same failure index."""
+    conv, rfp = P.convert, P.rfp
+    for cplx in (False, True):
+        a = O.spd_matrix(n, 3 + n, "n", complex_=cplx)
+        buf = O.trttf(a, uplo, transr)
+        host = torch.from_numpy(buf.copy()).pin_memory()
+        r, info = rfp.pftrf_from_host(host, n, uplo, transr)
+        ref = conv.RfpTriangle(buf.copy(), P.layout.make_descriptor(n, uplo, transr))
+        assert info == 0 == rfp.pftrf(ref)
+        assert bits(r.data) == bits(ref.data)
+        assert r.state is conv.FactorState.CHOLESKY
+    bad = O.trttf(np.eye(n) - 2.0 * (np.arange(n) == n // 2)[:, None] * np.eye(n), uplo, transr)
+    _, info = rfp.pftrf_from_host(bad, n, uplo, transr)
+    assert info == n // 2 + 1
