@@ -132,25 +132,7 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 // RFP buffer (2080) + RHS chunk (64 x 8) + scratch (64) = 21 KB, so ten
 // matrices (warps) are resident per SM.  W1 = L1^-1 and W2 = L2^-1 are formed
 // IN PLACE of the factor blocks T1 / T2 once those are safely in HBM.
-constexpr int B64_SMEM_DOUBLES = b64::NT + 64 * 8 + 96;
-
-// X (64 x 8, ld 64) <- columns [c0, c0 + cw) of the n x nrhs RHS, zero-padded;
-// 8-byte cp.async so the global latency overlaps the factorization.
-__device__ __forceinline__ void b64_fetch_rhs(double* X, const double* bk, i64 ldb, int c0,
-                                              int cw) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < 64 * 8; e += 32) {
-    const int i = e & 63, c = e >> 6;
-    if (c < cw) {
-      unsigned s = (unsigned)__cvta_generic_to_shared(X + e);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s),
-                   "l"(bk + i + (i64)(c0 + c) * ldb));
-    } else {
-      X[e] = 0.0;
-    }
-  }
-  asm volatile("cp.async.commit_group;\n" ::);
-}
+constexpr int B64_SMEM_DOUBLES = b64::NT + 96;
 
 template <bool FACTOR, bool SOLVE, int TRANS>
 __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
@@ -159,8 +141,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   using namespace b64;
   extern __shared__ __align__(16) double sm[];
   double* R = sm;
-  double* X = R + NT;      // RHS chunk, ld 64
-  double* colk = X + 512;  // 64 entries (factor_inv32)
+  double* colk = R + NT;      // 64 entries (factor_inv32)
   double* rdiag = colk + 64;  // 32 entries (inv32)
   const int lane = threadIdx.x;
   const i64 k = blockIdx.x;
@@ -175,13 +156,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   } else {
     for (int c = lane; c < NT; c += 32) R[c] = g[c];
   }
-  asm volatile("cp.async.commit_group;\n" ::);
-  if (SOLVE) {
-    b64_fetch_rhs(X, bk, ldb, 0, nrhs < 8 ? nrhs : 8);
-    asm volatile("cp.async.wait_group 1;\n" ::);
-  } else {
-    asm volatile("cp.async.wait_group 0;\n" ::);
-  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   __syncwarp();
   constexpr int rs = TRANS ? 32 : 1, cs = TRANS ? 1 : 65;
   using V = SV<rs, cs>;
@@ -191,7 +166,6 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   const V S1{R + (lower ? 33 : 0) * rs};
   const V V1 = T1;            // L1 (lower), later W1
   const auto V2 = T2.t();     // L2 (lower), later W2
-  const SV<1, 64> x1{X}, x2{X + 32};
   const i64 off1 = V1.p - R, off2 = V2.p - R;
   if (FACTOR) {
     // L1 goes to HBM inside factor_inv32 before W1 overwrites it
@@ -225,47 +199,61 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
   if (!SOLVE) return;
   const auto w1 = V1;
   const auto w2 = V2;
+  const int g8 = lane >> 2, t4 = lane & 3;
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
-    __syncwarp();
-    if (c0) b64_fetch_rhs(X, bk, ldb, c0, cw);
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncwarp();
-    double a8[2][1][4];
-    zero_acc<8>(a8);
-    mm32<8, 1, 0>(w1, x1, a8);                 // b1 = W1 b1
-    __syncwarp();
-    store_acc<8>(x1, a8, 1.0, 0.0, 0);
-    __syncwarp();
-    zero_acc<8>(a8);
-    if (lower) mm32<8, 0, 0>(S1, x1, a8);      // b2 -= S1 b1
-    else mm32<8, 0, 0>(S1.t(), x1, a8);        // b2 -= S1^T b1
-    store_acc<8>(x2, a8, -1.0, 1.0, 0);
-    __syncwarp();
-    zero_acc<8>(a8);
-    mm32<8, 1, 0>(w2, x2, a8);                 // b2 = W2 b2
-    __syncwarp();
-    store_acc<8>(x2, a8, 1.0, 0.0, 0);
-    __syncwarp();
-    zero_acc<8>(a8);
-    mm32<8, 2, 0>(w2.t(), x2, a8);             // b2 = W2^T b2
-    __syncwarp();
-    store_acc<8>(x2, a8, 1.0, 0.0, 0);
-    __syncwarp();
-    zero_acc<8>(a8);
-    if (lower) mm32<8, 0, 0>(S1.t(), x2, a8);  // b1 -= S1^T b2
-    else mm32<8, 0, 0>(S1, x2, a8);            // b1 -= S1 b2
-    store_acc<8>(x1, a8, -1.0, 1.0, 0);
-    __syncwarp();
-    zero_acc<8>(a8);
-    mm32<8, 2, 0>(w1.t(), x1, a8);             // b1 = W1^T b1
-    __syncwarp();
-    store_acc<8>(x1, a8, 1.0, 0.0, 0);
-    __syncwarp();
-    for (int e = lane; e < 64 * cw; e += 32) {
-      const int i = e & 63, c = e >> 6;
-      bk[i + (i64)(c0 + c) * ldb] = X[e];
+    // b1 / b2 straight into the B-operand registers (column g8, rows 4s+t4)
+    double x1[8], x2[8], c[2][4];
+    const double* bc = bk + (i64)(c0 + g8) * ldb;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      x1[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
+      x2[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
     }
+    zero_c(c);
+    mm32r<1>(w1, x1, c);                         // b1 = W1 b1
+    c2b(c, x1);
+    zero_c(c);
+    if (lower) mm32r<0>(S1, x1, c);              // S1 b1
+    else mm32r<0>(S1.t(), x1, c);                // S1^T b1
+    {
+      double d[8];
+      c2b(c, d);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) x2[s] -= d[s];  // b2 -= ...
+    }
+    zero_c(c);
+    mm32r<1>(w2, x2, c);                         // b2 = W2 b2
+    c2b(c, x2);
+    zero_c(c);
+    mm32r<2>(w2.t(), x2, c);                     // b2 = W2^T b2
+    c2b(c, x2);
+    // b2 is final: store it from the accumulator layout
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = mi * 16 + g8 + ((r & 2) ? 8 : 0), col = 2 * t4 + (r & 1);
+        if (col < cw) bk[32 + row + (i64)(c0 + col) * ldb] = c[mi][r];
+      }
+    zero_c(c);
+    if (lower) mm32r<0>(S1.t(), x2, c);          // S1^T b2
+    else mm32r<0>(S1, x2, c);                    // S1 b2
+    {
+      double d[8];
+      c2b(c, d);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) x1[s] -= d[s];  // b1 -= ...
+    }
+    zero_c(c);
+    mm32r<2>(w1.t(), x1, c);                     // b1 = W1^T b1
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = mi * 16 + g8 + ((r & 2) ? 8 : 0), col = 2 * t4 + (r & 1);
+        if (col < cw) bk[row + (i64)(c0 + col) * ldb] = c[mi][r];
+      }
   }
 }
 

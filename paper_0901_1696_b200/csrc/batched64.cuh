@@ -221,6 +221,50 @@ __device__ __forceinline__ void put_view(SV<RS, CS> V, const double* R, double* 
   }
 }
 
+// ---- the right-hand side in registers (frees 4 KB of smem per matrix)
+// A 32 x 8 block X is held as the m16n8k4 B operand: lane (g, t) owns
+// xb[s] = X(4s + t, g), s = 0..7.  Products land in the accumulator layout
+// c[mi][r] = C(16 mi + g + 8 (r >> 1), 2t + (r & 1)).
+
+// c (32 x 8) += A (32 x 32 smem view, triangle mask TA) * X (registers)
+template <int TA, class VA>
+__device__ __forceinline__ void mm32r(VA A, const double (&xb)[8], double (&c)[2][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int kk = 4 * s + t;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      if (TA == 1 && mi == 0 && s >= 4) continue;  // strip above the lower triangle
+      if (TA == 2 && mi == 1 && s < 4) continue;   // strip below the upper triangle
+      const int r0 = mi * 16 + g, r1 = r0 + 8;
+      const double a0 = (TA == 1 && kk > r0) || (TA == 2 && kk < r0) ? 0.0 : A(r0, kk);
+      const double a1 = (TA == 1 && kk > r1) || (TA == 2 && kk < r1) ? 0.0 : A(r1, kk);
+      mma(c[mi], a0, a1, xb[s]);
+    }
+  }
+}
+
+// accumulator layout -> B-operand layout (16 shuffles)
+__device__ __forceinline__ void c2b(const double (&c)[2][4], double (&xb)[8]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int mi = s >> 2, half = (s & 3) >> 1;
+    const int src = (4 * (s & 1) + t) * 4 + (g >> 1);
+    const double v0 = __shfl_sync(0xffffffffu, c[mi][half * 2], src);
+    const double v1 = __shfl_sync(0xffffffffu, c[mi][half * 2 + 1], src);
+    xb[s] = (g & 1) ? v1 : v0;
+  }
+}
+
+__device__ __forceinline__ void zero_c(double (&c)[2][4]) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[mi][r] = 0.0;
+}
+
 template <int NC>
 __device__ __forceinline__ void zero_acc(double acc[2][NC / 8][4]) {
 #pragma unroll
