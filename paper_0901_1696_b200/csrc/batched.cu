@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
       if (lane == 0) info[k] = f;
       return;
     }
-    inv32(V1, rdiag);
+    inv32<rs, cs, TRANS ? 0 : 1>(V1, rdiag);
     double acc[2][4][4];
     zero_acc<32>(acc);
     if (lower) mm32<32, 0, 2>(S1, V1.t(), acc);   // S1 <- S1 W1^T
@@ -191,10 +191,10 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
     f = factor_inv32(V2.p, cs, rs, colk, g + off2, F32_FACTOR);
     if (lane == 0) info[k] = f ? 32 + f : 0;
     if (f) return;
-    if (SOLVE) inv32(V2, rdiag);
+    if (SOLVE) inv32<cs, rs, 0>(V2, rdiag);
   } else {
-    inv32(V1, rdiag);
-    inv32(V2, rdiag);
+    inv32<rs, cs, TRANS ? 0 : 1>(V1, rdiag);
+    inv32<cs, rs, 0>(V2, rdiag);
   }
   if (!SOLVE) return;
   const auto w1 = V1;

@@ -138,8 +138,18 @@ __device__ __noinline__ int factor_inv32(double* p, int rs, int cs, double* colk
 
 // In-place inverse of the lower 32x32 view L (only the lower triangle is read
 // or written: the slots above it belong to the other RFP block).  Lane j
-// computes column j; rdiag is a 32-entry scratch.
-template <int RS, int CS>
+// computes column j; rdiag is a 32-entry scratch.  The substitution runs
+// along L's unit-stride direction so that L is read two entries per 16-byte
+// LDS: right-looking (column k of L per step) when columns are contiguous
+// (RS == 1), left-looking (row i per step) when rows are (CS == 1).  PAR is
+// the parity of L.p's element offset from the 16-byte-aligned smem base, so
+// the pairing is resolved at compile time.
+template <int RS, int CS, int PAR>
+__device__ __forceinline__ double2 ld_pair(SV<RS, CS> L, int i, int k) {
+  // L(i, k) and its unit-stride neighbour (i+1, k) [RS == 1] / (i, k+1) [CS == 1]
+  return *reinterpret_cast<const double2*>(&L(i, k));
+}
+template <int RS, int CS, int PAR>
 __device__ __noinline__ void inv32(SV<RS, CS> L, double* rdiag) {
   __builtin_assume(__isShared(L.p));
   __builtin_assume(__isShared(rdiag));
@@ -147,18 +157,46 @@ __device__ __noinline__ void inv32(SV<RS, CS> L, double* rdiag) {
   rdiag[j] = 1.0 / L(j, j);
   __syncwarp();
   double w[32];
+  if constexpr (RS == 1) {
+    // right-looking: s <- e_j; for k: w_k = s_k / L_kk; s_i -= L(i, k) w_k
+    double sv[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int i = 0; i < 32; ++i) sv[i] = (i == j) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) {
-      const double l = L(i, k);
-      if ((k & 3) == 0) s0 = fma(-l, w[k], s0);
-      else if ((k & 3) == 1) s1 = fma(-l, w[k], s1);
-      else if ((k & 3) == 2) s2 = fma(-l, w[k], s2);
-      else s3 = fma(-l, w[k], s3);
+    for (int k = 0; k < 32; ++k) {
+      w[k] = sv[k] * rdiag[k];
+      int i = k + 1;
+      if (i < 32 && ((PAR + i + k * CS) & 1)) {  // odd start: single load
+        sv[i] = fma(-L(i, k), w[k], sv[i]);
+        ++i;
+      }
+#pragma unroll
+      for (; i + 1 < 32; i += 2) {
+        const double2 q = ld_pair<RS, CS, PAR>(L, i, k);
+        sv[i] = fma(-q.x, w[k], sv[i]);
+        sv[i + 1] = fma(-q.y, w[k], sv[i + 1]);
+      }
+      if (i < 32) sv[i] = fma(-L(i, k), w[k], sv[i]);
     }
-    w[i] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
+  } else {
+    // left-looking along rows: w_i = (e_j(i) - sum_k L(i, k) w_k) / L_ii
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = 0;
+      if (i > 0 && ((PAR + i * RS) & 1)) {
+        s0 = fma(-L(i, 0), w[0], s0);
+        k = 1;
+      }
+#pragma unroll
+      for (; k + 1 < i; k += 2) {
+        const double2 q = ld_pair<RS, CS, PAR>(L, i, k);
+        if ((k & 2) == 0) { s0 = fma(-q.x, w[k], s0); s1 = fma(-q.y, w[k + 1], s1); }
+        else { s2 = fma(-q.x, w[k], s2); s3 = fma(-q.y, w[k + 1], s3); }
+      }
+      if (k < i) s1 = fma(-L(i, k), w[k], s1);
+      w[i] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
+    }
   }
   __syncwarp();  // every lane has finished reading L
 #pragma unroll
