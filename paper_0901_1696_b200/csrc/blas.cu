@@ -428,61 +428,6 @@ int trsm_rest_upper(Ctx c, bool conj, View<T> Tm, View<T> B, i64 n1, T* W, bool 
   return trsm_rest_upper(c, conj, T11, B1, m1, W, wtrans, depth);
 }
 
-// Blocked right-looking trsm with look-ahead for a narrow right-hand side
-// (B.n <= 2048, e.g. pftrs with nrhs = 1024): the recursive form leaves its
-// bottom levels as 64 x N x 64 GEMMs of ~16 CTAs; here the critical path is
-// 256-row block solves (trsm_plain over the same 64-leaf inverses) plus the
-// update of the next block, and the rank-256 update of the remaining rows
-// runs on a side stream.  Same W slab layout as trsm_rec.
-constexpr i64 TRL_NB = 256;
-
-// SMs' worth of CTAs granted to an off-critical-path update (GemmCap); the
-// rest stay free for the critical path.  RFPK_SIDE_RESERVE = SMs kept free.
-int side_cap() {
-  static const int cap = [] {
-    const char* v = std::getenv("RFPK_SIDE_RESERVE");
-    const int r = v ? std::atoi(v) : 0;
-    return r > 0 ? num_sms() - r : 0;
-  }();
-  return cap;
-}
-
-template <typename T>
-int trsm_rl(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, T* W, bool wtrans) {
-  const i64 n = Tm.m, N = B.n;
-  const int cap = side_cap();
-  cudaStream_t side = la_streams().side[22];
-  int rc;
-  bool side_busy = false;
-  const i64 nblk = (n + TRL_NB - 1) / TRL_NB;
-  auto sz = [&](i64 k) { return (n - k * TRL_NB) < TRL_NB ? (n - k * TRL_NB) : TRL_NB; };
-  for (i64 step = 0; step < nblk; ++step) {
-    const i64 k = lower ? step : nblk - 1 - step;
-    const i64 o = k * TRL_NB, s = sz(k);
-    View<T> Xk = B.sub(o, 0, s, N);
-    if ((rc = trsm_plain(c, lower, conj, Tm.sub(o, o, s, s), Xk, W + o * 64, wtrans))) return rc;
-    if (step + 1 == nblk) break;
-    if (side_busy && (rc = la_link(side, c.st))) return rc;
-    // next block to be solved, and the rows beyond it
-    const i64 kn = lower ? k + 1 : k - 1;
-    const i64 on = kn * TRL_NB, sn = sz(kn);
-    if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(on, o, sn, s), conj, Xk, false, one<T>(),
-                      B.sub(on, 0, sn, N), false, c.info, c.st)))
-      return rc;
-    const i64 r0 = lower ? on + sn : 0, rn = lower ? n - (on + sn) : on;
-    if (rn > 0) {
-      if ((rc = la_link(c.st, side))) return rc;
-      GemmCap capped(cap);
-      if ((rc = gemm<T>(TRI_FULL, neg_one<T>(), Tm.sub(r0, o, rn, s), conj, Xk, false, one<T>(),
-                        B.sub(r0, 0, rn, N), false, c.info, side)))
-        return rc;
-      side_busy = true;
-    }
-  }
-  if (side_busy && (rc = la_link(side, c.st))) return rc;
-  return 0;
-}
-
 // conj?(T) X = alpha B.  If W is null the leaf inverses are computed here.
 template <typename T>
 int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B, T* W) {
@@ -504,9 +449,7 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
     ws_free(own, c.st);
     return rc;
   }
-  if (Tm.m >= 1024 && B.n <= 2048 && !std::getenv("RFPK_NO_TRSM_RL"))
-    rc = on_hi_stream(c, [&](Ctx h) { return trsm_rl(h, lower, conj, Tm, B, W, !lower); });
-  else if (Tm.m >= LA_MIN)
+  if (Tm.m >= LA_MIN)
     rc = on_hi_stream(c, [&](Ctx h) { return trsm_rec(h, lower, conj, Tm, B, W, !lower); });
   else rc = trsm_rec(c, lower, conj, Tm, B, W, !lower);
   ws_free(own, c.st);
@@ -604,82 +547,15 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
 }
 
 
-// Right-looking blocked Cholesky with look-ahead for large n (nb = 128 while
-// more than 4096 columns remain, then 64; measured best on B200 for 2048-8192).
-// Iteration k: factor the diagonal block and solve the panel below it on the
-// critical (high-priority) stream; update the NEXT panel's columns there too;
-// fork the rest of the rank-nb trailing update to a low-priority side stream,
-// where it overlaps the next iteration's panel factorization.  Every 64-leaf
-// is still factored by potf2_inv64 at a 64-aligned offset, so the W slabs are
-// exactly those the recursive trsm (pftrf's S1 solve) expects.
-static const i64 RL_NB = env_int("RFPK_RL_NB", 0);  // 0: adaptive 128 / 64
-static const i64 RL_MIN = env_int("RFPK_RL_MIN", 1024);
-static const i64 RL_TAIL = env_int("RFPK_RL_TAIL", 4096);  // tile kernel for the last columns
-
-template <typename T> int potrf_rl(Ctx c, View<T> A, int base, T* W) {
-  const i64 n = A.m;
-  const bool cplx = is_cplx<T>::value;
-  cudaStream_t side = la_streams().side[23];
-  Ctx cs{side, c.info};
-  int rc;
-  bool side_busy = false;
-  // panel width: wider while the trailing matrix is large (rank-nb updates stay
-  // GEMM-efficient), 64 (one leaf) near the end where the critical path rules
-  auto width = [&](i64 o) {
-    const i64 nb = RL_NB > 0 ? RL_NB : ((n - o) > 4096 ? 128 : 64);
-    return (n - o) < nb ? (n - o) : nb;
-  };
-  for (i64 o = 0, s = 0; o < n; o += s) {
-    // the latency-bound tail goes to the dataflow tile kernel once its
-    // columns have received every trailing update
-    if (n - o <= RL_TAIL && !std::getenv("RFPK_NO_TILE")) {
-      if (side_busy && (rc = la_link(side, c.st))) return rc;
-      return potrf_tiles(c, A.sub(o, o, n - o, n - o), base + (int)o, W + o * 64);
-    }
-    s = width(o);
-    const i64 rest = n - o - s;
-    View<T> Akk = A.sub(o, o, s, s);
-    // panel factorization (its columns are fully updated already)
-    if ((rc = potrf_node(c, Akk, base + (int)o, W + o * 64, 0))) return rc;
-    if (rest == 0) break;
-    View<T> P = A.sub(o + s, o, rest, s);
-    if ((rc = trsm_rec(c, true, cplx, Akk, P.t(), W + o * 64, false))) return rc;
-    // the side stream's previous trailing update also wrote the next panel
-    if (side_busy && (rc = la_link(side, c.st))) return rc;
-    const i64 s2 = width(o + s);
-    View<T> P1 = P.sub(0, 0, s2, s);
-    if ((rc = herk_core(c, TRI_LOWER, -1.0, P1, false, 1.0, A.sub(o + s, o + s, s2, s2), true)))
-      return rc;
-    if (rest > s2) {
-      const i64 r2 = rest - s2;
-      View<T> P2 = P.sub(s2, 0, r2, s);
-      if ((rc = gemm<T>(TRI_FULL, sc_from<T>(-1.0), P2, false, P1.t(), cplx, sc_from<T>(1.0),
-                        A.sub(o + s + s2, o + s, r2, s2), false, c.info, c.st)))
-        return rc;
-      // trailing update of the columns after the next panel, off the critical path
-      if ((rc = la_link(c.st, side))) return rc;
-      GemmCap capped(side_cap());
-      if ((rc = herk_core(cs, TRI_LOWER, -1.0, P2, false, 1.0, A.sub(o + s + s2, o + s + s2, r2, r2),
-                          true)))
-        return rc;
-      side_busy = true;
-    }
-  }
-  if (side_busy && (rc = la_link(side, c.st))) return rc;
-  return 0;
-}
-
 static const i64 TILE_MAX = env_int("RFPK_TILE_MAX", (i64)1 << 40);  // measured: the tile kernel wins at every n
 
 template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
   // the dataflow tile kernel (tile_potrf.cu) wherever the critical path rules
   if (A.m > LEAF && A.m <= TILE_MAX && W && !std::getenv("RFPK_NO_TILE"))
     return potrf_tiles(c, A, base, W);
+  // (fallback / n <= 64: the recursive driver with look-ahead streams)
   if (A.m < LA_MIN) return potrf_node(c, A, base, W, 0);
-  return on_hi_stream(c, [&](Ctx h) {
-    if (A.m >= RL_MIN && !std::getenv("RFPK_NO_RL")) return potrf_rl(h, A, base, W);
-    return potrf_node(h, A, base, W, 0);
-  });
+  return on_hi_stream(c, [&](Ctx h) { return potrf_node(h, A, base, W, 0); });
 }
 
 // A <- L^{-1} in place (lower): all 64-leaves are inverted in one launch,

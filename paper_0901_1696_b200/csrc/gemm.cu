@@ -269,18 +269,16 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
                           (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
                           sizeof(T);
   auto kern = gemm_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
-  static int per_sm = [&] {
+  static const bool configured = [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, smem);
-    return nb > 0 ? nb : 1;
+    return true;
   }();
+  (void)configured;
   const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   GemmArgs<T> g = a;
   g.tiles_m = tm;
   g.ntiles = MODE == TRI_FULL ? (long long)tm * tn : (long long)tm * (tm + 1) / 2;
-  long long grid = g.ntiles;
-  if (a.ntiles > 0 && grid > a.ntiles * per_sm) grid = a.ntiles * per_sm;  // GemmCap (SMs)
+  const long long grid = g.ntiles;
   kern<<<(unsigned)grid, NT, smem, st>>>(g);
   RFPK_CHECK_LAUNCH();
   return 0;
@@ -307,12 +305,7 @@ int launch_mode(const GemmArgs<T>& a, int mode, bool ak, bool bk, cudaStream_t s
 
 }  // namespace
 
-namespace {
-thread_local int tl_cta_cap = 0;
-}
-int gemm_cta_cap() { return tl_cta_cap; }
-GemmCap::GemmCap(int n) : prev(tl_cta_cap) { tl_cta_cap = n; }
-GemmCap::~GemmCap() { tl_cta_cap = prev; }
+
 
 template <typename T>
 int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T beta,
@@ -354,7 +347,7 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
   g.herm_diag = herm_diag ? 1 : 0;
   g.skip = skip;
   g.tiles_m = 0;
-  g.ntiles = gemm_cta_cap();  // launch_one turns this into the tile count
+  g.ntiles = 0;  // set by launch_one
   g.a_tri = transposed ? A_FULL : a_tri;
   g.b_tri = transposed ? a_tri : A_FULL;
   // operand "K-major": A contiguous along K  <=> la.kmajor; for B, B^T (N x K)

@@ -34,20 +34,9 @@ template <typename T> struct GemmArgs {
   int tiles_m;        // tiles along M (for the triangular mapping)
   int a_tri;          // A operand mask: 0 none, 1 lower, 2 upper, 3 strict lower, 4 strict upper
   int b_tri;          // same mask applied to B (k, n) as if it were A (n, k) (transposed problems)
-  long long ntiles;   // tiles of the launch; CTAs stride over them (grid may be capped)
+  long long ntiles;   // tiles of the launch (CTAs stride over them)
 };
 
-// Cap, in SMs' worth of resident CTAs, on subsequent gemm launches from this
-// host thread (0 = one CTA per tile).  Off-critical-path updates run under a
-// cap so that part of the GPU stays free for the latency-bound critical path
-// of a look-ahead schedule (its kernels would otherwise queue behind a full
-// wave of long update tiles).  RAII: GemmCap g(n);
-int gemm_cta_cap();
-struct GemmCap {
-  int prev;
-  explicit GemmCap(int n);
-  ~GemmCap();
-};
 
 // A-operand triangle masks (for triangular-times-matrix leaves)
 enum ATri : int { A_FULL = 0, A_LOWER = 1, A_UPPER = 2, A_SLOWER = 3, A_SUPPER = 4 };
