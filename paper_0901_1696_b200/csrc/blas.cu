@@ -443,8 +443,11 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
     if ((rc = leaf_inverses(c, lower ? Tm : Tm.t(), unit, own))) return rc;
     W = own;
   }
+  // the dataflow trsm for real data (complex tiles need 133 KB of smem -> one
+  // CTA per SM, where the recursive GEMM form measured faster: 65 vs 78 ms on
+  // config 5's S1 solve at n = 16000)
   static const i64 tile_min = env_int("RFPK_TILE_TRSM_MIN", 512);
-  if (Tm.m >= tile_min && !std::getenv("RFPK_NO_TILE_TRSM") &&
+  if (!is_cplx<T>::value && Tm.m >= tile_min && !std::getenv("RFPK_NO_TILE_TRSM") &&
       (rc = trsm_tiles(c, lower, conj, Tm, B, (const T*)W, !lower)) != -100) {
     ws_free(own, c.st);
     return rc;
