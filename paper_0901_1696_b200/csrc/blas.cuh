@@ -39,6 +39,10 @@ int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta
 template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W = nullptr);
 // dataflow tile Cholesky of a lower view (tile_potrf.cu); W required
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
+// the same on a tall panel P (m x n): potrf of its n x n head + solve of the
+// rows below (pftrf's potrf(T1) and S1 <- S1 T1^-H in one launch); -100 if
+// the layout is not supported (m > n needs n % 64 == 0)
+template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W);
 // dataflow tile trsm: conj?(Tm) X = B in place (tile_potrf.cu); W = lower-form
 // 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
 template <typename T>

@@ -91,12 +91,27 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
   int rc = 0;
   PhaseTrace tr(c.st, "pftrf");
   if (d.lower) {
-    rc = blas_potrf(c, 'L', t1, 0, W);
-    tr.mark("potrf(T1)");
-    if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
-    if (!rc && d.n2) {
-      if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
+    // RFPK_PANEL=1: potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over
+    // the tall panel [T1; S1] (contiguous rows of the normal rectangle).
+    // Measured neutral at n = 16384 (26.6 ms vs 7.8 + 18.2: the S1 tiles slow
+    // the diagonal chain as much as they fill its idle SMs), so off by default.
+    int fused = -100;
+    static const bool panel = std::getenv("RFPK_PANEL") != nullptr;
+    if (panel && !is_cplx<T>::value && !s1_ready && d.n2 && d.n1 % 64 == 0) {
+      View<T> panel{t1.p, d.n1 + d.n2, d.n1, t1.rs, t1.cs};
+      fused = potrf_panel_tiles(c, panel, d.n1, 0, W);
+    }
+    if (fused != -100) {
+      rc = fused;
+      tr.mark("potrf(T1)+trsm(S1)");
+    } else {
+      rc = blas_potrf(c, 'L', t1, 0, W);
+      tr.mark("potrf(T1)");
+      if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
+      if (!rc && d.n2) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
       tr.mark("trsm(S1)");
+    }
+    if (!rc && d.n2) {
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
       tr.mark("syrk(T2)");
       if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n1, W);

@@ -167,7 +167,8 @@ template <typename T> struct CholCtx {
   int* done;    // nt x nt tile flags
   int* pready;  // nt flags: diagonal partial sums written
   int* abort;
-  int base, n, nt;
+  int base, n, nt;  // columns (the factored order) and their tiles
+  int m, mt;        // rows and row tiles (m >= n: a tall panel [L11; L21])
 };
 
 template <typename T>
@@ -219,8 +220,8 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
   T* Bs = sm + STAGES * LA::SIZE;
   const i64 ld = KM ? X.A.rs : X.A.cs;
   TileLoader<T, TP, BK, TPT, KM> la, lb;
-  la.init(X.A.p, ld, i * TP, X.n, tid);
-  lb.init(X.A.p, ld, j * TP, X.n, tid);
+  la.init(X.A.p, ld, i * TP, X.m, tid);
+  lb.init(X.A.p, ld, j * TP, X.m, tid);
   auto ready = [&](int kc) -> bool {
     if (tid == 0) {
       bool ok = spin_wait(X.done + (i64)i * X.nt + kc, X.abort);
@@ -316,7 +317,7 @@ template <typename T>
 __device__ void build_c(const CholCtx<T>& X, int i, int j,
                         const double (&acc)[TileCfg<T>::NACC][2][4][4], T* S) {
   const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
-  const int mrows = X.n - (int)i0 < TP ? X.n - (int)i0 : TP;
+  const int mrows = X.m - (int)i0 < TP ? X.m - (int)i0 : TP;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -334,7 +335,7 @@ __device__ void apply_w(const CholCtx<T>& X, int i, int j, T* S, T* Ws,
                         double (&x)[TileCfg<T>::NACC][2][4][4], T* Xs) {
   const int tid = threadIdx.x;
   const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
-  const int mrows = X.n - (int)i0 < TP ? X.n - (int)i0 : TP;
+  const int mrows = X.m - (int)i0 < TP ? X.m - (int)i0 : TP;
   const T* w = X.W + (i64)j * TP * TP;
 #pragma unroll 8
   for (int e = tid; e < TP * TP; e += TPT) {
@@ -533,21 +534,27 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   return ok;
 }
 
-// Task list: DIAG0, then for g = 0 .. nt-2 the group
-//   [ SUPER(g) = tile (g+1, g) + diag g+1,  NORMAL (i, g) for i = g+2 .. nt-1,
-//     PARTIAL(g+2) (diag g+2 over chunks k <= g) ]
-// Every task depends only on tasks listed before it.
-__host__ __device__ inline long long chol_task_count(int nt) {
+// Task list: DIAG0, then for every column block g = 0 .. nt-1 the group
+//   [ SUPER(g) = tile (g+1, g) + diag g+1          (if g+1 < nt),
+//     NORMAL (i, g) for i = g+2 .. mt-1 (g+1 .. mt-1 when there is no SUPER),
+//     PARTIAL(g+2) = diag g+2 over chunks k <= g  (if g+2 < nt) ]
+// Every task depends only on tasks listed before it.  mt > nt: a tall panel
+// whose rows below the last diagonal tile are solved like any other tile.
+__host__ __device__ inline long long chol_group_size(int g, int nt, int mt) {
+  const int sup = g + 1 < nt ? 1 : 0;
+  const int first = g + 1 + sup;  // first NORMAL row tile
+  return sup + (mt > first ? mt - first : 0) + (g + 2 < nt ? 1 : 0);
+}
+__host__ __device__ inline long long chol_task_count(int nt, int mt) {
   long long t = nt > 0 ? 1 : 0;
-  for (int g = 0; g + 1 < nt; ++g) t += (g + 2 < nt) ? nt - g : 1;
+  for (int g = 0; g < nt; ++g) t += chol_group_size(g, nt, mt);
   return t;
 }
 
 template <typename T, bool KM>
 __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
-    tile_potrf_kernel(View<T> A, T* W, int* info, int base,
-                                                         int* sync, int nt,
-                                                         unsigned long long* trace) {
+    tile_potrf_kernel(View<T> A, int ncols, T* W, int* info, int base, int* sync, int nt, int mt,
+                      unsigned long long* trace) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
@@ -558,13 +565,15 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
   X.info = info;
   X.abort = sync + 1;
   X.done = sync + SYNC_HDR;
-  X.pready = X.done + (i64)nt * nt;
+  X.pready = X.done + (i64)mt * nt;
   X.base = base;
-  X.n = (int)A.m;
+  X.n = ncols;
   X.nt = nt;
-  const long long total = chol_task_count(nt);
+  X.m = (int)A.m;
+  X.mt = mt;
+  const long long total = chol_task_count(nt, mt);
   int g = 0;
-  long long gbase = 1;  // task index of SUPER(g)
+  long long gbase = 1;  // first task of group g
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(sync, 1);
     __syncthreads();
@@ -576,14 +585,17 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
       kind = TK_DIAG0; a = 0; b = 0;
     } else {
       for (;;) {
-        const long long gs = (g + 2 < nt) ? nt - g : 1;
+        const long long gs = chol_group_size(g, nt, mt);
         if (t < gbase + gs) break;
         gbase += gs;
         ++g;
       }
-      const int o = (int)(t - gbase);
-      if (o == 0) { kind = TK_SUPER; a = g + 1; b = g; }
-      else if (o <= nt - g - 2) { kind = TK_NORMAL; a = g + 1 + o; b = g; }
+      int o = (int)(t - gbase);
+      const int sup = g + 1 < nt ? 1 : 0;
+      const int first = g + 1 + sup;
+      const int nnorm = mt > first ? mt - first : 0;
+      if (sup && o == 0) { kind = TK_SUPER; a = g + 1; b = g; }
+      else if ((o -= sup) < nnorm) { kind = TK_NORMAL; a = first + o; b = g; }
       else { kind = TK_PARTIAL; a = g + 2; b = 0; }
     }
     if (!run_task<T, KM>(X, kind, a, b, sm, &s_ok, trace ? trace + 8 * t : nullptr)) return;
@@ -591,12 +603,12 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
 }
 
 template <typename T, bool KM>
-int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
+int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, int mt) {
   // RFPK_TILE_TRACE=file: per-task globaltimer stamps (start, acc done, diag
   // ready, published), tile and CTA -> CSV (debug only; synchronises)
   static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
   unsigned long long* trace = nullptr;
-  const long long ntask = chol_task_count(nt);
+  const long long ntask = chol_task_count(nt, mt);
   if (trace_file) {
     cudaMallocManaged(&trace, ntask * 8 * sizeof(unsigned long long));
     cudaMemset(trace, 0, ntask * 8 * sizeof(unsigned long long));
@@ -616,7 +628,7 @@ int tile_launch(View<T> A, T* W, Ctx c, int base, int* sync, int nt) {
   }();
   long long grid = (long long)(cap > 0 && cap < per_sm ? cap : per_sm) * num_sms();
   if (grid > tasks) grid = tasks;
-  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, W, c.info, base, sync, nt, trace);
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt, trace);
   RFPK_CHECK_LAUNCH();
   if (trace) {
     cudaStreamSynchronize(c.st);
@@ -990,26 +1002,36 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
 template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, const double*, bool);
 template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool);
 
-// Factor the lower view A (col- or row-major) with the dataflow kernel.
-// W (leaf-inverse slabs for ceil(n/64) tiles) is required.
-template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
-  const i64 n = A.m;
+// Factor the tall lower panel P (m x n, m >= n, col- or row-major): the
+// Cholesky of its leading n x n block and the solve of the rows below it,
+// P = [L11; L21] with L21 = P21 L11^-H, in one dataflow launch.  m == n is
+// potrf.  W (leaf-inverse slabs for ceil(n/64) tiles) is required.
+template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W) {
+  const i64 m = P.m;
   if (n == 0) return 0;
-  if (!W) return -100;
-  const bool km = !(A.rs == 1);
-  if (km && A.cs != 1) return -100;
-  const int nt = (int)((n + TP - 1) / TP);
-  const size_t ints = SYNC_HDR + (size_t)nt * nt + nt;  // + the partial-ready flags
+  if (!W || m < n) return -100;
+  const bool km = !(P.rs == 1);
+  if (km && P.cs != 1) return -100;
+  const int nt = (int)((n + TP - 1) / TP), mt = (int)((m + TP - 1) / TP);
+  // the row tiles must break at n: the rows below are off-diagonal tiles
+  if (mt > nt && n % TP) return -100;
+  const size_t ints = SYNC_HDR + (size_t)mt * nt + nt;  // + the partial-ready flags
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
   if (e != cudaSuccess) return (int)e;
   if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
-  int rc = km ? tile_launch<T, true>(A, W, c, base, sync, nt)
-              : tile_launch<T, false>(A, W, c, base, sync, nt);
+  int rc = km ? tile_launch<T, true>(P, (int)n, W, c, base, sync, nt, mt)
+              : tile_launch<T, false>(P, (int)n, W, c, base, sync, nt, mt);
   cudaFreeAsync(sync, c.st);
   return rc;
 }
 
+template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
+  return potrf_panel_tiles(c, A, A.m, base, W);
+}
+
+template int potrf_panel_tiles<double>(Ctx, View<double>, i64, int, double*);
+template int potrf_panel_tiles<Z>(Ctx, View<Z>, i64, int, Z*);
 template int potrf_tiles<double>(Ctx, View<double>, int, double*);
 template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
 
