@@ -44,20 +44,40 @@ constexpr int TPT = 128;  // threads per CTA (4 warps, 2 x 2 of 32 x 32)
 constexpr int STAGES = 3;
 constexpr int SYNC_HDR = 32;  // ints before the flag array: [0] counter, [1] abort
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// acquire side of the flag protocol: relaxed polls (no L1 invalidation per
+// poll), then ONE acquire fence once the flags are seen set
+__device__ __forceinline__ void fence_acquire() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// one thread: wait for *f != 0 with acquire loads (the tile trsm's chain
+// wait: measured faster there than relaxed polling + a fence)
+__device__ void spin_wait_acquire(const int* f) {
+  unsigned ns = 32;
+  while (!ld_acquire(f)) {
+    __nanosleep(ns);
+    if (ns < 256) ns *= 2;
+  }
 }
-// one thread: wait for *f != 0 (true) or an abort (false; abort may be null)
+// one thread: wait for *f != 0 (true) or an abort (false; abort may be null);
+// the caller issues fence_acquire() before trusting data guarded by *f
 __device__ bool spin_wait(const int* f, const int* abort) {
   unsigned ns = 32;
   for (;;) {
-    if (ld_acquire(f)) return true;
-    if (abort && ld_acquire(abort)) return false;
+    if (ld_relaxed(f)) return true;
+    if (abort && ld_relaxed(abort)) return false;
     __nanosleep(ns);
     if (ns < 256) ns *= 2;
   }
@@ -199,7 +219,10 @@ __device__ __forceinline__ void publish(int* f) {
   }
 }
 __device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok) {
-  if (threadIdx.x == 0) *s_ok = spin_wait(f, abort);
+  if (threadIdx.x == 0) {
+    *s_ok = spin_wait(f, abort);
+    fence_acquire();
+  }
   __syncthreads();
   return *s_ok != 0;
 }
@@ -222,14 +245,27 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
   TileLoader<T, TP, BK, TPT, KM> la, lb;
   la.init(X.A.p, ld, i * TP, X.m, tid);
   lb.init(X.A.p, ld, j * TP, X.m, tid);
+  // chunk kc's tiles are final.  Thread 0 also scans ahead over chunks that
+  // are already published, so a task whose inputs are all done pays ONE
+  // barrier instead of one per chunk.  *s_ok = 1 + last verified chunk, or 0
+  // on abort (read by all threads before the loop's next barrier).
+  int known = -1;
   auto ready = [&](int kc) -> bool {
+    if (kc <= known) return true;
     if (tid == 0) {
       bool ok = spin_wait(X.done + (i64)i * X.nt + kc, X.abort);
       if (ok && i != j) ok = spin_wait(X.done + (i64)j * X.nt + kc, X.abort);
-      *s_ok = ok;
+      int k2 = kc;
+      if (ok)
+        while (k2 + 1 < kend && ld_relaxed(X.done + (i64)i * X.nt + k2 + 1) &&
+               (i == j || ld_relaxed(X.done + (i64)j * X.nt + k2 + 1)))
+          ++k2;
+      fence_acquire();
+      *s_ok = ok ? k2 + 1 : 0;
     }
     __syncthreads();
-    return *s_ok != 0;
+    known = *s_ok - 1;
+    return known >= kc;
   };
   auto load_stage = [&](int stage) {
     la.load(As + stage * LA::SIZE);
@@ -743,14 +779,14 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   int kvalid = TP;  // valid k of the chunk being loaded
   // wait for X(kk, c) and point the loaders at chunk kk
   auto open_chunk = [&](int kk) -> bool {
-    if (tid == 0) *s_ok = spin_wait(done + (i64)kk * a.nc + c, nullptr);
+    if (tid == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
     __syncthreads();
     const T* ta = AK ? Tm.p + (i64)kk * TP : Tm.p + (i64)kk * TP * Tm.cs;
     la.init(ta, lda, i * TP, a.n, tid);
     const T* tb = BKM ? B.p + (i64)kk * TP : B.p + (i64)kk * TP * B.rs;
     lb.init(tb, ldb, c * TP, a.nrhs, tid);
     kvalid = a.n - kk * TP < TP ? a.n - kk * TP : TP;
-    return *s_ok != 0;
+    return true;  // (the solve never aborts: trsm inputs cannot fail)
   };
   auto load_stage = [&](int stage, int q) {
     const int k0 = (q % SPC) * BK;
