@@ -1,6 +1,9 @@
-// Recursive full-format kernels (potrf / trsm / trmm / trtri / lauum / herk)
-// built on the DMMA GEMM, with one-CTA shared-memory leaf kernels for the
-// <= LEAF diagonal blocks.
+// Full-format drivers (potrf / trsm / trmm / trtri / lauum / herk).
+//
+// potrf (every n > 64) and real trsm (n >= 512) dispatch to the dataflow tile
+// kernels of tile_potrf.cu.  Everything else -- trmm, trtri, lauum, complex
+// trsm, small orders -- is the recursive form below, built on the DMMA GEMM
+// with one-CTA shared-memory leaf kernels for the <= LEAF diagonal blocks.
 //
 // Reference semantics (kernels.py) are kept; the *algorithm* is B200-first:
 // instead of the reference's blocked loops with per-row Python updates
