@@ -119,6 +119,15 @@ int rfpk_ztftri(char transr, char uplo, char diag, int64_t n, void* arf, int* in
 int rfpk_dpftri(char transr, char uplo, int64_t n, double* arf, int* info, rfpk_stream_t stream);
 int rfpk_zpftri(char transr, char uplo, int64_t n, void* arf, int* info, rfpk_stream_t stream);
 
+/* Phase clock (measurement only, no reference counterpart): when enabled,
+   every direct (non-graph) pftrf / pftrs call records CUDA events around its
+   SRPA steps on its own stream without synchronising; rfpk_phase_time()
+   waits for them and returns the summed milliseconds and the count for one
+   label, e.g. "pftrf trsm(S1)".  Enabling resets the sums.  Returns 1 if
+   the label was never seen. */
+int rfpk_phase_clock(int enable);
+int rfpk_phase_time(const char* label, double* total_ms, int64_t* count);
+
 /* packed Cholesky ------------------------------------ */
 /* replaces packed.pptrf_ref(p)   packed.py:70-108 -- in place on the
    column-packed triangle ap (n(n+1)/2 elements, LAPACK 'L'/'U' packing);

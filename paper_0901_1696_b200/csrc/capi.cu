@@ -314,6 +314,19 @@ int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s
 
 int rfpk_dpftrf_host(char t, char u, int64_t n, const double* h, double* d, int* info, rfpk_stream_t s) { return pftrf_host_t<double>(t, u, n, h, d, info, S(s)); }
 int rfpk_zpftrf_host(char t, char u, int64_t n, const void* h, void* d, int* info, rfpk_stream_t s) { return pftrf_host_t<Z>(t, u, n, h, d, info, S(s)); }
+int rfpk_phase_clock(int enable) {
+  phase_clock_enable(enable != 0);
+  return 0;
+}
+int rfpk_phase_time(const char* label, double* total_ms, int64_t* count) {
+  if (!label || !total_ms || !count) return -1;
+  long long c = 0;
+  double t = 0;
+  if (!phase_clock_read(label, &t, &c)) { *total_ms = 0; *count = 0; return 1; }
+  *total_ms = t;
+  *count = c;
+  return 0;
+}
 int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }
 int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { return pptrf_t<Z>(u, n, ap, info, S(s)); }
 int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }

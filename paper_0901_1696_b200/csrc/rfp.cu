@@ -3,6 +3,10 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 
 namespace rfpk {
 
@@ -40,10 +44,42 @@ template <typename T> static T m_one() { return sc_from<T>(-1.0); }
 
 // RFPK_TRACE=1: per-phase GPU times of the SRPA steps (direct, non-captured
 // calls only), printed to stderr -- a poor man's timeline without nsys.
+// Phase timing of the SRPA steps.  RFPK_TRACE=1 prints each direct call's
+// phases to stderr (synchronising); the phase clock (rfpk_phase_clock) only
+// records event pairs, summed per "routine phase" label when
+// rfpk_phase_time() is asked -- so a benchmark can time its dominant kernel
+// live inside the timed region without perturbing it.  Captured (graph)
+// calls are never traced.
+struct PhaseClock {
+  std::mutex mu;
+  bool on = false;
+  struct Pending { std::string label; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> owned;  // destroyed once read
+  std::map<std::string, std::pair<double, long long>> sums;
+  static PhaseClock& get() {
+    static PhaseClock c;
+    return c;
+  }
+  void drain() {  // caller holds mu
+    for (auto& p : pending) {
+      cudaEventSynchronize(p.b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      auto& e = sums[p.label];
+      e.first += ms;
+      e.second += 1;
+    }
+    pending.clear();
+    for (cudaEvent_t e : owned) cudaEventDestroy(e);
+    owned.clear();
+  }
+};
+
 struct PhaseTrace {
   cudaStream_t st;
   const char* name;
-  bool on = false;
+  bool print = false, clock = false;
   cudaEvent_t ev[8];
   const char* lab[8];
   int k = 0;
@@ -51,17 +87,27 @@ struct PhaseTrace {
     const char* v = std::getenv("RFPK_TRACE");
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
-    on = v && v[0] == '1' && cs == cudaStreamCaptureStatusNone;
-    if (on) mark("start");
+    if (cs != cudaStreamCaptureStatusNone) return;
+    print = v && v[0] == '1';
+    clock = PhaseClock::get().on;
+    if (print || clock) mark("start");
   }
   void mark(const char* l) {
-    if (!on || k >= 8) return;
+    if (!(print || clock) || k >= 8) return;
     cudaEventCreate(&ev[k]);
     cudaEventRecord(ev[k], st);
     lab[k++] = l;
   }
   ~PhaseTrace() {
-    if (!on) return;
+    if (!(print || clock)) return;
+    if (clock) {
+      PhaseClock& pc = PhaseClock::get();
+      std::lock_guard<std::mutex> g(pc.mu);
+      for (int i = 1; i < k; ++i)
+        pc.pending.push_back({std::string(name) + " " + lab[i], ev[i - 1], ev[i]});
+      for (int i = 0; i < k; ++i) pc.owned.push_back(ev[i]);
+      return;  // read (and synchronised) only by rfpk_phase_time
+    }
     cudaEventSynchronize(ev[k - 1]);
     for (int i = 1; i < k; ++i) {
       float ms = 0;
@@ -622,5 +668,23 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
   template int lansf<T>(cudaStream_t, const RfpDesc&, char, const T*, double*);
 RFPK_RFP_INST(double)
 RFPK_RFP_INST(Z)
+
+void phase_clock_enable(bool on) {
+  PhaseClock& pc = PhaseClock::get();
+  std::lock_guard<std::mutex> g(pc.mu);
+  pc.drain();
+  pc.sums.clear();
+  pc.on = on;
+}
+bool phase_clock_read(const char* label, double* total_ms, long long* count) {
+  PhaseClock& pc = PhaseClock::get();
+  std::lock_guard<std::mutex> g(pc.mu);
+  pc.drain();
+  auto it = pc.sums.find(label);
+  if (it == pc.sums.end()) return false;
+  *total_ms = it->second.first;
+  *count = it->second.second;
+  return true;
+}
 
 }  // namespace rfpk

@@ -40,6 +40,10 @@ int sfrk(Ctx c, const RfpDesc& d, char trans, i64 k, double alpha, View<T> a, do
 template <typename T> int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf,
                                 double* out);
 
+// phase clock (see PhaseTrace in rfp.cu)
+void phase_clock_enable(bool on);
+bool phase_clock_read(const char* label, double* total_ms, long long* count);
+
 // Storage descriptors for the conversion kernel.
 enum StorageKind : int { ST_FULL = 0, ST_PACKED = 1, ST_RFP = 2 };
 struct Storage {

@@ -500,3 +500,21 @@ def test_pftrf_from_host_streamed(P, uplo, transr, n):
     bad = O.trttf(np.eye(n) - 2.0 * (np.arange(n) == n // 2)[:, None] * np.eye(n), uplo, transr)
     _, info = rfp.pftrf_from_host(bad, n, uplo, transr)
     assert info == n // 2 + 1
+
+
+def test_phase_clock_times_srpa_steps(P):
+    """rfpk_phase_clock / rfpk_phase_time: event pairs around the SRPA steps of
+    direct calls, read without synchronising the calls themselves."""
+    import ctypes
+    from paper_0901_1696_b200 import _capi
+    lib = _capi.lib()
+    n = 1037  # an order no other test uses: the first call is direct (not a graph replay)
+    a = O.spd_matrix(n, 9, "n")
+    lib.rfpk_phase_clock(1)
+    r = P.convert.trttf(a, "L", "N")
+    assert P.rfp.pftrf(r) == 0  # first call of this shape: direct
+    tot, cnt = ctypes.c_double(0), ctypes.c_int64(0)
+    assert lib.rfpk_phase_time(b"pftrf syrk(T2)", ctypes.byref(tot), ctypes.byref(cnt)) == 0
+    assert cnt.value >= 1 and tot.value > 0
+    assert lib.rfpk_phase_time(b"no such phase", ctypes.byref(tot), ctypes.byref(cnt)) == 1
+    lib.rfpk_phase_clock(0)
