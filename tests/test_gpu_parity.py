@@ -518,3 +518,38 @@ def test_phase_clock_times_srpa_steps(P):
     assert cnt.value >= 1 and tot.value > 0
     assert lib.rfpk_phase_time(b"no such phase", ctypes.byref(tot), ctypes.byref(cnt)) == 1
     lib.rfpk_phase_clock(0)
+
+
+def test_concurrent_host_threads_on_own_streams(P):
+    """Four host threads, each on its own CUDA stream, factor and solve
+    different matrices at the same time (tile kernels with per-call sync
+    buffers, thread-local graph capture, per-thread info buffers)."""
+    import threading
+    conv, rfp = P.convert, P.rfp
+    errs, res = [], {}
+
+    def work(tid):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    n = 700 + 37 * tid
+                    uplo, transr = "LU"[tid % 2], "NT"[(tid // 2) % 2]
+                    a = O.spd_matrix(n, 100 + tid, "n")
+                    r = conv.trttf(a, uplo, transr)
+                    assert rfp.pftrf(r) == 0
+                    b = np.random.default_rng(tid).standard_normal((n, 3))
+                    x = torch.from_numpy(b.copy()).cuda()
+                    rfp.pftrs(r, x)
+                    s.synchronize()
+                    res[(tid, rep)] = float(np.abs(a @ x.cpu().numpy() - b).max() / np.abs(b).max())
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert len(res) == 12 and max(res.values()) < 1e-9
