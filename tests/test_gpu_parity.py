@@ -553,3 +553,45 @@ def test_concurrent_host_threads_on_own_streams(P):
         t.join()
     assert not errs, errs
     assert len(res) == 12 and max(res.values()) < 1e-9
+
+
+# ---------------------------------------------------------------- SPEC acceptance checks
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("cplx", [False, True])
+def test_poisoned_other_triangle_never_read(P, uplo, transr, cplx):
+    """the unused triangle of the full input may hold NaN; trttf
+    (and trttp) read only the declared triangle, so the RFP buffer is NaN-free
+    and equal to the clean conversion bit for bit."""
+    conv, packed = P.convert, P.packed
+    n = 67
+    a = O.spd_matrix(n, 4, "n", complex_=cplx)
+    bad = a.copy()
+    iu = np.triu_indices(n, 1) if uplo == "L" else np.tril_indices(n, -1)
+    bad[iu] = np.nan
+    r = conv.trttf(bad, uplo, transr)
+    assert not torch.isnan(r.data).any()
+    assert bits(r.data) == bits(conv.trttf(a, uplo, transr).data)
+    p = packed.pack(bad, uplo)
+    assert not torch.isnan(p.data).any()
+
+
+@pytest.mark.parametrize("n", [129, 700])
+def test_inverse_residual_and_determinism(P, n):
+    """||A inv(A) - I||_F <= 1000 n eps, and SPEC.md:440: the same
+    input gives bit-identical factor and inverse on repeated runs."""
+    conv, rfp, layout = P.convert, P.rfp, P.layout
+    eps = 2.0 ** -53
+    for uplo, transr in [("L", "N"), ("U", "T")]:
+        a = O.spd_matrix(n, 21, "n")
+        outs = []
+        for rep in range(2):
+            r = conv.trttf(a, uplo, transr)
+            assert rfp.pftrf(r) == 0
+            f = bits(r.data)
+            assert rfp.pftri(r) == 0
+            outs.append((f, bits(r.data)))
+            inv = O.expand_hermitian(r.data.cpu().numpy(), n, uplo, transr)
+            res = np.linalg.norm(a @ inv - np.eye(n)) / (n * eps)
+            assert res <= 1000, (uplo, transr, res)
+        assert outs[0] == outs[1]
