@@ -662,7 +662,12 @@ int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, 
     const char* v = std::getenv("RFPK_TILE_PER_SM");
     return v ? std::atoi(v) : 0;
   }();
-  long long grid = (long long)(cap > 0 && cap < per_sm ? cap : per_sm) * num_sms();
+  // two CTAs per SM up to ~12k columns: the diagonal chain's CTA then shares
+  // its SM with one other task instead of two (measured: potrf 8192 7.69 ->
+  // 7.22 ms, 4000 2.22 -> 2.13); the bulk-bound larger orders keep three
+  int ps = per_sm > 2 && nt <= 192 ? 2 : per_sm;
+  if (cap > 0 && cap < per_sm) ps = cap;
+  long long grid = (long long)ps * num_sms();
   if (grid > tasks) grid = tasks;
   kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt, trace);
   RFPK_CHECK_LAUNCH();
