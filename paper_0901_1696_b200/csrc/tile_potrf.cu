@@ -748,6 +748,11 @@ __device__ __forceinline__ void smem_mm_ab(const T* As, const T* Bs,
   }
 }
 
+// prefetch W'_i into its own smem tile at the task start: only where the
+// register budget already limits the kernel to two CTAs per SM (the
+// column-major-B variants), so the extra 33 KB costs no occupancy
+template <typename T, bool BKM> constexpr bool trsm_prew() { return BKM && !is_cplx<T>::value; }
+
 struct TrsmArgs {
   int n, nrhs, nb, nc;
   int lower, conj, wtrans;
@@ -767,6 +772,20 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   T* Bs = sm + STAGES * LA::SIZE;
   const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
   const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
+  constexpr bool PREW = trsm_prew<T, BKM>();
+  constexpr int PIPE = STAGES * (LA::SIZE + LB::SIZE);
+  T* const Wpre = sm + (PIPE > TP * LD64 ? PIPE : TP * LD64);  // PREW only
+  if constexpr (PREW) {
+    // W'_i does not depend on any task: fetch it now (oldest cp.async group,
+    // complete before the first pipeline wait returns)
+    const T* w = W + (i64)i * TP * TP;
+    for (int e = tid; e < TP * TP; e += TPT) {
+      const int r = e & 63, k = e >> 6;
+      T* dst = a.wtrans ? Wpre + (k + r * LD64) : Wpre + (r + k * LD64);
+      cp_async8(dst, w + e, true);
+    }
+    cp_async_commit();
+  }
   auto chunk = [&](int q) { return a.lower ? q : a.nb - 1 - q; };
 
   TileLoader<T, TP, BK, TPT, AK> la;
@@ -875,7 +894,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
 
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
   T* S = sm;
-  T* Ws = S + TP * LD64;
+  T* Ws = PREW ? Wpre : S + TP * LD64;
   const i64 i0 = (i64)i * TP, c0 = (i64)c * TP;
   const int mrows = a.n - (int)i0 < TP ? a.n - (int)i0 : TP;
   const int ncols = a.nrhs - (int)c0 < TP ? a.nrhs - (int)c0 : TP;
@@ -892,7 +911,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
                                   : zero_<T>();
       }
   const T* w = W + (i64)i * TP * TP;
-  for (int e = tid; e < TP * TP; e += TPT) {
+  for (int e = tid; e < (PREW ? 0 : TP * TP); e += TPT) {
     const int r = e & 63, k = e >> 6;
     T v;
     if constexpr (is_cplx<T>::value) {
@@ -963,6 +982,10 @@ template <typename T, bool AK, bool BKM> size_t trsm_smem_bytes() {
   using C = TileCfg<T>;
   const size_t pipe = (size_t)STAGES * (SmemLayout<T, TP, C::BK, AK>::SIZE +
                                         SmemLayout<T, TP, C::BK, BKM>::SIZE);
+  if (trsm_prew<T, BKM>()) {
+    const size_t one = (size_t)TP * LD64;
+    return ((pipe > one ? pipe : one) + one) * sizeof(T);
+  }
   const size_t tiles = (size_t)2 * TP * LD64;
   return (pipe > tiles ? pipe : tiles) * sizeof(T);
 }
