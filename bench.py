@@ -361,13 +361,10 @@ def run_b200(args, rank, world, local):
     e2e_steps = max(1, args.steps // 2)
 
     def e2e_step():
-        # the RFP buffer's H2D copy is streamed under potrf(T1) by the API
-        r_, inf = rfp.pftrf_from_host(host_rfp, n, uplo, transr)
+        # one public call: pftrf + pftrs from pinned host memory, every copy
+        # overlapped with the computation by the library (rfp.pfsv_from_host)
+        r_, inf = rfp.pfsv_from_host(host_rfp, host_b.t(), n, uplo, transr, out=out_x.t())
         assert inf == 0
-        xb = host_b.to(dev, non_blocking=True).t()
-        rfp.pftrs(r_, xb)
-        out_x.copy_(xb.t(), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
 
     e2e_step()
     barrier(world)
@@ -411,7 +408,7 @@ def run_b200(args, rank, world, local):
         "residual_scaled": resid,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "path": "rfp.pftrf_from_host (H2D streamed under potrf(T1)) + rfp.pftrs (public API) on pinned host buffers"},
+                "path": "rfp.pfsv_from_host (public API): pinned host RFP + RHS in, solution out, transfers overlapped with pftrf/pftrs"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -110,6 +110,18 @@ int rfpk_dpftrf_host(char transr, char uplo, int64_t n, const double* h_arf, dou
                      int* info, rfpk_stream_t stream);
 int rfpk_zpftrf_host(char transr, char uplo, int64_t n, const void* h_arf, void* d_arf, int* info,
                      rfpk_stream_t stream);
+/* rfp.pftrf(r) then rfp.pftrs(r, b) on a problem that sits in pinned HOST
+   memory (h_arf: the RFP buffer; h_b: n x nrhs column-major, ld ldb), with
+   every transfer overlapped with the computation; the solution lands in
+   h_x (may equal h_b), the factor in d_arf, the device copy of B in d_b
+   (n x nrhs, ld ldb).  info as rfpk_?pftrf; on failure h_x is unspecified.
+   rfp.py:55-136 + the caller's copies. */
+int rfpk_dpfsv_host(char transr, char uplo, int64_t n, int64_t nrhs, const double* h_arf,
+                    double* d_arf, const double* h_b, double* d_b, double* h_x, int64_t ldb,
+                    int* info, rfpk_stream_t stream);
+int rfpk_zpfsv_host(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_arf,
+                    void* d_arf, const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info,
+                    rfpk_stream_t stream);
 /* replaces rfp.tftri(r, diag)   rfp.py:286-325 */
 int rfpk_dtftri(char transr, char uplo, char diag, int64_t n, double* arf, int* info,
                 rfpk_stream_t stream);

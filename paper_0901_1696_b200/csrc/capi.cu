@@ -214,6 +214,67 @@ int pftrf_host_t(char transr, char uplo, int64_t n, const void* h_arf, void* d_a
   return pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done);
 }
 
+// pftrf + pftrs of a pinned HOST problem with every transfer overlapped:
+// T1/T2 rows first (stream), S1 rows then the right-hand side on a side
+// stream (hidden under potrf(T1) and the S1 solve), and the solution's
+// trailing block copied back while the last two solve steps still run.
+template <typename T>
+int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_arf, void* d_arf,
+                const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (nrhs < 0) return -4;
+  if (ldb < (n > 1 ? n : 1)) return -10;
+  if (!info) return -11;
+  if (int rc = reset_info(info, st)) return rc;
+  if (n == 0) return 0;
+  const RfpDesc d = rfp_desc(n, uplo, transr);
+  static thread_local cudaStream_t side = [] {
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    return s;
+  }();
+  static thread_local cudaEvent_t ev[4] = {};
+  if (!ev[0])
+    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEvent_t fork = ev[0], s1_done = ev[1], b_done = ev[2], b2_final = ev[3];
+  cudaError_t e = cudaEventRecord(fork, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+  if (e != cudaSuccess) return (int)e;
+  if (int rc = rfp_h2d_split<T>(d, (const T*)h_arf, (T*)d_arf, st, side)) return rc;
+  cudaEventRecord(s1_done, side);
+  const size_t col = (size_t)n * sizeof(T), pitch = (size_t)ldb * sizeof(T);
+  if (nrhs) {
+    e = cudaMemcpy2DAsync(d_b, pitch, h_b, pitch, col, (size_t)nrhs, cudaMemcpyHostToDevice, side);
+    if (e != cudaSuccess) return (int)e;
+  }
+  cudaEventRecord(b_done, side);
+  if (int rc = pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done)) return rc;
+  if (nrhs == 0) return 0;
+  cudaStreamWaitEvent(st, b_done, 0);
+  // (after a failed factorization every solve kernel skips on *info)
+  const i64 split = d.lower ? d.n1 : d.n2;  // first row of the trailing block
+  const bool trail = n - split > 0 && !(d.lower && d.n2 == 0);
+  if (int rc = pftrs<T>(Ctx{st, info}, d, (const T*)d_arf, V<T>(d_b, n, nrhs, 1, ldb),
+                        trail ? b2_final : nullptr))
+    return rc;
+  if (trail) {
+    cudaStreamWaitEvent(side, b2_final, 0);
+    e = cudaMemcpy2DAsync((T*)h_x + split, pitch, (const T*)d_b + split, pitch,
+                          (size_t)(n - split) * sizeof(T), (size_t)nrhs, cudaMemcpyDeviceToHost,
+                          side);
+    if (e != cudaSuccess) return (int)e;
+  }
+  e = cudaMemcpy2DAsync(h_x, pitch, d_b, pitch, (size_t)(trail ? split : n) * sizeof(T),
+                        (size_t)nrhs, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return (int)e;
+  cudaEventRecord(fork, side);  // join the side stream back into `st`
+  cudaStreamWaitEvent(st, fork, 0);
+  return 0;
+}
+
 // ---------------------------------------------------------------- packed Cholesky
 // the reference's Level-2 packed comparator
 // (packed.py:70-146 pptrf_ref / pptrs_ref).  B200 design: the column-packed
@@ -327,6 +388,8 @@ int rfpk_phase_time(const char* label, double* total_ms, int64_t* count) {
   *count = c;
   return 0;
 }
+int rfpk_dpfsv_host(char t, char u, int64_t n, int64_t nrhs, const double* h_arf, double* d_arf, const double* h_b, double* d_b, double* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<double>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
+int rfpk_zpfsv_host(char t, char u, int64_t n, int64_t nrhs, const void* h_arf, void* d_arf, const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<Z>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
 int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }
 int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { return pptrf_t<Z>(u, n, ap, info, S(s)); }
 int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }

@@ -209,7 +209,8 @@ int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first,
 }
 
 // forward/back substitution through T1/S1/T2 (rfp.py:106-136)
-template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b) {
+template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
+                                cudaEvent_t b2_final) {
   if (d.n == 0 || b.n == 0) return 0;
   View<T> t1, t2, s1;
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
@@ -226,6 +227,7 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
       tr.mark("trsm2");
       TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false));
       tr.mark("trsm3");
+      if (b2_final) cudaEventRecord(b2_final, c.st);
       TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
       tr.mark("gemm2");
     }
@@ -240,6 +242,7 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
   }
   TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t2, b2, false));
   TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false));
+  if (b2_final) cudaEventRecord(b2_final, c.st);
   if (n2) {
     TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
     TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false));
@@ -659,7 +662,7 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
   template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t);                               \
   template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);                                            \
-  template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>);                             \
+  template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>, cudaEvent_t);                             \
   template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
   template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \
   template int convert<T>(const Storage&, const T*, const Storage&, T*, bool, cudaStream_t);  \

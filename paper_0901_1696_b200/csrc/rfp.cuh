@@ -25,7 +25,10 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
 // solve on) as two copies; see rfpk_?pftrf_host
 template <typename T>
 int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first, cudaStream_t second);
-template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b);
+template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
+                                cudaEvent_t b2_final = nullptr);
+// (b2_final: recorded once the trailing block of b -- rows [n1, n) for 'L',
+//  [n2, n) for 'U' -- holds its final values, before the last two steps)
 template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf);
 template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf);
 

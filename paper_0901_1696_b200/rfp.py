@@ -25,6 +25,7 @@ from .layout import make_descriptor, normalize_flag
 __all__ = [
     "pftrf",
     "pftrf_from_host",
+    "pfsv_from_host",
     "pftrs",
     "tfsm",
     "sfrk_hfrk",
@@ -108,6 +109,70 @@ def pftrf_from_host(data, n: int, uplo: str, transr: str):
     v = int(info.item())
     if v == 0:
         r.state = FactorState.CHOLESKY
+    return r, v
+
+
+def pfsv_from_host(data, b, n: int, uplo: str, transr: str, out=None):
+    """:func:`pftrf` then :func:`pftrs` for a problem that sits in host
+    memory, with every transfer overlapped with the computation (C ABI
+    ``rfpk_?pfsv_host``): the RFP buffer's T1/T2 rows first, its S1 rows and
+    the right-hand side on a side stream under potrf(T1) and the S1 solve,
+    and the solution's trailing block copied back during the last two solve
+    steps.  ``data``: ``n(n+1)/2`` scalars, ``b``: (n,) or (n, nrhs) host
+    arrays (pinned CPU tensors for truly asynchronous copies).  The solution
+    is written into ``out`` (default: ``b``).  Returns ``(RfpTriangle on the
+    device, info)`` like ``pftrf``; on failure the solution is unspecified."""
+    desc = make_descriptor(n, uplo, transr)
+    host = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+    bh = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b))
+    if host.is_cuda or bh.is_cuda:
+        raise ValueError("pfsv_from_host expects host memory; use pftrf/pftrs for device buffers")
+    cplx = host.is_complex() or bh.is_complex()
+    dt = torch.complex128 if cplx else torch.float64
+    host = host.to(dt).reshape(-1).contiguous()
+    if host.shape[0] != desc.nt:
+        raise ValueError(f"buffer length {host.shape[0]} != nt={desc.nt} for n={desc.n}")
+    flat = bh.dim() == 1
+    b2 = bh.reshape(-1, 1) if flat else bh
+    if b2.dim() != 2 or b2.shape[0] != n:
+        raise ValueError(f"right-hand side shape {tuple(bh.shape)} does not match order {n}")
+    bc = b2.to(dt)
+    if not (bc.stride(0) == 1 and bc.stride(1) == max(n, 1)):
+        bc = bc.t().contiguous().t()  # column-major, ld = n
+    dst = out if out is not None else b
+
+    def colmajor_view(t):
+        """t as an (n, nrhs) column-major ld=n dt tensor sharing memory, or None"""
+        if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != dt:
+            return None
+        v = t.reshape(-1, 1) if t.dim() == 1 else t
+        if v.shape != bc.shape or v.stride(0) != 1 or (v.shape[1] > 1 and v.stride(1) != max(n, 1)):
+            return None
+        return v
+
+    xc = colmajor_view(dst)
+    direct = xc is not None
+    if not direct:
+        xc = torch.empty((bc.shape[1], n), dtype=dt).t()
+    _capi.lib()
+    devn = torch.device("cuda", torch.cuda.current_device())
+    d_arf = torch.empty(desc.nt, dtype=dt, device=devn)
+    nrhs = bc.shape[1]
+    d_b = torch.empty((nrhs, n), dtype=dt, device=devn).t()
+    r = RfpTriangle(d_arf, desc)
+    info = _info(devn)
+    _run(f"rfpk_{_prefix(dt)}pfsv_host", _capi.flag(desc.transr), _capi.flag(desc.uplo), desc.n,
+         nrhs, host.data_ptr(), d_arf.data_ptr(), bc.data_ptr(), d_b.data_ptr(), xc.data_ptr(),
+         max(n, 1), info.data_ptr(), _capi.stream_handle(devn))
+    v = int(info.item())  # synchronises: the solution is on the host
+    if v == 0:
+        r.state = FactorState.CHOLESKY
+    if not direct:
+        res = xc.reshape(bh.shape) if flat else xc
+        if isinstance(dst, torch.Tensor):
+            dst.copy_(res)
+        else:
+            dst[...] = res.numpy()
     return r, v
 
 

@@ -595,3 +595,32 @@ def test_inverse_residual_and_determinism(P, n):
             res = np.linalg.norm(a @ inv - np.eye(n)) / (n * eps)
             assert res <= 1000, (uplo, transr, res)
         assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n", [1, 2, 130, 601])
+def test_pfsv_from_host_overlapped(P, uplo, transr, n):
+    """pftrf + pftrs of a host problem with the transfers overlapped: the same
+    factor (bit-identical) and solution as the device path."""
+    conv, rfp = P.convert, P.rfp
+    for cplx in (False, True):
+        a = O.spd_matrix(n, 5 + n, "n", complex_=cplx)
+        buf = O.trttf(a, uplo, transr)
+        g = np.random.default_rng(n)
+        b = g.standard_normal((n, 5)) + (1j * g.standard_normal((n, 5)) if cplx else 0)
+        hb = torch.from_numpy(b.T.copy()).pin_memory().t()  # pinned, column-major n x 5
+        out = torch.from_numpy(np.zeros((5, n), dtype=b.dtype)).pin_memory().t()
+        r, info = rfp.pfsv_from_host(torch.from_numpy(buf.copy()).pin_memory(), hb, n, uplo,
+                                     transr, out=out)
+        assert info == 0
+        ref = conv.RfpTriangle(buf.copy(), P.layout.make_descriptor(n, uplo, transr))
+        assert rfp.pftrf(ref) == 0
+        assert bits(r.data) == bits(ref.data)
+        xd = torch.from_numpy(b.copy()).cuda()
+        rfp.pftrs(ref, xd)
+        assert rel(out, xd.cpu()) <= 1e-12
+        # numpy in, solved in place; 1-D right-hand side
+        bn = np.array(b[:, 0])
+        rfp.pfsv_from_host(buf.copy(), bn, n, uplo, transr)
+        assert rel(bn, xd[:, 0].cpu()) <= 1e-12
