@@ -37,6 +37,21 @@ int blas_syrk(Ctx c, char uplo, char trans, double alpha, View<T> A, double beta
               bool herm);
 // potrf: L L^H (uplo L) / U^H U (uplo U); *info = base + first failing pivot
 template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W = nullptr);
+// Input gate for the dataflow kernels (host->device streaming): while an
+// InputGate is alive on this host thread, the next tile potrf waits for
+// flags[j] before reading any original tile of column block j, and the next
+// tile trsm waits for flags[mode == 0 ? i : c] before reading B's original
+// block (i, c).  The flags are set by the copy stream after each 64-column
+// chunk of the input has landed (rfpk_?pftrf_host / rfpk_?pfsv_host).
+struct InputGate {
+  const int* prev_flags;
+  int prev_mode;
+  InputGate(const int* flags, int mode);
+  ~InputGate();
+  static const int* flags();
+  static int mode();
+};
+
 // dataflow tile Cholesky of a lower view (tile_potrf.cu); W required
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
 // the same on a tall panel P (m x n): potrf of its n x n head + solve of the

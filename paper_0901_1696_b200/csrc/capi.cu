@@ -173,6 +173,38 @@ namespace rfpk {
 std::atomic<long long> g_launch_count{0};
 }
 
+// ---------------------------------------------------------------- host streaming
+// Start the host->device transfer of an RFP buffer on `copy` (forked from
+// `st`).  Real data at orders where pftrf's potrf(T1) and S1 solve run on
+// the dataflow tile kernels: 64-column chunks with per-chunk flags, so those
+// two steps consume the buffer while it arrives (*cflags / *sflags set,
+// `in_done` marks the end).  Otherwise two region copies, the S1 rows on the
+// copy stream (`in_done` = the S1 rows landed) and T1/T2's on `st`.
+template <typename T>
+static int h2d_rfp_begin(const RfpDesc& d, const void* h, void* dv, cudaStream_t st,
+                         cudaStream_t copy, cudaEvent_t fork, cudaEvent_t in_done, int** cflags,
+                         int** sflags) {
+  *cflags = *sflags = nullptr;
+  const bool chunked = !is_cplx<T>::value && d.n1 >= 512 && !std::getenv("RFPK_NO_TILE") &&
+                       !std::getenv("RFPK_NO_TILE_TRSM") && !std::getenv("RFPK_NO_STREAM_IN");
+  const i64 nch = (d.n1 + 63) / 64;
+  cudaError_t e = cudaSuccess;
+  if (chunked) {
+    int* f = nullptr;
+    if ((e = cudaMallocAsync((void**)&f, (size_t)2 * nch * sizeof(int), st)) != cudaSuccess)
+      return (int)e;
+    if ((e = cudaMemsetAsync(f, 0, (size_t)2 * nch * sizeof(int), st)) != cudaSuccess) return (int)e;
+    *cflags = f;
+    *sflags = f + nch;
+  }
+  if ((e = cudaEventRecord(fork, st)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamWaitEvent(copy, fork, 0)) != cudaSuccess) return (int)e;
+  int rc = chunked ? rfp_h2d_chunked<T>(d, (const T*)h, (T*)dv, *cflags, *sflags, copy)
+                   : rfp_h2d_split<T>(d, (const T*)h, (T*)dv, st, copy);
+  if (rc) return rc;
+  return (int)cudaEventRecord(in_done, copy);
+}
+
 // ---------------------------------------------------------------- pftrf from host
 // The factorization of a pinned HOST RFP buffer with the transfer streamed:
 // the rows holding T1/T2 are copied on `st` and potrf(T1) starts as soon as
@@ -205,13 +237,13 @@ int pftrf_host_t(char transr, char uplo, int64_t n, const void* h_arf, void* d_a
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     return e;
   }();
-  // the side copy must not overtake earlier work on `st` that uses d_arf
-  cudaError_t e = cudaEventRecord(fork, st);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
-  if (e != cudaSuccess) return (int)e;
-  if (int rc = rfp_h2d_split<T>(d, (const T*)h_arf, (T*)d_arf, st, side)) return rc;
-  if ((e = cudaEventRecord(s1_done, side)) != cudaSuccess) return (int)e;
-  return pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done);
+  int* cflags;
+  int* sflags;
+  if (int rc = h2d_rfp_begin<T>(d, h_arf, d_arf, st, side, fork, s1_done, &cflags, &sflags))
+    return rc;
+  int rc = pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done, cflags, sflags);
+  if (cflags) cudaFreeAsync(cflags, st);
+  return rc;
 }
 
 // pftrf + pftrs of a pinned HOST problem with every transfer overlapped:
@@ -240,18 +272,20 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   if (!ev[0])
     for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaEvent_t fork = ev[0], s1_done = ev[1], b_done = ev[2], b2_final = ev[3];
-  cudaError_t e = cudaEventRecord(fork, st);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
-  if (e != cudaSuccess) return (int)e;
-  if (int rc = rfp_h2d_split<T>(d, (const T*)h_arf, (T*)d_arf, st, side)) return rc;
-  cudaEventRecord(s1_done, side);
+  int* cflags;
+  int* sflags;
+  if (int rc = h2d_rfp_begin<T>(d, h_arf, d_arf, st, side, fork, s1_done, &cflags, &sflags))
+    return rc;
+  cudaError_t e;
   const size_t col = (size_t)n * sizeof(T), pitch = (size_t)ldb * sizeof(T);
   if (nrhs) {
     e = cudaMemcpy2DAsync(d_b, pitch, h_b, pitch, col, (size_t)nrhs, cudaMemcpyHostToDevice, side);
     if (e != cudaSuccess) return (int)e;
   }
   cudaEventRecord(b_done, side);
-  if (int rc = pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done)) return rc;
+  int rcf = pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done, cflags, sflags);
+  if (cflags) cudaFreeAsync(cflags, st);
+  if (rcf) return rcf;
   if (nrhs == 0) return 0;
   cudaStreamWaitEvent(st, b_done, 0);
   // (after a failed factorization every solve kernel skips on *info)

@@ -125,7 +125,9 @@ struct PhaseTrace {
   } while (0)
 
 // SRPA factorization (rfp.py:55-91)
-template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready) {
+template <typename T>
+int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cflags,
+          const int* sflags) {
   if (d.n == 0) return 0;
   const bool herm = is_cplx<T>::value;
   View<T> t1, t2, s1;
@@ -136,6 +138,16 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
   TRY(ws_alloc(&W, d.n1, c.st));
   int rc = 0;
   PhaseTrace tr(c.st, "pftrf");
+  // streamed input (cflags/sflags): potrf(T1) and the S1 solve read each
+  // 64-column chunk as soon as its flag is set; the remaining steps wait for
+  // the whole transfer (s1_ready) -- by then every chunk has been seen
+  const bool gated = cflags != nullptr;
+  auto before_s1 = [&]() {
+    if (!gated && !rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
+  };
+  auto after_s1 = [&]() {
+    if (gated && !rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
+  };
   if (d.lower) {
     // RFPK_PANEL=1: potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over
     // the tall panel [T1; S1] (contiguous rows of the normal rectangle).
@@ -151,10 +163,17 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
       rc = fused;
       tr.mark("potrf(T1)+trsm(S1)");
     } else {
-      rc = blas_potrf(c, 'L', t1, 0, W);
+      {
+        InputGate g(cflags, 0);
+        rc = blas_potrf(c, 'L', t1, 0, W);
+      }
       tr.mark("potrf(T1)");
-      if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
-      if (!rc && d.n2) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
+      before_s1();
+      if (!rc && d.n2) {
+        InputGate g(sflags, 0);  // B = S1^T: block row i <-> column chunk i
+        rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), t1, s1, false, W);
+      }
+      after_s1();
       tr.mark("trsm(S1)");
     }
     if (!rc && d.n2) {
@@ -165,10 +184,17 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
     }
   } else {
     if (d.n2) {
-      rc = blas_potrf(c, 'L', t1, 0, W);
+      {
+        InputGate g(cflags, 0);
+        rc = blas_potrf(c, 'L', t1, 0, W);
+      }
       tr.mark("potrf(T1)");
-      if (!rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
-      if (!rc) rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
+      before_s1();
+      if (!rc) {
+        InputGate g(sflags, 1);  // B = S1: block column c <-> column chunk c
+        rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
+      }
+      after_s1();
       tr.mark("trsm(S1)");
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
       tr.mark("syrk(T2)");
@@ -176,36 +202,72 @@ template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_
     if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n2, W);
     tr.mark("potrf(T2)");
   }
-  // (the S1 copy must also be complete on every early-exit path)
+  // (the transfers must also be complete on every early-exit path)
   if (s1_ready) cudaStreamWaitEvent(c.st, s1_ready, 0);
   ws_free(W, c.st);
   return rc;
 }
 
-// Rows [a, b) of the normal ldar x n1 rectangle as one copy: a 2-D strided
-// copy for TRANSR='N' (column-major rectangle), a contiguous block for 'T'.
+// Rows [r0, r1) x columns [c0, c1) of the normal ldar x n1 rectangle as one
+// 2-D copy (column-major rectangle for TRANSR='N', row-major for 'T').
 template <typename T>
-static cudaError_t copy_rows(const RfpDesc& d, const T* host, T* dev, i64 a, i64 b,
-                             cudaStream_t st) {
-  if (b <= a) return cudaSuccess;
-  if (d.trans)  // row r of the normal rectangle = n1 contiguous elements at r * n1
-    return cudaMemcpyAsync(dev + a * d.n1, host + a * d.n1, (size_t)(b - a) * d.n1 * sizeof(T),
+static cudaError_t copy_block(const RfpDesc& d, const T* host, T* dev, i64 r0, i64 r1, i64 c0,
+                              i64 c1, cudaStream_t st) {
+  if (r1 <= r0 || c1 <= c0) return cudaSuccess;
+  const size_t es = sizeof(T);
+  if (d.trans)  // element (r, c) at r * n1 + c
+    return cudaMemcpy2DAsync(dev + r0 * d.n1 + c0, (size_t)d.n1 * es, host + r0 * d.n1 + c0,
+                             (size_t)d.n1 * es, (size_t)(c1 - c0) * es, (size_t)(r1 - r0),
+                             cudaMemcpyHostToDevice, st);
+  return cudaMemcpy2DAsync(dev + r0 + c0 * d.ldar, (size_t)d.ldar * es, host + r0 + c0 * d.ldar,
+                           (size_t)d.ldar * es, (size_t)(r1 - r0) * es, (size_t)(c1 - c0),
                            cudaMemcpyHostToDevice, st);
-  return cudaMemcpy2DAsync(dev + a, (size_t)d.ldar * sizeof(T), host + a,
-                           (size_t)d.ldar * sizeof(T), (size_t)(b - a) * sizeof(T), (size_t)d.n1,
-                           cudaMemcpyHostToDevice, st);
+}
+
+// T1 and T2 live in the rows [0, n1 + d) (lower) / [n2, ldar) (upper) of the
+// normal rectangle, S1 in the rest (rfp_blocks)
+template <typename T>
+static void rfp_row_regions(const RfpDesc& d, i64& t0, i64& t1, i64& s0, i64& s1) {
+  t0 = d.lower ? 0 : d.n2;
+  t1 = d.lower ? d.n1 + d.d : d.ldar;
+  s0 = d.lower ? d.n1 + d.d : 0;
+  s1 = d.lower ? d.ldar : d.n2;
 }
 
 template <typename T>
 int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first,
                   cudaStream_t second) {
-  // T1 and T2 live in the rows [0, n1 + d) (lower) / [n2, ldar) (upper) of the
-  // normal rectangle, S1 in the rest (rfp_blocks)
-  const i64 t0 = d.lower ? 0 : d.n2, t1 = d.lower ? d.n1 + d.d : d.ldar;
-  const i64 s0 = d.lower ? d.n1 + d.d : 0, s1 = d.lower ? d.ldar : d.n2;
-  cudaError_t e = copy_rows(d, host, dev, t0, t1, first);
-  if (e == cudaSuccess) e = copy_rows(d, host, dev, s0, s1, second);
+  i64 t0, t1, s0, s1;
+  rfp_row_regions<T>(d, t0, t1, s0, s1);
+  cudaError_t e = copy_block(d, host, dev, t0, t1, 0, d.n1, first);
+  if (e == cudaSuccess) e = copy_block(d, host, dev, s0, s1, 0, d.n1, second);
   return (int)e;
+}
+
+template <typename T>
+int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* sflags,
+                    cudaStream_t copy) {
+  static int* one = [] {  // pinned source of the flag value
+    int* p = nullptr;
+    cudaMallocHost((void**)&p, sizeof(int));
+    *p = 1;
+    return p;
+  }();
+  i64 t0, t1, s0, s1;
+  rfp_row_regions<T>(d, t0, t1, s0, s1);
+  const i64 nch = (d.n1 + 63) / 64;
+  for (int region = 0; region < 2; ++region) {
+    const i64 r0 = region ? s0 : t0, r1 = region ? s1 : t1;
+    int* flags = region ? sflags : cflags;
+    for (i64 j = 0; j < nch; ++j) {
+      const i64 c0 = j * 64, c1 = c0 + 64 < d.n1 ? c0 + 64 : d.n1;
+      cudaError_t e = copy_block(d, host, dev, r0, r1, c0, c1, copy);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(flags + j, one, sizeof(int), cudaMemcpyHostToDevice, copy);
+      if (e != cudaSuccess) return (int)e;
+    }
+  }
+  return 0;
 }
 
 // forward/back substitution through T1/S1/T2 (rfp.py:106-136)
@@ -660,8 +722,9 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
 
 #define RFPK_RFP_INST(T)                                                                     \
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
-  template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t);                               \
-  template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);                                            \
+  template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t, const int*, const int*);                               \
+  template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);   \
+  template int rfp_h2d_chunked<T>(const RfpDesc&, const T*, T*, int*, int*, cudaStream_t);                                            \
   template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>, cudaEvent_t);                             \
   template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
   template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \

@@ -19,12 +19,24 @@ RfpDesc rfp_desc(i64 n, char uplo, char transr);
 template <typename T> void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2,
                                       View<T>& s1);
 
-template <typename T> int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr);
+template <typename T>
+int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr,
+          const int* cflags = nullptr, const int* sflags = nullptr);
+// (s1_ready: the S1 rows' transfer; with cflags / sflags the input is being
+//  streamed in 64-column chunks of the normal rectangle, chunk j of the T1/T2
+//  rows flagged in cflags[j] and of the S1 rows in sflags[j], and s1_ready
+//  marks the end of the whole transfer; see rfp_h2d_chunked)
 // host -> device streaming helper for pftrf: the rows of the normal rectangle
 // holding T1 and T2 (first needed) and those holding S1 (needed from the S1
 // solve on) as two copies; see rfpk_?pftrf_host
 template <typename T>
 int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first, cudaStream_t second);
+// the same two row regions, each in 64-column chunks of the normal
+// rectangle, on ONE copy stream, setting cflags[j] / sflags[j] (device ints,
+// zeroed by the caller) after chunk j of the T1/T2 rows / of the S1 rows
+template <typename T>
+int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* sflags,
+                    cudaStream_t copy);
 template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
                                 cudaEvent_t b2_final = nullptr);
 // (b2_final: recorded once the trailing block of b -- rows [n1, n) for 'L',

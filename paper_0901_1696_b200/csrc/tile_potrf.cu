@@ -37,6 +37,22 @@
 #include <cstdlib>
 
 namespace rfpk {
+
+namespace {
+thread_local const int* tl_gate = nullptr;
+thread_local int tl_gate_mode = 0;
+}  // namespace
+InputGate::InputGate(const int* f, int m) : prev_flags(tl_gate), prev_mode(tl_gate_mode) {
+  tl_gate = f;
+  tl_gate_mode = m;
+}
+InputGate::~InputGate() {
+  tl_gate = prev_flags;
+  tl_gate_mode = prev_mode;
+}
+const int* InputGate::flags() { return tl_gate; }
+int InputGate::mode() { return tl_gate_mode; }
+
 namespace {
 
 constexpr int TP = 64;    // tile order (== LEAF)
@@ -189,6 +205,7 @@ template <typename T> struct CholCtx {
   int* abort;
   int base, n, nt;  // columns (the factored order) and their tiles
   int m, mt;        // rows and row tiles (m >= n: a tall panel [L11; L21])
+  const int* ext;   // optional input gate: column block j readable once ext[j]
 };
 
 template <typename T>
@@ -453,6 +470,13 @@ template <typename T> __device__ void load_diag(const CholCtx<T>& X, int d, T* S
   }
 }
 
+// the input gate (if any): column block j of A's original data has landed
+template <typename T>
+__device__ __forceinline__ bool wait_input(const CholCtx<T>& X, int j, int* s_ok) {
+  if (!X.ext) return true;
+  return wait_flag(const_cast<int*>(X.ext) + j, X.abort, s_ok);
+}
+
 template <typename T, bool KM>
 __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int* s_ok,
                          unsigned long long* tr) {
@@ -464,6 +488,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   double acc[C::NACC][2][4][4];
   zero_acc<T>(acc);
   if (kind == TK_DIAG0) {
+    if (!wait_input(X, 0, s_ok)) return false;
     load_diag(X, 0, S);
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
@@ -475,6 +500,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
     // A(d, d) <- A(d, d) - sum_{k < d-1} L(d, k) L(d, k)^H  (lower part)
     const int d = a;
     if (!accumulate<T, KM>(X, d, d, d - 1, sm, s_ok, acc)) return false;
+    if (!wait_input(X, d, s_ok)) return false;
     const i64 d0 = (i64)d * TP;
     const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
 #pragma unroll
@@ -498,6 +524,9 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   const int i = a, j = b;
   if (!accumulate<T, KM>(X, i, j, j, sm, s_ok, acc)) return false;
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
+  if (!wait_input(X, j, s_ok)) return false;
+  // (diag 1 has no partial task: its original tile is read below)
+  if (kind == TK_SUPER && i == 1 && !wait_input(X, 1, s_ok)) return false;
   build_c(X, i, j, acc, S);
   const int d = i;  // super: the diagonal tile factored next
   const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
@@ -590,7 +619,7 @@ __host__ __device__ inline long long chol_task_count(int nt, int mt) {
 template <typename T, bool KM>
 __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
     tile_potrf_kernel(View<T> A, int ncols, T* W, int* info, int base, int* sync, int nt, int mt,
-                      unsigned long long* trace) {
+                      const int* ext, unsigned long long* trace) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
@@ -607,6 +636,7 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
   X.nt = nt;
   X.m = (int)A.m;
   X.mt = mt;
+  X.ext = ext;
   const long long total = chol_task_count(nt, mt);
   int g = 0;
   long long gbase = 1;  // first task of group g
@@ -669,7 +699,8 @@ int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, 
   if (cap > 0 && cap < per_sm) ps = cap;
   long long grid = (long long)ps * num_sms();
   if (grid > tasks) grid = tasks;
-  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt, trace);
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt,
+                                            InputGate::flags(), trace);
   RFPK_CHECK_LAUNCH();
   if (trace) {
     cudaStreamSynchronize(c.st);
@@ -756,6 +787,8 @@ template <typename T, bool BKM> constexpr bool trsm_prew() { return BKM && !is_c
 struct TrsmArgs {
   int n, nrhs, nb, nc;
   int lower, conj, wtrans;
+  const int* ext;  // input gate (see InputGate): B(i, c) readable once ext[ext_mode ? c : i]
+  int ext_mode;
 };
 
 template <typename T, bool AK, bool BKM>
@@ -892,6 +925,10 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   if (nprev > 0 && !*s_ok) return false;
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
+  if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
+    if (tid == 0) spin_wait_acquire(a.ext + (a.ext_mode ? c : i));
+    __syncthreads();
+  }
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
   T* S = sm;
   T* Ws = PREW ? Wpre : S + TP * LD64;
@@ -1047,6 +1084,8 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.lower = lower ? 1 : 0;
   a.conj = conj ? 1 : 0;
   a.wtrans = wtrans ? 1 : 0;
+  a.ext = InputGate::flags();
+  a.ext_mode = InputGate::mode();
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);

@@ -483,7 +483,7 @@ def test_packed_cholesky_large_vs_oracle(P, uplo, cplx):
 
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
-@pytest.mark.parametrize("n", [7, 130, 601])
+@pytest.mark.parametrize("n", [7, 130, 601, 1100, 2049])
 def test_pftrf_from_host_streamed(P, uplo, transr, n):
     """The streamed host->device pftrf gives the same factor (bit-identical)
     as a device pftrf of the same buffer, and the same failure index."""
@@ -599,7 +599,7 @@ def test_inverse_residual_and_determinism(P, n):
 
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
-@pytest.mark.parametrize("n", [1, 2, 130, 601])
+@pytest.mark.parametrize("n", [1, 2, 130, 601, 1100, 2049])
 def test_pfsv_from_host_overlapped(P, uplo, transr, n):
     """pftrf + pftrs of a host problem with the transfers overlapped: the same
     factor (bit-identical) and solution as the device path."""
