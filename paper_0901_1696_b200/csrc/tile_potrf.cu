@@ -991,8 +991,11 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   return true;
 }
 
+// row-major-B variants: 175 registers would round to two CTAs per SM; capped
+// at 168 they fit three (the column-major-B ones need ~250 and run two)
 template <typename T, bool AK, bool BKM>
-__global__ void __launch_bounds__(TPT) tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
+__global__ void __launch_bounds__(TPT, (BKM || is_cplx<T>::value) ? 1 : 3)
+    tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
                                                         TrsmArgs a, int* sync, const int* info,
                                                         unsigned long long* trace) {
   extern __shared__ __align__(16) double smem_d[];
