@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librfpk_b200.so")
+LIB_PATH = os.environ.get("RFPK_LIB") or os.path.join(_HERE, "librfpk_b200.so")
 
 _c = ctypes.c_char
 _i64 = ctypes.c_int64

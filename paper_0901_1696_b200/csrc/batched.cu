@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 namespace rfpk {
 
@@ -128,77 +129,65 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 
 
 // ---------------------------------------------------------------- n == 64
-// One warp per matrix; see batched64.cuh for the algorithm.  Shared memory:
-// RFP buffer (2080) + RHS chunk (64 x 8) + scratch (64) = 21 KB, so ten
-// matrices (warps) are resident per SM.  W1 = L1^-1 and W2 = L2^-1 are formed
-// IN PLACE of the factor blocks T1 / T2 once those are safely in HBM.
-constexpr int B64_SMEM_DOUBLES = b64::NT + 96;
+// One warp per matrix; see batched64.cuh for the algorithm and the swizzled
+// shared-memory rectangle.  Shared memory: rectangle (2176) + pivot column
+// (64) + reciprocal diagonal (32) doubles = 17.8 KB, so twelve matrices
+// (warps) are resident per SM.  W1 = L1^-1 and W2 = L2^-1 are formed IN PLACE
+// of the factor blocks once those are safely in HBM.
+constexpr int B64_SMEM_DOUBLES = b64::RECT + 96;
 
-template <bool FACTOR, bool SOLVE, int TRANS>
-__global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
-                                                       i64 stride_arf, int nrhs, double* b,
-                                                       i64 ldb, i64 stride_b, int* info) {
+template <bool LOWER, int TRANS, bool FACTOR, bool SOLVE>
+__global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_arf, int nrhs,
+                                                       double* b, i64 ldb, i64 stride_b,
+                                                       int* info) {
   using namespace b64;
   extern __shared__ __align__(16) double sm[];
   double* R = sm;
-  double* colk = R + NT;      // 64 entries (factor_inv32)
+  double* colk = R + RECT;    // 64 entries (factor32)
   double* rdiag = colk + 64;  // 32 entries (inv32)
   const int lane = threadIdx.x;
   const i64 k = blockIdx.x;
   double* g = arf + k * stride_arf;
-  double* bk = SOLVE ? b + k * stride_b : nullptr;
-  const bool al16 = ((reinterpret_cast<uintptr_t>(g) & 15) == 0);
-  if (al16) {
-    for (int c = lane; c < NT / 2; c += 32) {
-      unsigned s = (unsigned)__cvta_generic_to_shared(R + 2 * c);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g + 2 * c));
-    }
-  } else {
-    for (int c = lane; c < NT; c += 32) R[c] = g[c];
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-  __syncwarp();
-  constexpr int rs = TRANS ? 32 : 1, cs = TRANS ? 1 : 65;
-  using V = SV<rs, cs>;
-  // T1 / T2 / S1 of the normal 65 x 32 rectangle (convert.py:142-153, d = 1)
-  const V T1{R + (lower ? 1 : 33) * rs};
-  const V T2{R + (lower ? 0 : 32) * rs};
-  const V S1{R + (lower ? 33 : 0) * rs};
-  const V V1 = T1;            // L1 (lower), later W1
-  const auto V2 = T2.t();     // L2 (lower), later W2
-  const i64 off1 = V1.p - R, off2 = V2.p - R;
+  load_rect<TRANS>(R, g);
+  // T1 / T2 / S1 of the normal 65 x 32 rectangle (convert.py:142-153, d = 1):
+  // V1 = T1 (L1, lower), V2 = T2^T (L2, lower), S = S1 ('L') | S1^T ('U')
+  constexpr int r1 = LOWER ? 1 : 33, r2 = LOWER ? 0 : 32, rs = LOWER ? 33 : 0;
+  const RV<false> V1{R + r1};
+  const RV<true> V2{R + r2};
+  const RV<!LOWER> S{R + rs};
+  const LaneOff o;
   if (FACTOR) {
-    // L1 goes to HBM inside factor_inv32 before W1 overwrites it
-    int f = factor_inv32(V1.p, rs, cs, colk, g + off1, F32_FACTOR);
+    int f = factor32<false>(V1.p, colk);
     if (f) {
       if (lane == 0) info[k] = f;
       return;
     }
-    inv32<rs, cs, TRANS ? 0 : 1>(V1, rdiag);
+    store_band<TRANS, 1>(R, g, r1);
+    inv32<false, r1 & 1>(V1.p, rdiag);
     double acc[2][4][4];
     zero_acc<32>(acc);
-    if (lower) mm32<32, 0, 2>(S1, V1.t(), acc);   // S1 <- S1 W1^T
-    else mm32<32, 1, 0>(V1, S1, acc);             // S1 <- W1 S1
+    mm32<32, 0, 2, false>(o, S, V1.t(), acc);  // S <- S W1^T
     __syncwarp();
-    store_acc<32>(S1, acc, 1.0, 0.0, 0);
+    store_acc<false, false>(o, S, acc, 1.0);
     __syncwarp();
     zero_acc<32>(acc);
-    if (lower) mm32<32, 0, 0>(S1, S1.t(), acc);   // T2 -= S1 S1^T
-    else mm32<32, 0, 0>(S1.t(), S1, acc);         // T2 -= S1^T S1
-    store_acc<32>(T2, acc, -1.0, 1.0, 2);
+    mm32<32, 0, 0, true>(o, S, S.t(), acc);    // T2 -= S S^T (its lower view V2)
+    store_acc<true, true>(o, V2, acc, -1.0);
     __syncwarp();
-    put_view<0>(S1, R, g);
-    f = factor_inv32(V2.p, cs, rs, colk, g + off2, F32_FACTOR);
+    store_band<TRANS, 0>(R, g, rs);
+    f = factor32<true>(V2.p, colk);
     if (lane == 0) info[k] = f ? 32 + f : 0;
     if (f) return;
-    if (SOLVE) inv32<cs, rs, 0>(V2, rdiag);
+    store_band<TRANS, 2>(R, g, r2);
+    if (SOLVE) inv32<true, r2 & 1>(V2.p, rdiag);
   } else {
-    inv32<rs, cs, TRANS ? 0 : 1>(V1, rdiag);
-    inv32<cs, rs, 0>(V2, rdiag);
+    inv32<false, r1 & 1>(V1.p, rdiag);
+    inv32<true, r2 & 1>(V2.p, rdiag);
   }
   if (!SOLVE) return;
-  const auto w1 = V1;
-  const auto w2 = V2;
+  double* bk = b + k * stride_b;
+  const auto W1 = V1;
+  const auto W2 = V2;
   const int g8 = lane >> 2, t4 = lane & 3;
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
@@ -211,22 +200,21 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
       x2[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
     }
     zero_c(c);
-    mm32r<1>(w1, x1, c);                         // b1 = W1 b1
+    mm32r<1>(o, W1, x1, c);                      // b1 = W1 b1
     c2b(c, x1);
     zero_c(c);
-    if (lower) mm32r<0>(S1, x1, c);              // S1 b1
-    else mm32r<0>(S1.t(), x1, c);                // S1^T b1
+    mm32r<0>(o, S, x1, c);                       // S b1
     {
       double d[8];
       c2b(c, d);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) x2[s] -= d[s];  // b2 -= ...
+      for (int s = 0; s < 8; ++s) x2[s] -= d[s];  // b2 -= S b1
     }
     zero_c(c);
-    mm32r<1>(w2, x2, c);                         // b2 = W2 b2
+    mm32r<1>(o, W2, x2, c);                      // b2 = W2 b2
     c2b(c, x2);
     zero_c(c);
-    mm32r<2>(w2.t(), x2, c);                     // b2 = W2^T b2
+    mm32r<2>(o, W2.t(), x2, c);                  // b2 = W2^T b2
     c2b(c, x2);
     // b2 is final: store it from the accumulator layout
 #pragma unroll
@@ -237,16 +225,15 @@ __global__ void __launch_bounds__(32) batched64_kernel(int lower, double* arf,
         if (col < cw) bk[32 + row + (i64)(c0 + col) * ldb] = c[mi][r];
       }
     zero_c(c);
-    if (lower) mm32r<0>(S1.t(), x2, c);          // S1^T b2
-    else mm32r<0>(S1, x2, c);                    // S1 b2
+    mm32r<0>(o, S.t(), x2, c);                   // S^T b2
     {
       double d[8];
       c2b(c, d);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) x1[s] -= d[s];  // b1 -= ...
+      for (int s = 0; s < 8; ++s) x1[s] -= d[s];  // b1 -= S^T b2
     }
     zero_c(c);
-    mm32r<2>(w1.t(), x1, c);                     // b1 = W1^T b1
+    mm32r<2>(o, W1.t(), x1, c);                  // b1 = W1^T b1
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -263,17 +250,25 @@ int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, i
   const size_t sm = B64_SMEM_DOUBLES * sizeof(double);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<(unsigned)batch, 32, sm, st>>>(r.lower ? 1 : 0, arf, stride_arf, nrhs, b, ldb,
-                                          stride_b, info);
+    kern<<<(unsigned)batch, 32, sm, st>>>(arf, stride_arf, nrhs, b, ldb, stride_b, info);
   };
-  if (r.trans) {
-    if (factor && solve) launch(batched64_kernel<true, true, 1>);
-    else if (factor) launch(batched64_kernel<true, false, 1>);
-    else launch(batched64_kernel<false, true, 1>);
+  auto pick = [&](auto lower_tag, auto trans_tag) {
+    constexpr bool L = decltype(lower_tag)::value;
+    constexpr int T = decltype(trans_tag)::value;
+    if (factor && solve) launch(batched64_kernel<L, T, true, true>);
+    else if (factor) launch(batched64_kernel<L, T, true, false>);
+    else launch(batched64_kernel<L, T, false, true>);
+  };
+  using F = std::false_type;
+  using Tr = std::true_type;
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  if (r.lower) {
+    if (r.trans) pick(Tr{}, I1{});
+    else pick(Tr{}, I0{});
   } else {
-    if (factor && solve) launch(batched64_kernel<true, true, 0>);
-    else if (factor) launch(batched64_kernel<true, false, 0>);
-    else launch(batched64_kernel<false, true, 0>);
+    if (r.trans) pick(F{}, I1{});
+    else pick(F{}, I0{});
   }
   RFPK_CHECK_LAUNCH();
   return 0;

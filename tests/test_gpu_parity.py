@@ -210,17 +210,19 @@ def test_batched_failure_info(P, uplo, transr):
     bufs, want = [], []
     for k in range(batch):
         a = O.spd_matrix(n, k, "n")
-        if k % 3 == 1:
-            a[k + 5, k + 5] = -1e9
-            a[:, k + 5] = 0.0
-            a[k + 5, :] = 0.0
-            a[k + 5, k + 5] = -1.0
+        if k % 3:
+            # a non-PD pivot in the first (T1) or the second (T2) half
+            p = k + 5 if k % 3 == 1 else 33 + k
+            a[:, p] = 0.0
+            a[p, :] = 0.0
+            a[p, p] = -1.0
         buf = O.trttf(a, uplo, transr)
         want.append(O.pftrf(buf.copy(), n, uplo, transr))
         bufs.append(buf)
     arf = torch.from_numpy(np.stack(bufs)).cuda()
     info = rfp.pftrf_batched(arf, n, uplo, transr)
     assert info.cpu().tolist() == want
+    assert any(0 < w <= 32 for w in want) and any(w > 32 for w in want)
 
 
 def test_graph_replay_matches_direct(P):
