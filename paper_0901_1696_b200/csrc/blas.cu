@@ -449,8 +449,12 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
   // the dataflow trsm for real data (complex tiles need 133 KB of smem -> one
   // CTA per SM, where the recursive GEMM form measured faster: 65 vs 78 ms on
   // config 5's S1 solve at n = 16000)
+  // (narrow right-hand sides run 64 x 16 tiles, which win from two tiles up)
   static const i64 tile_min = env_int("RFPK_TILE_TRSM_MIN", 512);
-  if (!is_cplx<T>::value && Tm.m >= tile_min && !std::getenv("RFPK_NO_TILE_TRSM") &&
+  static const i64 tile_min_narrow = env_int("RFPK_TILE_TRSM_MIN_NARROW", 128);
+  static const i64 narrow = env_int("RFPK_TRSM_NARROW", 256);
+  const i64 tmin = B.n <= narrow ? tile_min_narrow : tile_min;
+  if (!is_cplx<T>::value && Tm.m >= tmin && !std::getenv("RFPK_NO_TILE_TRSM") &&
       (rc = trsm_tiles(c, lower, conj, Tm, B, (const T*)W, !lower)) != -100) {
     ws_free(own, c.st);
     return rc;
@@ -703,6 +707,10 @@ template <typename T> int blas_potrf(Ctx c, char uplo, View<T> A, int base, T* W
   return rc;
 }
 
+template <typename T> int blas_leaf_inverses(Ctx c, View<T> L, T* W) {
+  return leaf_inverses(c, L, false, W);
+}
+
 template <typename T> int blas_trtri(Ctx c, char uplo, char diag, View<T> A, int base) {
   View<T> v = uplo == 'L' ? A : A.t();
   if (diag == 'N') {
@@ -724,6 +732,7 @@ template <typename T> int blas_lauum(Ctx c, char uplo, View<T> A) {
   template int blas_syrk<T>(Ctx, char, char, double, View<T>, double, View<T>, bool);          \
   template int blas_potrf<T>(Ctx, char, View<T>, int, T*);                                     \
   template int blas_trtri<T>(Ctx, char, char, View<T>, int);                                   \
+  template int blas_leaf_inverses<T>(Ctx, View<T>, T*);                                        \
   template int blas_lauum<T>(Ctx, char, View<T>);                                              \
   template int ws_alloc<T>(T**, i64, cudaStream_t);                                            \
   template void ws_free<T>(T*, cudaStream_t);

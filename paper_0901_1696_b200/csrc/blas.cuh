@@ -65,6 +65,9 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
 // stream-ordered workspace for leaf inverses of an order-n triangle
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
 template <typename T> void ws_free(T* p, cudaStream_t st);
+// the 64-block inverses of a lower view into W (ws_alloc(n)): what trsm computes
+// when called without W, so a caller solving twice with one triangle shares it
+template <typename T> int blas_leaf_inverses(Ctx c, View<T> L, T* W);
 // trtri: in-place inverse; zero diagonal -> *info (matrix untouched) (kernels.py:515)
 template <typename T> int blas_trtri(Ctx c, char uplo, char diag, View<T> A, int base);
 // lauum: L^H L (uplo L) / U U^H (uplo U)                        (kernels.py:575)

@@ -189,6 +189,50 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   }
 }
 
+// ------------------------------------------------------------ split-K
+// Few output tiles and a long K (pftrs' C = B2 -= S1 B1 at nrhs = 64: 32
+// tiles, K = 2000): split K into S slices, one CTA per (tile, slice) writes
+// its partial product to a workspace, and a second kernel sums the slices in
+// a fixed order -- deterministic, unlike atomics.
+template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 4)
+    gemm_splitk_kernel(GemmArgs<T> g, T* ws, int kchunk) {
+  using LA = SmemLayout<T, BM, BK, AK>;
+  extern __shared__ __align__(16) double smem_d[];
+  T* As = reinterpret_cast<T*>(smem_d);
+  T* Bs = As + STAGES * LA::SIZE;
+  if (g.skip && *g.skip) return;
+  const int s = blockIdx.y;
+  const int k0 = s * kchunk;
+  GemmArgs<T> p = g;
+  p.K = g.K - k0 < kchunk ? g.K - k0 : kchunk;
+  p.A = g.A + (AK ? (i64)k0 : (i64)k0 * g.lda);
+  p.B = g.B + (BKM ? (i64)k0 : (i64)k0 * g.ldb);
+  p.C = ws + (i64)s * g.M * g.N;
+  p.ldc = g.M;
+  p.alpha = sc_from<T>(1.0);
+  p.beta = sc_from<T>(0.0);
+  const int tm = (int)(blockIdx.x % g.tiles_m), tn = (int)(blockIdx.x / g.tiles_m);
+  gemm_tile<T, BM, BN, BK, WM, WN, STAGES, AK, BKM, TRI_FULL>(p, tm, tn, As, Bs);
+}
+
+template <typename T>
+__global__ void splitk_reduce_kernel(GemmArgs<T> g, const T* ws, int S) {
+  if (g.skip && *g.skip) return;
+  const i64 total = (i64)g.M * g.N;
+  const bool use_beta = !is_zero(g.beta);
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    T acc = ws[e];
+    for (int s = 1; s < S; ++s) acc = acc + ws[(i64)s * total + e];
+    const i64 i = e % g.M, j = e / g.M;
+    T* c = g.C + i + j * g.ldc;
+    T v = g.alpha * acc;
+    if (use_beta) v = v + g.beta * (*c);
+    *c = v;
+  }
+}
+
 // ------------------------------------------------------------ scale kernel
 template <typename T>
 __global__ void scale_kernel(View<T> C, T beta, int mode, int herm_diag, const int* skip) {
@@ -303,6 +347,56 @@ int launch_mode(const GemmArgs<T>& a, int mode, bool ak, bool bk, cudaStream_t s
   }
 }
 
+template <typename T, bool AK, bool BKM>
+int splitk_launch(const GemmArgs<T>& a, int S, int kchunk, cudaStream_t st) {
+  constexpr int BM = 64, BN = 64, BK = is_cplx<T>::value ? 8 : 16, WM = 32, WN = 32, ST = 3;
+  constexpr size_t smem = (size_t)ST *
+                          (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
+                          sizeof(T);
+  auto kern = gemm_splitk_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM>;
+  static const bool configured = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return true;
+  }();
+  (void)configured;
+  GemmArgs<T> g = a;
+  g.tiles_m = (g.M + BM - 1) / BM;
+  const int tiles = g.tiles_m * ((g.N + BN - 1) / BN);
+  T* ws = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ws, (size_t)S * g.M * g.N * sizeof(T), st);
+  if (e != cudaSuccess) return (int)e;
+  kern<<<dim3((unsigned)tiles, (unsigned)S), (BM / WM) * (BN / WN) * 32, smem, st>>>(g, ws, kchunk);
+  RFPK_CHECK_LAUNCH();
+  const i64 total = (i64)g.M * g.N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  splitk_reduce_kernel<T><<<blocks, 256, 0, st>>>(g, ws, S);
+  RFPK_CHECK_LAUNCH();
+  cudaFreeAsync(ws, st);
+  return 0;
+}
+
+// -100: not worth splitting (enough tiles, or a short K)
+template <typename T> int gemm_splitk(const GemmArgs<T>& g, bool ak, bool bk, cudaStream_t st) {
+  static const int min_k = [] {
+    const char* v = std::getenv("RFPK_SPLITK_MIN_K");
+    return v ? std::atoi(v) : 256;
+  }();
+  const long long tiles = (long long)((g.M + 63) / 64) * ((g.N + 63) / 64);
+  if (min_k <= 0 || g.K < min_k || tiles * 2 > num_sms()) return -100;
+  // about two CTAs per SM in total, slices of at least 128 (a multiple of 16)
+  int S = (int)((2 * num_sms() + tiles - 1) / tiles);
+  const int smax = g.K / 128;
+  if (S > smax) S = smax;
+  if (S < 2) return -100;
+  const int kchunk = ((g.K + S - 1) / S + 15) / 16 * 16;
+  S = (g.K + kchunk - 1) / kchunk;
+  if (ak) return bk ? splitk_launch<T, true, true>(g, S, kchunk, st)
+                    : splitk_launch<T, true, false>(g, S, kchunk, st);
+  return bk ? splitk_launch<T, false, true>(g, S, kchunk, st)
+            : splitk_launch<T, false, false>(g, S, kchunk, st);
+}
+
 }  // namespace
 
 
@@ -356,6 +450,10 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
   if (inplace_leaf) {
     return launch_mode<T, 64, 64, 16 / (is_cplx<T>::value ? 2 : 1), 32, 32, 3>(g, tri_mode, ak,
                                                                                bk, st);
+  }
+  if (tri_mode == TRI_FULL && a_tri == A_FULL) {
+    const int rc = gemm_splitk(g, ak, bk, st);
+    if (rc != -100) return rc;
   }
   if constexpr (is_cplx<T>::value) {
     long long tiles = (long long)((g.M + 63) / 64) * ((g.N + 63) / 64);

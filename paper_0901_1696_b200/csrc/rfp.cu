@@ -270,7 +270,9 @@ int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* s
   return 0;
 }
 
-// forward/back substitution through T1/S1/T2 (rfp.py:106-136)
+// forward/back substitution through T1/S1/T2 (rfp.py:106-136).  The 64-block
+// inverses of T1 and T2 are formed once and shared by the two solves with
+// each triangle (forward and back).
 template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
                                 cudaEvent_t b2_final) {
   if (d.n == 0 || b.n == 0) return 0;
@@ -278,36 +280,50 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
   const i64 n1 = d.n1, n2 = d.n2, r = b.n;
   PhaseTrace tr(c.st, "pftrs");
+  // W1: inverses of T1 (lower as stored for 'L', T1^T's for 'U' -- the same
+  // view either way is the lower one); W2: of T2^T (T2 is upper)
+  T *W1 = nullptr, *W2 = nullptr;
+  struct Free {
+    T** p[2];
+    cudaStream_t st;
+    ~Free() { for (T** q : p) ws_free(*q, st); }
+  } fr{{&W1, &W2}, c.st};
+  TRY(ws_alloc(&W1, t1.m, c.st));
+  TRY(blas_leaf_inverses(c, t1, W1));
+  if (t2.m) {
+    TRY(ws_alloc(&W2, t2.m, c.st));
+    TRY(blas_leaf_inverses(c, t2.t(), W2));
+  }
   if (d.lower) {
     View<T> b1 = b.sub(0, 0, n1, r), b2 = b.sub(n1, 0, n2, r);
-    TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false));
+    TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false, W1));
     tr.mark("trsm1");
     if (n2) {
       TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b1, one<T>(), b2));
       tr.mark("gemm1");
-      TRY(blas_trsm(c, 'L', 'U', 'T', 'N', one<T>(), t2, b2, false));
+      TRY(blas_trsm(c, 'L', 'U', 'T', 'N', one<T>(), t2, b2, false, W2));
       tr.mark("trsm2");
-      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false));
+      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false, W2));
       tr.mark("trsm3");
       if (b2_final) cudaEventRecord(b2_final, c.st);
       TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
       tr.mark("gemm2");
     }
-    TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false));
+    TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false, W1));
     tr.mark("trsm4");
     return 0;
   }
   View<T> b1 = b.sub(0, 0, n2, r), b2 = b.sub(n2, 0, n1, r);
   if (n2) {
-    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false));
+    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false, W1));
     TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b1, one<T>(), b2));
   }
-  TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t2, b2, false));
-  TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false));
+  TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t2, b2, false, W2));
+  TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false, W2));
   if (b2_final) cudaEventRecord(b2_final, c.st);
   if (n2) {
     TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
-    TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false));
+    TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
   }
   return 0;
 }

@@ -132,6 +132,13 @@ __device__ __forceinline__ T frag(const double (&acc)[TileCfg<T>::NACC][2][4][4]
   if constexpr (is_cplx<T>::value) return Z{acc[0][mi][ni][r], acc[1][mi][ni][r]};
   else return acc[0][mi][ni][r];
 }
+// the same for any fragment grid (re / im planes passed separately)
+template <typename T, int MI, int NI>
+__device__ __forceinline__ T fragn(const double (&re)[MI][NI][4], const double (&im)[MI][NI][4],
+                                   int mi, int ni, int r) {
+  if constexpr (is_cplx<T>::value) return Z{re[mi][ni][r], im[mi][ni][r]};
+  else return re[mi][ni][r];
+}
 
 // acc += X Y^H for 64-wide K from two LD64 shared tiles (rows of X and of Y
 // along M / N): the off-diagonal solve L(i, j) = C W_j^H.
@@ -730,46 +737,58 @@ int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, 
 // every column block's chain of row blocks advances in parallel and all
 // off-chain accumulation overlaps it.
 
-// acc += A B for 64 x 64 LD64 shared tiles (A(r, k) = A[r + k*LD64],
-// B(k, n) = B[k + n*LD64]).
-template <typename T>
-__device__ __forceinline__ void smem_mm_ab(const T* As, const T* Bs,
-                                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+// Warp layout of a 64 x TN trsm tile: TN = 64 -> 2 x 2 warps of 32 x 32,
+// TN = 16 (narrow right-hand sides) -> 4 x 1 warps of 16 x 16.
+template <int TN> struct TrsmTile {
+  static constexpr int WN = TN == 64 ? 2 : 1;   // warps along N
+  static constexpr int WMW = 4 / WN;            // warps along M
+  static constexpr int RW = TP / WMW;           // rows per warp
+  static constexpr int CW = TN / WN;            // columns per warp
+  static constexpr int MI = RW / 16, NI = CW / 8;
+};
+
+// acc += A B for LD64 shared tiles, A 64 x 64 (A(r, k) = A[r + k*LD64]) and
+// B 64 x TN (B(k, n) = B[k + n*LD64]).
+template <typename T, int TN>
+__device__ __forceinline__ void smem_mm_ab(
+    const T* As, const T* Bs,
+    double (&acc)[TileCfg<T>::NACC][TrsmTile<TN>::MI][TrsmTile<TN>::NI][4]) {
+  using W = TrsmTile<TN>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, t = lane & 3;
+  const int wm = warp % W::WMW, wn = warp / W::WMW, g = lane >> 2, t = lane & 3;
 #pragma unroll 4
   for (int k = 0; k < TP; k += 4) {
     if constexpr (!is_cplx<T>::value) {
-      double a[2][2], b[4];
+      double a[W::MI][2], b[W::NI];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        a[mi][0] = As[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
-        a[mi][1] = As[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+      for (int mi = 0; mi < W::MI; ++mi) {
+        a[mi][0] = As[(wm * W::RW + mi * 16 + g) + (k + t) * LD64];
+        a[mi][1] = As[(wm * W::RW + mi * 16 + g + 8) + (k + t) * LD64];
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k + t) + (wn * 32 + ni * 8 + g) * LD64];
+      for (int ni = 0; ni < W::NI; ++ni) b[ni] = Bs[(k + t) + (wn * W::CW + ni * 8 + g) * LD64];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < W::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], a[mi][0], a[mi][1], b[ni]);
+        for (int ni = 0; ni < W::NI; ++ni) dmma16x8x4(acc[0][mi][ni], a[mi][0], a[mi][1], b[ni]);
     } else {
-      double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+      double ar[W::MI][2], ai[W::MI][2], nai[W::MI][2], br[W::NI], bi[W::NI];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const Z v0 = As[(wm * 32 + mi * 16 + g) + (k + t) * LD64];
-        const Z v1 = As[(wm * 32 + mi * 16 + g + 8) + (k + t) * LD64];
+      for (int mi = 0; mi < W::MI; ++mi) {
+        const Z v0 = As[(wm * W::RW + mi * 16 + g) + (k + t) * LD64];
+        const Z v1 = As[(wm * W::RW + mi * 16 + g + 8) + (k + t) * LD64];
         ar[mi][0] = v0.x; ai[mi][0] = v0.y; nai[mi][0] = -v0.y;
         ar[mi][1] = v1.x; ai[mi][1] = v1.y; nai[mi][1] = -v1.y;
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const Z w = Bs[(k + t) + (wn * 32 + ni * 8 + g) * LD64];
+      for (int ni = 0; ni < W::NI; ++ni) {
+        const Z w = Bs[(k + t) + (wn * W::CW + ni * 8 + g) * LD64];
         br[ni] = w.x; bi[ni] = w.y;
       }
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < W::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < W::NI; ++ni) {
           dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
           dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
           dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
@@ -791,16 +810,18 @@ struct TrsmArgs {
   int ext_mode;
 };
 
-template <typename T, bool AK, bool BKM>
+template <typename T, bool AK, bool BKM, int TN>
 __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const TrsmArgs& a,
                           int* done, int i, int c, T* sm, int* s_ok, unsigned long long* tr) {
   if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | c); tr[5] = blockIdx.x; }
   using C = TileCfg<T>;
   using LA = SmemLayout<T, TP, C::BK, AK>;
-  using LB = SmemLayout<T, TP, C::BK, BKM>;
+  using LB = SmemLayout<T, TN, C::BK, BKM>;
+  using WL = TrsmTile<TN>;
+  constexpr int MI = WL::MI, NI = WL::NI;
   constexpr int NACC = C::NACC, BK = C::BK, SPC = C::SPC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
+  const int wm = warp % WL::WMW, wn = warp / WL::WMW, gq = lane >> 2, tq = lane & 3;
   T* As = sm;
   T* Bs = sm + STAGES * LA::SIZE;
   const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
@@ -822,14 +843,14 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   auto chunk = [&](int q) { return a.lower ? q : a.nb - 1 - q; };
 
   TileLoader<T, TP, BK, TPT, AK> la;
-  TileLoader<T, TP, BK, TPT, BKM> lb;
-  double acc[NACC][2][4][4];
+  TileLoader<T, TN, BK, TPT, BKM> lb;
+  double acc[NACC][MI][NI][4];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[q][mi][ni][r] = 0.0;
 
@@ -841,7 +862,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     const T* ta = AK ? Tm.p + (i64)kk * TP : Tm.p + (i64)kk * TP * Tm.cs;
     la.init(ta, lda, i * TP, a.n, tid);
     const T* tb = BKM ? B.p + (i64)kk * TP : B.p + (i64)kk * TP * B.rs;
-    lb.init(tb, ldb, c * TP, a.nrhs, tid);
+    lb.init(tb, ldb, c * TN, a.nrhs, tid);
     kvalid = a.n - kk * TP < TP ? a.n - kk * TP : TP;
     return true;  // (the solve never aborts: trsm inputs cannot fail)
   };
@@ -877,41 +898,41 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
       load_stage(nk % STAGES, nk);
     }
     cp_async_commit();
-    const T* as = As + (kt % STAGES) * LA::SIZE + (wm * 32 + gq) * LA::RS + tq * LA::KS;
-    const T* bs = Bs + (kt % STAGES) * LB::SIZE + (wn * 32 + gq) * LB::RS + tq * LB::KS;
+    const T* as = As + (kt % STAGES) * LA::SIZE + (wm * WL::RW + gq) * LA::RS + tq * LA::KS;
+    const T* bs = Bs + (kt % STAGES) * LB::SIZE + (wn * WL::CW + gq) * LB::RS + tq * LB::KS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       if constexpr (!C::CPLX) {
-        double af[2][2], bf[4];
+        double af[MI][2], bf[NI];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
+        for (int mi = 0; mi < MI; ++mi) {
           af[mi][0] = as[kk * LA::KS + (mi * 16) * LA::RS];
           af[mi][1] = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[kk * LB::KS + (ni * 8) * LB::RS];
+        for (int ni = 0; ni < NI; ++ni) bf[ni] = bs[kk * LB::KS + (ni * 8) * LB::RS];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma16x8x4(acc[0][mi][ni], af[mi][0], af[mi][1], bf[ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma16x8x4(acc[0][mi][ni], af[mi][0], af[mi][1], bf[ni]);
       } else {
-        double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+        double ar[MI][2], ai[MI][2], nai[MI][2], br[NI], bi[NI];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
+        for (int mi = 0; mi < MI; ++mi) {
           const Z v0 = as[kk * LA::KS + (mi * 16) * LA::RS];
           const Z v1 = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
           ar[mi][0] = v0.x; ai[mi][0] = sa * v0.y; nai[mi][0] = -ai[mi][0];
           ar[mi][1] = v1.x; ai[mi][1] = sa * v1.y; nai[mi][1] = -ai[mi][1];
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
           const Z w = bs[kk * LB::KS + (ni * 8) * LB::RS];
           br[ni] = w.x; bi[ni] = w.y;
         }
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
+          for (int ni = 0; ni < NI; ++ni) {
             dmma16x8x4(acc[0][mi][ni], ar[mi][0], ar[mi][1], br[ni]);
             dmma16x8x4(acc[0][mi][ni], nai[mi][0], nai[mi][1], bi[ni]);
             dmma16x8x4(acc[1][mi][ni], ar[mi][0], ar[mi][1], bi[ni]);
@@ -932,19 +953,19 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
   T* S = sm;
   T* Ws = PREW ? Wpre : S + TP * LD64;
-  const i64 i0 = (i64)i * TP, c0 = (i64)c * TP;
+  const i64 i0 = (i64)i * TP, c0 = (i64)c * TN;
   const int mrows = a.n - (int)i0 < TP ? a.n - (int)i0 : TP;
-  const int ncols = a.nrhs - (int)c0 < TP ? a.nrhs - (int)c0 : TP;
+  const int ncols = a.nrhs - (int)c0 < TN ? a.nrhs - (int)c0 : TN;
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
+        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
         S[row + col * LD64] = (row < mrows && col < ncols)
-                                  ? *B.at(i0 + row, c0 + col) - frag<T>(acc, mi, ni, r)
+                                  ? *B.at(i0 + row, c0 + col) - fragn<T>(acc[0], acc[NACC - 1], mi, ni, r)
                                   : zero_<T>();
       }
   const T* w = W + (i64)i * TP * TP;
@@ -962,25 +983,25 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     else Ws[r + k * LD64] = v;
   }
   __syncthreads();
-  double x[NACC][2][4][4];
+  double x[NACC][MI][NI][4];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int r = 0; r < 4; ++r) x[q][mi][ni][r] = 0.0;
-  smem_mm_ab<T>(Ws, S, x);
+  smem_mm_ab<T, TN>(Ws, S, x);
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int row = wm * 32 + mi * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = wn * 32 + ni * 8 + 2 * tq + (r & 1);
-        if (row < mrows && col < ncols) *B.at(i0 + row, c0 + col) = frag<T>(x, mi, ni, r);
+        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+        if (row < mrows && col < ncols) *B.at(i0 + row, c0 + col) = fragn<T>(x[0], x[NACC - 1], mi, ni, r);
       }
   __syncthreads();
   if (tid == 0) {
@@ -993,8 +1014,8 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
 
 // row-major-B variants: 175 registers would round to two CTAs per SM; capped
 // at 168 they fit three (the column-major-B ones need ~250 and run two)
-template <typename T, bool AK, bool BKM>
-__global__ void __launch_bounds__(TPT, (BKM || is_cplx<T>::value) ? 1 : 3)
+template <typename T, bool AK, bool BKM, int TN>
+__global__ void __launch_bounds__(TPT, TN < TP ? 3 : ((BKM || is_cplx<T>::value) ? 1 : 3))
     tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
                                                         TrsmArgs a, int* sync, const int* info,
                                                         unsigned long long* trace) {
@@ -1013,15 +1034,15 @@ __global__ void __launch_bounds__(TPT, (BKM || is_cplx<T>::value) ? 1 : 3)
     if (t >= total) return;
     const int step = (int)(t / a.nc), c = (int)(t % a.nc);
     const int i = a.lower ? step : a.nb - 1 - step;
-    if (!trsm_task<T, AK, BKM>(Tm, B, W, a, done, i, c, sm, &s_ok, trace ? trace + 8 * t : nullptr))
+    if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok, trace ? trace + 8 * t : nullptr))
       return;
   }
 }
 
-template <typename T, bool AK, bool BKM> size_t trsm_smem_bytes() {
+template <typename T, bool AK, bool BKM, int TN> size_t trsm_smem_bytes() {
   using C = TileCfg<T>;
   const size_t pipe = (size_t)STAGES * (SmemLayout<T, TP, C::BK, AK>::SIZE +
-                                        SmemLayout<T, TP, C::BK, BKM>::SIZE);
+                                        SmemLayout<T, TN, C::BK, BKM>::SIZE);
   if (trsm_prew<T, BKM>()) {
     const size_t one = (size_t)TP * LD64;
     return ((pipe > one ? pipe : one) + one) * sizeof(T);
@@ -1030,10 +1051,10 @@ template <typename T, bool AK, bool BKM> size_t trsm_smem_bytes() {
   return (pipe > tiles ? pipe : tiles) * sizeof(T);
 }
 
-template <typename T, bool AK, bool BKM>
+template <typename T, bool AK, bool BKM, int TN>
 int trsm_launch(View<T> Tm, View<T> B, const T* W, const TrsmArgs& a, int* sync, Ctx c) {
-  auto kern = tile_trsm_kernel<T, AK, BKM>;
-  const size_t smem = trsm_smem_bytes<T, AK, BKM>();
+  auto kern = tile_trsm_kernel<T, AK, BKM, TN>;
+  const size_t smem = trsm_smem_bytes<T, AK, BKM, TN>();
   static const int per_sm = [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
@@ -1083,7 +1104,14 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.n = (int)n;
   a.nrhs = (int)B.n;
   a.nb = (int)((n + TP - 1) / TP);
-  a.nc = (int)((B.n + TP - 1) / TP);
+  // narrow right-hand sides: 64 x 16 tiles give four times the chains and a
+  // four times shorter step on each (pftrs at n = 4000, nrhs = 64)
+  static const int narrow_max = [] {
+    const char* v = std::getenv("RFPK_TRSM_NARROW");
+    return v ? std::atoi(v) : 256;
+  }();
+  const int tn = (!is_cplx<T>::value && B.n <= narrow_max) ? 16 : TP;
+  a.nc = (int)((B.n + tn - 1) / tn);
   a.lower = lower ? 1 : 0;
   a.conj = conj ? 1 : 0;
   a.wtrans = wtrans ? 1 : 0;
@@ -1097,10 +1125,22 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   // B operand = X^T (nrhs x K): K-major when B is column-major
   const bool bkm = B.rs == 1;
   int rc;
-  if (ak) rc = bkm ? trsm_launch<T, true, true>(Tm, B, W, a, sync, c)
-                   : trsm_launch<T, true, false>(Tm, B, W, a, sync, c);
-  else rc = bkm ? trsm_launch<T, false, true>(Tm, B, W, a, sync, c)
-                : trsm_launch<T, false, false>(Tm, B, W, a, sync, c);
+  if (tn == 16) {
+    if constexpr (!is_cplx<T>::value) {
+      if (ak) rc = bkm ? trsm_launch<T, true, true, 16>(Tm, B, W, a, sync, c)
+                       : trsm_launch<T, true, false, 16>(Tm, B, W, a, sync, c);
+      else rc = bkm ? trsm_launch<T, false, true, 16>(Tm, B, W, a, sync, c)
+                    : trsm_launch<T, false, false, 16>(Tm, B, W, a, sync, c);
+    } else {
+      rc = -100;
+    }
+  } else if (ak) {
+    rc = bkm ? trsm_launch<T, true, true, TP>(Tm, B, W, a, sync, c)
+             : trsm_launch<T, true, false, TP>(Tm, B, W, a, sync, c);
+  } else {
+    rc = bkm ? trsm_launch<T, false, true, TP>(Tm, B, W, a, sync, c)
+             : trsm_launch<T, false, false, TP>(Tm, B, W, a, sync, c);
+  }
   cudaFreeAsync(sync, c.st);
   return rc;
 }

@@ -173,3 +173,19 @@ def test_tile_kernels_repeat_stress(K, cplx, uplo):
             lo = dev(np.asfortranarray(ref.copy()))
             K.trsm("L", "L", "N", "N", 1.0, lo, bd)
             assert rel(bd, xs) <= 1e-10, (n, rep)
+
+
+@pytest.mark.parametrize("side,uplo,trans", list(itertools.product("LR", "LU", "NT")))
+@pytest.mark.parametrize("r", [1, 37, 64, 200, 300])
+def test_tile_trsm_widths(K, side, uplo, trans, r):
+    """The dataflow trsm (n >= 512) in both tile widths: 64 x 16 tiles for
+    narrow right-hand sides (r <= 256) and 64 x 64 above; ragged last tiles
+    in both dimensions (n = 600), column- and row-major B."""
+    n = 600
+    a = tri_matrix(n, False, 11, rowmajor=(uplo == "U"))
+    b = rnd((n, r) if side == "L" else (r, n), False, 12 + r, rowmajor=(trans == "T"))
+    want = b.copy()
+    O.trsm(side, uplo, trans, "N", 1.5, a, want)
+    bd = dev(b)
+    K.trsm(side, uplo, trans, "N", 1.5, dev(a), bd)
+    assert rel(bd, want) <= TOL

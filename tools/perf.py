@@ -181,6 +181,11 @@ if __name__ == "__main__":
     w = args.what
     if w in ("all", "gemm"):
         gemm_bench()
+    if w == "small":
+        rfp_bench(1000, "L", "N", 100, do_pftri=True)
+        rfp_bench(300, "L", "N", 100, do_pftri=True)
+        rfp_bench(2000, "U", "N", 64, do_pftri=True)
+        rfp_bench(4000, "L", "N", 64)
     if w in ("all", "rfp"):
         rfp_bench(1000, "L", "N", 100, do_pftri=True)
         for n in (4000, 4001):
