@@ -247,6 +247,57 @@ int herk_core(Ctx c, int tri, double alpha, View<T> Gv, bool gconj, double beta,
 }
 
 // Inverses of all 64-leaves of the lower-in-view triangle L into W slabs.
+// ---------------------------------------------------------------- one-launch forms
+// For small and medium orders the in-place recursions (trmm / trtri / lauum)
+// are chains of small launches; these out-of-place forms are one parallel
+// GEMM-shaped launch each (plus O(n^2) copies), at the price of an n x n (or
+// m x n) workspace.  Measured crossover in rfpk_oop_max (tools/perf.py).
+enum CopyMode : int { CP_ALL = 0, CP_LOWER0 = 1, CP_LOWER_ONLY = 2, CP_EYE = 3, CP_SLOWER_ONLY = 4 };
+
+template <typename T>
+__global__ void tri_copy_kernel(View<T> src, View<T> dst, int mode, const int* skip) {
+  if (skip && *skip) return;
+  const i64 total = dst.m * dst.n;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 i = e % dst.m, j = e / dst.m;
+    switch (mode) {
+      case CP_ALL: *dst.at(i, j) = *src.at(i, j); break;
+      case CP_LOWER0: *dst.at(i, j) = i >= j ? *src.at(i, j) : sc_from<T>(0.0); break;
+      case CP_LOWER_ONLY: if (i >= j) *dst.at(i, j) = *src.at(i, j); break;
+      case CP_SLOWER_ONLY: if (i > j) *dst.at(i, j) = *src.at(i, j); break;
+      default: *dst.at(i, j) = sc_from<T>(i == j ? 1.0 : 0.0);
+    }
+  }
+}
+
+template <typename T> int tri_copy(Ctx c, View<T> src, View<T> dst, int mode) {
+  if (dst.empty()) return 0;
+  const i64 total = dst.m * dst.n;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+  tri_copy_kernel<T><<<blocks, 256, 0, c.st>>>(src, dst, mode, c.info);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+// column-major m x n workspace view
+template <typename T> int ws_matrix(Ctx c, i64 m, i64 n, View<T>& v) {
+  T* p = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&p, (size_t)(m > 0 ? m : 1) * (n > 0 ? n : 1) * sizeof(T),
+                                  c.st);
+  v = View<T>{p, m, n, 1, m};
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+inline i64 oop_max() {
+  static const i64 v = [] {
+    const char* s = std::getenv("RFPK_OOP_MAX");
+    return s ? std::atoll(s) : (i64)4096;
+  }();
+  return v;
+}
+
 template <typename T> int leaf_inverses(Ctx c, View<T> L, bool unit, T* W) {
   if (L.m == 0) return 0;
   const size_t sm = leaf_smem<T>(2);
@@ -494,10 +545,29 @@ int trmm_rec(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<
   return trmm_rec(c, lower, conj, unit, alpha, Tm.sub(n1, n1, n2, n2), B2);
 }
 
+// B <- alpha conj?(T) B as ONE masked GEMM from a copy of B: C = B is read
+// by the epilogue only (unit diagonal: strict mask + beta = alpha)
+template <typename T>
+int trmm_oop(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
+  View<T> Bc;
+  int rc = ws_matrix(c, B.m, B.n, Bc);
+  if (!rc) rc = tri_copy(c, B, Bc, CP_ALL);
+  const int mask = lower ? (unit ? A_SLOWER : A_LOWER) : (unit ? A_SUPPER : A_UPPER);
+  if (!rc)
+    rc = gemm<T>(TRI_FULL, alpha, Tm, conj, Bc, false, unit ? alpha : sc_from<T>(0.0), B, false,
+                 c.info, c.st, mask, false);
+  if (Bc.p) cudaFreeAsync(Bc.p, c.st);
+  return rc;
+}
+
 template <typename T>
 int trmm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
   if (B.empty()) return 0;
   if (is_zero(alpha)) return scale_view<T>(B, alpha, TRI_FULL, false, c.info, c.st);
+  if (Tm.m > LEAF && Tm.m <= oop_max() && B.n <= oop_max()) {
+    const int rc = trmm_oop(c, lower, conj, unit, alpha, Tm, B);
+    if (rc != -100) return rc;
+  }
   return trmm_rec(c, lower, conj, unit, alpha, Tm, B);
 }
 
@@ -583,17 +653,54 @@ template <typename T> int trtri_rec(Ctx c, bool unit, View<T> A) {
   return trmm_rec(c, true, false, unit, neg_one<T>(), A22, A21);
 }
 
+// A <- L^{-1} by the dataflow tile trsm on an identity workspace (every column
+// chain of the inverse in parallel), then the lower triangle copied back
+template <typename T> int trtri_oop(Ctx c, bool unit, View<T> A) {
+  const i64 n = A.m;
+  T* W = nullptr;
+  View<T> X{nullptr, 0, 0, 1, 1};
+  int rc = ws_alloc(&W, n, c.st);
+  if (!rc) rc = leaf_inverses(c, A, unit, W);
+  if (!rc) rc = ws_matrix(c, n, n, X);
+  if (!rc) rc = tri_copy(c, X, X, CP_EYE);
+  if (!rc) rc = trsm_tiles(c, true, false, A, X, (const T*)W, false);
+  // (unit diagonal: the stored diagonal is never referenced nor written)
+  if (!rc) rc = tri_copy(c, X, A, unit ? CP_SLOWER_ONLY : CP_LOWER_ONLY);
+  if (X.p) cudaFreeAsync(X.p, c.st);
+  ws_free(W, c.st);
+  return rc;
+}
+
 template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
   if (A.m == 0) return 0;
+  if (A.m > LEAF && A.m <= oop_max() && !is_cplx<T>::value) {
+    const int rc = trtri_oop(c, unit, A);
+    if (rc != -100) return rc;
+  }
   int rc = leaf_inverses<T>(c, A, unit, nullptr);
   if (rc) return rc;
   return trtri_rec(c, unit, A);
+}
+
+// A <- L^H L (lower triangle) as ONE herk launch from a zero-padded copy of L
+template <typename T> int lauum_oop(Ctx c, View<T> A) {
+  View<T> Lw;
+  int rc = ws_matrix(c, A.m, A.m, Lw);
+  if (!rc) rc = tri_copy(c, A, Lw, CP_LOWER0);
+  // L^H L = G G^H with G = conj(L^T)
+  if (!rc) rc = herk_core(c, TRI_LOWER, 1.0, Lw.t(), is_cplx<T>::value, 0.0, A, true);
+  if (Lw.p) cudaFreeAsync(Lw.p, c.st);
+  return rc;
 }
 
 // A <- L^H L in place, lower triangle
 template <typename T> int lauum_lower(Ctx c, View<T> A) {
   const i64 n = A.m;
   if (n == 0) return 0;
+  if (n > LEAF && n <= oop_max()) {
+    const int rc = lauum_oop(c, A);
+    if (rc != -100) return rc;
+  }
   if (n <= LEAF) {
     const size_t sm = leaf_smem<T>(2);
     auto k = lauum_leaf_kernel<T>;

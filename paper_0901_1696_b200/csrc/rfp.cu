@@ -333,20 +333,29 @@ template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf) {
   if (d.n == 0) return 0;
   View<T> t1, t2, s1;
   rfp_blocks(d, arf, t1, t2, s1);
+  PhaseTrace tr(c.st, "tftri");
   if (d.lower) {
     TRY(blas_trtri(c, 'L', diag, t1, 0));
+    tr.mark("trtri(T1)");
     if (d.n2) {
       TRY(blas_trmm(c, 'R', 'L', 'N', diag, m_one<T>(), t1, s1));
+      tr.mark("trmm(S1)");
       TRY(blas_trtri(c, 'U', diag, t2, (int)d.n1));
+      tr.mark("trtri(T2)");
       TRY(blas_trmm(c, 'L', 'U', 'T', diag, one<T>(), t2, s1));
+      tr.mark("trmm(S1)");
     }
     return 0;
   }
   if (d.n2) {
     TRY(blas_trtri(c, 'L', diag, t1, 0));
+    tr.mark("trtri(T1)");
     TRY(blas_trmm(c, 'L', 'L', 'T', diag, m_one<T>(), t1, s1));
+    tr.mark("trmm(S1)");
     TRY(blas_trtri(c, 'U', diag, t2, (int)d.n2));
+    tr.mark("trtri(T2)");
     TRY(blas_trmm(c, 'R', 'U', 'N', diag, one<T>(), t2, s1));
+    tr.mark("trmm(S1)");
     return 0;
   }
   return blas_trtri(c, 'U', diag, t2, 0);
@@ -359,21 +368,31 @@ template <typename T> int pftri(Ctx c, const RfpDesc& d, T* arf) {
   const bool herm = is_cplx<T>::value;
   View<T> t1, t2, s1;
   rfp_blocks(d, arf, t1, t2, s1);
+  PhaseTrace tr(c.st, "pftri");
   if (d.lower) {
     TRY(blas_lauum(c, 'L', t1));
+    tr.mark("lauum(T1)");
     if (d.n2) {
       TRY(blas_syrk(c, 'L', 'C', 1.0, s1, 1.0, t1, herm));
+      tr.mark("syrk(T1)");
       TRY(blas_trmm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), s1));
+      tr.mark("trmm(S1)");
       TRY(blas_lauum(c, 'U', t2));
+      tr.mark("lauum(T2)");
     }
     return 0;
   }
   if (d.n2) {
     TRY(blas_lauum(c, 'L', t1));
+    tr.mark("lauum(T1)");
     TRY(blas_syrk(c, 'L', 'C', 1.0, s1.t(), 1.0, t1, herm));
+    tr.mark("syrk(T1)");
     TRY(blas_trmm(c, 'R', 'U', 'C', 'N', one<T>(), t2, s1));
+    tr.mark("trmm(S1)");
   }
-  return blas_lauum(c, 'U', t2);
+  TRY(blas_lauum(c, 'U', t2));
+  tr.mark("lauum(T2)");
+  return 0;
 }
 
 // ============================================================ conversions
