@@ -673,7 +673,8 @@ template <typename T> int trtri_oop(Ctx c, bool unit, View<T> A) {
 
 template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
   if (A.m == 0) return 0;
-  if (A.m > LEAF && A.m <= oop_max() && !is_cplx<T>::value) {
+  static const bool cplx_oop = env_int("RFPK_TRTRI_OOP_CPLX", 1) != 0;
+  if (A.m > LEAF && A.m <= oop_max() && (!is_cplx<T>::value || cplx_oop)) {
     const int rc = trtri_oop(c, unit, A);
     if (rc != -100) return rc;
   }
