@@ -11,6 +11,7 @@
 // kernel and a 10x slowdown from instruction-cache misses.
 #pragma once
 #include "common.cuh"
+#include "dmma.cuh"
 
 namespace rfpk {
 
@@ -72,98 +73,222 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-// One warp: in-place Cholesky (A = L L^H) of the 32 x 32 lower block of S at
-// (off, off), right-looking, lane i holding row i in registers.  Column k is
-// broadcast through a 32-entry shared-memory vector (one LDS per update, no
-// shuffles); the trailing update runs unpredicated on every lane -- values
-// that land above the diagonal are never read back or stored, so lower
-// entries only ever combine valid factor entries.  Not inlined: one copy of
-// the unrolled body serves both diagonal blocks.  Returns 0 or the 1-based
-// failing pivot (warp-uniform); `not d > 0` catches NaN (kernels.py:441).
-template <typename T>
-__device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
-  const int lane = threadIdx.x & 31;
-  T r[32];
+// One warp: C(16 x 16) = A(16 x 16) * op(B) on FP64 DMMA (m16n8k4, two n8
+// tiles), A(i, k) = A[i + k*LD64], B(k, n) = B[k*bk + n*bn] (BC: conjugated).
+// c[q][ni][r]: q = re / im plane; element (g + 8(r>>1), 8ni + 2t + (r&1)).
+template <typename T> struct Frag16 {
+  double c[is_cplx<T>::value ? 2 : 1][2][4];
+};
+
+template <typename T, bool BC>
+__device__ __forceinline__ void mm16_warp(const T* A, const T* B, int bk, int bn, Frag16<T>& f) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  constexpr bool CPLX = is_cplx<T>::value;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) r[j] = S[(off + lane) + (off + j) * LD64];
+  for (int q = 0; q < (CPLX ? 2 : 1); ++q)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) f.c[q][ni][r] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 16; k0 += 4) {
+    const int k = k0 + t;
+    const T a0 = A[g + k * LD64], a1 = A[g + 8 + k * LD64];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      T b = B[k * bk + (8 * ni + g) * bn];
+      if (BC) b = conj_(b);
+      if constexpr (!CPLX) {
+        dmma16x8x4(f.c[0][ni], a0, a1, b);
+      } else {
+        dmma16x8x4(f.c[0][ni], a0.x, a1.x, b.x);
+        dmma16x8x4(f.c[0][ni], -a0.y, -a1.y, b.y);
+        dmma16x8x4(f.c[1][ni], a0.x, a1.x, b.y);
+        dmma16x8x4(f.c[1][ni], a0.y, a1.y, b.x);
+      }
+    }
+  }
+}
+
+template <typename T, class F>
+__device__ __forceinline__ void frag16_each(const Frag16<T>& f, F fn) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = g + ((r & 2) ? 8 : 0), j = 8 * ni + 2 * t + (r & 1);
+      if constexpr (is_cplx<T>::value) fn(i, j, Z{f.c[0][ni][r], f.c[1][ni][r]});
+      else fn(i, j, f.c[0][ni][r]);
+    }
+}
+
+// One warp: right-looking Cholesky of the 16 columns [c0, c0 + 16) of the
+// 32 x 32 lower block of S at (off, off), rows c0 .. 31 (lane i holds row i's
+// 16 panel entries; lanes below c0 idle).  The pivot column is broadcast
+// through colk (double-buffered); the next pivot is taken straight from lane
+// p+1's registers and its rsqrt issued before the trailing update, so the
+// serial chain per step is mul -> fma -> shfl -> rsqrt.  16-wide rows keep the
+// per-step update short enough that this chain, not the warp's in-order
+// issue of the update, sets the pace.  Returns 0 or the failing pivot
+// (1-based within the 32-block; `not d > 0` catches NaN, kernels.py:441).
+template <typename T>
+__device__ __noinline__ int chol_panel16(T* S, int off, int c0, T* colk) {
+  const int lane = threadIdx.x & 31;
+  const bool act = lane >= c0;
+  T* prow = S + (off + lane) + (off + c0) * LD64;
+  T r[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) r[j] = act ? prow[j * LD64] : zero_<T>();
   int fail = 0;
-  double dkk = shfl(sc_re(r[0]), 0);
+  double dkk = shfl(sc_re(r[0]), c0);
   double rd = rsqrt(dkk);
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
-    const T lk = (lane == k) ? sc_from<T>(dkk * rd) : rd * r[k];
+  for (int k = 0; k < 16; ++k) {
+    const int p = c0 + k;
+    if (!(dkk > 0.0)) fail = fail ? fail : p + 1;
+    const T lk = (lane == p) ? sc_from<T>(dkk * rd) : rd * r[k];
     r[k] = lk;
-    // the next pivot straight from lane k+1's own registers (its update with
-    // its own lk); its rsqrt is issued before this step's trailing update so
-    // the two overlap -- the serial chain per step is mul -> fma -> shfl ->
-    // rsqrt, everything else runs beside it
     double dnext = 1.0;
-    if (k + 1 < 32) dnext = shfl(sc_re(fnmac(lk, conj_(lk), r[k + 1])), k + 1);
-    T* cb = colk + (k & 1) * 32;  // double-buffered column broadcast
+    if (k + 1 < 16) dnext = shfl(sc_re(fnmac(lk, conj_(lk), r[k + 1])), p + 1);
+    T* cb = colk + (k & 1) * 32;
     cb[lane] = conj_(lk);
     __syncwarp();
     const double rd_next = rsqrt(dnext);
+    if constexpr (is_cplx<T>::value) {
 #pragma unroll
-    for (int j = k + 1; j < 32; ++j) r[j] = fnmac(lk, cb[j], r[j]);
+      for (int j = k + 1; j < 16; ++j) r[j] = fnmac(lk, cb[c0 + j], r[j]);
+    } else {
+#pragma unroll
+      for (int jj = (k + 1) & ~1; jj < 16; jj += 2) {
+        const double2 c2 = *reinterpret_cast<const double2*>(cb + c0 + jj);
+        if (jj >= k + 1) r[jj] = fnmac(lk, c2.x, r[jj]);
+        r[jj + 1] = fnmac(lk, c2.y, r[jj + 1]);
+      }
+    }
     dkk = dnext;
     rd = rd_next;
   }
   if (fail) return fail;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j <= lane) S[(off + lane) + (off + j) * LD64] = r[j];
+  for (int j = 0; j < 16; ++j)
+    if (act && c0 + j <= lane) prow[j * LD64] = r[j];
+  __syncwarp();
   return 0;
 }
 
+// One warp: in-place Cholesky (A = L L^H) of the 32 x 32 lower block of S at
+// (off, off): panel [0, 16) (L11 and L21), A22 -= L21 L21^H on DMMA, panel
+// [16, 32).  Returns 0 or the 1-based failing pivot (warp-uniform).
+template <typename T>
+__device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
+  int f = chol_panel16(S, off, 0, colk);
+  if (f) return f;
+  const T* L21 = S + (off + 16) + off * LD64;
+  Frag16<T> fr;
+  mm16_warp<T, true>(L21, L21, LD64, 1, fr);  // B(k, n) = conj(L21(n, k))
+  T* A22 = S + (off + 16) + (off + 16) * LD64;
+  frag16_each(fr, [&](int i, int j, T v) {
+    if (j <= i) A22[i + j * LD64] = A22[i + j * LD64] - v;
+  });
+  __syncwarp();
+  return chol_panel16(S, off, 16, colk);
+}
+
 // One warp: W(offw.., offw..) = inverse of the 32 x 32 lower block of S at
-// (off, off); lane j holds column j of W in registers (rows above j are 0).
-// Row i of L is read with shared-memory broadcasts; reciprocals of the
-// diagonal are computed once per lane into `rdiag`.
+// (off, off), zeros above the diagonal.  The two 16 x 16 diagonal inverses
+// run side by side (lane j < 16: column j of W11; lane 16 + j: of W22),
+// right-looking (w_k = s_k / L_kk, s_i -= L(i, k) w_k: the chain per step is
+// one multiply and one FMA); then W21 = -W22 (L21 W11) on DMMA, with L21 W11
+// staged in W's upper-right block (zeroed afterwards).
 template <typename T>
 __device__ __noinline__ void inv32_warp(const T* S, int off, T* W, int offw, bool unit, T* rdiag) {
-  const int j = threadIdx.x & 31;
-  const T* L = S + off + off * LD64;
-  rdiag[j] = unit ? one_<T>() : one_<T>() / L[j + j * LD64];
+  const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15;
+  const T* L = S + (off + 16 * h) + (off + 16 * h) * LD64;
+  rdiag[lane] = unit ? one_<T>() : one_<T>() / L[j + j * LD64];
   __syncwarp();
-  T w[32];
+  T sv[16], w[16];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    T s0 = (i == j) ? one_<T>() : zero_<T>(), s1 = zero_<T>();
+  for (int i = 0; i < 16; ++i) sv[i] = (i == j) ? one_<T>() : zero_<T>();
 #pragma unroll
-    for (int k = 0; k < i; ++k) {
-      if (k & 1) s1 = fnmac(L[i + k * LD64], w[k], s1);
-      else s0 = fnmac(L[i + k * LD64], w[k], s0);
-    }
-    w[i] = (s0 + s1) * rdiag[i];
+  for (int k = 0; k < 16; ++k) {
+    w[k] = sv[k] * rdiag[16 * h + k];
+#pragma unroll
+    for (int i = k + 1; i < 16; ++i) sv[i] = fnmac(L[i + k * LD64], w[k], sv[i]);
   }
-  T* wc = W + offw + (offw + j) * LD64;
+  T* wc = W + (offw + 16 * h) + (offw + 16 * h + j) * LD64;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) wc[i] = (i >= j) ? w[i] : zero_<T>();
+  for (int i = 0; i < 16; ++i) wc[i] = (i >= j) ? w[i] : zero_<T>();
+  __syncwarp();
+  T* W11 = W + offw + offw * LD64;
+  T* W12 = W11 + 16 * LD64;
+  T* W21 = W11 + 16;
+  T* W22 = W12 + 16;
+  Frag16<T> fr;
+  mm16_warp<T, false>(S + (off + 16) + off * LD64, W11, 1, LD64, fr);  // L21 W11
+  frag16_each(fr, [&](int i, int c, T v) { W12[i + c * LD64] = v; });
+  __syncwarp();
+  mm16_warp<T, false>(W22, W12, 1, LD64, fr);  // W22 (L21 W11)
+  __syncwarp();
+  frag16_each(fr, [&](int i, int c, T v) {
+    W21[i + c * LD64] = zero_<T>() - v;
+    W12[i + c * LD64] = zero_<T>();
+  });
   __syncwarp();
 }
 
-// 128 threads: R(32x32) = op(X) * op(Y) over 32 x 32 blocks of LD64 smem
-// tiles.  Thread t computes rows (t & 31), columns 8*(t>>5) .. +7, returned
-// in `acc`; X is read as X[i][k] and Y as Y[k][j] (Ytrans: Y[j][k], with
-// optional conjugation).
+// 128 threads: R(32x32) = X * op(Y) over 32 x 32 blocks of LD64 smem tiles on
+// FP64 DMMA; warp w owns the two 16 x 8 tiles of columns 8w .. 8w+7.  X is
+// read as X[i][k], Y as Y[k][j] (YT: Y[j][k], YC: conjugated).
+template <typename T> struct Frag32 {
+  double c[is_cplx<T>::value ? 2 : 1][2][4];
+};
+
 template <typename T, bool YT, bool YC>
-__device__ __forceinline__ void mm32(const T* X, int xr, int xc, const T* Y, int yr, int yc,
-                                     T acc[8]) {
-  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
+__device__ __forceinline__ void mm32_mma(const T* X, int xr, int xc, const T* Y, int yr, int yc,
+                                         Frag32<T>& f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  constexpr bool CPLX = is_cplx<T>::value;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = zero_<T>();
-#pragma unroll 8
-  for (int k = 0; k < 32; ++k) {
-    const T x = X[(xr + i) + (xc + k) * LD64];
+  for (int q = 0; q < (CPLX ? 2 : 1); ++q)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = jg + q;
-      T y = YT ? Y[(yr + j) + (yc + k) * LD64] : Y[(yr + k) + (yc + j) * LD64];
-      if (YC) y = conj_(y);
-      acc[q] = fmac(x, y, acc[q]);
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) f.c[q][mi][r] = 0.0;
+  const int nj = 8 * w + g;
+#pragma unroll
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    const int k = k0 + t;
+    T b = YT ? Y[(yr + nj) + (yc + k) * LD64] : Y[(yr + k) + (yc + nj) * LD64];
+    if (YC) b = conj_(b);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const T a0 = X[(xr + mi * 16 + g) + (xc + k) * LD64];
+      const T a1 = X[(xr + mi * 16 + g + 8) + (xc + k) * LD64];
+      if constexpr (!CPLX) {
+        dmma16x8x4(f.c[0][mi], a0, a1, b);
+      } else {
+        dmma16x8x4(f.c[0][mi], a0.x, a1.x, b.x);
+        dmma16x8x4(f.c[0][mi], -a0.y, -a1.y, b.y);
+        dmma16x8x4(f.c[1][mi], a0.x, a1.x, b.y);
+        dmma16x8x4(f.c[1][mi], a0.y, a1.y, b.x);
+      }
     }
   }
+}
+
+// fn(i, j, v) for every element of the warp's fragments
+template <typename T, class F>
+__device__ __forceinline__ void frag32_each(const Frag32<T>& f, F fn) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = mi * 16 + g + ((r & 2) ? 8 : 0), j = 8 * w + 2 * t + (r & 1);
+      if constexpr (is_cplx<T>::value) fn(i, j, Z{f.c[0][mi][r], f.c[1][mi][r]});
+      else fn(i, j, f.c[0][mi][r]);
+    }
 }
 
 // Full inverse of the 64 x 64 lower leaf in S into W (zeros above the
@@ -178,19 +303,16 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
     __syncthreads();
   }
   // Y = L21 * W11  (scratch: S rows 0..31, cols 32..63)
-  T acc[8];
-  mm32<T, false, false>(S, 32, 0, W, 0, 0, acc);
-  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) S[i + (32 + jg + q) * LD64] = acc[q];
+  Frag32<T> f;
+  mm32_mma<T, false, false>(S, 32, 0, W, 0, 0, f);
+  frag32_each(f, [&](int i, int j, T v) { S[i + (32 + j) * LD64] = v; });
   __syncthreads();
   // W21 = -W22 * Y ; W12 = 0
-  mm32<T, false, false>(W, 32, 32, S, 0, 32, acc);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    W[(32 + i) + (jg + q) * LD64] = zero_<T>() - acc[q];
-    W[i + (32 + jg + q) * LD64] = zero_<T>();
-  }
+  mm32_mma<T, false, false>(W, 32, 32, S, 0, 32, f);
+  frag32_each(f, [&](int i, int j, T v) {
+    W[(32 + i) + j * LD64] = zero_<T>() - v;
+    W[i + (32 + j) * LD64] = zero_<T>();
+  });
 }
 
 // The whole 64-leaf on 128 threads: S (lower, LD64, identity-padded) is
@@ -211,17 +333,15 @@ __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
   if (*s_fail) return *s_fail;
   if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
   __syncthreads();
-  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
-  T acc[8];
-  mm32<T, true, true>(S, 32, 0, Ws, 0, 0, acc);  // L21 = A21 W11^H
+  Frag32<T> f;
+  mm32_mma<T, true, true>(S, 32, 0, Ws, 0, 0, f);  // L21 = A21 W11^H
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 8; ++q) S[(32 + i) + (jg + q) * LD64] = acc[q];
+  frag32_each(f, [&](int i, int j, T v) { S[(32 + i) + j * LD64] = v; });
   __syncthreads();
-  mm32<T, true, true>(S, 32, 0, S, 32, 0, acc);  // L21 L21^H
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
+  mm32_mma<T, true, true>(S, 32, 0, S, 32, 0, f);  // L21 L21^H
+  frag32_each(f, [&](int i, int j, T v) {
+    if (j <= i) S[(32 + i) + (32 + j) * LD64] = S[(32 + i) + (32 + j) * LD64] - v;
+  });
   __syncthreads();
   if (warp == 0) {
     const int f = chol32_warp(S, 32, scratch);

@@ -23,16 +23,16 @@ __global__ void __launch_bounds__(128) leaf_phases(T* A, long long* tick) {
   if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scr);
   __syncthreads();
   long long t3 = clock64();
-  T acc[8];
-  mm32<T, true, true>(S, 32, 0, Ws, 0, 0, acc);
+  Frag32<T> f;
+  mm32_mma<T, true, true>(S, 32, 0, Ws, 0, 0, f);
   __syncthreads();
-  const int i = threadIdx.x & 31, jg = (threadIdx.x >> 5) * 8;
-  for (int q = 0; q < 8; ++q) S[(32 + i) + (jg + q) * LD64] = acc[q];
+  frag32_each(f, [&](int i, int j, T v) { S[(32 + i) + j * LD64] = v; });
   __syncthreads();
   long long t4 = clock64();
-  mm32<T, true, true>(S, 32, 0, S, 32, 0, acc);
-  for (int q = 0; q < 8; ++q)
-    if (jg + q <= i) S[(32 + i) + (32 + jg + q) * LD64] = S[(32 + i) + (32 + jg + q) * LD64] - acc[q];
+  mm32_mma<T, true, true>(S, 32, 0, S, 32, 0, f);
+  frag32_each(f, [&](int i, int j, T v) {
+    if (j <= i) S[(32 + i) + (32 + j) * LD64] = S[(32 + i) + (32 + j) * LD64] - v;
+  });
   __syncthreads();
   long long t5 = clock64();
   if (warp == 0) chol32_warp(S, 32, scr);
