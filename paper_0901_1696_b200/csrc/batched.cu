@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
   const RV<!LOWER> S{R + rs};
   const LaneOff o;
   if (FACTOR) {
-    int f = factor32<false>(V1.p, colk);
+    int f = factor32<false>(o, V1.p, colk);
     if (f) {
       if (lane == 0) info[k] = f;
       return;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
     store_acc<true, true>(o, V2, acc, -1.0);
     __syncwarp();
     store_band<TRANS, 0>(R, g, rs);
-    f = factor32<true>(V2.p, colk);
+    f = factor32<true>(o, V2.p, colk);
     if (lane == 0) info[k] = f ? 32 + f : 0;
     if (f) return;
     store_band<TRANS, 2>(R, g, r2);

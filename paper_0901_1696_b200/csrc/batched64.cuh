@@ -93,37 +93,43 @@ template <bool T> struct RV {
   __device__ __forceinline__ RV<!T> t() const { return RV<!T>{p}; }
 };
 
-// 32x32 lower Cholesky of the view in place (lower triangle only; the slots
-// above it belong to the other RFP block) by one warp.  Lane i holds row i in
-// registers; 32 right-looking steps, the pivot column broadcast through colk
-// (64 entries, double-buffered).  Returns 0 or the 1-based failing pivot
-// (warp-uniform; NaN fails like the reference's `not d > 0`, kernels.py:436).
+// One warp: right-looking Cholesky of the 16 columns [c0, c0 + 16) of the
+// lower 32x32 view at p, rows c0 .. 31 (lane i holds row i's 16 panel
+// entries; lanes above c0 idle).  The pivot column is broadcast through colk
+// (double-buffered, 16-byte pairs); the next pivot comes straight from lane
+// p+1's registers.  16-wide rows halve the broadcast volume of a 32-wide
+// right-looking sweep.  Returns 0 or the failing pivot (1-based in the view;
+// NaN fails like the reference's `not d > 0`, kernels.py:436).
 template <bool T>
-__device__ __noinline__ int factor32(double* p, double* colk) {
+__device__ __noinline__ int panel16(double* p, double* colk, int c0) {
   __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(colk));
+  __builtin_assume(c0 == 0 || c0 == 16);
   const int lane = threadIdx.x & 31;
-  // row `lane`: element j at prow[T ? j : colstart(j)]
-  double* prow = p + (T ? colstart(lane) : lane);
-  double r[32];
+  // row `lane`, panel column j: prow[T ? j : colstart(j)] (colstart is
+  // additive over the 16-aligned c0, so one body serves both panels)
+  double* prow = p + (T ? colstart(lane) + c0 : lane + colstart(c0));
+  double r[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) r[j] = (j <= lane) ? prow[T ? j : colstart(j)] : 0.0;
+  for (int j = 0; j < 16; ++j) r[j] = (c0 + j <= lane) ? prow[T ? j : colstart(j)] : 0.0;
   int fail = 0;
-  double dkk = shfl(r[0], 0);
+  double dkk = shfl(r[0], c0);
+  const double* cbase = colk + c0;
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (!(dkk > 0.0)) fail = fail ? fail : k + 1;
+  for (int k = 0; k < 16; ++k) {
+    const int pv = c0 + k;
+    if (!(dkk > 0.0)) fail = fail ? fail : pv + 1;
     const double rd = rsqrt(dkk);
-    const double lk = (lane == k) ? dkk * rd : rd * r[k];
+    const double lk = (lane == pv) ? dkk * rd : rd * r[k];
     r[k] = lk;
     double dnext = 0.0;
-    if (k + 1 < 32) dnext = shfl(fma(-lk, lk, r[k + 1]), k + 1);  // lane k+1's new pivot
-    double* cb = colk + (k & 1) * 32;
-    cb[lane] = lk;
+    if (k + 1 < 16) dnext = shfl(fma(-lk, lk, r[k + 1]), pv + 1);  // lane pv+1's new pivot
+    const int buf = (k & 1) * 32;
+    colk[buf + lane] = lk;
     __syncwarp();
 #pragma unroll
-    for (int jj = (k + 1) & ~1; jj < 32; jj += 2) {
-      const double2 c = *reinterpret_cast<const double2*>(cb + jj);
+    for (int jj = (k + 1) & ~1; jj < 16; jj += 2) {
+      const double2 c = *reinterpret_cast<const double2*>(cbase + buf + jj);
       if (jj >= k + 1) r[jj] = fma(-lk, c.x, r[jj]);
       r[jj + 1] = fma(-lk, c.y, r[jj + 1]);
     }
@@ -131,75 +137,144 @@ __device__ __noinline__ int factor32(double* p, double* colk) {
   }
   if (fail) return fail;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j <= lane) prow[T ? j : colstart(j)] = r[j];
+  for (int j = 0; j < 16; ++j)
+    if (c0 + j <= lane) prow[T ? j : colstart(j)] = r[j];
   __syncwarp();
   return 0;
 }
 
-// In-place inverse of the lower 32x32 view L (only the lower triangle is read
-// or written).  Lane j computes column j; rdiag is a 32-entry scratch.  The
-// substitution runs along L's unit-stride direction so that L is read two
-// entries per 16-byte broadcast LDS: right-looking (column k of L per step)
-// for a normal view, left-looking (row i per step) for a transposed one.  PAR
-// is the parity of p's element offset from the 16-byte-aligned smem base, so
-// the pairing is resolved at compile time.
+// 32x32 lower Cholesky of the view in place (lower triangle only; the slots
+// above it belong to the other RFP block) by one warp: panel [0, 16) (L11 and
+// L21), V22 -= L21 L21^T on DMMA (m16n8k4, lower tiles), panel [16, 32).
+template <bool T>
+__device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* colk) {
+  int f = panel16<T>(p, colk, 0);
+  if (f) return f;
+  const RV<T> V{p};
+  double acc[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[ni][r] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 16; k0 += 4) {
+    const double a0 = V.gt(o, 16, k0), a1 = V.gt(o, 24, k0);   // L21(g (+8), k0 + t)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+      mma(acc[ni], a0, a1, V.t().tg(o, k0, 16 + 8 * ni));      // L21(8ni + g, k0 + t)
+  }
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = g + ((r & 2) ? 8 : 0), j = 8 * ni + 2 * t + (r & 1);
+      if (j <= i) {
+        double& c = V.acc(o, 16 + ((r & 2) ? 8 : 0), 16 + 8 * ni, r & 1);
+        c -= acc[ni][r];
+      }
+    }
+  __syncwarp();
+  return panel16<T>(p, colk, 16);
+}
+
+// In-place inverse of the lower 32x32 view (only its lower triangle is read
+// or written) by one warp.  The two 16x16 diagonal blocks are inverted side
+// by side: lane (h, j) = (lane / 16, lane % 16) forms column j of W_hh by
+// right-looking substitution (w_k = s_k / L_kk, s_i -= L(i, k) w_k: chain of
+// one multiply + one FMA per step), reading column k of its block by
+// broadcast (16-byte pairs along a contiguous column, PAR = parity of p's
+// element offset).  Then W21 = -W22 (L21 W11) on DMMA, the product L21 W11
+// moved from accumulator to B-operand layout by shuffles.
 template <bool T, int PAR>
 __device__ __noinline__ void inv32(double* p, double* rdiag) {
   __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(rdiag));
-  const RV<T> L{p};
-  const int j = threadIdx.x & 31;
-  rdiag[j] = 1.0 / p[j + colstart(j)];
+  const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15;
+  const RV<T> V{p};
+  // block h at pb: element (i, k) at pb[T ? k + colstart(i) : i + colstart(k)]
+  // (colstart additive over the 16-aligned 16h; 16 + colstart(16) is even)
+  const double* pb = p + 16 * h + colstart(16 * h);
+  rdiag[lane] = 1.0 / pb[j + colstart(j)];
   __syncwarp();
-  double w[32];
-  if constexpr (!T) {
-    // right-looking: s <- e_j; for k: w_k = s_k / L_kk; s_i -= L(i, k) w_k
-    double sv[32];
+  double sv[16], w[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) sv[i] = (i == j) ? 1.0 : 0.0;
+  for (int i = 0; i < 16; ++i) sv[i] = (i == j) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      w[k] = sv[k] * rdiag[k];
+  for (int k = 0; k < 16; ++k) {
+    w[k] = sv[k] * rdiag[16 * h + k];
+    if constexpr (!T) {
       int i = k + 1;
-      if (i < 32 && ((PAR + i + colstart(k)) & 1)) {  // odd start: single load
-        sv[i] = fma(-L(i, k), w[k], sv[i]);
+      if (i < 16 && ((PAR + i + colstart(k)) & 1)) {
+        sv[i] = fma(-pb[i + colstart(k)], w[k], sv[i]);
         ++i;
       }
 #pragma unroll
-      for (; i + 1 < 32; i += 2) {
-        const double2 q = *reinterpret_cast<const double2*>(&L(i, k));
+      for (; i + 1 < 16; i += 2) {
+        const double2 q = *reinterpret_cast<const double2*>(pb + i + colstart(k));
         sv[i] = fma(-q.x, w[k], sv[i]);
         sv[i + 1] = fma(-q.y, w[k], sv[i + 1]);
       }
-      if (i < 32) sv[i] = fma(-L(i, k), w[k], sv[i]);
-    }
-  } else {
-    // left-looking along rows: w_i = (e_j(i) - sum_k L(i, k) w_k) / L_ii
+      if (i < 16) sv[i] = fma(-pb[i + colstart(k)], w[k], sv[i]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = 0;
-      if (i > 0 && ((PAR + colstart(i)) & 1)) {
-        s0 = fma(-L(i, 0), w[0], s0);
-        k = 1;
-      }
-#pragma unroll
-      for (; k + 1 < i; k += 2) {
-        const double2 q = *reinterpret_cast<const double2*>(&L(i, k));
-        if ((k & 2) == 0) { s0 = fma(-q.x, w[k], s0); s1 = fma(-q.y, w[k + 1], s1); }
-        else { s2 = fma(-q.x, w[k], s2); s3 = fma(-q.y, w[k + 1], s3); }
-      }
-      if (k < i) s1 = fma(-L(i, k), w[k], s1);
-      w[i] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
+      for (int i = k + 1; i < 16; ++i) sv[i] = fma(-pb[k + colstart(i)], w[k], sv[i]);
     }
   }
-  __syncwarp();  // every lane has finished reading L
-  // column j: element i at pcol[T ? colstart(i) : i]
-  double* pcol = p + (T ? j : colstart(j));
+  __syncwarp();  // every lane has finished reading its block
+  double* pw = const_cast<double*>(pb);
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (i >= j) pcol[T ? colstart(i) : i] = w[i];
+  for (int i = 0; i < 16; ++i)
+    if (i >= j) pw[T ? j + colstart(i) : i + colstart(j)] = w[i];
+  __syncwarp();
+  // T1 = L21 W11 (16 x 16, W11 lower: its upper slots hold the other block)
+  const LaneOff o;
+  const int g = lane >> 2, t = lane & 3;
+  double c1[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c1[ni][r] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 16; k0 += 4) {
+    const double a0 = V.gt(o, 16, k0), a1 = V.gt(o, 24, k0);
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      if (k0 + 4 <= 8 * ni) continue;  // rows k < 8ni: W11 above its diagonal
+      const double bv = (k0 + t < 8 * ni + g) ? 0.0 : V.tg(o, k0, 8 * ni);
+      mma(c1[ni], a0, a1, bv);
+    }
+  }
+  // accumulator -> B operand: xb[ni][s] = T1(4s + t, 8ni + g)
+  double xb[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      const int half = s4 >> 1, src = (4 * (s4 & 1) + t) * 4 + (g >> 1);
+      const double v0 = __shfl_sync(0xffffffffu, c1[ni][half * 2], src);
+      const double v1 = __shfl_sync(0xffffffffu, c1[ni][half * 2 + 1], src);
+      xb[ni][s4] = (g & 1) ? v1 : v0;
+    }
+  // W21 = -W22 T1 (W22 lower)
+  double c2[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c2[ni][r] = 0.0;
+#pragma unroll
+  for (int s4 = 0; s4 < 4; ++s4) {
+    const int kk = 4 * s4 + t;
+    const double a0 = (kk > g) ? 0.0 : V.gt(o, 16, 16 + 4 * s4);
+    const double a1 = (kk > g + 8) ? 0.0 : V.gt(o, 24, 16 + 4 * s4);
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) mma(c2[ni], a0, a1, xb[ni][s4]);
+  }
+  __syncwarp();  // L21 fully read (T1) before W21 overwrites it
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) V.acc(o, 16 + ((r & 2) ? 8 : 0), 8 * ni, r & 1) = -c2[ni][r];
   __syncwarp();
 }
 

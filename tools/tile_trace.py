@@ -38,3 +38,14 @@ for k in kinds:
     st = sorted(rs, key=lambda r: r[2])
     gaps = [(st[i + 1][6] - st[i][7]) / 1e3 for i in range(len(st) - 1)]
     print("  W_j published -> next super sees it: mean %.1f us" % np.mean(gaps))
+
+# utilisation: busy CTA-time / (span x CTAs), and over time in 10 slices
+ctas = len({r[3] for r in rows})
+busy = sum(r[7] - r[4] for r in rows)
+span = tend - t00
+print("CTAs %d  utilisation %.1f%%" % (ctas, 100.0 * busy / (span * ctas)))
+edges = np.linspace(t00, tend, 11)
+for s in range(10):
+    a0, a1 = edges[s], edges[s + 1]
+    b = sum(max(0, min(r[7], a1) - max(r[4], a0)) for r in rows)
+    print("  slice %d: %.0f%% busy" % (s, 100.0 * b / ((a1 - a0) * ctas)))
