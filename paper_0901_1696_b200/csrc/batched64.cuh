@@ -100,14 +100,15 @@ template <bool T> struct RV {
 // p+1's registers.  16-wide rows halve the broadcast volume of a 32-wide
 // right-looking sweep.  Returns 0 or the failing pivot (1-based in the view;
 // NaN fails like the reference's `not d > 0`, kernels.py:436).
-template <bool T>
-__device__ __noinline__ int panel16(double* p, double* colk, int c0) {
+__device__ __noinline__ int panel16(double* p, double* colk, int c0, bool T) {
   __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(colk));
   __builtin_assume(c0 == 0 || c0 == 16);
   const int lane = threadIdx.x & 31;
   // row `lane`, panel column j: prow[T ? j : colstart(j)] (colstart is
-  // additive over the 16-aligned c0, so one body serves both panels)
+  // additive over the 16-aligned c0, so one body serves both panels and, with
+  // the orientation a runtime select, both views: 4 uses per matrix of one
+  // copy in the instruction cache)
   double* prow = p + (T ? colstart(lane) + c0 : lane + colstart(c0));
   double r[16];
 #pragma unroll
@@ -148,7 +149,7 @@ __device__ __noinline__ int panel16(double* p, double* colk, int c0) {
 // L21), V22 -= L21 L21^T on DMMA (m16n8k4, lower tiles), panel [16, 32).
 template <bool T>
 __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* colk) {
-  int f = panel16<T>(p, colk, 0);
+  int f = panel16(p, colk, 0, T);
   if (f) return f;
   const RV<T> V{p};
   double acc[2][4];
@@ -175,7 +176,7 @@ __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* col
       }
     }
   __syncwarp();
-  return panel16<T>(p, colk, 16);
+  return panel16(p, colk, 16, T);
 }
 
 // In-place inverse of the lower 32x32 view (only its lower triangle is read
