@@ -15,6 +15,28 @@ __device__ __forceinline__ void tri_tile(int mode, long long b, int& tm, int& tn
   if (mode == TRI_LOWER) { tm = ti; tn = tj; } else { tm = tj; tn = ti; }
 }
 
+// the same for BM x BN tiles with BN a multiple of BM (64 x 128): column tile
+// tn spans rows tiles from (TRI_LOWER) BN/BM*tn, or up to (TRI_UPPER)
+// BN/BM*(tn+1)-1; scanned column by column (<= tiles_n steps per CTA)
+template <int BM, int BN>
+__host__ __device__ inline long long tri_rect_count(int mode, int tn, int tiles_m) {
+  constexpr int R = BN / BM;
+  if (mode == TRI_LOWER) return tiles_m > R * tn ? tiles_m - R * tn : 0;
+  return R * (tn + 1) < tiles_m ? R * (tn + 1) : tiles_m;
+}
+template <int BM, int BN>
+__device__ __forceinline__ void tri_tile_rect(int mode, long long b, int tiles_m, int& tm, int& tn) {
+  constexpr int R = BN / BM;
+  tn = 0;
+  for (;;) {
+    const long long c = tri_rect_count<BM, BN>(mode, tn, tiles_m);
+    if (b < c) break;
+    b -= c;
+    ++tn;
+  }
+  tm = (mode == TRI_LOWER ? R * tn : 0) + (int)b;
+}
+
 __device__ __forceinline__ bool tri_keep(int mode, int row, int col) {
   return mode == TRI_FULL || (mode == TRI_LOWER ? row >= col : row <= col);
 }
@@ -183,7 +205,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int tm, tn;
     if (MODE == TRI_FULL) { tm = (int)(t % g.tiles_m); tn = (int)(t / g.tiles_m); }
-    else tri_tile(MODE, t, tm, tn);
+    else if constexpr (BM == BN) tri_tile(MODE, t, tm, tn);
+    else tri_tile_rect<BM, BN>(MODE, t, g.tiles_m, tm, tn);
     gemm_tile<T, BM, BN, BK, WM, WN, STAGES, AK, BKM, MODE>(g, tm, tn, As, Bs);
     if (t + gridDim.x < g.ntiles) __syncthreads();  // smem stages are reused
   }
@@ -321,7 +344,14 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
   const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   GemmArgs<T> g = a;
   g.tiles_m = tm;
-  g.ntiles = MODE == TRI_FULL ? (long long)tm * tn : (long long)tm * (tm + 1) / 2;
+  if (MODE == TRI_FULL) {
+    g.ntiles = (long long)tm * tn;
+  } else if (BM == BN) {
+    g.ntiles = (long long)tm * (tm + 1) / 2;
+  } else {
+    g.ntiles = 0;
+    for (int j = 0; j < tn; ++j) g.ntiles += tri_rect_count<BM, BN>(MODE, j, tm);
+  }
   const long long grid = g.ntiles;
   kern<<<(unsigned)grid, NT, smem, st>>>(g);
   RFPK_CHECK_LAUNCH();
@@ -469,6 +499,15 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
       return v ? std::atoi(v) : 0;
     }();
     if (force == 128) return launch_mode<T, 128, 128, 16, 64, 32, 4>(g, tri_mode, ak, bk, st);
+    // 64 x 128 tiles (4 warps of 32 x 64: 12 fragment loads per 16 DMMAs
+    // instead of 8 per 8) for full products with >= 4 waves of them at 2
+    // CTAs/SM: DGEMM 8192^3 32.4-33.5 -> 34.2-34.4 TFLOP/s; at 8192 x 1024 the
+    // tile count is too small (29.8 vs 32.5).  SYRK/HERK keep 64 x 64: on the
+    // odd-ld RFP operands of pftrf the wide tiles measured slower (T2 -= S1
+    // S1^T at n = 16384: 17.46 vs 17.02 ms); RFPK_TILE=64128 forces them.
+    const long long t128 = (long long)((g.M + 63) / 64) * ((g.N + 127) / 128);
+    if (force == 64128 || (force == 0 && tri_mode == TRI_FULL && t128 >= 8LL * num_sms()))
+      return launch_mode<T, 64, 128, 16, 32, 64, 3>(g, tri_mode, ak, bk, st);
     return launch_mode<T, 64, 64, 16, 32, 32, 3>(g, tri_mode, ak, bk, st);
   }
 }

@@ -212,3 +212,63 @@ def test_gemm_splitk_deterministic(K, cplx):
         outs.append(cd.cpu().numpy())
     assert rel(outs[0], want) <= TOL
     assert all(np.array_equal(o, outs[0]) for o in outs[1:])
+
+
+def test_gemm_wide_tiles(K):
+    """Large outputs take the 64 x 128 tile configuration (>= 4 waves of
+    tiles); ragged edges in both dimensions."""
+    m, n, k = 4096 + 17, 4096 + 33, 40
+    a = rnd((m, k), False, 31)
+    b = rnd((n, k), False, 32)
+    c = rnd((m, n), False, 33)
+    want = c.copy()
+    O.gemm("N", "T", 1.5, a, b, -0.5, want)
+    cd = dev(c)
+    K.gemm("N", "T", 1.5, dev(a), dev(b), -0.5, cd)
+    assert rel(cd, want) <= TOL
+
+
+@pytest.mark.parametrize("uplo,trans", [("L", "N"), ("U", "N"), ("L", "T"), ("U", "T")])
+def test_syrk_large(K, uplo, trans):
+    """SYRK over many triangular tiles with ragged edges: exactly the declared
+    triangle is updated (the other one stays bit-identical)."""
+    n, k = 4700, 24
+    a = rnd((n, k) if trans == "N" else (k, n), False, 34)
+    c = rnd((n, n), False, 35, rowmajor=(uplo == "U"))
+    want = c.copy()
+    O.syrk_herk(uplo, trans, -1.0, a, 1.0, want, False)
+    cd = dev(c)
+    K.syrk_herk(uplo, trans, -1.0, dev(a), 1.0, cd, hermitian=False)
+    assert rel(cd, want) <= TOL
+    other = np.triu(np.ones((n, n), bool), 1) if uplo == "L" else np.tril(np.ones((n, n), bool), -1)
+    assert np.array_equal(cd.cpu().numpy()[other], c[other])
+
+
+def test_forced_wide_tiles_triangular():
+    """RFPK_TILE=64128 forces the 64 x 128 tiles onto SYRK too (the non-square
+    triangular tile enumeration); the env is read once per process, so this
+    runs in a child interpreter."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch
+from oracle import rfp_oracle as O
+from paper_0901_1696_b200 import kernels as K
+for uplo in "LU":
+    g = np.random.default_rng(5)
+    a = np.asfortranarray(g.standard_normal((700, 19)))
+    c = np.asfortranarray(g.standard_normal((700, 700)))
+    want = c.copy(); O.syrk_herk(uplo, "N", -1.0, a, 1.0, want, False)
+    cd = torch.from_numpy(c).cuda(); K.syrk_herk(uplo, "N", -1.0, torch.from_numpy(a).cuda(), 1.0, cd)
+    got = cd.cpu().numpy()
+    assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max(), uplo
+    other = np.triu(np.ones((700, 700), bool), 1) if uplo == "L" else np.tril(np.ones((700, 700), bool), -1)
+    assert np.array_equal(got[other], c[other]), uplo
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RFPK_TILE="64128", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -12,7 +12,14 @@ ld = d.ldar
 t2 = buf.data_ptr()                       # rect[0:n2, 0:n2] (d = 1)
 s1 = buf.data_ptr() + 8 * (d.n1 + d.shift)  # rect[n1+1:, 0:n1]
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-for _ in range(reps):
+def call():
     rc = lib.rfpk_dsyrk(b"U", b"C", -1.0, s1, d.n2, d.n1, 1, ld, 1.0, t2, d.n2, 1, ld, st)
     assert rc == 0
-torch.cuda.synchronize(); print("ok")
+call()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize(); e0.record()
+for _ in range(reps):
+    call()
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / reps
+print("ok syrk %.3f ms  %.2f TFLOP/s" % (ms, d.n2 * d.n2 * d.n1 / ms / 1e9))
