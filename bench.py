@@ -9,7 +9,7 @@ the RHS exceed the 126 MB L2, so no flush is needed).  Metric: FP64 GFLOP/s
 with the LAPACK flop model n^3/3 + 2 n^2 nrhs.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-  --workload c3 (default) | c1 | c2 | c4 | c5   (other BASELINE configs)
+  --workload c3 (default) | c4   (c1, c2, c5: tools/perf.py, tools/config5.py)
 
 Under torchrun (N > 1) every rank factors its own replica (single matrices
 do not shard: "replicas only", weak scaling); config 4 (--workload c4) is
@@ -211,9 +211,64 @@ def cpu_sample(n=4096, nrhs=256, reps=2, seed=3):
                       f"{t:.2f} s each; numpy/OpenBLAS {cores} threads)"}
 
 
+def c3_config(n, nrhs, world):
+    return {"workload": "BASELINE config 3: pftrf+pftrs, n=16384, TRANSR=N, UPLO=L, nrhs=1024",
+            "n": n, "nrhs": nrhs, "transr": "N", "uplo": "L",
+            "l2": "no flush: RFP buffer 1.07 GB + RHS 134 MB exceed the 126 MB L2",
+            "parallelism": "replicas" if world > 1 else "single GPU"}
+
+
+def c4_config(total, n, nrhs, world):
+    return {"workload": "BASELINE config 4: 65536 x n=64 UN pftrf+pftrs(nrhs=8), sharded by matrix",
+            "batch": total, "n": n, "nrhs": nrhs, "parallelism": f"dp{world} (contiguous shards)",
+            "l2": "no flush: every step factors its own fresh 1.6 GB copy"}
+
+
+def _batched_worker(args):
+    """One process's share of the reference's batched sample (single-threaded
+    BLAS, as SURVEY 8(d) prescribes for config 4)."""
+    first, count = args
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return cpu_sample_batched(count=count, first=first)["value"]
+
+
+def run_reference_c4(args, rank, world):
+    """Reference arm for config 4: the reference's own pftrf+pftrs on n=64
+    matrices, one process per host core (each single-threaded), a bounded
+    sample of the 65,536 per step."""
+    import concurrent.futures as cf
+    cores = _threads()
+    per = 48
+    steps = []
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            list(ex.map(_batched_worker, [(1000 * i + c * per, per) for c in range(cores)]))
+            t = time.perf_counter() - t0
+            if i >= args.warmup:
+                steps.append(cores * per / t)
+    value = float(np.mean(steps))
+    kind = "reference" if _reference_module() is not None else "port"
+    line = {
+        "impl": "reference", "metric": METRIC_C4, "value": value, "unit": "matrices/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cores * per / value * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy)",
+        "config": c4_config(args.batch, 64, 8, world),
+        "cpu_baseline": {"value": value, "unit": "matrices/s", "cores": cores, "kind": kind,
+                         "sample": f"{cores} processes x {per} matrices n=64 UN pftrf+pftrs(8) per "
+                                   f"step, single-threaded BLAS each"},
+        "e2e": {"value": value, "unit": "matrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.workload == "c4":
+        return run_reference_c4(args, rank, world)
     steps = []
     res = None
     for i in range(args.warmup + args.steps):
@@ -228,8 +283,7 @@ def run_reference(args, rank, world):
         "ms_per_step": (args.ref_n ** 3 / 3 + 2 * args.ref_n ** 2 * args.ref_nrhs) / value / 1e6,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy)",
-        "config": {"workload": f"config3 sample: n={args.ref_n} LN pftrf+pftrs nrhs={args.ref_nrhs} "
-                               f"(bounded CPU sample of n={n}, nrhs={nrhs})"},
+        "config": c3_config(n, nrhs, world),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"],
                          "kind": res["kind"], "sample": res["sample"]},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -387,10 +441,7 @@ def run_b200(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: B~N(0,1) seeded numpy, A=B B^T/n+I (formed on device), RHS~N(0,1)",
-        "config": {"workload": "BASELINE config 3: pftrf+pftrs, n=16384, TRANSR=N, UPLO=L, nrhs=1024",
-                   "n": n, "nrhs": nrhs, "transr": transr, "uplo": uplo,
-                   "l2": "no flush: RFP buffer 1.07 GB + RHS 134 MB exceed the 126 MB L2",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "config": c3_config(n, nrhs, world),
         "fraction_of_fp64_nominal": value / 1e3 / NOMINAL_FP64_TFLOPS,
         "fraction_of_fp64_measured_dgemm": value / 1e3 / dgemm_tflops,
         "roofline": {"bound": "tensor",
@@ -550,9 +601,7 @@ def run_c4(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: B_k~N(0,1) from default_rng(seed0+k), A_k=B_k B_k^T+64 I",
-        "config": {"workload": "BASELINE config 4: 65536 x n=64 UN pftrf+pftrs(nrhs=8), sharded by matrix",
-                   "batch": total, "n": n, "nrhs": nrhs, "parallelism": f"dp{world} (contiguous shards)",
-                   "l2": "no flush: every step factors its own fresh 1.6 GB copy"},
+        "config": c4_config(total, n, nrhs, world),
         "roofline": {"bound": "hbm", "kernel": "batched64_kernel (fused pftrf+pftrs)",
                      "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved_gbs / hbm_peak,
@@ -570,13 +619,14 @@ def run_c4(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
-def cpu_sample_batched(count=256, n=64, nrhs=8):
+def cpu_sample_batched(count=256, n=64, nrhs=8, first=0):
     """Reference (or oracle) pftrf+pftrs on `count` n=64 UN matrices, one
     process, BLAS single-threaded semantics are the reference's own."""
     from oracle import rfp_oracle as O
     ref = _reference_module()
-    mats = [O.spd_matrix(n, k, "n") for k in range(count)]
-    rhs = [np.asfortranarray(np.random.default_rng(k).standard_normal((n, nrhs))) for k in range(count)]
+    mats = [O.spd_matrix(n, first + k, "n") for k in range(count)]
+    rhs = [np.asfortranarray(np.random.default_rng(first + k).standard_normal((n, nrhs)))
+           for k in range(count)]
     t0 = time.perf_counter()
     for a, b in zip(mats, rhs):
         x = b.copy(order="F")
