@@ -504,7 +504,8 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
   static const i64 tile_min = env_int("RFPK_TILE_TRSM_MIN", 512);
   static const i64 tile_min_narrow = env_int("RFPK_TILE_TRSM_MIN_NARROW", 128);
   static const i64 narrow = env_int("RFPK_TRSM_NARROW", 256);
-  const i64 tmin = B.n <= narrow ? tile_min_narrow : tile_min;
+  const i64 tasks64 = ((Tm.m + 63) / 64) * ((B.n + 63) / 64);
+  const i64 tmin = (B.n <= narrow || tasks64 <= 10 * (i64)num_sms()) ? tile_min_narrow : tile_min;
   if (!is_cplx<T>::value && Tm.m >= tmin && !std::getenv("RFPK_NO_TILE_TRSM") &&
       (rc = trsm_tiles(c, lower, conj, Tm, B, (const T*)W, !lower)) != -100) {
     ws_free(own, c.st);

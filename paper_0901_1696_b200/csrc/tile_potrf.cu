@@ -947,7 +947,8 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
-    if (tid == 0) spin_wait_acquire(a.ext + (a.ext_mode ? c : i));
+    // (the gate's flags cover 64-column chunks; c counts TN-wide blocks)
+    if (tid == 0) spin_wait_acquire(a.ext + (a.ext_mode ? c * TN / TP : i));
     __syncthreads();
   }
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
@@ -1104,13 +1105,19 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.n = (int)n;
   a.nrhs = (int)B.n;
   a.nb = (int)((n + TP - 1) / TP);
-  // narrow right-hand sides: 64 x 16 tiles give four times the chains and a
-  // four times shorter step on each (pftrs at n = 4000, nrhs = 64)
+  // 64 x 16 tiles give four times the chains and a four times shorter step
+  // on each: used for narrow right-hand sides (pftrs at n = 4000, nrhs = 64:
+  // 1.63 -> 0.74 ms) and whenever the 64-wide tiles would be few (<= ~10 per
+  // SM: pftrf's S1 solve at n = 4000 0.72 -> 0.52 ms, n = 1000 0.16 ->
+  // 0.07 ms); measured slower with more tasks (S1 at n = 6000 1.48 vs 1.31
+  // ms, 16384 26.8 vs 17.6 ms; pftrs 16384 x 1024 3.4 vs 2.7 ms per solve)
   static const int narrow_max = [] {
     const char* v = std::getenv("RFPK_TRSM_NARROW");
     return v ? std::atoi(v) : 256;
   }();
-  const int tn = (!is_cplx<T>::value && B.n <= narrow_max) ? 16 : TP;
+  const long long tasks64 = (long long)a.nb * ((B.n + TP - 1) / TP);
+  const int tn = (!is_cplx<T>::value &&
+                  (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;
   a.nc = (int)((B.n + tn - 1) / tn);
   a.lower = lower ? 1 : 0;
   a.conj = conj ? 1 : 0;
