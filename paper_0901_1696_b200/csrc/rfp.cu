@@ -438,6 +438,29 @@ __device__ __forceinline__ int tile_mode(const Storage& s, i64 j0) {
   return 3;
 }
 
+// Addressing of one storage over a tile that lies inside one RFP block: the
+// RFP and full maps are affine there (base + i*si + j*sj, from three probes of
+// storage_addr), the packed map is affine in i within each column.
+struct TileAff {
+  i64 base, si, sj;
+  int packed;
+};
+__device__ __forceinline__ TileAff tile_aff(const Storage& s, i64 i0, i64 j0) {
+  TileAff a{0, 1, 0, 0};
+  if (s.kind == ST_PACKED) {
+    a.packed = 1;
+    return a;
+  }
+  bool f;
+  a.base = storage_addr(s, i0, j0, f);
+  a.si = storage_addr(s, i0 + 1, j0, f) - a.base;
+  a.sj = storage_addr(s, i0, j0 + 1, f) - a.base;
+  return a;
+}
+__device__ __forceinline__ i64 packed_addr(const RfpDesc& r, i64 i, i64 j) {
+  return r.lower ? j * r.n - j * (j - 1) / 2 + (i - j) : j * (j + 1) / 2 + i;
+}
+
 // One 64x64 tile of the logical (i, j) space per CTA (256 threads, 16
 // elements per thread per pass, all loads of a pass issued before the shared
 // stores).  Loads use an i-fast or j-fast thread mapping according to the
@@ -466,6 +489,48 @@ __global__ void __launch_bounds__(256) convert_kernel(Storage src, const T* __re
   }
   const int smode = tile_mode(src, j0);
   const int dmode = zero_fill ? 1 : tile_mode(dst, j0);
+  // interior tiles (strictly inside the triangle, inside the matrix, one RFP
+  // block on each side): affine addressing, one add per element
+  const bool interior = (lower ? i0 >= j0 + 64 : i0 + 64 <= j0) && i0 + 63 < n && j0 + 63 < n;
+  if (interior && smode != 3 && dmode != 3) {
+    const TileAff sa = tile_aff(src, i0, j0), da = tile_aff(dst, i0, j0);
+    const int a = tid & 63, b = tid >> 6;
+    T v[16];
+    if (smode == 1) {  // i-fast: lanes along i, r along j
+      if (sa.packed) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = sp[packed_addr(src.r, i0 + a, j0 + b + 4 * r)];
+      } else {
+        const T* p = sp + sa.base + a * sa.si + b * sa.sj;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = p[(i64)r * 4 * sa.sj];
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) tile[(b + 4 * r) * TL + a] = v[r];
+    } else {           // j-fast: lanes along j, r along i
+      const T* p = sp + sa.base + b * sa.si + a * sa.sj;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = p[(i64)r * 4 * sa.si];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) tile[a * TL + b + 4 * r] = v[r];
+    }
+    __syncthreads();
+    if (dmode == 1) {
+      if (da.packed) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) dp[packed_addr(dst.r, i0 + a, j0 + b + 4 * r)] = tile[(b + 4 * r) * TL + a];
+      } else {
+        T* p = dp + da.base + a * da.si + b * da.sj;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) p[(i64)r * 4 * da.sj] = tile[(b + 4 * r) * TL + a];
+      }
+    } else {
+      T* p = dp + da.base + b * da.si + a * da.sj;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) p[(i64)r * 4 * da.si] = tile[a * TL + b + 4 * r];
+    }
+    return;
+  }
 #pragma unroll
   for (int pass = 1; pass <= 2; ++pass) {
     if (!(smode & pass)) continue;

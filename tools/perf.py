@@ -139,17 +139,28 @@ def rfp_bench(n, uplo, transr, nrhs, do_pftri=False, cplx=False, reps=5):
             tflops=mul * 2 * n ** 3 / 3 / ms / 1e9, info=int(info.item()))
 
 
-def conv_bench(n):
-    from paper_0901_1696_b200 import convert
-    a = spd_gpu(n)
+def conv_bench(n, uplos="L", cplx=False, reps=5):
+    """Conversions at order n: bytes = every element read once + written once
+    (tfttr also writes the zeroed other triangle of the n x n output)."""
     nt = n * (n + 1) // 2
-    arf = torch.empty(nt, dtype=torch.float64, device=dev)
-    full = torch.empty(n, n, dtype=torch.float64, device=dev)
-    for tr in "NT":
-        ms = ev_time(lambda: lib.rfpk_dtrttf(tr.encode(), b"L", n, a.data_ptr(), n, arf.data_ptr(), st()), 5)
-        out(kind="trttf", n=n, transr=tr, ms=ms, gbs=2 * nt * 8 / ms / 1e6)
-        ms = ev_time(lambda: lib.rfpk_dtfttr(tr.encode(), b"L", n, arf.data_ptr(), full.data_ptr(), n, st()), 5)
-        out(kind="tfttr", n=n, transr=tr, ms=ms, gbs=(nt * 8 + n * n * 8) / ms / 1e6)
+    dt = torch.complex128 if cplx else torch.float64
+    es = 16 if cplx else 8
+    p = "z" if cplx else "d"
+    a = torch.randn(n, n, dtype=dt, device=dev)
+    arf = torch.empty(nt, dtype=dt, device=dev)
+    pk = torch.empty(nt, dtype=dt, device=dev)
+    full = torch.empty(n, n, dtype=dt, device=dev)
+    f = lambda name: getattr(lib, f"rfpk_{p}{name}")
+    for u in uplos:
+        for tr in "NT":
+            ms = ev_time(lambda: f("trttf")(tr.encode(), u.encode(), n, a.data_ptr(), n, arf.data_ptr(), st()), reps)
+            out(kind="trttf", n=n, uplo=u, transr=tr, dtype=p, ms=ms, gbs=2 * nt * es / ms / 1e6)
+            ms = ev_time(lambda: f("tfttr")(tr.encode(), u.encode(), n, arf.data_ptr(), full.data_ptr(), n, st()), reps)
+            out(kind="tfttr", n=n, uplo=u, transr=tr, dtype=p, ms=ms, gbs=(nt + n * n) * es / ms / 1e6)
+            ms = ev_time(lambda: f("tfttp")(tr.encode(), u.encode(), n, arf.data_ptr(), pk.data_ptr(), st()), reps)
+            out(kind="tfttp", n=n, uplo=u, transr=tr, dtype=p, ms=ms, gbs=2 * nt * es / ms / 1e6)
+            ms = ev_time(lambda: f("tpttf")(tr.encode(), u.encode(), n, pk.data_ptr(), arf.data_ptr(), st()), reps)
+            out(kind="tpttf", n=n, uplo=u, transr=tr, dtype=p, ms=ms, gbs=2 * nt * es / ms / 1e6)
 
 
 def batched_bench(batch=65536, n=64, nrhs=8):
@@ -200,5 +211,9 @@ if __name__ == "__main__":
         rfp_bench(6000, "L", "T", 0, do_pftri=True, cplx=True, reps=2)
     if w in ("all", "conv"):
         conv_bench(16384)
+    if w == "convall":
+        conv_bench(16384, "LU")
+        conv_bench(16383, "LU")
+        conv_bench(11584, "L", cplx=True)
     if w in ("all", "batched"):
         batched_bench()
