@@ -730,19 +730,6 @@ int sfrk(Ctx c, const RfpDesc& d, char trans, i64 k, double alpha, View<T> a, do
 // (i, j) of the triangle stands for |A(i,j)| = |A(j,i)|: 'M' takes the max,
 // 'F' sums |a|^2 twice off the diagonal, '1'/'I' add |a| to the column sums
 // of columns j and i (the implied full matrix is symmetric in magnitude).
-__device__ __forceinline__ void rfp_slot_cell(const RfpDesc& d, i64 p, i64& i, i64& j) {
-  i64 r, c;
-  if (!d.trans) { c = p / d.ldar; r = p - c * d.ldar; }
-  else { r = p / d.n1; c = p - r * d.n1; }
-  if (d.lower) {
-    if (r >= c + d.d) { i = r - d.d; j = c; }
-    else { j = r + d.n1; i = c + d.n1 - 1 + d.d; }
-  } else {
-    if (r <= c + d.n2) { i = r; j = c + d.n2; }
-    else { j = r - d.n2 - 1; i = c; }
-  }
-}
-
 __device__ __forceinline__ double mag(double v) { return fabs(v); }
 __device__ __forceinline__ double mag(Z v) { return hypot(v.x, v.y); }
 
@@ -751,27 +738,17 @@ __device__ __forceinline__ void atomic_max_pos(double* a, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(a), __double_as_longlong(v));
 }
 
+// 'M' and the bulk of 'F': one grid-stride pass over the buffer with no index
+// arithmetic (F^2 = 2 sum |a|^2 - sum_diag |a|^2: every stored off-diagonal
+// cell stands for two entries of the full matrix).
 template <typename T>
-__global__ void lansf_kernel(RfpDesc d, const T* __restrict__ arf, int mode, double* acc,
-                             double* colsum) {
+__global__ void lansf_sum_kernel(const T* __restrict__ arf, i64 nt, int mode, double* acc) {
   double local = 0.0;
-  for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < d.nt;
+  for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < nt;
        p += (i64)gridDim.x * blockDim.x) {
     const double m = mag(arf[p]);
-    if (mode == 0) {
-      local = fmax(local, m);
-    } else if (mode == 2) {
-      i64 i, j;
-      rfp_slot_cell(d, p, i, j);
-      local += (i == j ? 1.0 : 2.0) * m * m;
-    } else {
-      i64 i, j;
-      rfp_slot_cell(d, p, i, j);
-      atomicAdd(colsum + j, m);
-      if (i != j) atomicAdd(colsum + i, m);
-    }
+    local = mode == 0 ? fmax(local, m) : local + 2.0 * m * m;
   }
-  if (mode == 1) return;
   for (int o = 16; o > 0; o >>= 1) {
     const double v = __shfl_down_sync(0xffffffffu, local, o);
     local = mode == 0 ? fmax(local, v) : local + v;
@@ -779,6 +756,128 @@ __global__ void lansf_kernel(RfpDesc d, const T* __restrict__ arf, int mode, dou
   if ((threadIdx.x & 31) == 0) {
     if (mode == 0) atomic_max_pos(acc, local);
     else atomicAdd(acc, local);
+  }
+}
+
+// acc -= sum over the n diagonal cells of |a|^2
+template <typename T>
+__global__ void lansf_diag_kernel(RfpDesc d, const T* __restrict__ arf, double* acc) {
+  double local = 0.0;
+  const Storage s{ST_RFP, 0, d};
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < d.n; k += (i64)gridDim.x * blockDim.x) {
+    bool f;
+    const double m = mag(arf[storage_addr(s, k, k, f)]);
+    local += m * m;
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc, -local);
+}
+
+// '1' / 'I': column sums of the implied full matrix.  Cell (row, col) of the
+// normal rectangle (ldar x n1) stands for (i, j) of the triangle, and in each
+// of its two regions one index depends on the row only, the other on the
+// column only:
+//   L, A (row >= col+d):  i = row-d,    j = col;        diagonal: row-d == col
+//   L, B:                 j = row+n1,   i = col+n1-1+d; diagonal: col+d-1 == row
+//   U, A (row <= col+n2): i = row,      j = col+n2;     diagonal: row == col+n2
+//   U, B:                 j = row-n2-1, i = col;        diagonal: col == row-n2-1
+// so colsum[row target] += sum over a rectangle ROW and colsum[column target]
+// += sum over a rectangle COLUMN (the diagonal counted once, with the row).
+// Two coalesced passes: BY_RUN reduces each contiguous run of the buffer (a
+// warp per run, 2 atomics per run), !BY_RUN gives each thread one position of
+// the run and sums across 64 runs (2 atomics per thread per 64 runs).
+// Per fixed coordinate (the run for BY_RUN, the position within the runs
+// otherwise) the region boundary, the two diagonal positions and both targets
+// are computed once; each element then costs a compare-select-add.
+struct LansfFixed {
+  long long bound;  // region A <=> v >= bound (aGE) or v <= bound (!aGE)
+  bool aGE;
+  long long dA, dB;  // varying-index positions of the A / B diagonal cells
+  i64 tA, tB;        // targets of the two regions
+};
+__device__ __forceinline__ LansfFixed lansf_fixed(const RfpDesc& d, i64 f, bool fixed_is_row,
+                                                  bool col_target) {
+  LansfFixed q;
+  if (d.lower) {
+    if (fixed_is_row) {  // A <=> col <= row - d
+      q.bound = f - d.d; q.aGE = false; q.dA = f - d.d; q.dB = f + 1 - d.d;
+      q.tA = col_target ? -1 : f - d.d; q.tB = col_target ? -1 : f + d.n1;
+    } else {             // A <=> row >= col + d
+      q.bound = f + d.d; q.aGE = true; q.dA = f + d.d; q.dB = f + d.d - 1;
+      q.tA = col_target ? f : -1; q.tB = col_target ? f + d.n1 - 1 + d.d : -1;
+    }
+  } else {
+    if (fixed_is_row) {  // A <=> col >= row - n2
+      q.bound = f - d.n2; q.aGE = true; q.dA = f - d.n2; q.dB = f - d.n2 - 1;
+      q.tA = col_target ? -1 : f; q.tB = col_target ? -1 : f - d.n2 - 1;
+    } else {             // A <=> row <= col + n2
+      q.bound = f + d.n2; q.aGE = false; q.dA = f + d.n2; q.dB = f + d.n2 + 1;
+      q.tA = col_target ? f + d.n2 : -1; q.tB = col_target ? f : -1;
+    }
+  }
+  return q;
+}
+
+template <typename T, bool BY_RUN>
+__global__ void __launch_bounds__(256) lansf_colsum_kernel(RfpDesc d, const T* __restrict__ arf,
+                                                           double* colsum) {
+  // buffer = column-major (L x NR): runs of length L; 'N': runs are rectangle
+  // columns (L = ldar), 'T': rectangle rows (L = n1)
+  const i64 L = d.trans ? d.n1 : d.ldar, NR = d.trans ? d.ldar : d.n1;
+  // the index this pass accumulates: along a run (BY_RUN) the run's own index
+  // is fixed -- 'N' runs fix the column (column target), 'T' runs fix the row
+  const bool col_target = BY_RUN != (bool)d.trans;
+  // the fixed coordinate is a row when: BY_RUN and 'T', or !BY_RUN and 'N'
+  const bool fixed_is_row = BY_RUN == (bool)d.trans;
+  double sA = 0.0, sB = 0.0;
+  LansfFixed q{};
+  auto acc = [&](double m, long long v) {
+    const bool inA = q.aGE ? v >= q.bound : v <= q.bound;
+    // the diagonal cell counts once, with the row target
+    if (col_target && (v == q.dA || v == q.dB)) {
+      const bool diagA = v == q.dA && inA, diagB = v == q.dB && !inA;
+      if (diagA || diagB) m = 0.0;
+    }
+    if (inA) sA += m;
+    else sB += m;
+  };
+  if (BY_RUN) {
+    const i64 run = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (run >= NR) return;
+    q = lansf_fixed(d, run, fixed_is_row, col_target);
+    const T* pr = arf + run * L;
+    for (i64 x0 = lane; x0 < L; x0 += 8 * 32) {
+      double mv[8];  // eight independent loads in flight per lane
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = x0 + 32 * u < L ? mag(pr[x0 + 32 * u]) : -1.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (mv[u] >= 0.0) acc(mv[u], x0 + 32 * u);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sA += __shfl_down_sync(0xffffffffu, sA, o);
+      sB += __shfl_down_sync(0xffffffffu, sB, o);
+    }
+    if (lane == 0) {
+      if (q.tA >= 0 && sA != 0.0) atomicAdd(colsum + q.tA, sA);
+      if (q.tB >= 0 && sB != 0.0) atomicAdd(colsum + q.tB, sB);
+    }
+  } else {
+    const i64 x = blockIdx.x * (i64)blockDim.x + threadIdx.x;  // position within the runs
+    if (x >= L) return;
+    q = lansf_fixed(d, x, fixed_is_row, col_target);
+    const i64 r0 = (i64)blockIdx.y * 64, r1 = r0 + 64 < NR ? r0 + 64 : NR;
+    for (i64 q0 = r0; q0 < r1; q0 += 8) {
+      double mv[8];  // eight independent loads in flight per thread
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = q0 + u < r1 ? mag(arf[(q0 + u) * L + x]) : -1.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (mv[u] >= 0.0) acc(mv[u], q0 + u);
+    }
+    if (q.tA >= 0 && sA != 0.0) atomicAdd(colsum + q.tA, sA);
+    if (q.tB >= 0 && sB != 0.0) atomicAdd(colsum + q.tB, sB);
   }
 }
 
@@ -798,25 +897,34 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
   if (e != cudaSuccess) return (int)e;
   if (d.n == 0) return 0;
   const int mode = norm == 'M' ? 0 : (norm == 'F' || norm == 'E') ? 2 : 1;
-  int blocks = (int)((d.nt + 255) / 256);
-  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   double* colsum = nullptr;
-  if (mode == 1) {
-    if ((e = cudaMallocAsync((void**)&colsum, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
-    if ((e = cudaMemsetAsync(colsum, 0, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
+  if (mode != 1) {
+    int blocks = (int)((d.nt + 255) / 256);
+    if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+    lansf_sum_kernel<T><<<blocks, 256, 0, st>>>(arf, d.nt, mode, out);
+    RFPK_CHECK_LAUNCH();
+    if (mode == 2) {
+      lansf_diag_kernel<T><<<(unsigned)((d.n + 255) / 256 < 1024 ? (d.n + 255) / 256 : 1024), 256, 0,
+                             st>>>(d, arf, out);
+      RFPK_CHECK_LAUNCH();
+      sqrt_kernel<<<1, 1, 0, st>>>(out);
+      RFPK_CHECK_LAUNCH();
+    }
+    return 0;
   }
-  lansf_kernel<T><<<blocks, 256, 0, st>>>(d, arf, mode, out, colsum);
+  if ((e = cudaMallocAsync((void**)&colsum, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(colsum, 0, sizeof(double) * d.n, st)) != cudaSuccess) return (int)e;
+  const i64 L = d.trans ? d.n1 : d.ldar, NR = d.trans ? d.ldar : d.n1;
+  lansf_colsum_kernel<T, true><<<(unsigned)((NR * 32 + 255) / 256), 256, 0, st>>>(d, arf, colsum);
   RFPK_CHECK_LAUNCH();
-  if (mode == 1) {
-    int cb = (int)((d.n + 255) / 256);
-    if (cb > 4 * num_sms()) cb = 4 * num_sms();
-    colmax_kernel<<<cb, 256, 0, st>>>(colsum, d.n, out);
-    RFPK_CHECK_LAUNCH();
-    cudaFreeAsync(colsum, st);
-  } else if (mode == 2) {
-    sqrt_kernel<<<1, 1, 0, st>>>(out);
-    RFPK_CHECK_LAUNCH();
-  }
+  lansf_colsum_kernel<T, false><<<dim3((unsigned)((L + 255) / 256), (unsigned)((NR + 63) / 64)), 256,
+                                  0, st>>>(d, arf, colsum);
+  RFPK_CHECK_LAUNCH();
+  int cb = (int)((d.n + 255) / 256);
+  if (cb > 4 * num_sms()) cb = 4 * num_sms();
+  colmax_kernel<<<cb, 256, 0, st>>>(colsum, d.n, out);
+  RFPK_CHECK_LAUNCH();
+  cudaFreeAsync(colsum, st);
   return 0;
 }
 

@@ -163,6 +163,29 @@ def conv_bench(n, uplos="L", cplx=False, reps=5):
             out(kind="tpttf", n=n, uplo=u, transr=tr, dtype=p, ms=ms, gbs=2 * nt * es / ms / 1e6)
 
 
+def frows_bench(n=16384, k=8192, nrhs=1024):
+    """SURVEY 8(f) rows at config-3 size: lansf (HBM: nt*8 bytes read),
+    sfrk (n^2 k flops), tfsm (n^2 nrhs flops)."""
+    nt = n * (n + 1) // 2
+    arf = torch.randn(nt, dtype=torch.float64, device=dev)
+    res = torch.zeros(1, dtype=torch.float64, device=dev)
+    for norm in "M1IF":
+        ms = ev_time(lambda: lib.rfpk_dlansf(norm.encode(), b"N", b"L", n, arf.data_ptr(), res.data_ptr(), st()), 5)
+        out(kind="lansf", norm=norm, n=n, ms=ms, gbs=nt * 8 / ms / 1e6)
+    a = torch.randn(k, n, dtype=torch.float64, device=dev).t()  # n x k column-major
+    ms = ev_time(lambda: lib.rfpk_dsfrk(b"N", b"L", b"N", n, k, -1.0, a.data_ptr(), 1, n, 1.0, arf.data_ptr(), st()), 3)
+    out(kind="sfrk", n=n, k=k, ms=ms, tflops=n * n * k / ms / 1e9)
+    g = torch.randn(n, n, dtype=torch.float64, device=dev); s = g @ g.t() / n; s.diagonal().add_(1.0)
+    from paper_0901_1696_b200 import convert
+    r = convert.trttf(s, "L", "N"); del g, s
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib.rfpk_dpftrf(b"N", b"L", n, r.data.data_ptr(), info.data_ptr(), st())
+    b0 = torch.randn(nrhs, n, dtype=torch.float64, device=dev).t(); b = b0.clone()
+    ms = ev_time(lambda: lib.rfpk_dtfsm(b"N", b"L", b"L", b"N", b"N", n, nrhs, 1.0, r.data.data_ptr(),
+                                        b.data_ptr(), 1, n, info.data_ptr(), st()), 3, lambda: b.copy_(b0))
+    out(kind="tfsm", n=n, nrhs=nrhs, ms=ms, tflops=n * n * nrhs / ms / 1e9)
+
+
 def batched_bench(batch=65536, n=64, nrhs=8):
     nt = n * (n + 1) // 2
     from paper_0901_1696_b200 import convert
@@ -211,6 +234,8 @@ if __name__ == "__main__":
         rfp_bench(6000, "L", "T", 0, do_pftri=True, cplx=True, reps=2)
     if w in ("all", "conv"):
         conv_bench(16384)
+    if w in ("all", "frows"):
+        frows_bench()
     if w == "convall":
         conv_bench(16384, "LU")
         conv_bench(16383, "LU")
