@@ -672,16 +672,35 @@ template <typename T> int trtri_oop(Ctx c, bool unit, View<T> A) {
   return rc;
 }
 
-template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
-  if (A.m == 0) return 0;
-  static const bool cplx_oop = env_int("RFPK_TRTRI_OOP_CPLX", 1) != 0;
-  if (A.m > LEAF && A.m <= oop_max() && (!is_cplx<T>::value || cplx_oop)) {
-    const int rc = trtri_oop(c, unit, A);
-    if (rc != -100) return rc;
-  }
+template <typename T> int trtri_lower_rec(Ctx c, bool unit, View<T> A);
+
+// Above the one-launch size: the top levels of the trmm recursion, with every
+// sub-block <= oop_max inverted by trtri_oop from the original L (config 5's
+// complex trtri at 12000: children 3000 on the tile trsm instead of a chain
+// of leaf inverses and small trmms)
+template <typename T> int trtri_hyb(Ctx c, bool unit, View<T> A) {
+  const i64 n = A.m;
+  if (n <= oop_max()) return n > LEAF ? trtri_oop(c, unit, A) : trtri_lower_rec(c, unit, A);
+  const i64 n1 = split_point(n), n2 = n - n1;
+  View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
+  int rc;
+  if ((rc = trtri_hyb(c, unit, A11))) return rc;
+  if ((rc = trtri_hyb(c, unit, A22))) return rc;
+  if ((rc = trmm_rec(c, false, false, unit, one<T>(), A11.t(), A21.t()))) return rc;
+  return trmm_rec(c, true, false, unit, neg_one<T>(), A22, A21);
+}
+
+template <typename T> int trtri_lower_rec(Ctx c, bool unit, View<T> A) {
   int rc = leaf_inverses<T>(c, A, unit, nullptr);
   if (rc) return rc;
   return trtri_rec(c, unit, A);
+}
+
+template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
+  if (A.m == 0) return 0;
+  static const bool cplx_oop = env_int("RFPK_TRTRI_OOP_CPLX", 1) != 0;
+  if (A.m > LEAF && (!is_cplx<T>::value || cplx_oop)) return trtri_hyb(c, unit, A);
+  return trtri_lower_rec(c, unit, A);
 }
 
 // A <- L^H L (lower triangle) as ONE herk launch from a zero-padded copy of L

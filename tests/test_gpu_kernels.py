@@ -272,3 +272,31 @@ print("ok")
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("diag", "NU")
+def test_trtri_hybrid_large(K, cplx, diag):
+    """Orders above the one-launch size (4096) run the hybrid recursion (top
+    trmm levels, sub-blocks <= 4096 on the tile trsm); checked against torch's
+    FP64 triangular solve with the identity."""
+    n = 4500
+    g = torch.Generator(device="cuda").manual_seed(7)
+    dt = torch.complex128 if cplx else torch.float64
+    a = torch.randn(n, n, dtype=dt, device="cuda", generator=g)
+    # unit diagonal: small off-diagonal entries keep L^-1 bounded (with N(0,1)
+    # entries a unit triangle's inverse grows exponentially and overflows)
+    scale = 1.0 / (2 * n) if diag == "U" else 1.0
+    a = torch.triu(a) + scale * torch.tril(a, -1) + 2 * n * torch.eye(n, dtype=dt, device="cuda")
+    want_l = torch.tril(a)
+    if diag == "U":
+        want_l = want_l - torch.diag(torch.diagonal(want_l)) + torch.eye(n, dtype=dt, device="cuda")
+    want = torch.linalg.solve_triangular(want_l, torch.eye(n, dtype=dt, device="cuda"), upper=False)
+    got = a.clone()
+    assert K.trtri_ref("L", diag, got) == 0
+    low = torch.tril(torch.ones(n, n, dtype=torch.bool, device="cuda"), -1 if diag == "U" else 0)
+    err = (got - want)[low].abs().max() / want[low].abs().max()
+    assert float(err) <= TOL
+    if diag == "U":  # the stored diagonal is never referenced nor written
+        assert torch.equal(torch.diagonal(got), torch.diagonal(a))
+    assert torch.equal(torch.triu(got, 1), torch.triu(a, 1))
