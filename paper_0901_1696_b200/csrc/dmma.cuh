@@ -110,6 +110,7 @@ struct TileLoader {
     }
   }
   __device__ __forceinline__ void advance() { ptr += kstep; }
+  __device__ __forceinline__ void skip(int stages) { ptr += (i64)stages * kstep; }
 
   __device__ __forceinline__ static void cp_async_t(T* s, const T* g, bool ok) {
     if constexpr (sizeof(T) == 8) cp_async8(s, g, ok);

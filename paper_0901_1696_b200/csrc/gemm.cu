@@ -67,6 +67,17 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs<T>& g, int tm, int tn, 
   la.init(g.A, g.lda, m0, M, tid);
   lb.init(g.B, g.ldb, n0, N, tid);
   const bool masked = g.a_tri != A_FULL || g.b_tri != A_FULL;
+  // a triangular operand is zero outside a band of K for this tile: lower
+  // (k <= row) ends the K loop at the tile's last row, upper (k >= row)
+  // starts it at the tile's first -- half the flops of a masked trmm GEMM
+  int kbeg = 0, kend = g.K;
+  if (g.a_tri == A_LOWER || g.a_tri == A_SLOWER) kend = min(kend, m0 + BM);
+  if (g.a_tri == A_UPPER || g.a_tri == A_SUPPER) kbeg = max(kbeg, m0);
+  if (g.b_tri == A_LOWER || g.b_tri == A_SLOWER) kend = min(kend, n0 + BN);
+  if (g.b_tri == A_UPPER || g.b_tri == A_SUPPER) kbeg = max(kbeg, n0);
+  const int kt0 = kbeg / BK;
+  la.skip(kt0);
+  lb.skip(kt0);
 
   double acc[NACC][MI][NI][4];
 #pragma unroll
@@ -78,11 +89,11 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs<T>& g, int tm, int tn, 
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[c][i][j][r] = 0.0;
 
-  const int KT = (K + BK - 1) / BK;
-  auto load_stage = [&](int stage, int kt) {
+  const int KT = kend > kbeg ? (kend + BK - 1) / BK - kt0 : 0;  // stages of this tile
+  auto load_stage = [&](int stage, int kt) {  // kt counts from kt0
     T* as = As + stage * LA::SIZE;
     T* bs = Bs + stage * LB::SIZE;
-    const int k0 = kt * BK;
+    const int k0 = (kt + kt0) * BK;
     if (!masked && k0 + BK <= K) {  // uniform
       la.load(as);
       lb.load(bs);
