@@ -258,9 +258,12 @@ template <typename T>
 __global__ void tri_copy_kernel(View<T> src, View<T> dst, int mode, const int* skip) {
   if (skip && *skip) return;
   const i64 total = dst.m * dst.n;
+  // the fast index runs along dst's contiguous dimension (the workspaces
+  // take the orientation of the view they shadow, so src matches it too)
+  const bool ifast = dst.rs == 1;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
-    const i64 i = e % dst.m, j = e / dst.m;
+    const i64 i = ifast ? e % dst.m : e / dst.n, j = ifast ? e / dst.m : e % dst.n;
     switch (mode) {
       case CP_ALL: *dst.at(i, j) = *src.at(i, j); break;
       case CP_LOWER0: *dst.at(i, j) = i >= j ? *src.at(i, j) : sc_from<T>(0.0); break;
@@ -281,14 +284,17 @@ template <typename T> int tri_copy(Ctx c, View<T> src, View<T> dst, int mode) {
   return 0;
 }
 
-// column-major m x n workspace view
-template <typename T> int ws_matrix(Ctx c, i64 m, i64 n, View<T>& v) {
+// m x n workspace view, column-major or (rowmajor) row-major -- callers take
+// the orientation of the view the workspace shadows, so copies are coalesced
+// on both sides (the RFP blocks of TRANSR='T'/'C' are row-major)
+template <typename T> int ws_matrix(Ctx c, i64 m, i64 n, View<T>& v, bool rowmajor = false) {
   T* p = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&p, (size_t)(m > 0 ? m : 1) * (n > 0 ? n : 1) * sizeof(T),
                                   c.st);
-  v = View<T>{p, m, n, 1, m};
+  v = rowmajor ? View<T>{p, m, n, n, 1} : View<T>{p, m, n, 1, m};
   return e == cudaSuccess ? 0 : (int)e;
 }
+template <typename T> bool is_rowmajor(const View<T>& v) { return v.rs != 1 && v.cs == 1; }
 
 inline i64 oop_max() {
   static const i64 v = [] {
@@ -551,7 +557,7 @@ int trmm_rec(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<
 template <typename T>
 int trmm_oop(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View<T> B) {
   View<T> Bc;
-  int rc = ws_matrix(c, B.m, B.n, Bc);
+  int rc = ws_matrix(c, B.m, B.n, Bc, is_rowmajor(B));
   if (!rc) rc = tri_copy(c, B, Bc, CP_ALL);
   const int mask = lower ? (unit ? A_SLOWER : A_LOWER) : (unit ? A_SUPPER : A_UPPER);
   if (!rc)
@@ -662,7 +668,7 @@ template <typename T> int trtri_oop(Ctx c, bool unit, View<T> A) {
   View<T> X{nullptr, 0, 0, 1, 1};
   int rc = ws_alloc(&W, n, c.st);
   if (!rc) rc = leaf_inverses(c, A, unit, W);
-  if (!rc) rc = ws_matrix(c, n, n, X);
+  if (!rc) rc = ws_matrix(c, n, n, X, is_rowmajor(A));
   if (!rc) rc = tri_copy(c, X, X, CP_EYE);
   if (!rc) rc = trsm_tiles(c, true, false, A, X, (const T*)W, false);
   // (unit diagonal: the stored diagonal is never referenced nor written)
@@ -706,7 +712,7 @@ template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
 // A <- L^H L (lower triangle) as ONE herk launch from a zero-padded copy of L
 template <typename T> int lauum_oop(Ctx c, View<T> A) {
   View<T> Lw;
-  int rc = ws_matrix(c, A.m, A.m, Lw);
+  int rc = ws_matrix(c, A.m, A.m, Lw, is_rowmajor(A));
   if (!rc) rc = tri_copy(c, A, Lw, CP_LOWER0);
   // L^H L = G G^H with G = conj(L^T)
   if (!rc) rc = herk_core(c, TRI_LOWER, 1.0, Lw.t(), is_cplx<T>::value, 0.0, A, true);
