@@ -740,7 +740,7 @@ int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, 
 // Warp layout of a 64 x TN trsm tile: TN = 64 -> 2 x 2 warps of 32 x 32,
 // TN = 16 (narrow right-hand sides) -> 4 x 1 warps of 16 x 16.
 template <int TN> struct TrsmTile {
-  static constexpr int WN = TN == 64 ? 2 : 1;   // warps along N
+  static constexpr int WN = TN >= 64 ? 2 : 1;   // warps along N
   static constexpr int WMW = 4 / WN;            // warps along M
   static constexpr int RW = TP / WMW;           // rows per warp
   static constexpr int CW = TN / WN;            // columns per warp
@@ -828,7 +828,8 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
   constexpr bool PREW = trsm_prew<T, BKM>();
   constexpr int PIPE = STAGES * (LA::SIZE + LB::SIZE);
-  T* const Wpre = sm + (PIPE > TP * LD64 ? PIPE : TP * LD64);  // PREW only
+  constexpr int STILE = (TN > TP ? TN : TP) * LD64;  // the S tile (64 x TN, LD64 columns)
+  T* const Wpre = sm + (PIPE > STILE ? PIPE : STILE);  // PREW only
   if constexpr (PREW) {
     // W'_i does not depend on any task: fetch it now (oldest cp.async group,
     // complete before the first pipeline wait returns)
@@ -948,12 +949,17 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
 
   if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
     // (the gate's flags cover 64-column chunks; c counts TN-wide blocks)
-    if (tid == 0) spin_wait_acquire(a.ext + (a.ext_mode ? c * TN / TP : i));
+    // (a TN-wide block may span several chunks: wait for its last one; the
+    // copy stream publishes the chunks in order)
+    if (tid == 0) {
+      const int last = (c * TN + TN - 1 < a.nrhs - 1 ? c * TN + TN - 1 : a.nrhs - 1) / TP;
+      spin_wait_acquire(a.ext + (a.ext_mode ? last : i));
+    }
     __syncthreads();
   }
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
   T* S = sm;
-  T* Ws = PREW ? Wpre : S + TP * LD64;
+  T* Ws = PREW ? Wpre : S + STILE;
   const i64 i0 = (i64)i * TP, c0 = (i64)c * TN;
   const int mrows = a.n - (int)i0 < TP ? a.n - (int)i0 : TP;
   const int ncols = a.nrhs - (int)c0 < TN ? a.nrhs - (int)c0 : TN;
@@ -1016,7 +1022,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
 // row-major-B variants: 175 registers would round to two CTAs per SM; capped
 // at 168 they fit three (the column-major-B ones need ~250 and run two)
 template <typename T, bool AK, bool BKM, int TN>
-__global__ void __launch_bounds__(TPT, TN < TP ? 3 : ((BKM || is_cplx<T>::value) ? 1 : 3))
+__global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_cplx<T>::value) ? 1 : 3)))
     tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
                                                         TrsmArgs a, int* sync, const int* info,
                                                         unsigned long long* trace) {
@@ -1044,11 +1050,9 @@ template <typename T, bool AK, bool BKM, int TN> size_t trsm_smem_bytes() {
   using C = TileCfg<T>;
   const size_t pipe = (size_t)STAGES * (SmemLayout<T, TP, C::BK, AK>::SIZE +
                                         SmemLayout<T, TN, C::BK, BKM>::SIZE);
-  if (trsm_prew<T, BKM>()) {
-    const size_t one = (size_t)TP * LD64;
-    return ((pipe > one ? pipe : one) + one) * sizeof(T);
-  }
-  const size_t tiles = (size_t)2 * TP * LD64;
+  const size_t stile = (size_t)(TN > TP ? TN : TP) * LD64, one = (size_t)TP * LD64;
+  if (trsm_prew<T, BKM>()) return ((pipe > stile ? pipe : stile) + one) * sizeof(T);
+  const size_t tiles = stile + one;  // S and W'_i
   return (pipe > tiles ? pipe : tiles) * sizeof(T);
 }
 
@@ -1115,6 +1119,9 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
     const char* v = std::getenv("RFPK_TRSM_NARROW");
     return v ? std::atoi(v) : 256;
   }();
+  // (a 64 x 128 tile with 2 x 2 warps of 32 x 64 measured slower on the S1
+  // solve of config 3: 255 registers with spills, two CTAs per SM, 18.4 vs
+  // 17.7 ms)
   const long long tasks64 = (long long)a.nb * ((B.n + TP - 1) / TP);
   const int tn = (!is_cplx<T>::value &&
                   (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;

@@ -17,8 +17,15 @@ t1 = buf.data_ptr() + 8 * d.shift           # rect[shift:, 0:n1]
 s1 = buf.data_ptr() + 8 * (d.n1 + d.shift)  # rect[n1+shift:, 0:n1]
 info = torch.zeros(1, dtype=torch.int32, device=dev)
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-for _ in range(reps):
+def call():
     rc = lib.rfpk_dtrsm(b"R", b"L", b"C", b"N", 1.0, t1, d.n1, 1, ld, s1, d.n2, d.n1, 1, ld,
                         info.data_ptr(), st)
     assert rc == 0, rc
-torch.cuda.synchronize(); print("ok", int(info.item()))
+call()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize(); e0.record()
+for _ in range(reps):
+    call()
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / reps
+print("ok", int(info.item()), "trsm %.3f ms  %.2f TFLOP/s" % (ms, d.n1 * d.n1 * d.n2 / ms / 1e9))
