@@ -256,13 +256,26 @@ int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* s
   i64 t0, t1, s0, s1;
   rfp_row_regions<T>(d, t0, t1, s0, s1);
   const i64 nch = (d.n1 + 63) / 64;
-  for (int region = 0; region < 2; ++region) {
-    const i64 r0 = region ? s0 : t0, r1 = region ? s1 : t1;
-    int* flags = region ? sflags : cflags;
+  // first rectangle row of T1 in column c: T1 = rect[d:, :] lower ('L') or
+  // rect[n2+1:, :n2] lower ('U'); the T rows above it belong to T2, which is
+  // first read by the SYRK after the whole transfer -- so T1's rows go first
+  // (half the T region: potrf(T1) no longer waits for T2's), then S1's, then
+  // T2's remainder, each chunk of the first two followed by its flag
+  auto t1first = [&](i64 c) {
+    i64 r = d.lower ? c + d.d : (c < d.n2 ? d.n2 + 1 + c : t1);
+    return r < t0 ? t0 : (r > t1 ? t1 : r);
+  };
+  for (int pass = 0; pass < 3; ++pass) {
     for (i64 j = 0; j < nch; ++j) {
       const i64 c0 = j * 64, c1 = c0 + 64 < d.n1 ? c0 + 64 : d.n1;
-      cudaError_t e = copy_block(d, host, dev, r0, r1, c0, c1, copy);
-      if (e == cudaSuccess)
+      i64 r0, r1;
+      int* flags = nullptr;
+      if (pass == 0) { r0 = t1first(c0); r1 = t1; flags = cflags; }
+      else if (pass == 1) { r0 = s0; r1 = s1; flags = sflags; }
+      else { r0 = t0; r1 = t1first(c0); }
+      cudaError_t e = cudaSuccess;
+      if (r1 > r0) e = copy_block(d, host, dev, r0, r1, c0, c1, copy);
+      if (e == cudaSuccess && flags)
         e = cudaMemcpyAsync(flags + j, one, sizeof(int), cudaMemcpyHostToDevice, copy);
       if (e != cudaSuccess) return (int)e;
     }
