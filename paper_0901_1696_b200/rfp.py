@@ -35,6 +35,7 @@ __all__ = [
     "pftrf_batched",
     "pftrs_batched",
     "pftrf_pftrs_batched",
+    "pftrf_pftrs_batched_from_host",
 ]
 
 
@@ -464,3 +465,58 @@ def pftrf_pftrs_batched(arf: torch.Tensor, b: torch.Tensor, n: int, uplo: str = 
     if work is not bv:
         bv.copy_(work)
     return info
+
+
+def pftrf_pftrs_batched_from_host(host_arf: torch.Tensor, host_b: torch.Tensor, n: int,
+                                  uplo: str = "U", transr: str = "N", out=None,
+                                  chunk: int = 4096):
+    """:func:`pftrf_pftrs_batched` for a batch that sits in (pinned) host
+    memory, pipelined in chunks of ``chunk`` matrices over three streams: the
+    host->device copy of chunk k+1 and the device->host copy of chunk k-1's
+    solutions overlap the fused kernel on chunk k (PCIe is full duplex), so
+    the call approaches the pure transfer time.  ``host_arf``: (batch, nt)
+    float64; ``host_b``: (batch, n) or (batch, n, nrhs) float64 with unit
+    stride along n.  Solutions go to ``out`` (default ``host_b``).  Returns
+    ``(arf on the device holding the factors, info)``; info is an int32 CUDA
+    tensor, valid once the current stream reaches it (no host sync here)."""
+    desc = make_descriptor(n, uplo, transr)
+    if not isinstance(host_arf, torch.Tensor) or host_arf.is_cuda or host_arf.dtype != torch.float64:
+        raise ValueError("host_arf must be a float64 CPU tensor of shape (batch, nt)")
+    if host_arf.dim() != 2 or host_arf.shape[1] != desc.nt or host_arf.stride(1) != 1:
+        raise ValueError(f"host_arf must be (batch, {desc.nt}) with unit inner stride")
+    batch = host_arf.shape[0]
+    if not isinstance(host_b, torch.Tensor) or host_b.is_cuda or host_b.dtype != torch.float64:
+        raise ValueError("host_b must be a float64 CPU tensor")
+    hb = host_b.unsqueeze(-1) if host_b.dim() == 2 else host_b
+    if hb.dim() != 3 or hb.shape[0] != batch or hb.shape[1] != n or (n > 1 and hb.stride(1) != 1):
+        raise ValueError(f"host_b must be (batch, {n}[, nrhs]) with unit stride along n")
+    ho = hb if out is None else (out.unsqueeze(-1) if out.dim() == 2 else out)
+    if ho.shape != hb.shape or ho.stride() != hb.stride():
+        raise ValueError("out must match host_b's shape and strides")
+    if chunk < 1:
+        raise ValueError("chunk must be positive")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    d_arf = torch.empty((batch, desc.nt), dtype=torch.float64, device=dev)
+    d_b = torch.empty_strided(hb.shape, hb.stride(), dtype=torch.float64, device=dev)
+    infos = []
+    s_in.wait_stream(main)
+    s_out.wait_stream(main)
+    for k0 in range(0, batch, chunk):
+        k1 = min(batch, k0 + chunk)
+        with torch.cuda.stream(s_in):
+            d_arf[k0:k1].copy_(host_arf[k0:k1], non_blocking=True)
+            d_b[k0:k1].copy_(hb[k0:k1], non_blocking=True)
+        main.wait_stream(s_in)
+        with torch.cuda.stream(main):
+            infos.append(pftrf_pftrs_batched(d_arf[k0:k1], d_b[k0:k1], n, uplo, transr))
+        s_out.wait_stream(main)
+        with torch.cuda.stream(s_out):
+            ho[k0:k1].copy_(d_b[k0:k1], non_blocking=True)
+    main.wait_stream(s_out)
+    for t in (d_arf, d_b):
+        t.record_stream(s_in)
+        t.record_stream(s_out)
+    info = torch.cat(infos) if infos else torch.empty(0, dtype=torch.int32, device=dev)
+    return d_arf, info

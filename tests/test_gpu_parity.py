@@ -626,3 +626,30 @@ def test_pfsv_from_host_overlapped(P, uplo, transr, n):
         bn = np.array(b[:, 0])
         rfp.pfsv_from_host(buf.copy(), bn, n, uplo, transr)
         assert rel(bn, xd[:, 0].cpu()) <= 1e-12
+
+
+@pytest.mark.parametrize("nrhs", [0, 3, 8])
+def test_batched_from_host_pipelined(P, nrhs):
+    """The chunked host pipeline gives bit-for-bit the device-resident fused
+    kernel's factors, solutions and info (ragged last chunk; nrhs 0 = a 2-D
+    (batch, n) right-hand side)."""
+    rfp = P.rfp
+    n, batch = 64, 37
+    bufs = [O.trttf(O.spd_matrix(n, 500 + k, "n"), "U", "N") for k in range(batch)]
+    host_arf = torch.from_numpy(np.stack(bufs)).pin_memory()
+    g = np.random.default_rng(9)
+    if nrhs:
+        base = torch.from_numpy(g.standard_normal((batch, nrhs, n))).pin_memory()
+        host_b = base.transpose(1, 2)                      # (batch, n, nrhs), unit stride along n
+        out = torch.empty_like(base).pin_memory().transpose(1, 2)
+    else:
+        host_b = torch.from_numpy(g.standard_normal((batch, n))).pin_memory()
+        out = torch.empty_like(host_b).pin_memory()
+    d_arf, info = rfp.pftrf_pftrs_batched_from_host(host_arf, host_b, n, "U", "N", out=out, chunk=10)
+    torch.cuda.synchronize()
+    ref_arf = host_arf.cuda()
+    ref_b = host_b.cuda()
+    ref_info = rfp.pftrf_pftrs_batched(ref_arf, ref_b, n, "U", "N")
+    assert torch.equal(info, ref_info) and int(info.abs().sum()) == 0
+    assert torch.equal(d_arf, ref_arf)
+    assert torch.equal(out, ref_b.cpu())
