@@ -880,6 +880,30 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     lb.advance();
   };
 
+  // narrow tiles: B(i, c) does not depend on the chain -- read it into
+  // registers now so the S build after the last chunk waits on nothing but
+  // the accumulation (not under the host-streaming gate, which must be
+  // waited first)
+  constexpr bool BPRE = TN < TP;
+  T bpre[BPRE ? MI : 1][BPRE ? NI : 1][4];
+  const bool bpre_ok = BPRE && !a.ext;
+  if constexpr (BPRE) {
+    if (bpre_ok) {
+      const i64 i0p = (i64)i * TP, c0p = (i64)c * TN;
+      const int mr = a.n - (int)i0p < TP ? a.n - (int)i0p : TP;
+      const int nc = a.nrhs - (int)c0p < TN ? a.nrhs - (int)c0p : TN;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+            const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+            bpre[mi][ni][r] = (row < mr && col < nc) ? *B.at(i0p + row, c0p + col) : zero_<T>();
+          }
+    }
+  }
   const int KT = nprev * SPC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -971,8 +995,11 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
       for (int r = 0; r < 4; ++r) {
         const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
         const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+        T bv;
+        if constexpr (BPRE) bv = bpre_ok ? bpre[mi][ni][r] : zero_<T>();
+        if (!bpre_ok) bv = (row < mrows && col < ncols) ? *B.at(i0 + row, c0 + col) : zero_<T>();
         S[row + col * LD64] = (row < mrows && col < ncols)
-                                  ? *B.at(i0 + row, c0 + col) - fragn<T>(acc[0], acc[NACC - 1], mi, ni, r)
+                                  ? bv - fragn<T>(acc[0], acc[NACC - 1], mi, ni, r)
                                   : zero_<T>();
       }
   const T* w = W + (i64)i * TP * TP;
