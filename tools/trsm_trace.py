@@ -38,3 +38,19 @@ for hdr, rows in blocks:
     edges = np.linspace(t00, tend, 11)
     print("   " + " ".join("%3.0f" % (100.0 * sum(max(0, min(x[6], e1) - max(x[3], e0)) for x in rows) / ((e1 - e0) * ctas))
                           for e0, e1 in zip(edges[:-1], edges[1:])))
+
+# chain breakdown per column block c: previous step published -> this task's
+# accumulation done (flag detection + last chunk + its GEMM) -> published
+for hdr, rows in blocks[:1]:
+    by = {(x[0], x[1]): x for x in rows}
+    nb = 1 + max(x[0] for x in rows)
+    steps = []
+    for (i, c), x in by.items():
+        p = by.get((i - 1, c))
+        if p is None:
+            continue
+        steps.append(((x[4] - p[6]) / 1e3, (x[6] - x[4]) / 1e3, (x[6] - p[6]) / 1e3))
+    if steps:
+        a = np.array(steps)
+        print("chain step (us): prev publish -> acc done %.2f | acc done -> publish %.2f | step %.2f"
+              % tuple(a.mean(0)))
