@@ -149,6 +149,21 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
   const i64 k = blockIdx.x;
   double* g = arf + k * stride_arf;
   load_rect<TRANS>(R, g);
+  // the first 8-column chunk of the right-hand side goes into its B-operand
+  // registers now: the load latency then hides under the factorization
+  // instead of sitting between the inverses and the solve (column g8, rows
+  // 4s + t4 of b1 / b2)
+  double x1p[8], x2p[8];
+  if (SOLVE) {
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int cw = nrhs < 8 ? nrhs : 8;
+    const double* bc = b + k * stride_b + (i64)g8 * ldb;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      x1p[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
+      x2p[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
+    }
+  }
   // T1 / T2 / S1 of the normal 65 x 32 rectangle (convert.py:142-153, d = 1):
   // V1 = T1 (L1, lower), V2 = T2^T (L2, lower), S = S1 ('L') | S1^T ('U')
   constexpr int r1 = LOWER ? 1 : 33, r2 = LOWER ? 0 : 32, rs = LOWER ? 33 : 0;
@@ -193,11 +208,19 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
     // b1 / b2 straight into the B-operand registers (column g8, rows 4s+t4)
     double x1[8], x2[8], c[2][4];
-    const double* bc = bk + (i64)(c0 + g8) * ldb;
+    if (c0 == 0) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      x1[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
-      x2[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
+      for (int s = 0; s < 8; ++s) {
+        x1[s] = x1p[s];
+        x2[s] = x2p[s];
+      }
+    } else {
+      const double* bc = bk + (i64)(c0 + g8) * ldb;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        x1[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
+        x2[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
+      }
     }
     zero_c(c);
     mm32r<1>(o, W1, x1, c);                      // b1 = W1 b1
