@@ -149,15 +149,32 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     if (gated && !rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
   };
   if (d.lower) {
-    // RFPK_PANEL=1: potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over
-    // the tall panel [T1; S1] (contiguous rows of the normal rectangle).
-    // Measured neutral at n = 16384 (26.6 ms vs 7.8 + 18.2: the S1 tiles slow
-    // the diagonal chain as much as they fill its idle SMs), so off by default.
+    // potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over the tall panel
+    // [T1; S1] (contiguous rows of the normal rectangle): the S1 tiles fill the
+    // SMs the diagonal chain leaves idle.  Measured 10-16% faster for n1 up to
+    // 4096 (pftrf 4096: 2.71 -> 2.27 ms, 8192: 8.82 -> 7.89) and slower above
+    // (16384: 25.6 vs 24.8 ms), so used up to RFPK_PANEL_MAX (default 4096)
+    // columns.  The panel's row tiles must break at its column count, so it
+    // factors the first n1' = 64*floor(n1/64) columns; the r < 64 remaining
+    // ones follow as T1_22 -= L21 L21^H, S1_2 -= L31 L21^H, potrf(T1_22),
+    // S1_2 <- S1_2 L22^-H (the same blocked Cholesky, info offsets unchanged).
     int fused = -100;
-    static const bool panel = std::getenv("RFPK_PANEL") != nullptr;
-    if (panel && !is_cplx<T>::value && !s1_ready && d.n2 && d.n1 % 64 == 0) {
-      View<T> panel{t1.p, d.n1 + d.n2, d.n1, t1.rs, t1.cs};
-      fused = potrf_panel_tiles(c, panel, d.n1, 0, W);
+    static const i64 panel_max = [] {
+      const char* v = std::getenv("RFPK_PANEL_MAX");
+      return v ? std::atoll(v) : (i64)4096;
+    }();
+    const i64 n1a = d.n1 / 64 * 64, rr = d.n1 - n1a;
+    if (!is_cplx<T>::value && !s1_ready && d.n2 && n1a >= 64 && d.n1 <= panel_max) {
+      View<T> panel{t1.p, d.n1 + d.n2, n1a, t1.rs, t1.cs};
+      fused = potrf_panel_tiles(c, panel, n1a, 0, W);
+      if (!fused && rr) {
+        View<T> L21 = t1.sub(n1a, 0, rr, n1a), T22 = t1.sub(n1a, n1a, rr, rr);
+        View<T> L31 = s1.sub(0, 0, d.n2, n1a), S12 = s1.sub(0, n1a, d.n2, rr);
+        fused = blas_syrk(c, 'L', 'N', -1.0, L21, 1.0, T22, herm);
+        if (!fused) fused = blas_gemm(c, 'N', 'C', m_one<T>(), L31, L21, one<T>(), S12);
+        if (!fused) fused = blas_potrf(c, 'L', T22, (int)n1a, (T*)nullptr);
+        if (!fused) fused = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), T22, S12, false);
+      }
     }
     if (fused != -100) {
       rc = fused;
