@@ -62,6 +62,11 @@ template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T
 // 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
 template <typename T>
 int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans);
+// one pftrs sweep through both RFP triangles in one launch (real):
+// op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0; lower = forward sweep, else
+// both triangles upper (W transposed); -100 = not supported (fall back)
+int trsm2_tiles(Ctx c, bool lower, View<double> Ta, View<double> B0, const double* Wa,
+                View<double> Tb, View<double> B1, const double* Wb, View<double> P);
 // stream-ordered workspace for leaf inverses of an order-n triangle
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
 template <typename T> void ws_free(T* p, cudaStream_t st);

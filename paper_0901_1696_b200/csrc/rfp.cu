@@ -124,6 +124,73 @@ struct PhaseTrace {
     if (rc_) return rc_;    \
   } while (0)
 
+// dst(i, j) = src(i, j) on the lower triangle (i >= j) of two n x n views of
+// OPPOSITE orientations: 32 x 32 tiles through shared memory, so the reads
+// run along src's contiguous dimension and the writes along dst's
+template <typename T>
+__global__ void tri_transpose_copy_kernel(View<T> src, View<T> dst, i64 n) {
+  __shared__ T tile[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const i64 i0 = (i64)bi * 32, j0 = (i64)bj * 32;
+  const bool sj = src.cs == 1;  // src contiguous along j
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const i64 i = sj ? i0 + r : i0 + tx, j = sj ? j0 + tx : j0 + r;
+    if (i < n && j <= i) {
+      if (sj) tile[r][tx] = *src.at(i, j);
+      else tile[tx][r] = *src.at(i, j);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const i64 i = sj ? i0 + tx : i0 + r, j = sj ? j0 + r : j0 + tx;
+    if (i < n && j <= i) *dst.at(i, j) = sj ? tile[tx][r] : tile[r][tx];
+  }
+}
+
+template <typename T> static int tri_transpose_copy(Ctx c, View<T> src, View<T> dst) {
+  const i64 nt = (src.m + 31) / 32;
+  if (nt == 0) return 0;
+  tri_transpose_copy_kernel<T><<<dim3((unsigned)nt, (unsigned)nt), dim3(32, 8), 0, c.st>>>(
+      src, dst, src.m);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
+// potrf('U', T2) (rfp.py:89 / :84).  The lower view the Cholesky factors is
+// T2^T; for TRANSR='N' that view is row-major with the RFP's odd leading
+// dimension, where every 16-wide K slice of a row straddles an extra sector
+// and the tile potrf runs a two-stage pipeline (potrf(T2) 8.1 ms against
+// potrf(T1)'s 7.0 at n = 16384).  Large blocks are therefore factored in a
+// column-major copy: two coalesced O(n^2) transposing copies buy the
+// column-major tile potrf (pftrf n = 16384: 'L','N' bench step 69.5 -> 68.8
+// ms; 'L','T' 49.2 -> 48.7 ms; 'U','N' 50.4 -> 49.5 ms).  Same kernels, same
+// pivots, same info offsets.
+// potrf(T1) of the TRANSR='T' / 'C' layouts has the same row-major lower
+// view and takes the same route when its input is not streamed in.
+template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int base, T* W) {
+  const View<T> v = uplo == 'L' ? blk : blk.t();
+  const char* env = std::getenv("RFPK_T2_COPY_MIN");
+  const i64 min_n = env ? (i64)std::atoll(env) : (i64)2048;
+  // (real only: for complex128 the row-major tile potrf measured as fast or
+  // faster -- config 5's pftrf 606 ms direct vs 663 ms through the copy)
+  if (is_cplx<T>::value || v.rs == 1 || v.cs != 1 || v.m < min_n)
+    return blas_potrf(c, uplo, blk, base, W);
+  const i64 n = v.m, ld = (n + 15) / 16 * 16 + 8;  // 64-byte aligned columns, ld off a power of 2
+  T* p = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&p, (size_t)ld * n * sizeof(T), c.st);
+  if (e != cudaSuccess) return (int)e;
+  View<T> x{p, n, n, 1, ld};
+  int rc = tri_transpose_copy(c, v, x);
+  if (!rc) rc = blas_potrf(c, 'L', x, base, W);
+  if (!rc) rc = tri_transpose_copy(c, x, v);
+  cudaFreeAsync(p, c.st);
+  return rc;
+}
+
 // SRPA factorization (rfp.py:55-91)
 template <typename T>
 int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cflags,
@@ -182,7 +249,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     } else {
       {
         InputGate g(cflags, 0);
-        rc = blas_potrf(c, 'L', t1, 0, W);
+        rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
       }
       tr.mark("potrf(T1)");
       before_s1();
@@ -196,14 +263,14 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     if (!rc && d.n2) {
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
       tr.mark("syrk(T2)");
-      if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n1, W);
+      if (!rc) rc = potrf_block(c, 'U', t2, (int)d.n1, W);
       tr.mark("potrf(T2)");
     }
   } else {
     if (d.n2) {
       {
         InputGate g(cflags, 0);
-        rc = blas_potrf(c, 'L', t1, 0, W);
+        rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
       }
       tr.mark("potrf(T1)");
       before_s1();
@@ -216,7 +283,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
       tr.mark("syrk(T2)");
     }
-    if (!rc) rc = blas_potrf(c, 'U', t2, (int)d.n2, W);
+    if (!rc) rc = potrf_block(c, 'U', t2, (int)d.n2, W);
     tr.mark("potrf(T2)");
   }
   // (the transfers must also be complete on every early-exit path)
@@ -324,8 +391,42 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
     TRY(ws_alloc(&W2, t2.m, c.st));
     TRY(blas_leaf_inverses(c, t2.t(), W2));
   }
+  // real data: each sweep through both triangles is ONE dataflow launch
+  // (trsm, the S1 gemm and the other triangle's trsm fused, trsm2_tiles);
+  // the back sweep stays split when the caller streams B2 out early
+  auto sweep2 = [&](bool fwd, View<T> ta, View<T> b0, const T* wa, View<T> tb, View<T> bb,
+                    const T* wb, View<T> p) -> int {
+    if constexpr (std::is_same<T, double>::value) {
+      static const i64 mn = [] {
+        const char* v = std::getenv("RFPK_TRSM2_MIN");
+        return v ? (i64)std::atoll(v) : (i64)128;
+      }();
+      if (n2 == 0 || n1 < mn || n2 < mn || (!fwd && b2_final)) return -100;
+      return trsm2_tiles(c, fwd, ta, b0, wa, tb, bb, wb, p);
+    } else {
+      return -100;
+    }
+  };
+  int rc2;
   if (d.lower) {
     View<T> b1 = b.sub(0, 0, n1, r), b2 = b.sub(n1, 0, n2, r);
+    if ((rc2 = sweep2(true, t1, b1, W1, t2.t(), b2, W2, s1)) != -100) {
+      TRY(rc2);
+      tr.mark("fwd(T1,S1,T2)");
+      if ((rc2 = sweep2(false, t2, b2, W2, t1.t(), b1, W1, s1.t())) != -100) {
+        TRY(rc2);
+        tr.mark("bwd(T2,S1,T1)");
+        return 0;
+      }
+      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false, W2));
+      tr.mark("trsm3");
+      if (b2_final) cudaEventRecord(b2_final, c.st);
+      TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+      tr.mark("gemm2");
+      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false, W1));
+      tr.mark("trsm4");
+      return 0;
+    }
     TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false, W1));
     tr.mark("trsm1");
     if (n2) {
@@ -344,6 +445,15 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
     return 0;
   }
   View<T> b1 = b.sub(0, 0, n2, r), b2 = b.sub(n2, 0, n1, r);
+  if ((rc2 = sweep2(true, t1, b1, W1, t2.t(), b2, W2, s1.t())) != -100) {
+    TRY(rc2);
+    if ((rc2 = sweep2(false, t2, b2, W2, t1.t(), b1, W1, s1)) != -100) return rc2;
+    TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false, W2));
+    if (b2_final) cudaEventRecord(b2_final, c.st);
+    TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+    TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
+    return 0;
+  }
   if (n2) {
     TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false, W1));
     TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b1, one<T>(), b2));

@@ -1121,7 +1121,368 @@ int trsm_launch(View<T> Tm, View<T> B, const T* W, const TrsmArgs& a, int* sync,
   return 0;
 }
 
+// ------------------------------------------------------ two-region solve
+// One substitution sweep of pftrs (rfp.py:118-136) through BOTH triangles of
+// the RFP buffer in ONE dataflow launch (real data):
+//
+//   region 0:  op(Ta) X0 = B0                  (tasks as in tile_trsm_kernel)
+//   region 1:  op(Tb) X1 = B1 - P X0           (P = S1 or S1^T)
+//
+// A region-1 task's K loop first runs over P's 64-column chunks, chunk k
+// gated on region 0's done(k, c) -- the reference's GEMM between the two
+// solves, folded in as a prefix of the left-looking accumulation -- then over
+// its own triangle's chain.  The GEMM work thereby fills the chains' tails
+// and the three launches (trsm, gemm, trsm) become one.  T1, T2 and S1 come
+// in both orientations depending on TRANSR / UPLO and the sweep direction, so
+// the A operand's smem layout (K-major or M-major) is chosen per chunk and
+// recorded per pipeline stage; B is column- or row-major for the whole sweep.
+struct Trsm2Region {
+  View<double> Tm, B;  // n x n triangle (lower, or upper solved bottom-up), n x nrhs
+  const double* W;     // its 64-leaf inverses (lower form; wtrans for upper)
+  int n, nb;
+  int* done;           // nb x nc flags
+};
+struct Trsm2Args {
+  Trsm2Region r[2];
+  View<double> P;  // r[1].n x r[0].n
+  int nrhs, nc, lower;
+};
+
+template <typename LA, typename LB, int TN>
+__device__ __forceinline__ void stage_mma(const double* as, const double* bs,
+                                          double (&acc)[TrsmTile<TN>::MI][TrsmTile<TN>::NI][4]) {
+  using WL = TrsmTile<TN>;
+#pragma unroll
+  for (int kk = 0; kk < TileCfg<double>::BK; kk += 4) {
+    double af[WL::MI][2], bf[WL::NI];
+#pragma unroll
+    for (int mi = 0; mi < WL::MI; ++mi) {
+      af[mi][0] = as[kk * LA::KS + (mi * 16) * LA::RS];
+      af[mi][1] = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
+    }
+#pragma unroll
+    for (int ni = 0; ni < WL::NI; ++ni) bf[ni] = bs[kk * LB::KS + (ni * 8) * LB::RS];
+#pragma unroll
+    for (int mi = 0; mi < WL::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < WL::NI; ++ni) dmma16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+  }
+}
+
+template <bool BKM, int TN, bool PREW> struct Trsm2Smem {
+  using C = TileCfg<double>;
+  using LK = SmemLayout<double, TP, C::BK, true>;
+  using LM = SmemLayout<double, TP, C::BK, false>;
+  using LB = SmemLayout<double, TN, C::BK, BKM>;
+  static constexpr int ASZ = LK::SIZE > LM::SIZE ? LK::SIZE : LM::SIZE;
+  static constexpr int PIPE = STAGES * (ASZ + LB::SIZE);
+  static constexpr int STILE = (TN > TP ? TN : TP) * LD64;
+  // W'_i: prefetched at the task start past the pipeline, or read after the
+  // accumulation into the slot behind the S tile
+  static constexpr int WOFF = PREW ? (PIPE > STILE ? PIPE : STILE) : STILE;
+  static constexpr int END = WOFF + TP * LD64;
+  static constexpr size_t BYTES = (size_t)(END > PIPE ? END : PIPE) * sizeof(double);
+};
+
+template <bool BKM, int TN, bool PREW>
+__device__ void trsm2_task(const Trsm2Args& a, int reg, int i, int c, double* sm, int& s_ready) {
+  using T = double;
+  using C = TileCfg<T>;
+  using SM = Trsm2Smem<BKM, TN, PREW>;
+  using LK = typename SM::LK;
+  using LM = typename SM::LM;
+  using LB = typename SM::LB;
+  using WL = TrsmTile<TN>;
+  constexpr int MI = WL::MI, NI = WL::NI, BK = C::BK, SPC = C::SPC;
+  const Trsm2Region& R = a.r[reg];
+  const Trsm2Region& R0 = a.r[0];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WL::WMW, wn = warp / WL::WMW, gq = lane >> 2, tq = lane & 3;
+  T* As = sm;
+  T* Bs = sm + STAGES * SM::ASZ;
+  T* const Wpre = sm + SM::WOFF;
+  if constexpr (PREW) {  // W'_i depends on no task: fetch it now (oldest cp.async group)
+    const T* w = R.W + (i64)i * TP * TP;
+    const bool wt = !a.lower;
+    for (int e = tid; e < TP * TP; e += TPT) {
+      const int r = e & 63, k = e >> 6;
+      cp_async8(wt ? Wpre + (k + r * LD64) : Wpre + (r + k * LD64), w + e, true);
+    }
+    cp_async_commit();
+  }
+  const int nprev = a.lower ? i : R.nb - 1 - i;
+  const int npre = reg ? R0.nb : 0;
+  const int KT = (npre + nprev) * SPC;
+
+  TileLoader<T, TP, BK, TPT, true> lk;
+  TileLoader<T, TP, BK, TPT, false> lm;
+  TileLoader<T, TN, BK, TPT, BKM> lb;
+  double acc[MI][NI][4];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[mi][ni][r] = 0.0;
+
+  int kvalid = TP;
+  bool akm = false;       // layout of the chunk being loaded
+  unsigned kmbits = 0;    // bit s: pipeline slot s holds a K-major A stage
+  const int nq = npre + nprev;
+  auto chunk_of = [&](int q) {
+    return q < npre ? (a.lower ? q : npre - 1 - q) : (a.lower ? q - npre : R.nb - 1 - (q - npre));
+  };
+  auto flag_of = [&](int q) { return (q < npre ? R0.done : R.done) + (i64)chunk_of(q) * a.nc + c; };
+  // chunks [0, ready) are known published: a chunk beyond waits for its flag,
+  // then warp 0 scans ahead 32 flags per round trip and one acquire fence
+  // covers every chunk found published (one barrier instead of one per chunk)
+  int ready = 0;
+  auto open_chunk = [&](int q) {
+    if (q >= ready) {
+      if (warp == 0) {
+        if (lane == 0) spin_wait_acquire(flag_of(q));  // the chain's critical wait: no fence
+        __syncwarp();
+        int rr = q + 1;
+        for (;;) {
+          const int qq = rr + lane;
+          const bool ok = qq < nq && ld_relaxed(flag_of(qq));
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (m == 0xffffffffu) { rr += 32; continue; }
+          rr += __ffs(~m) - 1;
+          break;
+        }
+        if (lane == 0) {
+          if (rr > q + 1) fence_acquire();
+          s_ready = rr;
+        }
+      }
+      __syncthreads();
+      ready = s_ready;
+    }
+    const bool pre = q < npre;
+    const int kk = chunk_of(q);
+    const View<T>& A = pre ? a.P : R.Tm;
+    const View<T>& Bv = pre ? R0.B : R.B;
+    akm = A.rs != 1;
+    if (akm) lk.init(A.p + (i64)kk * TP, A.rs, i * TP, R.n, tid);
+    else lm.init(A.p + (i64)kk * TP * A.cs, A.cs, i * TP, R.n, tid);
+    lb.init(Bv.p + (i64)kk * TP * Bv.rs, BKM ? Bv.cs : Bv.rs, c * TN, a.nrhs, tid);
+    const int kn = pre ? R0.n : R.n;
+    kvalid = kn - kk * TP < TP ? kn - kk * TP : TP;
+  };
+  auto load_stage = [&](int stage, int q) {
+    const int k0 = (q % SPC) * BK;
+    T* as = As + stage * SM::ASZ;
+    if (akm) {
+      if (kvalid == TP) lk.load(as);
+      else lk.load_pred(as, k0, kvalid, 0, A_FULL);
+      lk.advance();
+      kmbits |= 1u << stage;
+    } else {
+      if (kvalid == TP) lm.load(as);
+      else lm.load_pred(as, k0, kvalid, 0, A_FULL);
+      lm.advance();
+      kmbits &= ~(1u << stage);
+    }
+    if (kvalid == TP) lb.load(Bs + stage * LB::SIZE);
+    else lb.load_pred(Bs + stage * LB::SIZE, k0, kvalid, 0, A_FULL);
+    lb.advance();
+  };
+
+  constexpr bool BPRE = TN < TP;  // narrow tiles: B(i, c) into registers now
+  T bpre[BPRE ? MI : 1][BPRE ? NI : 1][4];
+  const i64 i0 = (i64)i * TP, c0 = (i64)c * TN;
+  const int mrows = R.n - (int)i0 < TP ? R.n - (int)i0 : TP;
+  const int ncols = a.nrhs - (int)c0 < TN ? a.nrhs - (int)c0 : TN;
+  if constexpr (BPRE) {
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+          bpre[mi][ni][r] = (row < mrows && col < ncols) ? *R.B.at(i0 + row, c0 + col) : 0.0;
+        }
+  }
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      if (s % SPC == 0) open_chunk(s / SPC);
+      load_stage(s, s);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int slot = kt % STAGES;
+    const bool km = (kmbits >> slot) & 1u;  // read before the refill below
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) {
+      if (nk % SPC == 0) open_chunk(nk / SPC);
+      load_stage(nk % STAGES, nk);
+    }
+    cp_async_commit();
+    const T* bs = Bs + slot * LB::SIZE + (wn * WL::CW + gq) * LB::RS + tq * LB::KS;
+    if (km) {
+      const T* as = As + slot * SM::ASZ + (wm * WL::RW + gq) * LK::RS + tq * LK::KS;
+      stage_mma<LK, LB, TN>(as, bs, acc);
+    } else {
+      const T* as = As + slot * SM::ASZ + (wm * WL::RW + gq) * LM::RS + tq * LM::KS;
+      stage_mma<LM, LB, TN>(as, bs, acc);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // S = B(i, c) - acc (zero outside the matrix), X = W'_i S
+  T* S = sm;
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+        const bool in = row < mrows && col < ncols;
+        T bv;
+        if constexpr (BPRE) bv = bpre[mi][ni][r];
+        else bv = in ? *R.B.at(i0 + row, c0 + col) : 0.0;
+        S[row + col * LD64] = in ? bv - acc[mi][ni][r] : 0.0;
+      }
+  if constexpr (!PREW) {
+    const T* w = R.W + (i64)i * TP * TP;
+    const bool wt = !a.lower;
+    for (int e = tid; e < TP * TP; e += TPT) {
+      const int r = e & 63, k = e >> 6;
+      Wpre[wt ? k + r * LD64 : r + k * LD64] = __ldcg(w + e);
+    }
+  }
+  __syncthreads();
+  double x[1][MI][NI][4];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) x[0][mi][ni][r] = 0.0;
+  smem_mm_ab<T, TN>(Wpre, S, x);
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+        if (row < mrows && col < ncols) *R.B.at(i0 + row, c0 + col) = x[0][mi][ni][r];
+      }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(R.done + (i64)i * a.nc + c, 1);
+  }
+}
+
+template <bool BKM, int TN, bool PREW>
+__global__ void __launch_bounds__(TPT, (PREW && TN == TP) ? 2 : 3)
+    tile_trsm2_kernel(Trsm2Args a, int* counter, const int* info) {
+  extern __shared__ __align__(16) double smem_d[];
+  __shared__ int s_task, s_ready;
+  if (info && *info) return;
+  const long long t0 = (long long)a.r[0].nb * a.nc;
+  const long long total = t0 + (long long)a.r[1].nb * a.nc;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long t = s_task;
+    __syncthreads();
+    if (t >= total) return;
+    const int reg = t >= t0;
+    const long long u = reg ? t - t0 : t;
+    const int step = (int)(u / a.nc), c = (int)(u % a.nc);
+    const int i = a.lower ? step : a.r[reg].nb - 1 - step;
+    trsm2_task<BKM, TN, PREW>(a, reg, i, c, smem_d, s_ready);
+  }
+}
+
+template <bool BKM, int TN, bool PREW> int trsm2_launch(Trsm2Args a, int* counter, Ctx c) {
+  auto kern = tile_trsm2_kernel<BKM, TN, PREW>;
+  const size_t smem = Trsm2Smem<BKM, TN, PREW>::BYTES;
+  static const int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
+    return nb > 0 ? nb : 1;
+  }();
+  const long long tasks = (long long)(a.r[0].nb + a.r[1].nb) * a.nc;
+  long long grid = (long long)per_sm * num_sms();
+  if (grid > tasks) grid = tasks;
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(a, counter, c.info);
+  RFPK_CHECK_LAUNCH();
+  return 0;
+}
+
 }  // namespace
+
+// One pftrs sweep through both RFP triangles (see tile_trsm2_kernel):
+// op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0, in place on B0 / B1, in ONE
+// launch.  lower: both triangles lower (forward sweep); else both upper,
+// solved bottom-up with their W taken transposed.  Returns -100 when the
+// operands do not fit the kernel (the caller then runs trsm, gemm, trsm).
+int trsm2_tiles(Ctx c, bool lower, View<double> Ta, View<double> B0, const double* Wa,
+                View<double> Tb, View<double> B1, const double* Wb, View<double> P) {
+  if (Ta.m == 0 || Tb.m == 0 || B0.n == 0) return -100;
+  // opt-in (RFPK_TRSM2=1): measured slower than trsm + gemm + trsm on the
+  // B200 (config 3's pftrs 22.8 vs 19.5 ms, n = 4000 0.78 vs 0.72 ms; see
+  // DESIGN.md section 9), kept parity-tested for the record
+  const char* on = std::getenv("RFPK_TRSM2");
+  if (!on || std::atoi(on) == 0 || InputGate::flags()) return -100;
+  auto unit_stride = [](const View<double>& v) { return v.rs == 1 || v.cs == 1; };
+  if (!unit_stride(Ta) || !unit_stride(Tb) || !unit_stride(P)) return -100;
+  // a degenerate (single-row / single-column) view: one fixed orientation
+  if ((Ta.rs == 1 && Ta.cs == 1) || (Tb.rs == 1 && Tb.cs == 1) || (P.rs == 1 && P.cs == 1))
+    return -100;
+  const bool bkm = B0.rs == 1 && B1.rs == 1;
+  if (!bkm && !(B0.cs == 1 && B1.cs == 1)) return -100;
+  if (B0.n != B1.n || P.m != Tb.m || P.n != Ta.m) return -100;
+  Trsm2Args a;
+  a.nrhs = (int)B0.n;
+  a.lower = lower ? 1 : 0;
+  a.P = P;
+  static const int narrow_max = [] {
+    const char* v = std::getenv("RFPK_TRSM_NARROW");
+    return v ? std::atoi(v) : 256;
+  }();
+  const int nb0 = (int)((Ta.m + TP - 1) / TP), nb1 = (int)((Tb.m + TP - 1) / TP);
+  const long long tasks64 = (long long)(nb0 + nb1) * ((B0.n + TP - 1) / TP);
+  const int tn = (B0.n <= narrow_max || tasks64 <= 10LL * num_sms()) ? 16 : TP;
+  a.nc = (int)((B0.n + tn - 1) / tn);
+  const size_t ints = SYNC_HDR + (size_t)(nb0 + nb1) * a.nc;
+  int* sync = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
+  if (e != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  a.r[0] = Trsm2Region{Ta, B0, Wa, (int)Ta.m, nb0, sync + SYNC_HDR};
+  a.r[1] = Trsm2Region{Tb, B1, Wb, (int)Tb.m, nb1, sync + SYNC_HDR + (size_t)nb0 * a.nc};
+  int rc;
+  // 64-wide tiles: W'_i prefetched at two CTAs per SM, or read late at three
+  static const bool prew = [] {
+    const char* v = std::getenv("RFPK_TRSM2_PREW");
+    return v && std::atoi(v) != 0;
+  }();
+  if (tn == 16) rc = bkm ? trsm2_launch<true, 16, true>(a, sync, c)
+                         : trsm2_launch<false, 16, true>(a, sync, c);
+  else if (prew) rc = bkm ? trsm2_launch<true, TP, true>(a, sync, c)
+                          : trsm2_launch<false, TP, true>(a, sync, c);
+  else rc = bkm ? trsm2_launch<true, TP, false>(a, sync, c)
+                : trsm2_launch<false, TP, false>(a, sync, c);
+  cudaFreeAsync(sync, c.st);
+  return rc;
+}
 
 // conj?(Tm) X = B in place with the dataflow kernel (W: lower-form 64-block
 // inverses; wtrans for Tm upper).  Returns -100 for unsupported strides.

@@ -688,3 +688,88 @@ def test_pftrf_panel_path(P, transr, bad):
         assert rel(r.data, f) <= TOL
     else:
         assert want == bad + 1
+
+
+def _pftrs_split_vs_fused(P, r, b, monkeypatch):
+    """pftrs with the two-region sweeps (opt-in RFPK_TRSM2=1) and with the
+    default split trsm / gemm / trsm sequence."""
+    monkeypatch.setenv("RFPK_TRSM2", "1")
+    x = b.clone()
+    P.rfp.pftrs(r, x)
+    monkeypatch.delenv("RFPK_TRSM2")
+    y = b.clone()
+    P.rfp.pftrs(r, y)
+    return x, y
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n,nrhs,rowmajor", [(300, 5, False), (1001, 100, False),
+                                             (2049, 300, True), (1100, 17, True)])
+def test_pftrs_two_region_sweeps_vs_oracle(P, monkeypatch, uplo, transr, n, nrhs, rowmajor):
+    """The fused forward / backward sweeps (trsm2_tiles: both triangles and the
+    S1 product in one launch each) against the oracle and the split sequence,
+    for column- and row-major right-hand sides, odd and even n."""
+    conv, rfp = P.convert, P.rfp
+    a = O.spd_matrix(n, 7 + n, "n")
+    buf = O.trttf(a, uplo, transr)
+    f = buf.copy()
+    assert O.pftrf(f, n, uplo, transr) == 0
+    r = conv.trttf(a, uplo, transr)
+    assert rfp.pftrf(r) == 0
+    bh = np.random.default_rng(n + nrhs).standard_normal((n, nrhs))
+    b = torch.from_numpy(np.ascontiguousarray(bh) if rowmajor else np.asfortranarray(bh)).cuda()
+    assert (b.stride(1) == 1) == rowmajor
+    x, y = _pftrs_split_vs_fused(P, r, b, monkeypatch)
+    xo = np.asfortranarray(bh)
+    O.pftrs(f, n, uplo, transr, xo)
+    assert rel(x, xo) <= TOL
+    assert rel(x, y) <= TOL
+
+
+@pytest.mark.parametrize("uplo,transr", [("L", "N"), ("U", "T")])
+def test_pftrs_two_region_wide_tiles(P, monkeypatch, uplo, transr):
+    """n = 6000, nrhs = 1024: enough tasks for the 64-wide tiles of the fused
+    sweeps; residual and agreement with the split sequence."""
+    conv, rfp = P.convert, P.rfp
+    n, nrhs = 6000, 1024
+    g = torch.Generator(device="cuda").manual_seed(11)
+    bm = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    a = bm @ bm.t() / n
+    a.diagonal().add_(1.0)
+    r = conv.trttf(a, uplo, transr)
+    assert rfp.pftrf(r) == 0
+    b = torch.randn(nrhs, n, dtype=torch.float64, device="cuda", generator=g).t()
+    x, y = _pftrs_split_vs_fused(P, r, b, monkeypatch)
+    res = float((a @ x - b).norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
+    assert res <= 10
+    assert rel(x, y) <= TOL
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n", [777, 1299])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_potrf_row_major_block_copy(P, monkeypatch, uplo, transr, n, cplx):
+    """A diagonal block whose lower view is row-major (T2 for TRANSR='N', T1
+    for 'T') is factored in a column-major copy (forced here with
+    RFPK_T2_COPY_MIN=64; default from order 2048 up, real data only -- the
+    complex cases check that the direct path is unaffected): factor within
+    TOL of the oracle, and failure indices inside either block are the
+    reference's."""
+    conv, rfp = P.convert, P.rfp
+    monkeypatch.setenv("RFPK_T2_COPY_MIN", "64")
+    a = O.spd_matrix(n, 31 + n, "n", complex_=cplx)
+    f = O.trttf(a, uplo, transr)
+    assert O.pftrf(f, n, uplo, transr) == 0
+    r = conv.trttf(a, uplo, transr)
+    assert rfp.pftrf(r) == 0
+    assert rel(r.data, f) <= TOL
+    for k in (2, n - 3):  # inside the leading block, inside the trailing one
+        bad = a.copy()
+        bad[k, k] = -1.0
+        fb = O.trttf(bad, uplo, transr)
+        want = O.pftrf(fb, n, uplo, transr)
+        assert want == k + 1
+        rb = conv.trttf(bad, uplo, transr)
+        assert rfp.pftrf(rb) == want
