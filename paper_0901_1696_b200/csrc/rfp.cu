@@ -124,40 +124,92 @@ struct PhaseTrace {
     if (rc_) return rc_;    \
   } while (0)
 
-// dst(i, j) = src(i, j) on the lower triangle (i >= j) of two n x n views of
-// OPPOSITE orientations: 32 x 32 tiles through shared memory, so the reads
-// run along src's contiguous dimension and the writes along dst's
+// dst(i, j) = src(i, j) for an m x n view pair of any orientations (lower:
+// the lower triangle i >= j only): 32 x 32 tiles through shared memory, read
+// along src's contiguous dimension and written along dst's
 template <typename T>
-__global__ void tri_transpose_copy_kernel(View<T> src, View<T> dst, i64 n) {
-  __shared__ T tile[32][33];
+__global__ void tile_copy_kernel(View<T> src, View<T> dst, int lower) {
+  __shared__ T tile[32][33];  // tile[a][b] = element (i0 + a, j0 + b)
   const int bi = blockIdx.y, bj = blockIdx.x;
-  if (bi < bj) return;
+  if (lower && bi < bj) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const i64 i0 = (i64)bi * 32, j0 = (i64)bj * 32;
-  const bool sj = src.cs == 1;  // src contiguous along j
+  const bool sj = src.cs == 1 && src.rs != 1;  // row-major: contiguous along j
+  const bool dj = dst.cs == 1 && dst.rs != 1;
 #pragma unroll
   for (int r = ty; r < 32; r += 8) {
-    const i64 i = sj ? i0 + r : i0 + tx, j = sj ? j0 + tx : j0 + r;
-    if (i < n && j <= i) {
-      if (sj) tile[r][tx] = *src.at(i, j);
-      else tile[tx][r] = *src.at(i, j);
-    }
+    const int ta = sj ? r : tx, tb = sj ? tx : r;
+    const i64 i = i0 + ta, j = j0 + tb;
+    if (i < src.m && j < src.n && (!lower || j <= i)) tile[ta][tb] = *src.at(i, j);
   }
   __syncthreads();
 #pragma unroll
   for (int r = ty; r < 32; r += 8) {
-    const i64 i = sj ? i0 + tx : i0 + r, j = sj ? j0 + r : j0 + tx;
-    if (i < n && j <= i) *dst.at(i, j) = sj ? tile[tx][r] : tile[r][tx];
+    const int ta = dj ? r : tx, tb = dj ? tx : r;
+    const i64 i = i0 + ta, j = j0 + tb;
+    if (i < src.m && j < src.n && (!lower || j <= i)) *dst.at(i, j) = tile[ta][tb];
   }
 }
 
-template <typename T> static int tri_transpose_copy(Ctx c, View<T> src, View<T> dst) {
-  const i64 nt = (src.m + 31) / 32;
-  if (nt == 0) return 0;
-  tri_transpose_copy_kernel<T><<<dim3((unsigned)nt, (unsigned)nt), dim3(32, 8), 0, c.st>>>(
-      src, dst, src.m);
+template <typename T> static int tile_copy(Ctx c, View<T> src, View<T> dst, bool lower) {
+  if (src.empty()) return 0;
+  const dim3 grid((unsigned)((src.n + 31) / 32), (unsigned)((src.m + 31) / 32));
+  tile_copy_kernel<T><<<grid, dim3(32, 8), 0, c.st>>>(src, dst, lower ? 1 : 0);
   RFPK_CHECK_LAUNCH();
   return 0;
+}
+
+// column-major m x n workspace, 64-byte aligned columns, ld off a power of 2
+template <typename T> static int ws_colmajor(Ctx c, i64 m, i64 n, View<T>& v) {
+  const i64 ld = (m + 15) / 16 * 16 + 8;
+  T* p = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&p, (size_t)ld * (n > 0 ? n : 1) * sizeof(T), c.st);
+  v = View<T>{p, m, n, 1, ld};
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+// Cholesky of the k x k lower view t1 and the solve of the m x k block s1
+// below it, L21 = S L11^-H, in ONE dataflow launch over the tall panel
+// [t1; s1] (s1 must continue t1's rows in the same strided view).  The
+// panel's row tiles must break at its column count, so it factors the first
+// k' = 64*floor(k/64) columns; the r < 64 remaining ones follow as
+// T22 -= L21 L21^H, S2 -= L31 L21^H, potrf(T22), S2 <- S2 L22^-H (the same
+// blocked Cholesky, info offsets unchanged).  -100: k < 64.
+template <typename T> static int panel_chol(Ctx c, View<T> t1, View<T> s1, T* W) {
+  const i64 k = t1.m, m = s1.m, ka = k / 64 * 64, rr = k - ka;
+  if (ka < 64) return -100;
+  View<T> panel{t1.p, k + m, ka, t1.rs, t1.cs};
+  int rc = potrf_panel_tiles(c, panel, ka, 0, W);
+  if (!rc && rr) {
+    const bool herm = is_cplx<T>::value;
+    View<T> L21 = t1.sub(ka, 0, rr, ka), T22 = t1.sub(ka, ka, rr, rr);
+    View<T> L31 = s1.sub(0, 0, m, ka), S12 = s1.sub(0, ka, m, rr);
+    rc = blas_syrk(c, 'L', 'N', -1.0, L21, 1.0, T22, herm);
+    if (!rc) rc = blas_gemm(c, 'N', 'C', m_one<T>(), L31, L21, one<T>(), S12);
+    if (!rc) rc = blas_potrf(c, 'L', T22, (int)ka, (T*)nullptr);
+    if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), T22, S12, false);
+  }
+  return rc;
+}
+
+// The same through a column-major workspace panel when T1 and S are not one
+// strided view (UPLO='U': S1 sits above T1 in the rectangle and enters
+// transposed): copy T1's lower triangle and S in, factor, copy back --
+// O(n^2) coalesced copies buy the one-launch panel.
+template <typename T> static int panel_chol_ws(Ctx c, View<T> t1, View<T> s, T* W) {
+  const i64 k = t1.m, m = s.m;
+  if (k / 64 * 64 < 64) return -100;
+  View<T> P;
+  int rc = ws_colmajor(c, k + m, k, P);
+  if (rc) return rc;
+  View<T> p1 = P.sub(0, 0, k, k), p2 = P.sub(k, 0, m, k);
+  rc = tile_copy(c, t1, p1, true);
+  if (!rc) rc = tile_copy(c, s, p2, false);
+  if (!rc) rc = panel_chol(c, p1, p2, W);
+  if (!rc) rc = tile_copy(c, p1, t1, true);
+  if (!rc) rc = tile_copy(c, p2, s, false);
+  cudaFreeAsync(P.p, c.st);
+  return rc;
 }
 
 // potrf('U', T2) (rfp.py:89 / :84).  The lower view the Cholesky factors is
@@ -179,16 +231,22 @@ template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int 
   // faster -- config 5's pftrf 606 ms direct vs 663 ms through the copy)
   if (is_cplx<T>::value || v.rs == 1 || v.cs != 1 || v.m < min_n)
     return blas_potrf(c, uplo, blk, base, W);
-  const i64 n = v.m, ld = (n + 15) / 16 * 16 + 8;  // 64-byte aligned columns, ld off a power of 2
-  T* p = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&p, (size_t)ld * n * sizeof(T), c.st);
-  if (e != cudaSuccess) return (int)e;
-  View<T> x{p, n, n, 1, ld};
-  int rc = tri_transpose_copy(c, v, x);
+  View<T> x;
+  int rc = ws_colmajor(c, v.m, v.m, x);
+  if (rc) return rc;
+  rc = tile_copy(c, v, x, true);
   if (!rc) rc = blas_potrf(c, 'L', x, base, W);
-  if (!rc) rc = tri_transpose_copy(c, x, v);
-  cudaFreeAsync(p, c.st);
+  if (!rc) rc = tile_copy(c, x, v, true);
+  cudaFreeAsync(x.p, c.st);
   return rc;
+}
+
+static i64 panel_max() {
+  static const i64 v = [] {
+    const char* e = std::getenv("RFPK_PANEL_MAX");
+    return e ? (i64)std::atoll(e) : (i64)4096;
+  }();
+  return v;
 }
 
 // SRPA factorization (rfp.py:55-91)
@@ -217,32 +275,16 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
   };
   if (d.lower) {
     // potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over the tall panel
-    // [T1; S1] (contiguous rows of the normal rectangle): the S1 tiles fill the
-    // SMs the diagonal chain leaves idle.  Measured 10-16% faster for n1 up to
-    // 4096 (pftrf 4096: 2.71 -> 2.27 ms, 8192: 8.82 -> 7.89) and slower above
-    // (16384: 25.6 vs 24.8 ms), so used up to RFPK_PANEL_MAX (default 4096)
-    // columns.  The panel's row tiles must break at its column count, so it
-    // factors the first n1' = 64*floor(n1/64) columns; the r < 64 remaining
-    // ones follow as T1_22 -= L21 L21^H, S1_2 -= L31 L21^H, potrf(T1_22),
-    // S1_2 <- S1_2 L22^-H (the same blocked Cholesky, info offsets unchanged).
+    // [T1; S1] (contiguous rows of the normal rectangle; panel_chol): the S1
+    // tiles fill the SMs the diagonal chain leaves idle.  Measured 10-16%
+    // faster for n1 up to 4096 (pftrf 4096: 2.71 -> 2.27 ms, 8192: 8.82 ->
+    // 7.89) and slower above (16384: 25.6 vs 24.8 ms), so used up to
+    // RFPK_PANEL_MAX (default 4096) columns.  (Row-major blocks, TRANSR='T',
+    // run the panel in place too: a column-major workspace copy measured
+    // 2.48 vs 2.39 ms at n = 4000 and 1.67 vs 1.65 at 3000.)
     int fused = -100;
-    static const i64 panel_max = [] {
-      const char* v = std::getenv("RFPK_PANEL_MAX");
-      return v ? std::atoll(v) : (i64)4096;
-    }();
-    const i64 n1a = d.n1 / 64 * 64, rr = d.n1 - n1a;
-    if (!is_cplx<T>::value && !s1_ready && d.n2 && n1a >= 64 && d.n1 <= panel_max) {
-      View<T> panel{t1.p, d.n1 + d.n2, n1a, t1.rs, t1.cs};
-      fused = potrf_panel_tiles(c, panel, n1a, 0, W);
-      if (!fused && rr) {
-        View<T> L21 = t1.sub(n1a, 0, rr, n1a), T22 = t1.sub(n1a, n1a, rr, rr);
-        View<T> L31 = s1.sub(0, 0, d.n2, n1a), S12 = s1.sub(0, n1a, d.n2, rr);
-        fused = blas_syrk(c, 'L', 'N', -1.0, L21, 1.0, T22, herm);
-        if (!fused) fused = blas_gemm(c, 'N', 'C', m_one<T>(), L31, L21, one<T>(), S12);
-        if (!fused) fused = blas_potrf(c, 'L', T22, (int)n1a, (T*)nullptr);
-        if (!fused) fused = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), T22, S12, false);
-      }
-    }
+    if (!is_cplx<T>::value && !s1_ready && d.n2 && d.n1 <= panel_max())
+      fused = panel_chol(c, t1, s1, W);
     if (fused != -100) {
       rc = fused;
       tr.mark("potrf(T1)+trsm(S1)");
@@ -267,7 +309,19 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       tr.mark("potrf(T2)");
     }
   } else {
-    if (d.n2) {
+    // UPLO='U': S1 <- T1^-H S1 is the tall panel [T1; S1^T] transposed; S1
+    // lies above T1 in the rectangle, so the one-launch panel runs on a
+    // column-major workspace copy (panel_chol_ws), same limit as 'L' (config
+    // 2, n = 4000/4001 'U': pftrf 2.59-2.71 -> 2.38-2.52 ms)
+    int fused = -100;
+    if (!is_cplx<T>::value && !s1_ready && !gated && d.n2 && d.n2 <= panel_max())
+      fused = panel_chol_ws(c, t1, s1.t(), W);
+    if (fused != -100) {
+      rc = fused;
+      tr.mark("potrf(T1)+trsm(S1)");
+      if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
+      tr.mark("syrk(T2)");
+    } else if (d.n2) {
       {
         InputGate g(cflags, 0);
         rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);

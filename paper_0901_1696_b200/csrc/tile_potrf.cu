@@ -1511,8 +1511,13 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   // solve of config 3: 255 registers with spills, two CTAs per SM, 18.4 vs
   // 17.7 ms)
   const long long tasks64 = (long long)a.nb * ((B.n + TP - 1) / TP);
-  const int tn = (!is_cplx<T>::value &&
-                  (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;
+  static const int tn_force = [] {
+    const char* v = std::getenv("RFPK_TRSM_TN");
+    return v ? std::atoi(v) : 0;
+  }();
+  int tn = (!is_cplx<T>::value &&
+            (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;
+  if (!is_cplx<T>::value && (tn_force == 16 || tn_force == 32 || tn_force == 64)) tn = tn_force;
   a.nc = (int)((B.n + tn - 1) / tn);
   a.lower = lower ? 1 : 0;
   a.conj = conj ? 1 : 0;
@@ -1527,7 +1532,16 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   // B operand = X^T (nrhs x K): K-major when B is column-major
   const bool bkm = B.rs == 1;
   int rc;
-  if (tn == 16) {
+  if (tn == 32) {
+    if constexpr (!is_cplx<T>::value) {
+      if (ak) rc = bkm ? trsm_launch<T, true, true, 32>(Tm, B, W, a, sync, c)
+                       : trsm_launch<T, true, false, 32>(Tm, B, W, a, sync, c);
+      else rc = bkm ? trsm_launch<T, false, true, 32>(Tm, B, W, a, sync, c)
+                    : trsm_launch<T, false, false, 32>(Tm, B, W, a, sync, c);
+    } else {
+      rc = -100;
+    }
+  } else if (tn == 16) {
     if constexpr (!is_cplx<T>::value) {
       if (ak) rc = bkm ? trsm_launch<T, true, true, 16>(Tm, B, W, a, sync, c)
                        : trsm_launch<T, true, false, 16>(Tm, B, W, a, sync, c);
