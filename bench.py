@@ -352,7 +352,7 @@ def run_b200(args, rank, world, local):
         torch.cuda.synchronize()
     launches = lib.rfpk_launch_count() - l0
     live_ms, live_n = ctypes.c_double(0.0), ctypes.c_int64(0)
-    lib.rfpk_phase_time(b"pftrf trsm(S1)", ctypes.byref(live_ms), ctypes.byref(live_n))
+    lib.rfpk_phase_time(b"pftrf syrk(T2)", ctypes.byref(live_ms), ctypes.byref(live_n))
     lib.rfpk_phase_clock(0)
     kms_live = live_ms.value / live_n.value if live_n.value else None
     barrier(world)
@@ -363,18 +363,21 @@ def run_b200(args, rank, world, local):
     r = a @ x - rhs0
     resid = float(r.norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
 
-    # dominant kernel: tile_trsm_kernel (the dataflow trsm).  Its largest launch
-    # is pftrf's S1 <- S1 T1^-H (conj(T1) X = S1^T, 8192 x 8192 triangle, 8192
-    # right-hand sides); it also runs the four pftrs solves.  Timed alone through
-    # the C ABI on the live factored RFP views, CUDA events on the launch stream.
+    # dominant kernel: the largest launch that runs on its own inside the step,
+    # pftrf's SYRK T2 <- T2 - S1 S1^T (gemm_kernel TRI: the 8192 x 8192 lower
+    # triangle of a rank-8192 update, ~25% of the step).  (The S1 solve,
+    # tile_trsm_kernel, is as long but now runs concurrently with potrf(T1) --
+    # potrf_trsm_overlap -- so no single-kernel duration exists for it inside
+    # the step.)  Timed live by the phase clock; alone through the C ABI on
+    # the live RFP views, CUDA events on the launch stream, as a cross-check.
     ld = desc.ldar
-    kern_flops = desc.n1 * desc.n1 * desc.n2  # m^2 n for a triangular solve
-    t1p = work.data_ptr() + 8 * desc.shift
+    kern_flops = desc.n2 * desc.n2 * desc.n1  # n^2 k for the triangle of a rank-k update
+    t2p = work.data_ptr()
     s1p = work.data_ptr() + 8 * (desc.n1 + desc.shift)
 
     def dom():
-        lib.rfpk_dtrsm(b"R", b"L", b"C", b"N", 1.0, t1p, desc.n1, 1, ld, s1p, desc.n2, desc.n1,
-                       1, ld, info.data_ptr(), sh)
+        lib.rfpk_dsyrk(b"U", b"C", -1.0, s1p, desc.n2, desc.n1, 1, ld, 1.0, t2p, desc.n2, 1, ld,
+                       sh)
 
     dom()
     torch.cuda.synchronize()
@@ -445,15 +448,15 @@ def run_b200(args, rank, world, local):
         "fraction_of_fp64_nominal": value / 1e3 / NOMINAL_FP64_TFLOPS,
         "fraction_of_fp64_measured_dgemm": value / 1e3 / dgemm_tflops,
         "roofline": {"bound": "tensor",
-                     "kernel": "tile_trsm_kernel (pftrf S1 <- S1 T1^-H: 8192x8192 triangle, 8192 RHS)",
+                     "kernel": "gemm_kernel TRI (pftrf SYRK T2 -= S1 S1^T: 8192x8192 lower triangle, k=8192)",
                      "achieved": k_tflops, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
                      "frac": k_tflops / NOMINAL_FP64_TFLOPS,
                      "algorithmic_flops": kern_flops, "ms_per_launch": kms,
                      "timing": ("live: CUDA events around the launch inside every timed step "
                                 f"({live_n.value} launches); alone: {kms_alone:.3f} ms")
                      if kms_live else "standalone launch (phase clock unavailable)",
-                     "traffic": ncu_traffic("trsm_S1_n16384_LN"),
-                     "algorithmic_bytes": 8 * (desc.n1 * (desc.n1 + 1) // 2 + 2 * desc.n1 * desc.n2),
+                     "traffic": ncu_traffic("syrk_T2_n16384_LN"),
+                     "algorithmic_bytes": 8 * (desc.n1 * desc.n2 + desc.n2 * (desc.n2 + 1)),
                      "peak_source": "nominal FP64 DMMA (MEASURED_PEAKS.json has no FP64 figure); "
                                     f"measured cuBLAS DGEMM here: {dgemm_tflops:.2f} TFLOP/s"},
         "residual_scaled": resid,

@@ -57,11 +57,21 @@ template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
 // the same on a tall panel P (m x n): potrf of its n x n head + solve of the
 // rows below (pftrf's potrf(T1) and S1 <- S1 T1^-H in one launch); -100 if
 // the layout is not supported (m > n needs n % 64 == 0)
-template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W);
+template <typename T>
+int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync = nullptr);
 // dataflow tile trsm: conj?(Tm) X = B in place (tile_potrf.cu); W = lower-form
 // 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
+// agate: row block i of Tm (and W_i) readable once agate[i * agate_stride]
+// is set by a concurrent producer (aabort != 0: it failed)
 template <typename T>
-int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans);
+int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans,
+               const int* agate = nullptr, int agate_stride = 0, const int* aabort = nullptr);
+// potrf('L', T) -> trsm with T's factor, overlapped: the tile potrf on the
+// high-priority stream, the tile trsm conj?(T) X = B (lower, W from the
+// potrf) on a side stream gated row block by row block on the potrf's
+// diagonal flags; -100 = not applicable (the caller runs them in sequence)
+template <typename T>
+int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B);
 // one pftrs sweep through both RFP triangles in one launch (real):
 // op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0; lower = forward sweep, else
 // both triangles upper (W transposed); -100 = not supported (fall back)

@@ -242,11 +242,8 @@ template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int 
 }
 
 static i64 panel_max() {
-  static const i64 v = [] {
-    const char* e = std::getenv("RFPK_PANEL_MAX");
-    return e ? (i64)std::atoll(e) : (i64)4096;
-  }();
-  return v;
+  const char* e = std::getenv("RFPK_PANEL_MAX");
+  return e ? (i64)std::atoll(e) : (i64)4096;
 }
 
 // SRPA factorization (rfp.py:55-91)
@@ -289,6 +286,17 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       rc = fused;
       tr.mark("potrf(T1)+trsm(S1)");
     } else {
+      // potrf(T1) and the S1 solve as two concurrent launches, the solve gated
+      // row block by row block on the factorization (device-resident input,
+      // real, column-major T1: potrf_trsm_overlap)
+      if (!gated && !s1_ready && d.n2)
+        fused = potrf_trsm_overlap(c, t1, W, herm, s1.t());
+      if (fused != -100) {
+        rc = fused;
+        tr.mark("potrf(T1)||trsm(S1)");
+      }
+    }
+    if (fused == -100) {
       {
         InputGate g(cflags, 0);
         rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
@@ -322,18 +330,25 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
       tr.mark("syrk(T2)");
     } else if (d.n2) {
-      {
-        InputGate g(cflags, 0);
-        rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
+      // larger leading blocks: potrf(T1) and the S1 solve concurrently (as 'L')
+      if (!gated && !s1_ready) fused = potrf_trsm_overlap(c, t1, W, herm, s1);
+      if (fused != -100) {
+        rc = fused;
+        tr.mark("potrf(T1)||trsm(S1)");
+      } else {
+        {
+          InputGate g(cflags, 0);
+          rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
+        }
+        tr.mark("potrf(T1)");
+        before_s1();
+        if (!rc) {
+          InputGate g(sflags, 1);  // B = S1: block column c <-> column chunk c
+          rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
+        }
+        after_s1();
+        tr.mark("trsm(S1)");
       }
-      tr.mark("potrf(T1)");
-      before_s1();
-      if (!rc) {
-        InputGate g(sflags, 1);  // B = S1: block column c <-> column chunk c
-        rc = blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), s1, false, W);
-      }
-      after_s1();
-      tr.mark("trsm(S1)");
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
       tr.mark("syrk(T2)");
     }

@@ -808,12 +808,32 @@ struct TrsmArgs {
   int lower, conj, wtrans;
   const int* ext;  // input gate (see InputGate): B(i, c) readable once ext[ext_mode ? c : i]
   int ext_mode;
+  // triangle gate (potrf_trsm_overlap): row block i of Tm and W_i are
+  // readable once agate[i * agate_stride] is set; aabort != 0 = the producer
+  // failed (every task then exits without touching B)
+  const int* agate;
+  int agate_stride;
+  const int* aabort;
 };
 
 template <typename T, bool AK, bool BKM, int TN>
 __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const TrsmArgs& a,
                           int* done, int i, int c, T* sm, int* s_ok, unsigned long long* tr) {
   if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | c); tr[5] = blockIdx.x; }
+  if (a.agate) {  // Tm's row block i and W_i come from a concurrent tile potrf
+    if (threadIdx.x == 0) {
+      const int* f = a.agate + (i64)i * a.agate_stride;
+      unsigned ns = 32;
+      int ok;
+      while (!(ok = ld_acquire(f)) && !ld_relaxed(a.aabort)) {
+        __nanosleep(ns);
+        if (ns < 256) ns *= 2;
+      }
+      *s_ok = ok;
+    }
+    __syncthreads();
+    if (!*s_ok) return false;
+  }
   using C = TileCfg<T>;
   using LA = SmemLayout<T, TP, C::BK, AK>;
   using LB = SmemLayout<T, TN, C::BK, BKM>;
@@ -1057,6 +1077,7 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
   if (info && *info) return;
+  if (threadIdx.x == 0) s_ok = 1;  // cleared only by a failed triangle gate
   int* counter = sync;
   int* done = sync + SYNC_HDR;
   const long long total = (long long)a.nb * a.nc;
@@ -1487,7 +1508,8 @@ int trsm2_tiles(Ctx c, bool lower, View<double> Ta, View<double> B0, const doubl
 // conj?(Tm) X = B in place with the dataflow kernel (W: lower-form 64-block
 // inverses; wtrans for Tm upper).  Returns -100 for unsupported strides.
 template <typename T>
-int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans) {
+int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans,
+               const int* agate, int agate_stride, const int* aabort) {
   const i64 n = Tm.m;
   if (n == 0 || B.n == 0) return 0;
   const bool ak = !(Tm.rs == 1);
@@ -1524,6 +1546,9 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.wtrans = wtrans ? 1 : 0;
   a.ext = InputGate::flags();
   a.ext_mode = InputGate::mode();
+  a.agate = agate;
+  a.agate_stride = agate_stride;
+  a.aabort = aabort;
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
@@ -1561,14 +1586,17 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   return rc;
 }
 
-template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, const double*, bool);
-template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool);
+template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, const double*, bool,
+                                const int*, int, const int*);
+template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool, const int*, int,
+                           const int*);
 
 // Factor the tall lower panel P (m x n, m >= n, col- or row-major): the
 // Cholesky of its leading n x n block and the solve of the rows below it,
 // P = [L11; L21] with L21 = P21 L11^-H, in one dataflow launch.  m == n is
 // potrf.  W (leaf-inverse slabs for ceil(n/64) tiles) is required.
-template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W) {
+template <typename T>
+int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) {
   const i64 m = P.m;
   if (n == 0) return 0;
   if (!W || m < n) return -100;
@@ -1584,7 +1612,11 @@ template <typename T> int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T
   if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
   int rc = km ? tile_launch<T, true>(P, (int)n, W, c, base, sync, nt, mt)
               : tile_launch<T, false>(P, (int)n, W, c, base, sync, nt, mt);
-  cudaFreeAsync(sync, c.st);
+  // keep_sync: the caller gates a concurrent kernel on the done flags
+  // (done(i, j) at sync + SYNC_HDR + i * nt + j; abort at sync + 1) and
+  // frees the array once that kernel is ordered after it
+  if (keep_sync) *keep_sync = sync;
+  else cudaFreeAsync(sync, c.st);
   return rc;
 }
 
@@ -1592,8 +1624,73 @@ template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
   return potrf_panel_tiles(c, A, A.m, base, W);
 }
 
-template int potrf_panel_tiles<double>(Ctx, View<double>, i64, int, double*);
-template int potrf_panel_tiles<Z>(Ctx, View<Z>, i64, int, Z*);
+// potrf('L', A) and the solve conj?(A) X = B that consumes its factor, as
+// two CONCURRENT dataflow launches: the tile potrf on a high-priority stream
+// (two CTAs per SM at these orders, so every SM keeps a third slot), the tile
+// trsm on a low-priority stream, each trsm task first waiting for the
+// potrf's diagonal flag of its row block (done(i, i): row block i of L and
+// W_i published).  The solve's first row blocks then run beside the
+// factorization's chain instead of after it.  Deadlock-free: the potrf never
+// waits on the solve, its CTAs are dispatched first (launched first, higher
+// priority), and a failing potrf raises its abort flag, on which every
+// waiting trsm task exits.
+template <typename T>
+int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
+  if constexpr (is_cplx<T>::value) {
+    return -100;
+  } else {
+    static const bool off = [] {
+      const char* v = std::getenv("RFPK_NO_OVERLAP");
+      return v && std::atoi(v) != 0;
+    }();
+    if (off || A.m <= TP || B.empty() || !W || InputGate::flags()) return -100;
+    if (A.rs != 1 || !(B.rs == 1 || B.cs == 1)) return -100;
+    // not under graph capture: captured kernel nodes lose the stream
+    // priorities the dispatch order relies on
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c.st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+      return -100;
+    struct Streams {
+      cudaStream_t hi = nullptr, lo = nullptr;
+      cudaEvent_t ev[3] = {};
+      bool ok = false;
+    };
+    static Streams per_dev[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Streams& S = per_dev[dev & 15];
+    if (!S.ok) {
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      cudaStreamCreateWithPriority(&S.hi, cudaStreamNonBlocking, greatest);
+      cudaStreamCreateWithPriority(&S.lo, cudaStreamNonBlocking, least);
+      for (auto& e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      S.ok = true;
+    }
+    cudaError_t e = cudaEventRecord(S.ev[0], c.st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(S.hi, S.ev[0], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(S.lo, S.ev[0], 0);
+    if (e != cudaSuccess) return (int)e;
+    int* psync = nullptr;
+    int rc = potrf_panel_tiles(Ctx{S.hi, c.info}, A, A.m, 0, W, &psync);
+    const int nt = (int)((A.m + TP - 1) / TP);
+    if (!rc)
+      rc = trsm_tiles(Ctx{S.lo, c.info}, true, conj, A, B, (const T*)W, false,
+                      psync + SYNC_HDR, nt + 1, psync + 1);
+    // join both streams back into the caller's (also on the error paths)
+    cudaEventRecord(S.ev[1], S.hi);
+    cudaEventRecord(S.ev[2], S.lo);
+    cudaStreamWaitEvent(c.st, S.ev[1], 0);
+    cudaStreamWaitEvent(c.st, S.ev[2], 0);
+    if (psync) cudaFreeAsync(psync, c.st);
+    return rc;
+  }
+}
+template int potrf_trsm_overlap<double>(Ctx, View<double>, double*, bool, View<double>);
+template int potrf_trsm_overlap<Z>(Ctx, View<Z>, Z*, bool, View<Z>);
+
+template int potrf_panel_tiles<double>(Ctx, View<double>, i64, int, double*, int**);
+template int potrf_panel_tiles<Z>(Ctx, View<Z>, i64, int, Z*, int**);
 template int potrf_tiles<double>(Ctx, View<double>, int, double*);
 template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
 

@@ -774,3 +774,27 @@ def test_potrf_row_major_block_copy(P, monkeypatch, uplo, transr, n, cplx):
         assert want == k + 1
         rb = conv.trttf(bad, uplo, transr)
         assert rfp.pftrf(rb) == want
+
+
+@pytest.mark.parametrize("uplo", "LU")
+def test_potrf_trsm_overlap_info_and_factor(P, monkeypatch, uplo):
+    """Above the panel limit (forced low: RFPK_PANEL_MAX=256) potrf(T1) and the
+    S1 solve run as two concurrent launches, the solve gated on the potrf's
+    diagonal flags: factor within TOL of the oracle, and a failure inside T1
+    (every gated solve task must then exit) returns the reference's index
+    without hanging."""
+    conv, rfp = P.convert, P.rfp
+    monkeypatch.setenv("RFPK_PANEL_MAX", "256")
+    n = 1403
+    a = O.spd_matrix(n, 99, "n")
+    f = O.trttf(a, uplo, "N")
+    assert O.pftrf(f, n, uplo, "N") == 0
+    r = conv.trttf(a, uplo, "N")
+    assert rfp.pftrf(r) == 0
+    assert rel(r.data, f) <= TOL
+    for k in (1, 300, 650):
+        bad = a.copy()
+        bad[k, k] = -1.0
+        want = O.pftrf(O.trttf(bad, uplo, "N"), n, uplo, "N")
+        assert want == k + 1
+        assert rfp.pftrf(conv.trttf(bad, uplo, "N")) == want
