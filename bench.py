@@ -215,6 +215,7 @@ def c3_config(n, nrhs, world):
     return {"workload": "BASELINE config 3: pftrf+pftrs, n=16384, TRANSR=N, UPLO=L, nrhs=1024",
             "n": n, "nrhs": nrhs, "transr": "N", "uplo": "L",
             "l2": "no flush: RFP buffer 1.07 GB + RHS 134 MB exceed the 126 MB L2",
+            "call": "rfpk_dpfsv (pftrf + pftrs in one C-ABI call; e2e: rfpk_dpfsv_host)",
             "parallelism": "replicas" if world > 1 else "single GPU"}
 
 
@@ -329,8 +330,9 @@ def run_b200(args, rank, world, local):
     def step():
         work.copy_(pristine)
         x.copy_(rhs0)
-        rc = lib.rfpk_dpftrf(T, U, n, work.data_ptr(), info.data_ptr(), sh)
-        rc |= lib.rfpk_dpftrs(T, U, n, nrhs, work.data_ptr(), x.data_ptr(), n, info.data_ptr(), sh)
+        # pftrf + pftrs in one C-ABI call (rfpk_dpfsv: the first T1 solve and
+        # the S1 product run beside potrf(T2)); the same work as the pair
+        rc = lib.rfpk_dpfsv(T, U, n, nrhs, work.data_ptr(), x.data_ptr(), n, info.data_ptr(), sh)
         if rc:
             raise RuntimeError(f"rfpk call failed rc={rc}")
 

@@ -110,6 +110,14 @@ int rfpk_dpftrf_host(char transr, char uplo, int64_t n, const double* h_arf, dou
                      int* info, rfpk_stream_t stream);
 int rfpk_zpftrf_host(char transr, char uplo, int64_t n, const void* h_arf, void* d_arf, int* info,
                      rfpk_stream_t stream);
+/* rfp.pftrf(r) then rfp.pftrs(r, b) on a device-resident problem in one
+   call (B column-major n x nrhs, ld ldb): the first solve with T1 and the S1
+   product run concurrently with potrf(T2).  info as rfpk_?pftrf (after a
+   failure b is unspecified).  rfp.py:55-136 (the pair of calls). */
+int rfpk_dpfsv(char transr, char uplo, int64_t n, int64_t nrhs, double* arf, double* b,
+               int64_t ldb, int* info, rfpk_stream_t stream);
+int rfpk_zpfsv(char transr, char uplo, int64_t n, int64_t nrhs, void* arf, void* b, int64_t ldb,
+               int* info, rfpk_stream_t stream);
 /* rfp.pftrf(r) then rfp.pftrs(r, b) on a problem that sits in pinned HOST
    memory (h_arf: the RFP buffer; h_b: n x nrhs column-major, ld ldb), with
    every transfer overlapped with the computation; the solution lands in

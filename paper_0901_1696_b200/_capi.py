@@ -52,6 +52,8 @@ SIGNATURES = {
     "rfpk_zpftri": ([_c, _c, _i64, _p, _p, _p], _int),
     "rfpk_dpftrf_host": ([_c, _c, _i64, _p, _p, _p, _p], _int),
     "rfpk_zpftrf_host": ([_c, _c, _i64, _p, _p, _p, _p], _int),
+    "rfpk_dpfsv": ([_c, _c, _i64, _i64, _p, _p, _i64, _p, _p], _int),
+    "rfpk_zpfsv": ([_c, _c, _i64, _i64, _p, _p, _i64, _p, _p], _int),
     "rfpk_dpfsv_host": ([_c, _c, _i64, _i64, _p, _p, _p, _p, _p, _i64, _p, _p], _int),
     "rfpk_zpfsv_host": ([_c, _c, _i64, _i64, _p, _p, _p, _p, _p, _i64, _p, _p], _int),
     "rfpk_phase_clock": ([_int], _int),

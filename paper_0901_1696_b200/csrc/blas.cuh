@@ -66,6 +66,14 @@ int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync =
 template <typename T>
 int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans,
                const int* agate = nullptr, int agate_stride = 0, const int* aabort = nullptr);
+// per-device streams for concurrent launches: hi = greatest priority (the
+// critical-path kernel), lo = least; ev = scratch fork/join events
+struct OverlapStreams {
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t ev[6] = {};
+  bool ok = false;
+};
+OverlapStreams& overlap_streams();
 // potrf('L', T) -> trsm with T's factor, overlapped: the tile potrf on the
 // high-priority stream, the tile trsm conj?(T) X = B (lower, W from the
 // potrf) on a side stream gated row block by row block on the potrf's

@@ -283,17 +283,16 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
     if (e != cudaSuccess) return (int)e;
   }
   cudaEventRecord(b_done, side);
-  int rcf = pftrf<T>(Ctx{st, info}, d, (T*)d_arf, s1_done, cflags, sflags);
+  // pftrf + pftrs as one driver (pfsv: the first T1 solve and the S1 product
+  // run beside potrf(T2)); after a failed factorization every solve kernel
+  // skips on *info
+  const i64 split = d.lower ? d.n1 : d.n2;  // first row of the trailing block
+  const bool trail = nrhs > 0 && n - split > 0 && !(d.lower && d.n2 == 0);
+  int rcf = pfsv<T>(Ctx{st, info}, d, (T*)d_arf, V<T>(d_b, n, nrhs, 1, ldb), s1_done, cflags,
+                    sflags, b_done, trail ? b2_final : nullptr);
   if (cflags) cudaFreeAsync(cflags, st);
   if (rcf) return rcf;
   if (nrhs == 0) return 0;
-  cudaStreamWaitEvent(st, b_done, 0);
-  // (after a failed factorization every solve kernel skips on *info)
-  const i64 split = d.lower ? d.n1 : d.n2;  // first row of the trailing block
-  const bool trail = n - split > 0 && !(d.lower && d.n2 == 0);
-  if (int rc = pftrs<T>(Ctx{st, info}, d, (const T*)d_arf, V<T>(d_b, n, nrhs, 1, ldb),
-                        trail ? b2_final : nullptr))
-    return rc;
   if (trail) {
     cudaStreamWaitEvent(side, b2_final, 0);
     e = cudaMemcpy2DAsync((T*)h_x + split, pitch, (const T*)d_b + split, pitch,
@@ -307,6 +306,23 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   cudaEventRecord(fork, side);  // join the side stream back into `st`
   cudaStreamWaitEvent(st, fork, 0);
   return 0;
+}
+
+// pftrf + pftrs of a device-resident problem in one call (the pfsv driver:
+// the first solve with T1 and the S1 product overlap potrf(T2))
+template <typename T>
+int pfsv_t(char transr, char uplo, int64_t n, int64_t nrhs, void* arf, void* b, int64_t ldb,
+           int* info, cudaStream_t st) {
+  transr = up(transr); uplo = up(uplo);
+  if (!one_of(transr, "NTC")) return -1;
+  if (!one_of(uplo, "LU")) return -2;
+  if (n < 0) return -3;
+  if (nrhs < 0) return -4;
+  if (ldb < (n > 1 ? n : 1)) return -7;
+  if (!info) return -8;
+  if (int rc = reset_info(info, st)) return rc;
+  if (n == 0) return 0;
+  return pfsv<T>(Ctx{st, info}, rfp_desc(n, uplo, transr), (T*)arf, V<T>(b, n, nrhs, 1, ldb));
 }
 
 // ---------------------------------------------------------------- packed Cholesky
@@ -422,6 +438,8 @@ int rfpk_phase_time(const char* label, double* total_ms, int64_t* count) {
   *count = c;
   return 0;
 }
+int rfpk_dpfsv(char t, char u, int64_t n, int64_t nrhs, double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_t<double>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
+int rfpk_zpfsv(char t, char u, int64_t n, int64_t nrhs, void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_t<Z>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
 int rfpk_dpfsv_host(char t, char u, int64_t n, int64_t nrhs, const double* h_arf, double* d_arf, const double* h_b, double* d_b, double* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<double>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
 int rfpk_zpfsv_host(char t, char u, int64_t n, int64_t nrhs, const void* h_arf, void* d_arf, const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<Z>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
 int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }

@@ -15,6 +15,42 @@ __device__ __forceinline__ void tri_tile(int mode, long long b, int& tm, int& tn
   if (mode == TRI_LOWER) { tm = ti; tn = tj; } else { tm = tj; tn = ti; }
 }
 
+// Banded order of the same lower-triangular tile grid: bands of H tile rows,
+// each band walked column by column (the H tiles of a column, then the next
+// column; the band's own triangle last).  The tiles resident at one time
+// then share ~H row panels and ~(resident / H) column panels instead of a
+// few rows and every column panel up to them, so the operand panels they
+// stream stay in L2 (SYRK T2 -= S1 S1^T at n = 16384, ncu: DRAM reads per
+// launch 20.6 GB row by row -> 7.05 GB at H = 24, 17.12 -> 16.73 ms; H = 16
+// and 32 measured the same time).  RFPK_TRI_BAND = H (0: row by row).
+__device__ __forceinline__ void tri_tile_banded(int mode, long long b, int tiles, int H, int& tm,
+                                                int& tn) {
+  int r0 = 0;
+  for (;;) {  // band starting at tile row r0: h full columns of r0 tiles + its triangle
+    const int h = tiles - r0 < H ? tiles - r0 : H;
+    const long long cnt = (long long)r0 * h + (long long)h * (h + 1) / 2;
+    if (b < cnt) {
+      int ti, tj;
+      if (b < (long long)r0 * h) {
+        tj = (int)(b / h);
+        ti = r0 + (int)(b % h);
+      } else {
+        long long o = b - (long long)r0 * h;
+        tj = r0;
+        while (o >= r0 + h - tj) {
+          o -= r0 + h - tj;
+          ++tj;
+        }
+        ti = tj + (int)o;
+      }
+      if (mode == TRI_LOWER) { tm = ti; tn = tj; } else { tm = tj; tn = ti; }
+      return;
+    }
+    b -= cnt;
+    r0 += h;
+  }
+}
+
 // the same for BM x BN tiles with BN a multiple of BM (64 x 128): column tile
 // tn spans rows tiles from (TRI_LOWER) BN/BM*tn, or up to (TRI_UPPER)
 // BN/BM*(tn+1)-1; scanned column by column (<= tiles_n steps per CTA)
@@ -216,7 +252,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int tm, tn;
     if (MODE == TRI_FULL) { tm = (int)(t % g.tiles_m); tn = (int)(t / g.tiles_m); }
-    else if constexpr (BM == BN) tri_tile(MODE, t, tm, tn);
+    else if constexpr (BM == BN) {
+      if (g.band > 0) tri_tile_banded(MODE, t, g.tiles_m, g.band, tm, tn);
+      else tri_tile(MODE, t, tm, tn);
+    }
     else tri_tile_rect<BM, BN>(MODE, t, g.tiles_m, tm, tn);
     gemm_tile<T, BM, BN, BK, WM, WN, STAGES, AK, BKM, MODE>(g, tm, tn, As, Bs);
     if (t + gridDim.x < g.ntiles) __syncthreads();  // smem stages are reused
@@ -355,6 +394,11 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
   const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   GemmArgs<T> g = a;
   g.tiles_m = tm;
+  static const int band = [] {
+    const char* v = std::getenv("RFPK_TRI_BAND");
+    return v ? std::atoi(v) : 24;
+  }();
+  g.band = band;
   if (MODE == TRI_FULL) {
     g.ntiles = (long long)tm * tn;
   } else if (BM == BN) {

@@ -35,6 +35,7 @@ template <typename T> struct GemmArgs {
   int a_tri;          // A operand mask: 0 none, 1 lower, 2 upper, 3 strict lower, 4 strict upper
   int b_tri;          // same mask applied to B (k, n) as if it were A (n, k) (transposed problems)
   long long ntiles;   // tiles of the launch (CTAs stride over them)
+  int band;           // TRI square tiles: rows per band of the rasterised order (0: row by row)
 };
 
 

@@ -246,10 +246,23 @@ static i64 panel_max() {
   return e ? (i64)std::atoll(e) : (i64)4096;
 }
 
+struct WsPair {  // two leaf-inverse workspaces, freed stream-ordered
+  cudaStream_t st;
+  void* p[2] = {nullptr, nullptr};
+  ~WsPair() {
+    for (void* q : p)
+      if (q) cudaFreeAsync(q, st);
+  }
+};
+
+template <typename T>
+static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T* W2,
+                      cudaEvent_t b2_final, int part);
+
 // SRPA factorization (rfp.py:55-91)
 template <typename T>
 int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cflags,
-          const int* sflags) {
+          const int* sflags, PfsvPlan<T>* plan) {
   if (d.n == 0) return 0;
   const bool herm = is_cplx<T>::value;
   View<T> t1, t2, s1;
@@ -260,6 +273,40 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
   TRY(ws_alloc(&W, d.n1, c.st));
   int rc = 0;
   PhaseTrace tr(c.st, "pftrf");
+  // potrf(T2); with a pfsv plan, beside pftrs part 1 (see pfsv)
+  auto t2_step = [&](int base) -> int {
+    static const i64 min_t2 = [] {
+      const char* v = std::getenv("RFPK_PFSV_OVERLAP_MIN");
+      return v ? (i64)std::atoll(v) : (i64)512;
+    }();
+    if (!plan || d.n2 == 0 || t2.m < min_t2) return potrf_block(c, 'U', t2, base, W);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c.st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+      return potrf_block(c, 'U', t2, base, W);
+    OverlapStreams& S = overlap_streams();
+    T *W1 = nullptr, *W2 = nullptr;
+    WsPair fr{c.st};
+    int r = ws_alloc(&W1, t1.m, c.st);
+    fr.p[0] = W1;
+    if (!r) r = ws_alloc(&W2, t2.m, c.st);
+    fr.p[1] = W2;
+    if (r) return r;
+    cudaEventRecord(S.ev[3], c.st);
+    cudaStreamWaitEvent(S.hi, S.ev[3], 0);
+    int rt2 = potrf_block(Ctx{S.hi, c.info}, 'U', t2, base, W);
+    if (plan->b_ready) cudaStreamWaitEvent(c.st, plan->b_ready, 0);
+    r = blas_leaf_inverses(c, t1, W1);
+    if (!r) r = pftrs_part(c, d, (const T*)arf, plan->b, W1, W2, nullptr, 1);
+    cudaEventRecord(S.ev[4], S.hi);  // join (also on the error paths)
+    cudaStreamWaitEvent(c.st, S.ev[4], 0);
+    tr.mark("potrf(T2)||pftrs(T1,S1)");
+    if (rt2) return rt2;
+    if (r) return r;
+    r = blas_leaf_inverses(c, t2.t(), W2);
+    if (!r) r = pftrs_part(c, d, (const T*)arf, plan->b, W1, W2, plan->b2_final, 2);
+    plan->done = true;
+    return r;
+  };
   // streamed input (cflags/sflags): potrf(T1) and the S1 solve read each
   // 64-column chunk as soon as its flag is set; the remaining steps wait for
   // the whole transfer (s1_ready) -- by then every chunk has been seen
@@ -313,7 +360,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     if (!rc && d.n2) {
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
       tr.mark("syrk(T2)");
-      if (!rc) rc = potrf_block(c, 'U', t2, (int)d.n1, W);
+      if (!rc) rc = t2_step((int)d.n1);
       tr.mark("potrf(T2)");
     }
   } else {
@@ -352,7 +399,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
       tr.mark("syrk(T2)");
     }
-    if (!rc) rc = potrf_block(c, 'U', t2, (int)d.n2, W);
+    if (!rc) rc = t2_step((int)d.n2);
     tr.mark("potrf(T2)");
   }
   // (the transfers must also be complete on every early-exit path)
@@ -436,33 +483,23 @@ int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* s
   return 0;
 }
 
-// forward/back substitution through T1/S1/T2 (rfp.py:106-136).  The 64-block
-// inverses of T1 and T2 are formed once and shared by the two solves with
-// each triangle (forward and back).
-template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
-                                cudaEvent_t b2_final) {
-  if (d.n == 0 || b.n == 0) return 0;
+// forward/back substitution through T1/S1/T2 (rfp.py:106-136), in parts:
+// part 1 = the first solve with T1 and the S1 product into the trailing
+// block (reads only T1 and S1 -- it can run while T2 is still being
+// factored, see pfsv), part 2 = the rest, part 0 = everything.  W1 / W2:
+// the 64-block inverses of T1 (lower as stored for 'L', T1^T's for 'U' --
+// the same view either way is the lower one) and of T2^T (T2 is upper),
+// formed once and shared by the two solves with each triangle.
+template <typename T>
+static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T* W2,
+                      cudaEvent_t b2_final, int part) {
   View<T> t1, t2, s1;
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
   const i64 n1 = d.n1, n2 = d.n2, r = b.n;
   PhaseTrace tr(c.st, "pftrs");
-  // W1: inverses of T1 (lower as stored for 'L', T1^T's for 'U' -- the same
-  // view either way is the lower one); W2: of T2^T (T2 is upper)
-  T *W1 = nullptr, *W2 = nullptr;
-  struct Free {
-    T** p[2];
-    cudaStream_t st;
-    ~Free() { for (T** q : p) ws_free(*q, st); }
-  } fr{{&W1, &W2}, c.st};
-  TRY(ws_alloc(&W1, t1.m, c.st));
-  TRY(blas_leaf_inverses(c, t1, W1));
-  if (t2.m) {
-    TRY(ws_alloc(&W2, t2.m, c.st));
-    TRY(blas_leaf_inverses(c, t2.t(), W2));
-  }
-  // real data: each sweep through both triangles is ONE dataflow launch
-  // (trsm, the S1 gemm and the other triangle's trsm fused, trsm2_tiles);
-  // the back sweep stays split when the caller streams B2 out early
+  // opt-in (RFPK_TRSM2=1): each sweep through both triangles as ONE dataflow
+  // launch (trsm, the S1 gemm and the other triangle's trsm fused,
+  // trsm2_tiles); the back sweep stays split when the caller streams B2 out
   auto sweep2 = [&](bool fwd, View<T> ta, View<T> b0, const T* wa, View<T> tb, View<T> bb,
                     const T* wb, View<T> p) -> int {
     if constexpr (std::is_same<T, double>::value) {
@@ -470,7 +507,7 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
         const char* v = std::getenv("RFPK_TRSM2_MIN");
         return v ? (i64)std::atoll(v) : (i64)128;
       }();
-      if (n2 == 0 || n1 < mn || n2 < mn || (!fwd && b2_final)) return -100;
+      if (part != 0 || n2 == 0 || n1 < mn || n2 < mn || (!fwd && b2_final)) return -100;
       return trsm2_tiles(c, fwd, ta, b0, wa, tb, bb, wb, p);
     } else {
       return -100;
@@ -496,11 +533,16 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
       tr.mark("trsm4");
       return 0;
     }
-    TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false, W1));
-    tr.mark("trsm1");
+    if (part != 2) {
+      TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false, W1));
+      tr.mark("trsm1");
+      if (n2) {
+        TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+        tr.mark("gemm1");
+      }
+      if (part == 1) return 0;
+    }
     if (n2) {
-      TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b1, one<T>(), b2));
-      tr.mark("gemm1");
       TRY(blas_trsm(c, 'L', 'U', 'T', 'N', one<T>(), t2, b2, false, W2));
       tr.mark("trsm2");
       TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false, W2));
@@ -523,9 +565,12 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
     TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
     return 0;
   }
-  if (n2) {
-    TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false, W1));
-    TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+  if (part != 2) {
+    if (n2) {
+      TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false, W1));
+      TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b1, one<T>(), b2));
+    }
+    if (part == 1) return 0;
   }
   TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t2, b2, false, W2));
   TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false, W2));
@@ -535,6 +580,39 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
     TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
   }
   return 0;
+}
+
+template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
+                                cudaEvent_t b2_final) {
+  if (d.n == 0 || b.n == 0) return 0;
+  View<T> t1, t2, s1;
+  rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
+  T *W1 = nullptr, *W2 = nullptr;
+  WsPair fr{c.st};
+  TRY(ws_alloc(&W1, t1.m, c.st));
+  fr.p[0] = W1;
+  TRY(blas_leaf_inverses(c, t1, W1));
+  if (t2.m) {
+    TRY(ws_alloc(&W2, t2.m, c.st));
+    fr.p[1] = W2;
+    TRY(blas_leaf_inverses(c, t2.t(), W2));
+  }
+  return pftrs_part(c, d, arf, b, W1, W2, b2_final, 0);
+}
+
+// pftrf + pftrs in one driver (the public pfsv paths).  The first solve with
+// T1 and the S1 product (pftrs part 1) read only T1 and S1, so they run on
+// the caller's stream WHILE potrf(T2) runs on the high-priority stream: the
+// factorization's diagonal chain leaves SM slots and DMMA cycles idle that
+// the solve fills.  No flags cross the two: they touch disjoint blocks.
+template <typename T>
+int pfsv(Ctx c, const RfpDesc& d, T* arf, View<T> b, cudaEvent_t s1_ready, const int* cflags,
+         const int* sflags, cudaEvent_t b_ready, cudaEvent_t b2_final) {
+  PfsvPlan<T> plan{b, b_ready, b2_final, false};
+  const int rc = pftrf<T>(c, d, arf, s1_ready, cflags, sflags, b.n ? &plan : nullptr);
+  if (rc || plan.done || b.n == 0 || d.n == 0) return rc;
+  if (b_ready) cudaStreamWaitEvent(c.st, b_ready, 0);
+  return pftrs<T>(c, d, arf, b, b2_final);
 }
 
 // triangular inverse in RFP (rfp.py:286-325)
@@ -1139,7 +1217,9 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
 
 #define RFPK_RFP_INST(T)                                                                     \
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
-  template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t, const int*, const int*);                               \
+  template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t, const int*, const int*, PfsvPlan<T>*); \
+  template int pfsv<T>(Ctx, const RfpDesc&, T*, View<T>, cudaEvent_t, const int*, const int*,      \
+                       cudaEvent_t, cudaEvent_t);                               \
   template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);   \
   template int rfp_h2d_chunked<T>(const RfpDesc&, const T*, T*, int*, int*, cudaStream_t);                                            \
   template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>, cudaEvent_t);                             \

@@ -19,9 +19,23 @@ RfpDesc rfp_desc(i64 n, char uplo, char transr);
 template <typename T> void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2,
                                       View<T>& s1);
 
+// pfsv plan: pftrf runs the whole pftrs of b at its end (part of it beside
+// potrf(T2)) and sets done; b_ready: b's transfer, b2_final as for pftrs
+template <typename T> struct PfsvPlan {
+  View<T> b;
+  cudaEvent_t b_ready;
+  cudaEvent_t b2_final;
+  bool done;
+};
 template <typename T>
 int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr,
-          const int* cflags = nullptr, const int* sflags = nullptr);
+          const int* cflags = nullptr, const int* sflags = nullptr,
+          PfsvPlan<T>* plan = nullptr);
+// pftrf + pftrs(b) with the independent parts overlapped (see rfp.cu)
+template <typename T>
+int pfsv(Ctx c, const RfpDesc& d, T* arf, View<T> b, cudaEvent_t s1_ready = nullptr,
+         const int* cflags = nullptr, const int* sflags = nullptr,
+         cudaEvent_t b_ready = nullptr, cudaEvent_t b2_final = nullptr);
 // (s1_ready: the S1 rows' transfer; with cflags / sflags the input is being
 //  streamed in 64-column chunks of the normal rectangle, chunk j of the T1/T2
 //  rows flagged in cflags[j] and of the S1 rows in sflags[j], and s1_ready

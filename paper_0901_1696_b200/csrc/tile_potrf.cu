@@ -1624,6 +1624,22 @@ template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
   return potrf_panel_tiles(c, A, A.m, base, W);
 }
 
+OverlapStreams& overlap_streams() {
+  static OverlapStreams per_dev[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  OverlapStreams& S = per_dev[dev & 15];
+  if (!S.ok) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&S.hi, cudaStreamNonBlocking, greatest);
+    cudaStreamCreateWithPriority(&S.lo, cudaStreamNonBlocking, least);
+    for (auto& e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    S.ok = true;
+  }
+  return S;
+}
+
 // potrf('L', A) and the solve conj?(A) X = B that consumes its factor, as
 // two CONCURRENT dataflow launches: the tile potrf on a high-priority stream
 // (two CTAs per SM at these orders, so every SM keeps a third slot), the tile
@@ -1650,23 +1666,7 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(c.st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
       return -100;
-    struct Streams {
-      cudaStream_t hi = nullptr, lo = nullptr;
-      cudaEvent_t ev[3] = {};
-      bool ok = false;
-    };
-    static Streams per_dev[16];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    Streams& S = per_dev[dev & 15];
-    if (!S.ok) {
-      int least = 0, greatest = 0;
-      cudaDeviceGetStreamPriorityRange(&least, &greatest);
-      cudaStreamCreateWithPriority(&S.hi, cudaStreamNonBlocking, greatest);
-      cudaStreamCreateWithPriority(&S.lo, cudaStreamNonBlocking, least);
-      for (auto& e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      S.ok = true;
-    }
+    OverlapStreams& S = overlap_streams();
     cudaError_t e = cudaEventRecord(S.ev[0], c.st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.hi, S.ev[0], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.lo, S.ev[0], 0);

@@ -26,6 +26,7 @@ __all__ = [
     "pftrf",
     "pftrf_from_host",
     "pfsv_from_host",
+    "pfsv",
     "pftrs",
     "tfsm",
     "sfrk_hfrk",
@@ -79,6 +80,37 @@ def pftrf(r: RfpTriangle) -> int:
     v = int(info.item())
     if v == 0:
         r.state = FactorState.CHOLESKY
+    return v
+
+
+def pfsv(r: RfpTriangle, b) -> int:
+    """:func:`pftrf` then :func:`pftrs` on ``b`` in one call
+    (rfp.py:55-136, the pair): the first solve with T1 and the S1 product run
+    on the device concurrently with potrf(T2).  Returns pftrf's info; ``b``
+    is solved in place only on success (0).  A device ``b`` that is not a
+    column-major float64/complex128 (n, nrhs) view of the factor's dtype
+    takes the two separate calls."""
+    if r.state is not FactorState.UNFACTORED:
+        raise ValueError(f"pfsv needs an unfactored matrix, state is {r.state.value}")
+    desc = r.desc
+    fast = (isinstance(b, torch.Tensor) and b.is_cuda and b.dim() == 2 and b.dtype == r.dtype
+            and b.device == r.data.device and b.shape[0] == desc.n and b.stride(0) == 1
+            and b.stride(1) >= max(desc.n, 1) and desc.n > 0)
+    if not fast:
+        v = pftrf(r)
+        if v == 0:
+            pftrs(r, b)
+        return v
+    keep = b.clone()
+    info = _info(r.data.device)
+    _run(f"rfpk_{_prefix(r.dtype)}pfsv", _capi.flag(desc.transr), _capi.flag(desc.uplo), desc.n,
+         b.shape[1], r.data.data_ptr(), b.data_ptr(), b.stride(1), info.data_ptr(),
+         _capi.stream_handle(r.data.device))
+    v = int(info.item())
+    if v == 0:
+        r.state = FactorState.CHOLESKY
+    else:
+        b.copy_(keep)  # the reference's pftrs never runs after a failed pftrf
     return v
 
 

@@ -798,3 +798,38 @@ def test_potrf_trsm_overlap_info_and_factor(P, monkeypatch, uplo):
         want = O.pftrf(O.trttf(bad, uplo, "N"), n, uplo, "N")
         assert want == k + 1
         assert rfp.pftrf(conv.trttf(bad, uplo, "N")) == want
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n", [1, 130, 1501, 2049])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_pfsv_device_matches_pftrf_pftrs(P, monkeypatch, uplo, transr, n, cplx):
+    """rfp.pfsv (the first T1 solve and the S1 product run beside potrf(T2);
+    forced from T2 order 64 here) gives pftrf + pftrs's factor and solution
+    within TOL of the oracle; a failing factorization leaves b untouched and
+    returns the reference's index."""
+    conv, rfp = P.convert, P.rfp
+    monkeypatch.setenv("RFPK_PFSV_OVERLAP_MIN", "64")
+    a = O.spd_matrix(n, 5 + n, "n", complex_=cplx)
+    f = O.trttf(a, uplo, transr)
+    assert O.pftrf(f, n, uplo, transr) == 0
+    rng = np.random.default_rng(n)
+    bh = rng.standard_normal((n, 9)) + (1j * rng.standard_normal((n, 9)) if cplx else 0)
+    xo = np.asfortranarray(bh.copy())
+    O.pftrs(f, n, uplo, transr, xo)
+    r = conv.trttf(a, uplo, transr)
+    b = torch.from_numpy(np.asfortranarray(bh)).cuda()
+    assert rfp.pfsv(r, b) == 0
+    assert r.state is conv.FactorState.CHOLESKY
+    assert rel(r.data, f) <= TOL
+    assert rel(b, xo) <= TOL
+    if n > 2:
+        bad = a.copy()
+        bad[n - 2, n - 2] = -1.0
+        want = O.pftrf(O.trttf(bad, uplo, transr), n, uplo, transr)
+        rb = conv.trttf(bad, uplo, transr)
+        b2 = torch.from_numpy(np.asfortranarray(bh)).cuda()
+        assert rfp.pfsv(rb, b2) == want > 0
+        assert rb.state is conv.FactorState.UNFACTORED
+        assert torch.equal(b2.cpu(), torch.from_numpy(np.asfortranarray(bh)))
