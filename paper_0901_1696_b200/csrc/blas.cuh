@@ -79,7 +79,8 @@ OverlapStreams& overlap_streams();
 // potrf) on a side stream gated row block by row block on the potrf's
 // diagonal flags; -100 = not applicable (the caller runs them in sequence)
 template <typename T>
-int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B);
+int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* pgate = nullptr,
+                       const int* bgate = nullptr, int bgate_mode = 0);
 // one pftrs sweep through both RFP triangles in one launch (real):
 // op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0; lower = forward sweep, else
 // both triangles upper (W transposed); -100 = not supported (fall back)

@@ -336,10 +336,13 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       // potrf(T1) and the S1 solve as two concurrent launches, the solve gated
       // row block by row block on the factorization (device-resident input,
       // real, column-major T1: potrf_trsm_overlap)
-      if (!gated && !s1_ready && d.n2)
-        fused = potrf_trsm_overlap(c, t1, W, herm, s1.t());
+      // (streamed input: each launch keeps its chunk gate; B = S1^T, block
+      // row i <-> column chunk i)
+      if (d.n2 && (gated || !s1_ready))
+        fused = potrf_trsm_overlap(c, t1, W, herm, s1.t(), cflags, sflags, 0);
       if (fused != -100) {
         rc = fused;
+        after_s1();
         tr.mark("potrf(T1)||trsm(S1)");
       }
     }
@@ -378,9 +381,11 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       tr.mark("syrk(T2)");
     } else if (d.n2) {
       // larger leading blocks: potrf(T1) and the S1 solve concurrently (as 'L')
-      if (!gated && !s1_ready) fused = potrf_trsm_overlap(c, t1, W, herm, s1);
+      if (gated || !s1_ready)  // B = S1: block column c <-> column chunk c
+        fused = potrf_trsm_overlap(c, t1, W, herm, s1, cflags, sflags, 1);
       if (fused != -100) {
         rc = fused;
+        after_s1();
         tr.mark("potrf(T1)||trsm(S1)");
       } else {
         {

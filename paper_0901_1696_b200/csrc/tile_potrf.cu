@@ -1651,7 +1651,8 @@ OverlapStreams& overlap_streams() {
 // priority), and a failing potrf raises its abort flag, on which every
 // waiting trsm task exits.
 template <typename T>
-int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
+int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* pgate,
+                       const int* bgate, int bgate_mode) {
   if constexpr (is_cplx<T>::value) {
     return -100;
   } else {
@@ -1659,7 +1660,7 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
       const char* v = std::getenv("RFPK_NO_OVERLAP");
       return v && std::atoi(v) != 0;
     }();
-    if (off || A.m <= TP || B.empty() || !W || InputGate::flags()) return -100;
+    if (off || A.m <= TP || B.empty() || !W) return -100;
     if (A.rs != 1 || !(B.rs == 1 || B.cs == 1)) return -100;
     // not under graph capture: captured kernel nodes lose the stream
     // priorities the dispatch order relies on
@@ -1671,12 +1672,20 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.hi, S.ev[0], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.lo, S.ev[0], 0);
     if (e != cudaSuccess) return (int)e;
+    // (pgate / bgate: host-streamed input, see InputGate -- the potrf reads
+    // A's column chunks, the trsm B's chunks as the copy engine flags them)
     int* psync = nullptr;
-    int rc = potrf_panel_tiles(Ctx{S.hi, c.info}, A, A.m, 0, W, &psync);
+    int rc;
+    {
+      InputGate g(pgate, 0);
+      rc = potrf_panel_tiles(Ctx{S.hi, c.info}, A, A.m, 0, W, &psync);
+    }
     const int nt = (int)((A.m + TP - 1) / TP);
-    if (!rc)
+    if (!rc) {
+      InputGate g(bgate, bgate_mode);
       rc = trsm_tiles(Ctx{S.lo, c.info}, true, conj, A, B, (const T*)W, false,
                       psync + SYNC_HDR, nt + 1, psync + 1);
+    }
     // join both streams back into the caller's (also on the error paths)
     cudaEventRecord(S.ev[1], S.hi);
     cudaEventRecord(S.ev[2], S.lo);
@@ -1686,8 +1695,9 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B) {
     return rc;
   }
 }
-template int potrf_trsm_overlap<double>(Ctx, View<double>, double*, bool, View<double>);
-template int potrf_trsm_overlap<Z>(Ctx, View<Z>, Z*, bool, View<Z>);
+template int potrf_trsm_overlap<double>(Ctx, View<double>, double*, bool, View<double>,
+                                        const int*, const int*, int);
+template int potrf_trsm_overlap<Z>(Ctx, View<Z>, Z*, bool, View<Z>, const int*, const int*, int);
 
 template int potrf_panel_tiles<double>(Ctx, View<double>, i64, int, double*, int**);
 template int potrf_panel_tiles<Z>(Ctx, View<Z>, i64, int, Z*, int**);
