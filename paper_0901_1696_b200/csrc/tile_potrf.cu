@@ -814,6 +814,11 @@ struct TrsmArgs {
   const int* agate;
   int agate_stride;
   const int* aabort;
+  // dispatch guard: a CTA at blockIdx >= aguard_keep that finds *aguard == 0
+  // (the producer has not started) exits at once, so a solve whose CTAs got
+  // dispatched first can never hold every slot the producer needs
+  const int* aguard;
+  int aguard_keep;
 };
 
 template <typename T, bool AK, bool BKM, int TN>
@@ -1078,6 +1083,11 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   __shared__ int s_task, s_ok;
   if (info && *info) return;
   if (threadIdx.x == 0) s_ok = 1;  // cleared only by a failed triangle gate
+  if (a.aguard && (int)blockIdx.x >= a.aguard_keep) {
+    if (threadIdx.x == 0) s_task = ld_relaxed(a.aguard);
+    __syncthreads();
+    if (s_task == 0) return;
+  }
   int* counter = sync;
   int* done = sync + SYNC_HDR;
   const long long total = (long long)a.nb * a.nc;
@@ -1549,6 +1559,8 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.agate = agate;
   a.agate_stride = agate_stride;
   a.aabort = aabort;
+  a.aguard = agate ? aabort - 1 : nullptr;  // the producer's task counter (sync[0])
+  a.aguard_keep = num_sms();
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
@@ -1591,6 +1603,8 @@ template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, con
 template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool, const int*, int,
                            const int*);
 
+size_t potrf_sync_ints(int nt, int mt) { return SYNC_HDR + (size_t)mt * nt + nt; }
+
 // Factor the tall lower panel P (m x n, m >= n, col- or row-major): the
 // Cholesky of its leading n x n block and the solve of the rows below it,
 // P = [L11; L21] with L21 = P21 L11^-H, in one dataflow launch.  m == n is
@@ -1605,16 +1619,21 @@ int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) 
   const int nt = (int)((n + TP - 1) / TP), mt = (int)((m + TP - 1) / TP);
   // the row tiles must break at n: the rows below are off-diagonal tiles
   if (mt > nt && n % TP) return -100;
-  const size_t ints = SYNC_HDR + (size_t)mt * nt + nt;  // + the partial-ready flags
-  int* sync = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
-  if (e != cudaSuccess) return (int)e;
-  if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  const size_t ints = potrf_sync_ints(nt, mt);
+  int* sync = keep_sync ? *keep_sync : nullptr;  // a caller-provided, zeroed array
+  if (!sync) {
+    cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
+    if (e != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  }
   int rc = km ? tile_launch<T, true>(P, (int)n, W, c, base, sync, nt, mt)
               : tile_launch<T, false>(P, (int)n, W, c, base, sync, nt, mt);
   // keep_sync: the caller gates a concurrent kernel on the done flags
-  // (done(i, j) at sync + SYNC_HDR + i * nt + j; abort at sync + 1) and
-  // frees the array once that kernel is ordered after it
+  // (done(i, j) at sync + SYNC_HDR + i * nt + j; abort at sync + 1; the task
+  // counter at sync[0] is nonzero once a CTA has started) and frees the array
+  // once that kernel is ordered after it.  *keep_sync non-null on entry: the
+  // caller allocated and zeroed the array (potrf_sync_ints) on a stream both
+  // kernels are ordered after.
   if (keep_sync) *keep_sync = sync;
   else cudaFreeAsync(sync, c.st);
   return rc;
@@ -1647,9 +1666,14 @@ OverlapStreams& overlap_streams() {
 // potrf's diagonal flag of its row block (done(i, i): row block i of L and
 // W_i published).  The solve's first row blocks then run beside the
 // factorization's chain instead of after it.  Deadlock-free: the potrf never
-// waits on the solve, its CTAs are dispatched first (launched first, higher
-// priority), and a failing potrf raises its abort flag, on which every
-// waiting trsm task exits.
+// waits on the solve and its CTAs are normally dispatched first (launched
+// first, higher priority); should the solve's CTAs still reach the SMs first,
+// every one beyond the first num_sms() exits at once while the potrf's task
+// counter reads zero (TrsmArgs::aguard), so at most one SM's worth of waiting
+// solve CTAs can be resident before the potrf runs.  A failing potrf raises
+// its abort flag, on which every waiting trsm task exits.  The potrf's flag
+// array is zeroed on the caller's stream before the fork (pool memory may
+// hold an earlier run's flags).
 template <typename T>
 int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* pgate,
                        const int* bgate, int bgate_mode) {
@@ -1661,26 +1685,41 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* 
       return v && std::atoi(v) != 0;
     }();
     if (off || A.m <= TP || B.empty() || !W) return -100;
-    if (A.rs != 1 || !(B.rs == 1 || B.cs == 1)) return -100;
+    // row-major B only: the column-major-B trsm variants take ~250 registers
+    // and do not fit beside two potrf CTAs on an SM (UPLO='U' at n = 12000:
+    // 11.18 ms overlapped vs 10.9 in sequence)
+    if (A.rs != 1 || B.cs != 1 || B.rs == 1) return -100;
     // not under graph capture: captured kernel nodes lose the stream
     // priorities the dispatch order relies on
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(c.st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
       return -100;
     OverlapStreams& S = overlap_streams();
-    cudaError_t e = cudaEventRecord(S.ev[0], c.st);
+    // the potrf's flag array, zeroed on the caller's stream BEFORE the fork:
+    // the trsm reads it from its first task on
+    const int nt = (int)((A.m + TP - 1) / TP);
+    const size_t ints = potrf_sync_ints(nt, nt);
+    int* psync = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&psync, ints * sizeof(int), c.st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(psync, 0, ints * sizeof(int), c.st);
+    if (e != cudaSuccess) {
+      if (psync) cudaFreeAsync(psync, c.st);
+      return (int)e;
+    }
+    e = cudaEventRecord(S.ev[0], c.st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.hi, S.ev[0], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.lo, S.ev[0], 0);
-    if (e != cudaSuccess) return (int)e;
+    if (e != cudaSuccess) {
+      cudaFreeAsync(psync, c.st);
+      return (int)e;
+    }
     // (pgate / bgate: host-streamed input, see InputGate -- the potrf reads
     // A's column chunks, the trsm B's chunks as the copy engine flags them)
-    int* psync = nullptr;
     int rc;
     {
       InputGate g(pgate, 0);
       rc = potrf_panel_tiles(Ctx{S.hi, c.info}, A, A.m, 0, W, &psync);
     }
-    const int nt = (int)((A.m + TP - 1) / TP);
     if (!rc) {
       InputGate g(bgate, bgate_mode);
       rc = trsm_tiles(Ctx{S.lo, c.info}, true, conj, A, B, (const T*)W, false,
@@ -1691,7 +1730,7 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* 
     cudaEventRecord(S.ev[2], S.lo);
     cudaStreamWaitEvent(c.st, S.ev[1], 0);
     cudaStreamWaitEvent(c.st, S.ev[2], 0);
-    if (psync) cudaFreeAsync(psync, c.st);
+    cudaFreeAsync(psync, c.st);
     return rc;
   }
 }
