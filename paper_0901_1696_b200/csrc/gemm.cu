@@ -251,7 +251,20 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
   if (g.skip && *g.skip) return;
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int tm, tn;
-    if (MODE == TRI_FULL) { tm = (int)(t % g.tiles_m); tn = (int)(t / g.tiles_m); }
+    if (MODE == TRI_FULL) {
+      if (g.band > 0) {  // bands of g.band tile rows, column by column inside a band
+        const int tiles_n = (g.N + BN - 1) / BN;
+        const long long per = (long long)g.band * tiles_n;
+        const int b = (int)(t / per), r0 = b * g.band;
+        const int h = g.tiles_m - r0 < g.band ? g.tiles_m - r0 : g.band;
+        const long long o = t - (long long)b * per;
+        tn = (int)(o / h);
+        tm = r0 + (int)(o % h);
+      } else {
+        tm = (int)(t % g.tiles_m);
+        tn = (int)(t / g.tiles_m);
+      }
+    }
     else if constexpr (BM == BN) {
       if (g.band > 0) tri_tile_banded(MODE, t, g.tiles_m, g.band, tm, tn);
       else tri_tile(MODE, t, tm, tn);
@@ -398,7 +411,15 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
     const char* v = std::getenv("RFPK_TRI_BAND");
     return v ? std::atoi(v) : 24;
   }();
-  g.band = band;
+  static const int full_band = [] {
+    const char* v = std::getenv("RFPK_FULL_BAND");
+    return v ? std::atoi(v) : 24;
+  }();
+  // full products: banded only when C is narrow (few column tiles, e.g.
+  // pftrs's 8192 x 1024 gemms: 32.0 -> 33.0 TFLOP/s, A streamed from DRAM once
+  // instead of once per resident column group); square products keep the
+  // column-major order (8192^3: 33.9 vs 33.5 TFLOP/s banded)
+  g.band = MODE == TRI_FULL ? (tn <= 32 ? full_band : 0) : band;
   if (MODE == TRI_FULL) {
     g.ntiles = (long long)tm * tn;
   } else if (BM == BN) {
