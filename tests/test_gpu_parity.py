@@ -833,3 +833,33 @@ def test_pfsv_device_matches_pftrf_pftrs(P, monkeypatch, uplo, transr, n, cplx):
         assert rfp.pfsv(rb, b2) == want > 0
         assert rb.state is conv.FactorState.UNFACTORED
         assert torch.equal(b2.cpu(), torch.from_numpy(np.asfortranarray(bh)))
+
+
+@pytest.mark.parametrize("uplo,transr,cplx", [("L", "N", False), ("U", "T", True), ("U", "N", False)])
+def test_banded_triangular_gemm_orders(P, uplo, transr, cplx):
+    """sfrk_hfrk (SYRK/HERK on T1 and T2 + GEMM on S1) at n = 3300, where each
+    triangle spans 26 tile rows -- two bands of the banded tile order, the
+    second partial -- against the oracle; then pftrf (SYRK of T2 in the same
+    order) and pftrs(300) (narrow full GEMMs in their banded order)."""
+    conv, rfp = P.convert, P.rfp
+    n, k = 3300, 40
+    a = O.spd_matrix(n, 17, "n", complex_=cplx)
+    buf = O.trttf(a, uplo, transr)
+    g = np.random.default_rng(5)
+    ga = np.asfortranarray(g.standard_normal((n, k)) + (1j * g.standard_normal((n, k)) if cplx else 0))
+    co = buf.copy()
+    O.sfrk_hfrk(co, n, uplo, transr, "N", k, 2.0, ga, -0.5, cplx)
+    c = conv.RfpTriangle(buf.copy(), P.layout.make_descriptor(n, uplo, transr))
+    rfp.sfrk_hfrk(transr, uplo, "N", n, k, 2.0, ga, -0.5, c)
+    assert rel(c.data, co) <= TOL
+    f = buf.copy()
+    assert O.pftrf(f, n, uplo, transr) == 0
+    r = conv.trttf(a, uplo, transr)
+    assert rfp.pftrf(r) == 0
+    assert rel(r.data, f) <= TOL
+    bh = g.standard_normal((n, 300)) + (1j * g.standard_normal((n, 300)) if cplx else 0)
+    xo = np.asfortranarray(bh.copy())
+    O.pftrs(f, n, uplo, transr, xo)
+    x = torch.from_numpy(np.asfortranarray(bh)).cuda()
+    rfp.pftrs(r, x)
+    assert rel(x, xo) <= TOL
