@@ -819,6 +819,7 @@ struct TrsmArgs {
   // dispatched first can never hold every slot the producer needs
   const int* aguard;
   int aguard_keep;
+  int scan;  // scan-ahead chunk waits (see trsm_task's open_chunk)
 };
 
 template <typename T, bool AK, bool BKM, int TN>
@@ -851,6 +852,8 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   T* Bs = sm + STAGES * LA::SIZE;
   const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
   const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
+  const bool scan_ahead = a.scan != 0;
+  __shared__ int s_ready_sh;
   constexpr bool PREW = trsm_prew<T, BKM>();
   constexpr int PIPE = STAGES * (LA::SIZE + LB::SIZE);
   constexpr int STILE = (TN > TP ? TN : TP) * LD64;  // the S tile (64 x TN, LD64 columns)
@@ -881,10 +884,39 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
         for (int r = 0; r < 4; ++r) acc[q][mi][ni][r] = 0.0;
 
   int kvalid = TP;  // valid k of the chunk being loaded
-  // wait for X(kk, c) and point the loaders at chunk kk
+  // chunks q < ready (in solve order) are known published: a chunk beyond
+  // waits for its flag with acquire polls (the chain's critical wait), then
+  // warp 0 scans ahead 32 flags per round trip and one acquire fence covers
+  // every further chunk found published -- one barrier for the long run of
+  // chunks solved well before this task instead of one per chunk
+  int ready = 0;
   auto open_chunk = [&](int kk) -> bool {
-    if (tid == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
-    __syncthreads();
+    const int q = a.lower ? kk : a.nb - 1 - kk;  // position in solve order
+    if (!scan_ahead) {
+      if (tid == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
+      __syncthreads();
+    } else if (q >= ready) {
+      if (warp == 0) {
+        if (lane == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
+        __syncwarp();
+        int rr = q + 1;
+        for (;;) {
+          const int qq = rr + lane;
+          const int k2 = a.lower ? qq : a.nb - 1 - qq;
+          const bool ok = qq < nprev && ld_relaxed(done + (i64)k2 * a.nc + c);
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (m == 0xffffffffu) { rr += 32; continue; }
+          rr += __ffs(~m) - 1;
+          break;
+        }
+        if (lane == 0) {
+          if (rr > q + 1) fence_acquire();
+          s_ready_sh = rr;
+        }
+      }
+      __syncthreads();
+      ready = s_ready_sh;
+    }
     const T* ta = AK ? Tm.p + (i64)kk * TP : Tm.p + (i64)kk * TP * Tm.cs;
     la.init(ta, lda, i * TP, a.n, tid);
     const T* tb = BKM ? B.p + (i64)kk * TP : B.p + (i64)kk * TP * B.rs;
@@ -1561,6 +1593,11 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.aabort = aabort;
   a.aguard = agate ? aabort - 1 : nullptr;  // the producer's task counter (sync[0])
   a.aguard_keep = num_sms();
+  static const int scan = [] {
+    const char* v = std::getenv("RFPK_TRSM_SCAN");
+    return v ? std::atoi(v) : 1;
+  }();
+  a.scan = scan;
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
