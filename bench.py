@@ -577,7 +577,7 @@ def run_c4(args, rank, world, local):
     def e2e_step():
         # one public call: the chunked host pipeline (copies in and out
         # overlapped with the fused kernel; rfp.pftrf_pftrs_batched_from_host)
-        _, inf = rfp.pftrf_pftrs_batched_from_host(host_arf, host_b.transpose(1, 2), n, "U", "N",
+        _, inf = rfp.pftrf_pftrs_batched_from_host(host_arf, "N", "U", n, host_b.transpose(1, 2),
                                                    out=out_b.transpose(1, 2))
         torch.cuda.current_stream().synchronize()
         return inf

@@ -458,9 +458,11 @@ def _batched_rhs(b, desc, batch):
     return bv, work, ldb
 
 
-def pftrf_batched(arf: torch.Tensor, n: int, uplo: str = "U", transr: str = "N") -> torch.Tensor:
-    """pftrf on ``batch`` independent RFP buffers (rows of ``arf``), in place.
-    Returns the per-matrix info as an int32 CUDA tensor (no host sync)."""
+def pftrf_batched(arf: torch.Tensor, transr: str, uplo: str, n: int) -> torch.Tensor:
+    """pftrf on ``batch`` independent RFP buffers (rows of ``arf``), in place,
+    LAPACK argument order (``pftrf_batched(arf[batch, nt],
+    transr, uplo, n) -> info[batch]``).  Returns the per-matrix info as an
+    int32 CUDA tensor (no host sync)."""
     desc = _batched_args(arf, n, uplo, transr)
     batch = arf.shape[0]
     info = torch.empty(batch, dtype=torch.int32, device=arf.device)
@@ -469,8 +471,7 @@ def pftrf_batched(arf: torch.Tensor, n: int, uplo: str = "U", transr: str = "N")
     return info
 
 
-def pftrs_batched(arf: torch.Tensor, b: torch.Tensor, n: int, uplo: str = "U",
-                  transr: str = "N") -> None:
+def pftrs_batched(arf: torch.Tensor, transr: str, uplo: str, n: int, b: torch.Tensor) -> None:
     """pftrs for each factor ``arf[k]`` against ``b[k]`` ((batch, n) or
     (batch, n, nrhs)), in place on ``b``."""
     desc = _batched_args(arf, n, uplo, transr)
@@ -484,8 +485,8 @@ def pftrs_batched(arf: torch.Tensor, b: torch.Tensor, n: int, uplo: str = "U",
         bv.copy_(work)
 
 
-def pftrf_pftrs_batched(arf: torch.Tensor, b: torch.Tensor, n: int, uplo: str = "U",
-                        transr: str = "N") -> torch.Tensor:
+def pftrf_pftrs_batched(arf: torch.Tensor, transr: str, uplo: str, n: int,
+                        b: torch.Tensor) -> torch.Tensor:
     """Fused pftrf + pftrs over a batch (one HBM pass per matrix)."""
     desc = _batched_args(arf, n, uplo, transr)
     batch = arf.shape[0]
@@ -499,9 +500,8 @@ def pftrf_pftrs_batched(arf: torch.Tensor, b: torch.Tensor, n: int, uplo: str = 
     return info
 
 
-def pftrf_pftrs_batched_from_host(host_arf: torch.Tensor, host_b: torch.Tensor, n: int,
-                                  uplo: str = "U", transr: str = "N", out=None,
-                                  chunk: int = 4096):
+def pftrf_pftrs_batched_from_host(host_arf: torch.Tensor, transr: str, uplo: str, n: int,
+                                  host_b: torch.Tensor, out=None, chunk: int = 4096):
     """:func:`pftrf_pftrs_batched` for a batch that sits in (pinned) host
     memory, pipelined in chunks of ``chunk`` matrices over three streams: the
     host->device copy of chunk k+1 and the device->host copy of chunk k-1's
@@ -542,7 +542,7 @@ def pftrf_pftrs_batched_from_host(host_arf: torch.Tensor, host_b: torch.Tensor, 
             d_b[k0:k1].copy_(hb[k0:k1], non_blocking=True)
         main.wait_stream(s_in)
         with torch.cuda.stream(main):
-            infos.append(pftrf_pftrs_batched(d_arf[k0:k1], d_b[k0:k1], n, uplo, transr))
+            infos.append(pftrf_pftrs_batched(d_arf[k0:k1], transr, uplo, n, d_b[k0:k1]))
         s_out.wait_stream(main)
         with torch.cuda.stream(s_out):
             ho[k0:k1].copy_(d_b[k0:k1], non_blocking=True)

@@ -188,18 +188,18 @@ def test_batched_vs_oracle(P):
         arf = torch.from_numpy(np.stack(bufs)).cuda()
         arf2 = arf.clone()
         bt = torch.from_numpy(np.stack([b.T for b in bs])).cuda().transpose(1, 2)[:, :, :nrhs]
-        info = rfp.pftrf_pftrs_batched(arf, bt, n, uplo, transr)
+        info = rfp.pftrf_pftrs_batched(arf, transr, uplo, n, bt)
         assert int(info.abs().sum()) == 0
         assert rel(arf, np.stack(facs)) <= TOL
         if nrhs:
             assert rel(bt, np.stack(xs)[:, :, :nrhs]) <= TOL
         # unfused
-        info2 = rfp.pftrf_batched(arf2, n, uplo, transr)
+        info2 = rfp.pftrf_batched(arf2, transr, uplo, n)
         assert int(info2.abs().sum()) == 0
         assert rel(arf2, np.stack(facs)) <= TOL
         if nrhs:
             b2 = torch.from_numpy(np.stack(bs)).cuda()[:, :, :nrhs].contiguous()
-            rfp.pftrs_batched(arf2, b2, n, uplo, transr)
+            rfp.pftrs_batched(arf2, transr, uplo, n, b2)
             assert rel(b2, np.stack(xs)[:, :, :nrhs]) <= TOL
 
 
@@ -220,7 +220,7 @@ def test_batched_failure_info(P, uplo, transr):
         want.append(O.pftrf(buf.copy(), n, uplo, transr))
         bufs.append(buf)
     arf = torch.from_numpy(np.stack(bufs)).cuda()
-    info = rfp.pftrf_batched(arf, n, uplo, transr)
+    info = rfp.pftrf_batched(arf, transr, uplo, n)
     assert info.cpu().tolist() == want
     assert any(0 < w <= 32 for w in want) and any(w > 32 for w in want)
 
@@ -655,11 +655,11 @@ def test_batched_from_host_pipelined(P, nrhs):
     else:
         host_b = torch.from_numpy(g.standard_normal((batch, n))).pin_memory()
         out = torch.empty_like(host_b).pin_memory()
-    d_arf, info = rfp.pftrf_pftrs_batched_from_host(host_arf, host_b, n, "U", "N", out=out, chunk=10)
+    d_arf, info = rfp.pftrf_pftrs_batched_from_host(host_arf, "N", "U", n, host_b, out=out, chunk=10)
     torch.cuda.synchronize()
     ref_arf = host_arf.cuda()
     ref_b = host_b.cuda()
-    ref_info = rfp.pftrf_pftrs_batched(ref_arf, ref_b, n, "U", "N")
+    ref_info = rfp.pftrf_pftrs_batched(ref_arf, "N", "U", n, ref_b)
     assert torch.equal(info, ref_info) and int(info.abs().sum()) == 0
     assert torch.equal(d_arf, ref_arf)
     assert torch.equal(out, ref_b.cpu())
