@@ -49,9 +49,19 @@ int rfpk_device_sms(void);
    kernels replayed from a cached CUDA graph are counted per replay) */
 long long rfpk_launch_count(void);
 /* pftrf/pftrs/tftri/pftri calls are captured into CUDA graphs keyed by their
-   full argument tuple (pointers included) and replayed on repeat calls;
-   RFPK_GRAPHS=0 disables.  This drops every cached graph. */
+   full argument tuple (pointers included) and replayed on repeat calls
+   (tuning "graphs" = 0 disables).  This drops every cached graph. */
 int rfpk_graph_cache_clear(void);
+/* Path thresholds (process-wide; there are no environment knobs).  Names and
+   defaults: "oop_max" 4096, "t2_copy_min" 2048, "panel_max" 4096,
+   "pfsv_overlap_min" 512, "overlap" 1, "graphs" 1, "graph_max_n" 8192,
+   "gemm_wide" 0, "batched_generic" 0, "trace" 0.
+   Setting a value drops every cached graph.  Returns 0, or -1 for an
+   unknown name.  Not meant to be changed while other threads are inside
+   the library. */
+int rfpk_set_tuning(const char* name, long long value);
+int rfpk_get_tuning(const char* name, long long* value);
+int rfpk_reset_tuning(void);
 
 /* conversions: verbatim copies, bit-exact (convert.py:156-275) ----------- */
 /* replaces convert.trttf(a, uplo, transr)   convert.py:156-186 */
@@ -147,6 +157,10 @@ int rfpk_zpftri(char transr, char uplo, int64_t n, void* arf, int* info, rfpk_st
    the label was never seen. */
 int rfpk_phase_clock(int enable);
 int rfpk_phase_time(const char* label, double* total_ms, int64_t* count);
+/* every label the clock has seen since it was enabled, newline-separated, into
+   out[cap] (truncated, NUL-terminated); returns the length needed incl. NUL.
+   Kernel launches appear as "kernel <name> <dims>" (see KernelClock) */
+int64_t rfpk_phase_labels(char* out, int64_t cap);
 
 /* packed Cholesky ------------------------------------ */
 /* replaces packed.pptrf_ref(p)   packed.py:70-108 -- in place on the

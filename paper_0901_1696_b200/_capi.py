@@ -28,6 +28,9 @@ SIGNATURES = {
     "rfpk_device_sms": ([], _int),
     "rfpk_launch_count": ([], ctypes.c_longlong),
     "rfpk_graph_cache_clear": ([], _int),
+    "rfpk_set_tuning": ([ctypes.c_char_p, ctypes.c_longlong], _int),
+    "rfpk_get_tuning": ([ctypes.c_char_p, _p], _int),
+    "rfpk_reset_tuning": ([], _int),
     "rfpk_dtrttf": ([_c, _c, _i64, _p, _i64, _p, _p], _int),
     "rfpk_ztrttf": ([_c, _c, _i64, _p, _i64, _p, _p], _int),
     "rfpk_dtfttr": ([_c, _c, _i64, _p, _p, _i64, _p], _int),
@@ -58,6 +61,7 @@ SIGNATURES = {
     "rfpk_zpfsv_host": ([_c, _c, _i64, _i64, _p, _p, _p, _p, _p, _i64, _p, _p], _int),
     "rfpk_phase_clock": ([_int], _int),
     "rfpk_phase_time": ([ctypes.c_char_p, _p, _p], _int),
+    "rfpk_phase_labels": ([_p, _i64], _i64),
     "rfpk_dpptrf": ([_c, _i64, _p, _p, _p], _int),
     "rfpk_zpptrf": ([_c, _i64, _p, _p, _p], _int),
     "rfpk_dpptrs": ([_c, _i64, _i64, _p, _p, _i64, _i64, _p, _p], _int),
@@ -119,6 +123,76 @@ def lib() -> ctypes.CDLL:
 
 def stream_handle(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class phase_clock:
+    """Context manager around the library's phase clock (rfpk_phase_clock):
+    CUDA event pairs on the launching streams around every SRPA step and
+    every library kernel launch (direct calls; graph replays are not
+    traced).  ``table()`` -> {label: (total_ms, count)} after the block."""
+
+    def __enter__(self):
+        load_library().rfpk_phase_clock(1)
+        self._table = None
+        return self
+
+    def __exit__(self, *exc):
+        self._table = self.table()
+        load_library().rfpk_phase_clock(0)
+        return False
+
+    def table(self):
+        if self._table is not None:
+            return self._table
+        lib = load_library()
+        need = lib.rfpk_phase_labels(None, 0)
+        buf = ctypes.create_string_buffer(int(need))
+        lib.rfpk_phase_labels(buf, need)
+        out = {}
+        for lab in buf.value.decode().splitlines():
+            ms, cnt = ctypes.c_double(0.0), ctypes.c_int64(0)
+            lib.rfpk_phase_time(lab.encode(), ctypes.byref(ms), ctypes.byref(cnt))
+            out[lab] = (float(ms.value), int(cnt.value))
+        return out
+
+
+TUNING_DEFAULTS = {"oop_max": 4096, "t2_copy_min": 2048, "panel_max": 4096,
+                   "pfsv_overlap_min": 512, "overlap": 1, "graphs": 1, "graph_max_n": 8192,
+                   "gemm_wide": 0, "batched_generic": 0, "trace": 0}
+
+
+def set_tuning(name: str, value: int) -> None:
+    """Set one of the library's path thresholds (rfpk_set_tuning; see
+    include/rfpk_b200.h).  Drops every cached CUDA graph."""
+    if load_library().rfpk_set_tuning(name.encode(), int(value)) != 0:
+        raise KeyError(f"unknown tuning knob {name!r}")
+
+
+def get_tuning(name: str) -> int:
+    v = ctypes.c_longlong(0)
+    if load_library().rfpk_get_tuning(name.encode(), ctypes.byref(v)) != 0:
+        raise KeyError(f"unknown tuning knob {name!r}")
+    return int(v.value)
+
+
+class tuning:
+    """Context manager: ``with tuning(panel_max=256): ...`` sets knobs and
+    restores their previous values on exit."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.knobs.items():
+            self.saved[k] = get_tuning(k)
+            set_tuning(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_tuning(k, v)
+        return False
 
 
 def flag(ch: str) -> bytes:

@@ -272,7 +272,7 @@ int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, i
                      cudaStream_t st) {
   const size_t sm = B64_SMEM_DOUBLES * sizeof(double);
   auto launch = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kernel_setup(kern, 32, sm);
     kern<<<(unsigned)batch, 32, sm, st>>>(arf, stride_arf, nrhs, b, ldb, stride_b, info);
   };
   auto pick = [&](auto lower_tag, auto trans_tag) {
@@ -286,6 +286,7 @@ int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, i
   using Tr = std::true_type;
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
+  KernelClock kc(st);
   if (r.lower) {
     if (r.trans) pick(Tr{}, I1{});
     else pick(Tr{}, I0{});
@@ -294,6 +295,7 @@ int batched64_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, i
     else pick(F{}, I0{});
   }
   RFPK_CHECK_LAUNCH();
+  kc.stop("batched64", batch, nrhs);
   return 0;
 }
 
@@ -303,7 +305,7 @@ int batched_launch(const RfpDesc& r, double* arf, i64 stride_arf, i64 batch, int
   cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int) * batch, st);
   if (e != cudaSuccess) return (int)e;
   if (r.n == 0) return 0;
-  if (r.n == 64 && !(std::getenv("RFPK_BATCHED_GENERIC")))
+  if (r.n == 64 && !tune(TK_BATCHED_GENERIC))
     return batched64_launch(r, arf, stride_arf, batch, nrhs, b, ldb, stride_b, info, factor, solve,
                             st);
   batched_kernel<128><<<(unsigned)batch, 128, 0, st>>>(r, arf, stride_arf, nrhs, b, ldb, stride_b,
@@ -332,6 +334,7 @@ extern "C" {
 
 int rfpk_dpftrf_batched(char transr, char uplo, int64_t n, double* arf, int64_t stride_arf,
                         int64_t batch, int* info, rfpk_stream_t s) {
+  StreamDevice dg_(s);
   if (int rc = check(transr, uplo, n)) return rc;
   if (stride_arf < n * (n + 1) / 2) return -5;
   if (batch < 0) return -6;
@@ -343,6 +346,7 @@ int rfpk_dpftrf_batched(char transr, char uplo, int64_t n, double* arf, int64_t 
 int rfpk_dpftrs_batched(char transr, char uplo, int64_t n, int64_t nrhs, const double* arf,
                         int64_t stride_arf, double* b, int64_t ldb, int64_t stride_b,
                         int64_t batch, int* info, rfpk_stream_t s) {
+  StreamDevice dg_(s);
   if (int rc = check(transr, uplo, n)) return rc;
   if (nrhs < 0) return -4;
   if (stride_arf < n * (n + 1) / 2) return -6;
@@ -357,6 +361,7 @@ int rfpk_dpftrs_batched(char transr, char uplo, int64_t n, int64_t nrhs, const d
 int rfpk_dpftrf_pftrs_batched(char transr, char uplo, int64_t n, int64_t nrhs, double* arf,
                               int64_t stride_arf, double* b, int64_t ldb, int64_t stride_b,
                               int64_t batch, int* info, rfpk_stream_t s) {
+  StreamDevice dg_(s);
   if (int rc = check(transr, uplo, n)) return rc;
   if (nrhs < 0) return -4;
   if (stride_arf < n * (n + 1) / 2) return -6;

@@ -24,10 +24,6 @@
 
 namespace rfpk {
 
-static i64 env_int(const char* name, i64 dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoll(v) : dflt;
-}
 
 // ============================================================ leaf kernels
 
@@ -180,8 +176,7 @@ template <typename T> size_t leaf_smem(int tiles) {
 }
 
 template <typename K> void allow_smem(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)bytes);
+  kernel_setup(kern, 128, bytes);  // per device, once
 }
 
 // Recursive split: n1 is a multiple of 64 (128 for large n), so every leaf
@@ -210,12 +205,11 @@ template <typename T> size_t leaf_ws_elems(i64 n) { return (size_t)((n + 63) / 6
 // The device's default memory pool keeps freed blocks (release threshold =
 // max), so the per-call workspace is a cheap stream-ordered suballocation.
 static void keep_pool_memory() {
-  static bool done = false;
-  if (done) return;
-  done = true;
-  int dev = 0;
+  static std::atomic<bool> done[MAX_DEVICES];
+  const int dev = cur_device();
+  if (done[dev & (MAX_DEVICES - 1)].exchange(true)) return;
   cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
@@ -296,13 +290,7 @@ template <typename T> int ws_matrix(Ctx c, i64 m, i64 n, View<T>& v, bool rowmaj
 }
 template <typename T> bool is_rowmajor(const View<T>& v) { return v.rs != 1 && v.cs == 1; }
 
-inline i64 oop_max() {
-  static const i64 v = [] {
-    const char* s = std::getenv("RFPK_OOP_MAX");
-    return s ? std::atoll(s) : (i64)4096;
-  }();
-  return v;
-}
+inline i64 oop_max() { return tune(TK_OOP_MAX); }
 
 template <typename T> int leaf_inverses(Ctx c, View<T> L, bool unit, T* W) {
   if (L.m == 0) return 0;
@@ -321,19 +309,26 @@ template <typename T> int leaf_inverses(Ctx c, View<T> L, bool unit, T* W) {
 // depth) so it overlaps the latency-bound factorization of the next diagonal
 // block.  Fork/join are event record/wait, which also work under CUDA-graph
 // stream capture (the forked streams join the capture).
+// Per host thread and device (thread_local): two threads never record or
+// wait on each other's events, and their look-ahead forks never share a
+// stream -- the library is re-entrant for callers on distinct streams.
 struct LaStreams {
   cudaStream_t hi = nullptr;
   cudaStream_t side[24] = {};
   cudaEvent_t ev[128] = {};
   int next = 0;
   bool ok = false;
+  ~LaStreams() {  // thread exit (errors after runtime teardown are ignored)
+    if (!ok) return;
+    cudaStreamDestroy(hi);
+    for (auto x : side) cudaStreamDestroy(x);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
 };
 
 static LaStreams& la_streams() {
-  static LaStreams s[16];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  LaStreams& L = s[dev & 15];
+  static thread_local LaStreams s[MAX_DEVICES];
+  LaStreams& L = s[cur_device() & (MAX_DEVICES - 1)];
   if (!L.ok) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -507,12 +502,10 @@ int trsm_left(Ctx c, bool lower, bool conj, bool unit, T alpha, View<T> Tm, View
   // CTA per SM, where the recursive GEMM form measured faster: 65 vs 78 ms on
   // config 5's S1 solve at n = 16000)
   // (narrow right-hand sides run 64 x 16 tiles, which win from two tiles up)
-  static const i64 tile_min = env_int("RFPK_TILE_TRSM_MIN", 512);
-  static const i64 tile_min_narrow = env_int("RFPK_TILE_TRSM_MIN_NARROW", 128);
-  static const i64 narrow = env_int("RFPK_TRSM_NARROW", 256);
+  constexpr i64 tile_min = 512, tile_min_narrow = 128, narrow = 256;
   const i64 tasks64 = ((Tm.m + 63) / 64) * ((B.n + 63) / 64);
   const i64 tmin = (B.n <= narrow || tasks64 <= 10 * (i64)num_sms()) ? tile_min_narrow : tile_min;
-  if (!is_cplx<T>::value && Tm.m >= tmin && !std::getenv("RFPK_NO_TILE_TRSM") &&
+  if (!is_cplx<T>::value && Tm.m >= tmin &&
       (rc = trsm_tiles(c, lower, conj, Tm, B, (const T*)W, !lower)) != -100) {
     ws_free(own, c.st);
     return rc;
@@ -634,11 +627,10 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
 }
 
 
-static const i64 TILE_MAX = env_int("RFPK_TILE_MAX", (i64)1 << 40);  // measured: the tile kernel wins at every n
-
 template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
-  // the dataflow tile kernel (tile_potrf.cu) wherever the critical path rules
-  if (A.m > LEAF && A.m <= TILE_MAX && W && !std::getenv("RFPK_NO_TILE"))
+  // the dataflow tile kernel (tile_potrf.cu) at every order above one leaf
+  // (measured faster than the recursion everywhere)
+  if (A.m > LEAF && W)
     return potrf_tiles(c, A, base, W);
   // (fallback / n <= 64: the recursive driver with look-ahead streams)
   if (A.m < LA_MIN) return potrf_node(c, A, base, W, 0);
@@ -704,8 +696,7 @@ template <typename T> int trtri_lower_rec(Ctx c, bool unit, View<T> A) {
 
 template <typename T> int trtri_lower(Ctx c, bool unit, View<T> A) {
   if (A.m == 0) return 0;
-  static const bool cplx_oop = env_int("RFPK_TRTRI_OOP_CPLX", 1) != 0;
-  if (A.m > LEAF && (!is_cplx<T>::value || cplx_oop)) return trtri_hyb(c, unit, A);
+  if (A.m > LEAF) return trtri_hyb(c, unit, A);
   return trtri_lower_rec(c, unit, A);
 }
 

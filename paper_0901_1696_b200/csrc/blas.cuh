@@ -68,10 +68,12 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
                const int* agate = nullptr, int agate_stride = 0, const int* aabort = nullptr);
 // per-device streams for concurrent launches: hi = greatest priority (the
 // critical-path kernel), lo = least; ev = scratch fork/join events
+// Per host thread and device (thread_local; see tile_potrf.cu)
 struct OverlapStreams {
   cudaStream_t hi = nullptr, lo = nullptr;
   cudaEvent_t ev[6] = {};
   bool ok = false;
+  ~OverlapStreams();
 };
 OverlapStreams& overlap_streams();
 // potrf('L', T) -> trsm with T's factor, overlapped: the tile potrf on the
@@ -81,11 +83,6 @@ OverlapStreams& overlap_streams();
 template <typename T>
 int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* pgate = nullptr,
                        const int* bgate = nullptr, int bgate_mode = 0);
-// one pftrs sweep through both RFP triangles in one launch (real):
-// op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0; lower = forward sweep, else
-// both triangles upper (W transposed); -100 = not supported (fall back)
-int trsm2_tiles(Ctx c, bool lower, View<double> Ta, View<double> B0, const double* Wa,
-                View<double> Tb, View<double> B1, const double* Wb, View<double> P);
 // stream-ordered workspace for leaf inverses of an order-n triangle
 template <typename T> int ws_alloc(T** p, i64 n, cudaStream_t st);
 template <typename T> void ws_free(T* p, cudaStream_t st);

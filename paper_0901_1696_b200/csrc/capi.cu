@@ -4,6 +4,10 @@
 #include "graph_cache.cuh"
 #include "rfp.cuh"
 
+#include <cstring>
+#include <map>
+#include <mutex>
+
 using namespace rfpk;
 
 namespace {
@@ -15,7 +19,7 @@ bool one_of(char c, const char* set) {
   return false;
 }
 cudaStream_t S(rfpk_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
-int cur_device();
+
 
 int reset_info(int* info, cudaStream_t st) {
   if (!info) return 0;
@@ -161,17 +165,51 @@ int pftri_t(char transr, char uplo, int64_t n, void* arf, int* info, cudaStream_
 
 Z zc(double re, double im) { return Z{re, im}; }
 
-int cur_device() {
-  int d = 0;
-  cudaGetDevice(&d);
-  return d;
-}
-
 }  // namespace
 
 namespace rfpk {
 std::atomic<long long> g_launch_count{0};
+
+namespace {
+struct TuneTable {
+  const char* name;
+  long long dflt;
+};
+constexpr TuneTable kTune[TK_COUNT] = {
+    {"oop_max", 4096},       {"t2_copy_min", 2048}, {"panel_max", 4096},
+    {"pfsv_overlap_min", 512}, {"overlap", 1},      {"graphs", 1},
+    {"graph_max_n", 8192},   {"gemm_wide", 0},      {"batched_generic", 0},
+    {"trace", 0}};
+std::atomic<long long> g_tune[TK_COUNT] = {
+    {kTune[0].dflt}, {kTune[1].dflt}, {kTune[2].dflt}, {kTune[3].dflt}, {kTune[4].dflt},
+    {kTune[5].dflt}, {kTune[6].dflt}, {kTune[7].dflt}, {kTune[8].dflt}, {kTune[9].dflt}};
+int tune_index(const char* name) {
+  if (!name) return -1;
+  for (int i = 0; i < TK_COUNT; ++i)
+    if (std::strcmp(name, kTune[i].name) == 0) return i;
+  return -1;
 }
+
+std::mutex g_setup_mu;
+std::map<std::pair<const void*, int>, int> g_setup;
+}  // namespace
+
+long long tune(TuneKey k) { return g_tune[k].load(std::memory_order_relaxed); }
+
+int kernel_setup(const void* kern, int threads, size_t smem) {
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  auto it = g_setup.find({kern, dev});
+  if (it != g_setup.end()) return it->second;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+  cudaGetLastError();
+  if (nb < 1) nb = 1;
+  g_setup.emplace(std::make_pair(kern, dev), nb);
+  return nb;
+}
+}  // namespace rfpk
 
 // ---------------------------------------------------------------- host streaming
 // Start the host->device transfer of an RFP buffer on `copy` (forked from
@@ -185,8 +223,7 @@ static int h2d_rfp_begin(const RfpDesc& d, const void* h, void* dv, cudaStream_t
                          cudaStream_t copy, cudaEvent_t fork, cudaEvent_t in_done, int** cflags,
                          int** sflags) {
   *cflags = *sflags = nullptr;
-  const bool chunked = !is_cplx<T>::value && d.n1 >= 512 && !std::getenv("RFPK_NO_TILE") &&
-                       !std::getenv("RFPK_NO_TILE_TRSM") && !std::getenv("RFPK_NO_STREAM_IN");
+  const bool chunked = !is_cplx<T>::value && d.n1 >= 512;
   const i64 nch = (d.n1 + 63) / 64;
   cudaError_t e = cudaSuccess;
   if (chunked) {
@@ -385,6 +422,27 @@ int rfpk_graph_cache_clear(void) {
   return 0;
 }
 
+int rfpk_set_tuning(const char* name, long long value) {
+  const int i = tune_index(name);
+  if (i < 0) return -1;
+  g_tune[i].store(value);
+  GraphCache::get().clear();  // no replay of a path chosen under the old value
+  return 0;
+}
+
+int rfpk_get_tuning(const char* name, long long* value) {
+  const int i = tune_index(name);
+  if (i < 0 || !value) return -1;
+  *value = g_tune[i].load();
+  return 0;
+}
+
+int rfpk_reset_tuning(void) {
+  for (int i = 0; i < TK_COUNT; ++i) g_tune[i].store(kTune[i].dflt);
+  GraphCache::get().clear();
+  return 0;
+}
+
 int rfpk_device_sms(void) {
   int dev = 0, sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -393,41 +451,50 @@ int rfpk_device_sms(void) {
   return e == cudaSuccess ? sms : -(int)e;
 }
 
-int rfpk_dtrttf(char t, char u, int64_t n, const double* a, int64_t lda, double* arf, rfpk_stream_t s) { return trttf_t<double>(t, u, n, a, lda, arf, S(s)); }
-int rfpk_ztrttf(char t, char u, int64_t n, const void* a, int64_t lda, void* arf, rfpk_stream_t s) { return trttf_t<Z>(t, u, n, a, lda, arf, S(s)); }
-int rfpk_dtfttr(char t, char u, int64_t n, const double* arf, double* a, int64_t lda, rfpk_stream_t s) { return tfttr_t<double>(t, u, n, arf, a, lda, S(s)); }
-int rfpk_ztfttr(char t, char u, int64_t n, const void* arf, void* a, int64_t lda, rfpk_stream_t s) { return tfttr_t<Z>(t, u, n, arf, a, lda, S(s)); }
-int rfpk_dtpttf(char t, char u, int64_t n, const double* ap, double* arf, rfpk_stream_t s) { return tpttf_t<double>(t, u, n, ap, arf, S(s)); }
-int rfpk_ztpttf(char t, char u, int64_t n, const void* ap, void* arf, rfpk_stream_t s) { return tpttf_t<Z>(t, u, n, ap, arf, S(s)); }
-int rfpk_dtfttp(char t, char u, int64_t n, const double* arf, double* ap, rfpk_stream_t s) { return tfttp_t<double>(t, u, n, arf, ap, S(s)); }
-int rfpk_ztfttp(char t, char u, int64_t n, const void* arf, void* ap, rfpk_stream_t s) { return tfttp_t<Z>(t, u, n, arf, ap, S(s)); }
-int rfpk_dtrttp(char u, int64_t n, const double* a, int64_t lda, double* ap, rfpk_stream_t s) { return trttp_t<double>(u, n, a, lda, ap, S(s)); }
-int rfpk_ztrttp(char u, int64_t n, const void* a, int64_t lda, void* ap, rfpk_stream_t s) { return trttp_t<Z>(u, n, a, lda, ap, S(s)); }
-int rfpk_dtpttr(char u, int64_t n, const double* ap, double* a, int64_t lda, rfpk_stream_t s) { return tpttr_t<double>(u, n, ap, a, lda, S(s)); }
-int rfpk_ztpttr(char u, int64_t n, const void* ap, void* a, int64_t lda, rfpk_stream_t s) { return tpttr_t<Z>(u, n, ap, a, lda, S(s)); }
+int rfpk_dtrttf(char t, char u, int64_t n, const double* a, int64_t lda, double* arf, rfpk_stream_t s) { StreamDevice dg_(s); return trttf_t<double>(t, u, n, a, lda, arf, S(s)); }
+int rfpk_ztrttf(char t, char u, int64_t n, const void* a, int64_t lda, void* arf, rfpk_stream_t s) { StreamDevice dg_(s); return trttf_t<Z>(t, u, n, a, lda, arf, S(s)); }
+int rfpk_dtfttr(char t, char u, int64_t n, const double* arf, double* a, int64_t lda, rfpk_stream_t s) { StreamDevice dg_(s); return tfttr_t<double>(t, u, n, arf, a, lda, S(s)); }
+int rfpk_ztfttr(char t, char u, int64_t n, const void* arf, void* a, int64_t lda, rfpk_stream_t s) { StreamDevice dg_(s); return tfttr_t<Z>(t, u, n, arf, a, lda, S(s)); }
+int rfpk_dtpttf(char t, char u, int64_t n, const double* ap, double* arf, rfpk_stream_t s) { StreamDevice dg_(s); return tpttf_t<double>(t, u, n, ap, arf, S(s)); }
+int rfpk_ztpttf(char t, char u, int64_t n, const void* ap, void* arf, rfpk_stream_t s) { StreamDevice dg_(s); return tpttf_t<Z>(t, u, n, ap, arf, S(s)); }
+int rfpk_dtfttp(char t, char u, int64_t n, const double* arf, double* ap, rfpk_stream_t s) { StreamDevice dg_(s); return tfttp_t<double>(t, u, n, arf, ap, S(s)); }
+int rfpk_ztfttp(char t, char u, int64_t n, const void* arf, void* ap, rfpk_stream_t s) { StreamDevice dg_(s); return tfttp_t<Z>(t, u, n, arf, ap, S(s)); }
+int rfpk_dtrttp(char u, int64_t n, const double* a, int64_t lda, double* ap, rfpk_stream_t s) { StreamDevice dg_(s); return trttp_t<double>(u, n, a, lda, ap, S(s)); }
+int rfpk_ztrttp(char u, int64_t n, const void* a, int64_t lda, void* ap, rfpk_stream_t s) { StreamDevice dg_(s); return trttp_t<Z>(u, n, a, lda, ap, S(s)); }
+int rfpk_dtpttr(char u, int64_t n, const double* ap, double* a, int64_t lda, rfpk_stream_t s) { StreamDevice dg_(s); return tpttr_t<double>(u, n, ap, a, lda, S(s)); }
+int rfpk_ztpttr(char u, int64_t n, const void* ap, void* a, int64_t lda, rfpk_stream_t s) { StreamDevice dg_(s); return tpttr_t<Z>(u, n, ap, a, lda, S(s)); }
 
-int rfpk_dpftrf(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftrf_t<double>(t, u, n, arf, info, S(s)); }
-int rfpk_zpftrf(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftrf_t<Z>(t, u, n, arf, info, S(s)); }
-int rfpk_dpftrs(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) {
+int rfpk_dpftrf(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrf_t<double>(t, u, n, arf, info, S(s)); }
+int rfpk_zpftrf(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrf_t<Z>(t, u, n, arf, info, S(s)); }
+int rfpk_dpftrs(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   if (ldb < (n > 1 ? n : 1)) return -7;
   return pftrs_t<double>(t, u, n, nrhs, arf, b, 1, ldb, info, S(s));
 }
-int rfpk_zpftrs(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) {
+int rfpk_zpftrs(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   if (ldb < (n > 1 ? n : 1)) return -7;
   return pftrs_t<Z>(t, u, n, nrhs, arf, b, 1, ldb, info, S(s));
 }
-int rfpk_dpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pftrs_t<double>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
-int rfpk_zpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pftrs_t<Z>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
-int rfpk_dtftri(char t, char u, char d, int64_t n, double* arf, int* info, rfpk_stream_t s) { return tftri_t<double>(t, u, d, n, arf, info, S(s)); }
-int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_stream_t s) { return tftri_t<Z>(t, u, d, n, arf, info, S(s)); }
-int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { return pftri_t<double>(t, u, n, arf, info, S(s)); }
-int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { return pftri_t<Z>(t, u, n, arf, info, S(s)); }
+int rfpk_dpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrs_t<double>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
+int rfpk_zpftrs_ex(char t, char u, int64_t n, int64_t nrhs, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrs_t<Z>(t, u, n, nrhs, arf, b, rsb, csb, info, S(s)); }
+int rfpk_dtftri(char t, char u, char d, int64_t n, double* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return tftri_t<double>(t, u, d, n, arf, info, S(s)); }
+int rfpk_ztftri(char t, char u, char d, int64_t n, void* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return tftri_t<Z>(t, u, d, n, arf, info, S(s)); }
+int rfpk_dpftri(char t, char u, int64_t n, double* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftri_t<double>(t, u, n, arf, info, S(s)); }
+int rfpk_zpftri(char t, char u, int64_t n, void* arf, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftri_t<Z>(t, u, n, arf, info, S(s)); }
 
-int rfpk_dpftrf_host(char t, char u, int64_t n, const double* h, double* d, int* info, rfpk_stream_t s) { return pftrf_host_t<double>(t, u, n, h, d, info, S(s)); }
-int rfpk_zpftrf_host(char t, char u, int64_t n, const void* h, void* d, int* info, rfpk_stream_t s) { return pftrf_host_t<Z>(t, u, n, h, d, info, S(s)); }
+int rfpk_dpftrf_host(char t, char u, int64_t n, const double* h, double* d, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrf_host_t<double>(t, u, n, h, d, info, S(s)); }
+int rfpk_zpftrf_host(char t, char u, int64_t n, const void* h, void* d, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pftrf_host_t<Z>(t, u, n, h, d, info, S(s)); }
 int rfpk_phase_clock(int enable) {
   phase_clock_enable(enable != 0);
   return 0;
+}
+int64_t rfpk_phase_labels(char* out, int64_t cap) {
+  const std::string l = phase_clock_labels();
+  if (out && cap > 0) {
+    const size_t k = l.size() < (size_t)cap - 1 ? l.size() : (size_t)cap - 1;
+    std::memcpy(out, l.data(), k);
+    out[k] = '\0';
+  }
+  return (int64_t)l.size() + 1;
 }
 int rfpk_phase_time(const char* label, double* total_ms, int64_t* count) {
   if (!label || !total_ms || !count) return -1;
@@ -438,14 +505,14 @@ int rfpk_phase_time(const char* label, double* total_ms, int64_t* count) {
   *count = c;
   return 0;
 }
-int rfpk_dpfsv(char t, char u, int64_t n, int64_t nrhs, double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_t<double>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
-int rfpk_zpfsv(char t, char u, int64_t n, int64_t nrhs, void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_t<Z>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
-int rfpk_dpfsv_host(char t, char u, int64_t n, int64_t nrhs, const double* h_arf, double* d_arf, const double* h_b, double* d_b, double* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<double>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
-int rfpk_zpfsv_host(char t, char u, int64_t n, int64_t nrhs, const void* h_arf, void* d_arf, const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info, rfpk_stream_t s) { return pfsv_host_t<Z>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
-int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { return pptrf_t<double>(u, n, ap, info, S(s)); }
-int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { return pptrf_t<Z>(u, n, ap, info, S(s)); }
-int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
-int rfpk_zpptrs(char u, int64_t n, int64_t nrhs, const void* ap, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { return pptrs_t<Z>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
+int rfpk_dpfsv(char t, char u, int64_t n, int64_t nrhs, double* arf, double* b, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pfsv_t<double>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
+int rfpk_zpfsv(char t, char u, int64_t n, int64_t nrhs, void* arf, void* b, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pfsv_t<Z>(t, u, n, nrhs, arf, b, ldb, info, S(s)); }
+int rfpk_dpfsv_host(char t, char u, int64_t n, int64_t nrhs, const double* h_arf, double* d_arf, const double* h_b, double* d_b, double* h_x, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pfsv_host_t<double>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
+int rfpk_zpfsv_host(char t, char u, int64_t n, int64_t nrhs, const void* h_arf, void* d_arf, const void* h_b, void* d_b, void* h_x, int64_t ldb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pfsv_host_t<Z>(t, u, n, nrhs, h_arf, d_arf, h_b, d_b, h_x, ldb, info, S(s)); }
+int rfpk_dpptrf(char u, int64_t n, double* ap, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pptrf_t<double>(u, n, ap, info, S(s)); }
+int rfpk_zpptrf(char u, int64_t n, void* ap, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pptrf_t<Z>(u, n, ap, info, S(s)); }
+int rfpk_dpptrs(char u, int64_t n, int64_t nrhs, const double* ap, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pptrs_t<double>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
+int rfpk_zpptrs(char u, int64_t n, int64_t nrhs, const void* ap, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s); return pptrs_t<Z>(u, n, nrhs, ap, b, rsb, csb, info, S(s)); }
 
 // ---------------------------------------------------------------- SURVEY 8(f) rows
 static int tfsm_check(char& transr, char& side, char& uplo, char& trans, char& diag, int64_t m,
@@ -463,7 +530,7 @@ static int tfsm_check(char& transr, char& side, char& uplo, char& trans, char& d
   return 0;
 }
 int rfpk_dtfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n, double alpha,
-               const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) {
+               const double* arf, double* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = tfsm_check(transr, side, uplo, trans, diag, m, n, rsb, csb, info)) return rc;
   if (int rc = reset_info(info, S(s))) return rc;
   const int64_t order = side == 'L' ? m : n;
@@ -471,7 +538,7 @@ int rfpk_dtfsm(char transr, char side, char uplo, char trans, char diag, int64_t
                       V<double>(b, m, n, rsb, csb));
 }
 int rfpk_ztfsm(char transr, char side, char uplo, char trans, char diag, int64_t m, int64_t n, double are,
-               double aim, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) {
+               double aim, const void* arf, void* b, int64_t rsb, int64_t csb, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = tfsm_check(transr, side, uplo, trans, diag, m, n, rsb, csb, info)) return rc;
   if (int rc = reset_info(info, S(s))) return rc;
   const int64_t order = side == 'L' ? m : n;
@@ -490,14 +557,14 @@ static int sfrk_check(char& transr, char& uplo, char& trans, int64_t n, int64_t 
   return 0;
 }
 int rfpk_dsfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
-               int64_t rsa, int64_t csa, double beta, double* arf, rfpk_stream_t s) {
+               int64_t rsa, int64_t csa, double beta, double* arf, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = sfrk_check(transr, uplo, trans, n, k, rsa, csa)) return rc;
   const int64_t r = trans == 'N' ? n : k, c = trans == 'N' ? k : n;
   return sfrk<double>(Ctx{S(s), nullptr}, rfp_desc(n, uplo, transr), trans, k, alpha,
                       V<double>(a, r, c, rsa, csa), beta, arf, false);
 }
 int rfpk_zhfrk(char transr, char uplo, char trans, int64_t n, int64_t k, double alpha, const void* a,
-               int64_t rsa, int64_t csa, double beta, void* arf, int hermitian, rfpk_stream_t s) {
+               int64_t rsa, int64_t csa, double beta, void* arf, int hermitian, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = sfrk_check(transr, uplo, trans, n, k, rsa, csa)) return rc;
   const int64_t r = trans == 'N' ? n : k, c = trans == 'N' ? k : n;
   return sfrk<Z>(Ctx{S(s), nullptr}, rfp_desc(n, uplo, transr), trans, k, alpha,
@@ -514,11 +581,11 @@ static int lansf_check(char& norm, char& transr, char& uplo, int64_t n, const do
   if (!out) return -6;
   return 0;
 }
-int rfpk_dlansf(char norm, char transr, char uplo, int64_t n, const double* arf, double* out, rfpk_stream_t s) {
+int rfpk_dlansf(char norm, char transr, char uplo, int64_t n, const double* arf, double* out, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = lansf_check(norm, transr, uplo, n, out)) return rc;
   return lansf<double>(S(s), rfp_desc(n, uplo, transr), norm, arf, out);
 }
-int rfpk_zlansf(char norm, char transr, char uplo, int64_t n, const void* arf, double* out, rfpk_stream_t s) {
+int rfpk_zlansf(char norm, char transr, char uplo, int64_t n, const void* arf, double* out, rfpk_stream_t s) { StreamDevice dg_(s);
   if (int rc = lansf_check(norm, transr, uplo, n, out)) return rc;
   return lansf<Z>(S(s), rfp_desc(n, uplo, transr), norm, (const Z*)arf, out);
 }
@@ -526,7 +593,7 @@ int rfpk_zlansf(char norm, char transr, char uplo, int64_t n, const void* arf, d
 // ---------------------------------------------------------------- dense kernels
 int rfpk_dgemm(char ta, char tb, double alpha, const double* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
                const double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, double beta,
-               double* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+               double* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) { StreamDevice dg_(s);
   ta = up(ta); tb = up(tb);
   if (!one_of(ta, "NTC")) return -1;
   if (!one_of(tb, "NTC")) return -2;
@@ -542,7 +609,7 @@ int rfpk_dgemm(char ta, char tb, double alpha, const double* a, int64_t ar, int6
 }
 int rfpk_zgemm(char ta, char tb, double are, double aim, const void* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
                const void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, double bre, double bim,
-               void* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+               void* c, int64_t cr, int64_t cc, int64_t crs, int64_t ccs, rfpk_stream_t s) { StreamDevice dg_(s);
   ta = up(ta); tb = up(tb);
   if (!one_of(ta, "NTC")) return -1;
   if (!one_of(tb, "NTC")) return -2;
@@ -567,33 +634,33 @@ int rfpk_zgemm(char ta, char tb, double are, double aim, const void* a, int64_t 
   if ((side == 'L' ? br : bc) != an) return -7;
 
 int rfpk_dtrsm(char side, char uplo, char trans, char diag, double alpha, const double* a, int64_t an, int64_t ars, int64_t acs,
-               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) {
+               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   TRI_ARGS_CHECK();
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_trsm<double>(Ctx{S(s), info}, side, uplo, trans, diag, alpha, V<double>(a, an, an, ars, acs),
                            V<double>(b, br, bc, brs, bcs), info != nullptr);
 }
 int rfpk_ztrsm(char side, char uplo, char trans, char diag, double are, double aim, const void* a, int64_t an, int64_t ars, int64_t acs,
-               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) {
+               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   TRI_ARGS_CHECK();
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_trsm<Z>(Ctx{S(s), info}, side, uplo, trans, diag, zc(are, aim), V<Z>(a, an, an, ars, acs),
                       V<Z>(b, br, bc, brs, bcs), info != nullptr);
 }
 int rfpk_dtrmm(char side, char uplo, char trans, char diag, double alpha, const double* a, int64_t an, int64_t ars, int64_t acs,
-               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) {
+               double* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) { StreamDevice dg_(s);
   TRI_ARGS_CHECK();
   return blas_trmm<double>(Ctx{S(s), nullptr}, side, uplo, trans, diag, alpha, V<double>(a, an, an, ars, acs),
                            V<double>(b, br, bc, brs, bcs));
 }
 int rfpk_ztrmm(char side, char uplo, char trans, char diag, double are, double aim, const void* a, int64_t an, int64_t ars, int64_t acs,
-               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) {
+               void* b, int64_t br, int64_t bc, int64_t brs, int64_t bcs, rfpk_stream_t s) { StreamDevice dg_(s);
   TRI_ARGS_CHECK();
   return blas_trmm<Z>(Ctx{S(s), nullptr}, side, uplo, trans, diag, zc(are, aim), V<Z>(a, an, an, ars, acs),
                       V<Z>(b, br, bc, brs, bcs));
 }
 int rfpk_dsyrk(char uplo, char trans, double alpha, const double* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
-               double beta, double* c, int64_t cn, int64_t crs, int64_t ccs, rfpk_stream_t s) {
+               double beta, double* c, int64_t cn, int64_t crs, int64_t ccs, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo); trans = up(trans);
   if (!one_of(uplo, "LU")) return -1;
   if (!one_of(trans, "NTC")) return -2;
@@ -604,7 +671,7 @@ int rfpk_dsyrk(char uplo, char trans, double alpha, const double* a, int64_t ar,
                            V<double>(c, cn, cn, crs, ccs), false);
 }
 int rfpk_zsyrk(char uplo, char trans, double alpha, const void* a, int64_t ar, int64_t ac, int64_t ars, int64_t acs,
-               double beta, void* c, int64_t cn, int64_t crs, int64_t ccs, int hermitian, rfpk_stream_t s) {
+               double beta, void* c, int64_t cn, int64_t crs, int64_t ccs, int hermitian, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo); trans = up(trans);
   if (!one_of(uplo, "LU")) return -1;
   if (!one_of(trans, "NTC")) return -2;
@@ -614,7 +681,7 @@ int rfpk_zsyrk(char uplo, char trans, double alpha, const void* a, int64_t ar, i
   return blas_syrk<Z>(Ctx{S(s), nullptr}, uplo, trans, alpha, V<Z>(a, ar, ac, ars, acs), beta,
                       V<Z>(c, cn, cn, crs, ccs), hermitian != 0);
 }
-int rfpk_dpotrf(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+int rfpk_dpotrf(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo);
   if (!one_of(uplo, "LU")) return -1;
   if (!unit_stride(n, n, rs, cs)) return -4;
@@ -622,7 +689,7 @@ int rfpk_dpotrf(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, int* in
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_potrf<double>(Ctx{S(s), info}, uplo, V<double>(a, n, n, rs, cs), 0);
 }
-int rfpk_zpotrf(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+int rfpk_zpotrf(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo);
   if (!one_of(uplo, "LU")) return -1;
   if (!unit_stride(n, n, rs, cs)) return -4;
@@ -630,7 +697,7 @@ int rfpk_zpotrf(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, int* info
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_potrf<Z>(Ctx{S(s), info}, uplo, V<Z>(a, n, n, rs, cs), 0);
 }
-int rfpk_dtrtri(char uplo, char diag, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+int rfpk_dtrtri(char uplo, char diag, double* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo); diag = up(diag);
   if (!one_of(uplo, "LU")) return -1;
   if (!one_of(diag, "NU")) return -2;
@@ -639,7 +706,7 @@ int rfpk_dtrtri(char uplo, char diag, double* a, int64_t n, int64_t rs, int64_t 
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_trtri<double>(Ctx{S(s), info}, uplo, diag, V<double>(a, n, n, rs, cs), 0);
 }
-int rfpk_ztrtri(char uplo, char diag, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) {
+int rfpk_ztrtri(char uplo, char diag, void* a, int64_t n, int64_t rs, int64_t cs, int* info, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo); diag = up(diag);
   if (!one_of(uplo, "LU")) return -1;
   if (!one_of(diag, "NU")) return -2;
@@ -648,13 +715,13 @@ int rfpk_ztrtri(char uplo, char diag, void* a, int64_t n, int64_t rs, int64_t cs
   if (int rc = reset_info(info, S(s))) return rc;
   return blas_trtri<Z>(Ctx{S(s), info}, uplo, diag, V<Z>(a, n, n, rs, cs), 0);
 }
-int rfpk_dlauum(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) {
+int rfpk_dlauum(char uplo, double* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo);
   if (!one_of(uplo, "LU")) return -1;
   if (!unit_stride(n, n, rs, cs)) return -4;
   return blas_lauum<double>(Ctx{S(s), nullptr}, uplo, V<double>(a, n, n, rs, cs));
 }
-int rfpk_zlauum(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) {
+int rfpk_zlauum(char uplo, void* a, int64_t n, int64_t rs, int64_t cs, rfpk_stream_t s) { StreamDevice dg_(s);
   uplo = up(uplo);
   if (!one_of(uplo, "LU")) return -1;
   if (!unit_stride(n, n, rs, cs)) return -4;

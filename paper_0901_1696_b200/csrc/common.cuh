@@ -103,15 +103,93 @@ enum { RFPK_OK = 0 };
 enum Uplo : int { LOWER = 0, UPPER = 1 };
 enum TriMode : int { TRI_FULL = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
 
-inline int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
 }
+
+constexpr int MAX_DEVICES = 64;
+
+// SM count of the CURRENT device (cached per device)
+inline int num_sms() {
+  static std::atomic<int> sms[MAX_DEVICES];
+  const int dev = cur_device() & (MAX_DEVICES - 1);
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// One-time per-(kernel, device) configuration: opts the kernel into `smem`
+// bytes of dynamic shared memory ON THE CURRENT DEVICE (function attributes
+// are per device context) and returns its resident CTAs per SM at
+// `threads` threads (>= 1).  Defined in capi.cu.
+int kernel_setup(const void* kern, int threads, size_t smem);
+template <typename K> int kernel_setup(K* kern, int threads, size_t smem) {
+  return kernel_setup(reinterpret_cast<const void*>(kern), threads, smem);
+}
+
+// Every entry point runs on the device that owns the caller's stream: the
+// drivers query the current device (SM count, library streams, kernel
+// attributes, graph keys), so a stream of device k is served with device k
+// current for the duration of the call, and the caller's current device is
+// restored on return.  The default streams (0 / legacy / per-thread) belong
+// to the current device already.
+struct StreamDevice {
+  int prev = -1;
+  explicit StreamDevice(void* s) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) return;
+    int dev = -1, cur = -1;
+    if (cudaStreamGetDevice(st, &dev) != cudaSuccess) {
+      cudaGetLastError();  // leave the error to the launch that uses the stream
+      return;
+    }
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+      prev = cur;
+  }
+  ~StreamDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------- kernel clock
+// With the phase clock on (rfpk_phase_clock(1)), a launch site bracketed by
+// a KernelClock records a CUDA event pair ON THE STREAM IT LAUNCHES ON and
+// files the pair under `label` ("kernel <name> <shape>"); rfpk_phase_time
+// sums them.  Nothing is recorded under graph capture or with the clock off.
+// Defined in rfp.cu.
+struct KernelClock {
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  explicit KernelClock(cudaStream_t s);
+  void stop(const char* name, long long d0, long long d1, long long d2 = -1);
+};
+
+// ---------------------------------------------------------------- tuning
+// Path thresholds, set only through the explicit C-ABI call
+// rfpk_set_tuning(name, value) (include/rfpk_b200.h) -- there are no
+// environment knobs.  The defaults are the measured crossovers (DESIGN.md
+// section 4); tests use the setter to force the alternative paths at small
+// orders.  Changing a value drops every cached CUDA graph, so a replay can
+// never run a path chosen under the old setting.
+enum TuneKey : int {
+  TK_OOP_MAX = 0,          // one-launch trmm / lauum / trtri up to this order (4096)
+  TK_T2_COPY_MIN,          // column-major workspace potrf of row-major blocks from (2048)
+  TK_PANEL_MAX,            // one-launch [T1; S1] panel Cholesky up to n1 (4096)
+  TK_PFSV_OVERLAP_MIN,     // pfsv: pftrs part 1 beside potrf(T2) from order (512)
+  TK_OVERLAP,              // potrf(T1) || S1 solve as two concurrent launches (1)
+  TK_GRAPHS,               // CUDA-graph replay of repeated calls (1)
+  TK_GRAPH_MAX_N,          // ... below this order (8192)
+  TK_GEMM_WIDE,            // force the 64 x 128 GEMM tile for every product (0)
+  TK_BATCHED_GENERIC,      // force the generic batched kernel at n = 64 (0)
+  TK_TRACE,                // print per-phase SRPA times to stderr (0)
+  TK_COUNT
+};
+long long tune(TuneKey k);  // defined in capi.cu
 
 }  // namespace rfpk

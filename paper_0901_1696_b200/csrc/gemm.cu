@@ -399,22 +399,11 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
                           (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
                           sizeof(T);
   auto kern = gemm_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM, MODE>;
-  static const bool configured = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return true;
-  }();
-  (void)configured;
+  kernel_setup(kern, NT, smem);
   const int tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   GemmArgs<T> g = a;
   g.tiles_m = tm;
-  static const int band = [] {
-    const char* v = std::getenv("RFPK_TRI_BAND");
-    return v ? std::atoi(v) : 24;
-  }();
-  static const int full_band = [] {
-    const char* v = std::getenv("RFPK_FULL_BAND");
-    return v ? std::atoi(v) : 24;
-  }();
+  constexpr int band = 24, full_band = 24;  // tile rows per band (see GemmArgs::band)
   // full products: banded only when C is narrow (few column tiles, e.g.
   // pftrs's 8192 x 1024 gemms: 32.0 -> 33.0 TFLOP/s, A streamed from DRAM once
   // instead of once per resident column group); square products keep the
@@ -429,8 +418,10 @@ int launch_one(const GemmArgs<T>& a, cudaStream_t st) {
     for (int j = 0; j < tn; ++j) g.ntiles += tri_rect_count<BM, BN>(MODE, j, tm);
   }
   const long long grid = g.ntiles;
+  KernelClock kc(st);
   kern<<<(unsigned)grid, NT, smem, st>>>(g);
   RFPK_CHECK_LAUNCH();
+  kc.stop(MODE == TRI_FULL ? "gemm" : "syrk", a.M, a.N, a.K);
   return 0;
 }
 
@@ -460,19 +451,17 @@ int splitk_launch(const GemmArgs<T>& a, int S, int kchunk, cudaStream_t st) {
                           (SmemLayout<T, BM, BK, AK>::SIZE + SmemLayout<T, BN, BK, BKM>::SIZE) *
                           sizeof(T);
   auto kern = gemm_splitk_kernel<T, BM, BN, BK, WM, WN, ST, AK, BKM>;
-  static const bool configured = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return true;
-  }();
-  (void)configured;
+  kernel_setup(kern, (BM / WM) * (BN / WN) * 32, smem);
   GemmArgs<T> g = a;
   g.tiles_m = (g.M + BM - 1) / BM;
   const int tiles = g.tiles_m * ((g.N + BN - 1) / BN);
   T* ws = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&ws, (size_t)S * g.M * g.N * sizeof(T), st);
   if (e != cudaSuccess) return (int)e;
+  KernelClock kc(st);
   kern<<<dim3((unsigned)tiles, (unsigned)S), (BM / WM) * (BN / WN) * 32, smem, st>>>(g, ws, kchunk);
   RFPK_CHECK_LAUNCH();
+  kc.stop("gemm_splitk", g.M, g.N, g.K);
   const i64 total = (i64)g.M * g.N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
@@ -484,12 +473,9 @@ int splitk_launch(const GemmArgs<T>& a, int S, int kchunk, cudaStream_t st) {
 
 // -100: not worth splitting (enough tiles, or a short K)
 template <typename T> int gemm_splitk(const GemmArgs<T>& g, bool ak, bool bk, cudaStream_t st) {
-  static const int min_k = [] {
-    const char* v = std::getenv("RFPK_SPLITK_MIN_K");
-    return v ? std::atoi(v) : 256;
-  }();
+  constexpr int min_k = 256;
   const long long tiles = (long long)((g.M + 63) / 64) * ((g.N + 63) / 64);
-  if (min_k <= 0 || g.K < min_k || tiles * 2 > num_sms()) return -100;
+  if (g.K < min_k || tiles * 2 > num_sms()) return -100;
   // about two CTAs per SM in total, slices of at least 128 (a multiple of 16)
   int S = (int)((2 * num_sms() + tiles - 1) / tiles);
   const int smax = g.K / 128;
@@ -570,19 +556,15 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
     // 64 x 64 tiles, 4 warps of 32 x 32, 3 stages, 4 CTAs per SM: the
     // measured best FP64 config (33 TFLOP/s at 8192^3 vs 31 for a 1-CTA/SM
     // 128 x 128 tile: more resident CTAs hide the per-stage barrier).
-    static const int force = [] {
-      const char* v = std::getenv("RFPK_TILE");
-      return v ? std::atoi(v) : 0;
-    }();
-    if (force == 128) return launch_mode<T, 128, 128, 16, 64, 32, 4>(g, tri_mode, ak, bk, st);
+    const bool force_wide = tune(TK_GEMM_WIDE) != 0;
     // 64 x 128 tiles (4 warps of 32 x 64: 12 fragment loads per 16 DMMAs
     // instead of 8 per 8) for full products with >= 4 waves of them at 2
     // CTAs/SM: DGEMM 8192^3 32.4-33.5 -> 34.2-34.4 TFLOP/s; at 8192 x 1024 the
     // tile count is too small (29.8 vs 32.5).  SYRK/HERK keep 64 x 64: on the
     // odd-ld RFP operands of pftrf the wide tiles measured slower (T2 -= S1
-    // S1^T at n = 16384: 17.46 vs 17.02 ms); RFPK_TILE=64128 forces them.
+    // S1^T at n = 16384: 17.46 vs 17.02 ms); tuning "gemm_wide" forces them.
     const long long t128 = (long long)((g.M + 63) / 64) * ((g.N + 127) / 128);
-    if (force == 64128 || (force == 0 && tri_mode == TRI_FULL && t128 >= 8LL * num_sms()))
+    if (force_wide || (tri_mode == TRI_FULL && t128 >= 8LL * num_sms()))
       return launch_mode<T, 64, 128, 16, 32, 64, 3>(g, tri_mode, ak, bk, st);
     return launch_mode<T, 64, 64, 16, 32, 32, 3>(g, tri_mode, ak, bk, st);
   }

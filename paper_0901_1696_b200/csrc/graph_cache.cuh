@@ -7,7 +7,8 @@
 // become graph memory nodes), instantiated, and replayed on every later call
 // with the same tuple -- one host launch, back-to-back kernels on the device.
 // Pointers are part of the key, so a replay always touches the caller's
-// current buffers.  RFPK_GRAPHS=0 disables the cache.
+// current buffers.  Tuning "graphs" = 0 disables the cache (rfpk_set_tuning,
+// which also clears it).
 #pragma once
 #include <cstdlib>
 #include <cstring>
@@ -56,7 +57,7 @@ class GraphCache {
     // direct: captured kernel nodes do not keep the high / low stream
     // priorities the look-ahead relies on (measured: n=16384 pftrf 61.1 ms
     // direct vs 64.8 ms replayed; n=4000 4.44 ms direct vs 4.23 replayed).
-    if (!enabled_ || key.n >= max_n_) return body(st);
+    if (!tune(TK_GRAPHS) || key.n >= tune(TK_GRAPH_MAX_N)) return body(st);
     std::lock_guard<std::mutex> lk(mu_);
     // The legacy NULL stream cannot be captured: use a library stream that is
     // a *blocking* stream, hence implicitly ordered with the legacy stream.
@@ -105,15 +106,8 @@ class GraphCache {
     seen_.clear();
   }
 
-  bool enabled() const { return enabled_; }
-
  private:
-  GraphCache() {
-    const char* v = std::getenv("RFPK_GRAPHS");
-    enabled_ = !(v && std::strcmp(v, "0") == 0);
-    const char* m = std::getenv("RFPK_GRAPH_MAX_N");
-    if (m) max_n_ = std::atoll(m);
-  }
+  GraphCache() = default;
   void evict_if_full() {
     const size_t cap = 64;
     if (cache_.size() < cap) return;
@@ -126,8 +120,6 @@ class GraphCache {
   std::map<GraphKey, GraphEntry> cache_;
   std::set<GraphKey> seen_;
   std::mutex mu_;
-  bool enabled_ = true;
-  long long max_n_ = 8192;
   cudaStream_t own_ = nullptr;
   unsigned long long clock_ = 0;
 };

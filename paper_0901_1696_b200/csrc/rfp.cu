@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace rfpk {
 
 RfpDesc rfp_desc(i64 n, char uplo, char transr) {
@@ -42,17 +44,15 @@ void rfp_blocks(const RfpDesc& d, T* buf, View<T>& t1, View<T>& t2, View<T>& s1)
 template <typename T> static T one() { return sc_from<T>(1.0); }
 template <typename T> static T m_one() { return sc_from<T>(-1.0); }
 
-// RFPK_TRACE=1: per-phase GPU times of the SRPA steps (direct, non-captured
-// calls only), printed to stderr -- a poor man's timeline without nsys.
-// Phase timing of the SRPA steps.  RFPK_TRACE=1 prints each direct call's
-// phases to stderr (synchronising); the phase clock (rfpk_phase_clock) only
+// Phase timing of the SRPA steps.  Tuning "trace" = 1 prints each direct
+// call's phases to stderr (synchronising); the phase clock (rfpk_phase_clock) only
 // records event pairs, summed per "routine phase" label when
 // rfpk_phase_time() is asked -- so a benchmark can time its dominant kernel
 // live inside the timed region without perturbing it.  Captured (graph)
 // calls are never traced.
 struct PhaseClock {
   std::mutex mu;
-  bool on = false;
+  std::atomic<bool> on{false};
   struct Pending { std::string label; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> owned;  // destroyed once read
@@ -76,6 +76,37 @@ struct PhaseClock {
   }
 };
 
+KernelClock::KernelClock(cudaStream_t s) : st(s) {
+  if (!PhaseClock::get().on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  if (cudaEventCreate(&a) != cudaSuccess) {
+    a = nullptr;
+    return;
+  }
+  cudaEventRecord(a, st);
+}
+
+void KernelClock::stop(const char* name, long long d0, long long d1, long long d2) {
+  if (!a) return;
+  cudaEvent_t b = nullptr;
+  if (cudaEventCreate(&b) != cudaSuccess) {
+    cudaEventDestroy(a);
+    a = nullptr;
+    return;
+  }
+  cudaEventRecord(b, st);
+  char lab[160];
+  if (d2 >= 0) snprintf(lab, sizeof lab, "kernel %s %lldx%lldx%lld", name, d0, d1, d2);
+  else snprintf(lab, sizeof lab, "kernel %s %lldx%lld", name, d0, d1);
+  PhaseClock& pc = PhaseClock::get();
+  std::lock_guard<std::mutex> g(pc.mu);
+  pc.pending.push_back({std::string(lab), a, b});
+  pc.owned.push_back(a);
+  pc.owned.push_back(b);
+  a = nullptr;
+}
+
 struct PhaseTrace {
   cudaStream_t st;
   const char* name;
@@ -84,21 +115,23 @@ struct PhaseTrace {
   const char* lab[8];
   int k = 0;
   PhaseTrace(cudaStream_t s, const char* nm) : st(s), name(nm) {
-    const char* v = std::getenv("RFPK_TRACE");
+    nvtxRangePushA(nm);  // NVTX: one range per SRPA routine, a mark per step
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
     if (cs != cudaStreamCaptureStatusNone) return;
-    print = v && v[0] == '1';
+    print = tune(TK_TRACE) != 0;
     clock = PhaseClock::get().on;
     if (print || clock) mark("start");
   }
   void mark(const char* l) {
+    nvtxMarkA(l);
     if (!(print || clock) || k >= 8) return;
     cudaEventCreate(&ev[k]);
     cudaEventRecord(ev[k], st);
     lab[k++] = l;
   }
   ~PhaseTrace() {
+    nvtxRangePop();
     if (!(print || clock)) return;
     if (clock) {
       PhaseClock& pc = PhaseClock::get();
@@ -154,8 +187,10 @@ __global__ void tile_copy_kernel(View<T> src, View<T> dst, int lower) {
 template <typename T> static int tile_copy(Ctx c, View<T> src, View<T> dst, bool lower) {
   if (src.empty()) return 0;
   const dim3 grid((unsigned)((src.n + 31) / 32), (unsigned)((src.m + 31) / 32));
+  KernelClock kc(c.st);
   tile_copy_kernel<T><<<grid, dim3(32, 8), 0, c.st>>>(src, dst, lower ? 1 : 0);
   RFPK_CHECK_LAUNCH();
+  kc.stop("tile_copy", src.m, src.n);
   return 0;
 }
 
@@ -225,8 +260,7 @@ template <typename T> static int panel_chol_ws(Ctx c, View<T> t1, View<T> s, T* 
 // view and takes the same route when its input is not streamed in.
 template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int base, T* W) {
   const View<T> v = uplo == 'L' ? blk : blk.t();
-  const char* env = std::getenv("RFPK_T2_COPY_MIN");
-  const i64 min_n = env ? (i64)std::atoll(env) : (i64)2048;
+  const i64 min_n = tune(TK_T2_COPY_MIN);
   // (real only: for complex128 the row-major tile potrf measured as fast or
   // faster -- config 5's pftrf 606 ms direct vs 663 ms through the copy)
   if (is_cplx<T>::value || v.rs == 1 || v.cs != 1 || v.m < min_n)
@@ -241,10 +275,7 @@ template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int 
   return rc;
 }
 
-static i64 panel_max() {
-  const char* e = std::getenv("RFPK_PANEL_MAX");
-  return e ? (i64)std::atoll(e) : (i64)4096;
-}
+static i64 panel_max() { return tune(TK_PANEL_MAX); }
 
 struct WsPair {  // two leaf-inverse workspaces, freed stream-ordered
   cudaStream_t st;
@@ -275,10 +306,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
   PhaseTrace tr(c.st, "pftrf");
   // potrf(T2); with a pfsv plan, beside pftrs part 1 (see pfsv)
   auto t2_step = [&](int base) -> int {
-    static const i64 min_t2 = [] {
-      const char* v = std::getenv("RFPK_PFSV_OVERLAP_MIN");
-      return v ? (i64)std::atoll(v) : (i64)512;
-    }();
+    const i64 min_t2 = tune(TK_PFSV_OVERLAP_MIN);
     if (!plan || d.n2 == 0 || t2.m < min_t2) return potrf_block(c, 'U', t2, base, W);
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(c.st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
@@ -364,7 +392,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1.t(), 1.0, t2, herm);
       tr.mark("syrk(T2)");
       if (!rc) rc = t2_step((int)d.n1);
-      tr.mark("potrf(T2)");
+      tr.mark(plan && plan->done ? "pftrs(rest)" : "potrf(T2)");
     }
   } else {
     // UPLO='U': S1 <- T1^-H S1 is the tall panel [T1; S1^T] transposed; S1
@@ -405,7 +433,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       tr.mark("syrk(T2)");
     }
     if (!rc) rc = t2_step((int)d.n2);
-    tr.mark("potrf(T2)");
+    tr.mark(plan && plan->done ? "pftrs(rest)" : "potrf(T2)");
   }
   // (the transfers must also be complete on every early-exit path)
   if (s1_ready) cudaStreamWaitEvent(c.st, s1_ready, 0);
@@ -452,9 +480,9 @@ int rfp_h2d_split(const RfpDesc& d, const T* host, T* dev, cudaStream_t first,
 template <typename T>
 int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* sflags,
                     cudaStream_t copy) {
-  static int* one = [] {  // pinned source of the flag value
+  static int* one = [] {  // pinned source of the flag value (every device)
     int* p = nullptr;
-    cudaMallocHost((void**)&p, sizeof(int));
+    cudaHostAlloc((void**)&p, sizeof(int), cudaHostAllocPortable);
     *p = 1;
     return p;
   }();
@@ -502,42 +530,8 @@ static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
   const i64 n1 = d.n1, n2 = d.n2, r = b.n;
   PhaseTrace tr(c.st, "pftrs");
-  // opt-in (RFPK_TRSM2=1): each sweep through both triangles as ONE dataflow
-  // launch (trsm, the S1 gemm and the other triangle's trsm fused,
-  // trsm2_tiles); the back sweep stays split when the caller streams B2 out
-  auto sweep2 = [&](bool fwd, View<T> ta, View<T> b0, const T* wa, View<T> tb, View<T> bb,
-                    const T* wb, View<T> p) -> int {
-    if constexpr (std::is_same<T, double>::value) {
-      static const i64 mn = [] {
-        const char* v = std::getenv("RFPK_TRSM2_MIN");
-        return v ? (i64)std::atoll(v) : (i64)128;
-      }();
-      if (part != 0 || n2 == 0 || n1 < mn || n2 < mn || (!fwd && b2_final)) return -100;
-      return trsm2_tiles(c, fwd, ta, b0, wa, tb, bb, wb, p);
-    } else {
-      return -100;
-    }
-  };
-  int rc2;
   if (d.lower) {
     View<T> b1 = b.sub(0, 0, n1, r), b2 = b.sub(n1, 0, n2, r);
-    if ((rc2 = sweep2(true, t1, b1, W1, t2.t(), b2, W2, s1)) != -100) {
-      TRY(rc2);
-      tr.mark("fwd(T1,S1,T2)");
-      if ((rc2 = sweep2(false, t2, b2, W2, t1.t(), b1, W1, s1.t())) != -100) {
-        TRY(rc2);
-        tr.mark("bwd(T2,S1,T1)");
-        return 0;
-      }
-      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t2.t(), b2, false, W2));
-      tr.mark("trsm3");
-      if (b2_final) cudaEventRecord(b2_final, c.st);
-      TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
-      tr.mark("gemm2");
-      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false, W1));
-      tr.mark("trsm4");
-      return 0;
-    }
     if (part != 2) {
       TRY(blas_trsm(c, 'L', 'L', 'N', 'N', one<T>(), t1, b1, false, W1));
       tr.mark("trsm1");
@@ -561,15 +555,6 @@ static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T
     return 0;
   }
   View<T> b1 = b.sub(0, 0, n2, r), b2 = b.sub(n2, 0, n1, r);
-  if ((rc2 = sweep2(true, t1, b1, W1, t2.t(), b2, W2, s1.t())) != -100) {
-    TRY(rc2);
-    if ((rc2 = sweep2(false, t2, b2, W2, t1.t(), b1, W1, s1)) != -100) return rc2;
-    TRY(blas_trsm(c, 'L', 'U', 'N', 'N', one<T>(), t2, b2, false, W2));
-    if (b2_final) cudaEventRecord(b2_final, c.st);
-    TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
-    TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
-    return 0;
-  }
   if (part != 2) {
     if (n2) {
       TRY(blas_trsm(c, 'L', 'U', 'C', 'N', one<T>(), t1.t(), b1, false, W1));
@@ -890,13 +875,11 @@ int convert(const Storage& src, const T* s, const Storage& dst, T* dptr, bool ze
   dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((n + 63) / 64));
   const size_t sm = 64 * 65 * sizeof(T);
   auto k = convert_kernel<T>;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    set = true;
-  }
+  kernel_setup(k, 256, sm);
+  KernelClock kc(st);
   k<<<grid, 256, sm, st>>>(src, s, dst, dptr, n, rows, src.r.lower ? 1 : 0, zero_fill ? 1 : 0);
   RFPK_CHECK_LAUNCH();
+  kc.stop("convert", src.kind * 10 + dst.kind, n);
   return 0;
 }
 
@@ -1243,6 +1226,17 @@ void phase_clock_enable(bool on) {
   pc.drain();
   pc.sums.clear();
   pc.on = on;
+}
+std::string phase_clock_labels() {
+  PhaseClock& pc = PhaseClock::get();
+  std::lock_guard<std::mutex> g(pc.mu);
+  pc.drain();
+  std::string out;
+  for (auto& kv : pc.sums) {
+    out += kv.first;
+    out += '\n';
+  }
+  return out;
 }
 bool phase_clock_read(const char* label, double* total_ms, long long* count) {
   PhaseClock& pc = PhaseClock::get();

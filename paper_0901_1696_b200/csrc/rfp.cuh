@@ -4,6 +4,8 @@
 #pragma once
 #include "blas.cuh"
 
+#include <string>
+
 namespace rfpk {
 
 struct RfpDesc {
@@ -72,6 +74,7 @@ template <typename T> int lansf(cudaStream_t st, const RfpDesc& d, char norm, co
 // phase clock (see PhaseTrace in rfp.cu)
 void phase_clock_enable(bool on);
 bool phase_clock_read(const char* label, double* total_ms, long long* count);
+std::string phase_clock_labels();  // every label seen, one per line
 
 // Storage descriptors for the conversion kernel.
 enum StorageKind : int { ST_FULL = 0, ST_PACKED = 1, ST_RFP = 2 };

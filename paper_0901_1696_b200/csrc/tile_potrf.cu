@@ -35,6 +35,7 @@
 #include "leaf.cuh"
 
 #include <cstdlib>
+#include <mutex>
 
 namespace rfpk {
 
@@ -187,12 +188,6 @@ __device__ __forceinline__ void smem_mm_yh(const T* X, const T* Y,
         }
     }
   }
-}
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
 }
 
 // ---------------------------------------------------------- task helpers
@@ -485,9 +480,7 @@ __device__ __forceinline__ bool wait_input(const CholCtx<T>& X, int j, int* s_ok
 }
 
 template <typename T, bool KM>
-__device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int* s_ok,
-                         unsigned long long* tr) {
-  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((kind << 28) | (a << 14) | b); tr[5] = blockIdx.x; }
+__device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int* s_ok) {
   using C = TileCfg<T>;
   T* S = sm;
   T* Ws = S + TP * LD64;
@@ -498,9 +491,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
     if (!wait_input(X, 0, s_ok)) return false;
     load_diag(X, 0, S);
     __syncthreads();
-    if (tr && threadIdx.x == 0) tr[1] = gtimer();
     const bool ok = finish_diag(X, 0, S, Ws, scr, s_ok);
-    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return ok;
   }
   if (kind == TK_PARTIAL) {
@@ -524,13 +515,11 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
           }
         }
     publish(X.pready + d);
-    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return true;
   }
   // TK_NORMAL (i, j) and TK_SUPER (j + 1, j)
   const int i = a, j = b;
   if (!accumulate<T, KM>(X, i, j, j, sm, s_ok, acc)) return false;
-  if (tr && threadIdx.x == 0) tr[1] = gtimer();
   if (!wait_input(X, j, s_ok)) return false;
   // (diag 1 has no partial task: its original tile is read below)
   if (kind == TK_SUPER && i == 1 && !wait_input(X, 1, s_ok)) return false;
@@ -566,13 +555,10 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
         }
   }
   if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok)) return false;
-  if (tr && threadIdx.x == 0) tr[2] = gtimer();
   double x[C::NACC][2][4][4];
   apply_w(X, i, j, S, Ws, x, kind == TK_SUPER ? Ws : S);
   publish(X.done + (i64)i * X.nt + j);
-  if (tr && threadIdx.x == 0) tr[6] = gtimer();
   if (kind == TK_NORMAL) {
-    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return true;
   }
   // super: diag d = partial - L(d, j) L(d, j)^H, then the leaf (X is in Ws)
@@ -600,9 +586,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
         }
       }
   __syncthreads();
-  if (tr && threadIdx.x == 0) tr[7] = gtimer();
   const bool ok = finish_diag(X, d, S, Ws, scr, s_ok);
-  if (tr && threadIdx.x == 0) tr[3] = gtimer();
   return ok;
 }
 
@@ -626,7 +610,7 @@ __host__ __device__ inline long long chol_task_count(int nt, int mt) {
 template <typename T, bool KM>
 __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
     tile_potrf_kernel(View<T> A, int ncols, T* W, int* info, int base, int* sync, int nt, int mt,
-                      const int* ext, unsigned long long* trace) {
+                      const int* ext) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
@@ -671,58 +655,27 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
       else if ((o -= sup) < nnorm) { kind = TK_NORMAL; a = first + o; b = g; }
       else { kind = TK_PARTIAL; a = g + 2; b = 0; }
     }
-    if (!run_task<T, KM>(X, kind, a, b, sm, &s_ok, trace ? trace + 8 * t : nullptr)) return;
+    if (!run_task<T, KM>(X, kind, a, b, sm, &s_ok)) return;
   }
 }
 
 template <typename T, bool KM>
 int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, int mt) {
-  // RFPK_TILE_TRACE=file: per-task globaltimer stamps (start, acc done, diag
-  // ready, published), tile and CTA -> CSV (debug only; synchronises)
-  static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
-  unsigned long long* trace = nullptr;
-  const long long ntask = chol_task_count(nt, mt);
-  if (trace_file) {
-    cudaMallocManaged(&trace, ntask * 8 * sizeof(unsigned long long));
-    cudaMemset(trace, 0, ntask * 8 * sizeof(unsigned long long));
-  }
   auto kern = tile_potrf_kernel<T, KM>;
   const size_t smem = tile_smem_bytes<T, KM>();
-  static const int per_sm = [&] {  // one per (T, KM) instantiation
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
-    return nb > 0 ? nb : 1;
-  }();
-  const long long tasks = ntask;
-  static const int cap = [] {
-    const char* v = std::getenv("RFPK_TILE_PER_SM");
-    return v ? std::atoi(v) : 0;
-  }();
+  const int per_sm = kernel_setup(kern, TPT, smem);
+  const long long tasks = chol_task_count(nt, mt);
   // two CTAs per SM up to ~12k columns: the diagonal chain's CTA then shares
   // its SM with one other task instead of two (measured: potrf 8192 7.69 ->
   // 7.22 ms, 4000 2.22 -> 2.13); the bulk-bound larger orders keep three
-  int ps = per_sm > 2 && nt <= 192 ? 2 : per_sm;
-  if (cap > 0 && cap < per_sm) ps = cap;
+  const int ps = per_sm > 2 && nt <= 192 ? 2 : per_sm;
   long long grid = (long long)ps * num_sms();
   if (grid > tasks) grid = tasks;
+  KernelClock kc(c.st);
   kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt,
-                                            InputGate::flags(), trace);
+                                            InputGate::flags());
   RFPK_CHECK_LAUNCH();
-  if (trace) {
-    cudaStreamSynchronize(c.st);
-    FILE* f = fopen(trace_file, "a");
-    if (f) {
-      fprintf(f, "# n=%lld nt=%d grid=%lld\n", (long long)A.m, nt, grid);
-      for (long long t = 0; t < ntask; ++t) {
-        const unsigned long long* r = trace + 8 * t;
-        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 28,
-                (r[4] >> 14) & 0x3fff, r[4] & 0x3fff, r[5], r[0], r[1], r[2], r[3], r[6], r[7]);
-      }
-      fclose(f);
-    }
-    cudaFree(trace);
-  }
+  kc.stop("tile_potrf", A.m, ncols);
   return 0;
 }
 
@@ -824,8 +777,7 @@ struct TrsmArgs {
 
 template <typename T, bool AK, bool BKM, int TN>
 __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const TrsmArgs& a,
-                          int* done, int i, int c, T* sm, int* s_ok, unsigned long long* tr) {
-  if (tr && threadIdx.x == 0) { tr[0] = gtimer(); tr[4] = (unsigned long long)((i << 16) | c); tr[5] = blockIdx.x; }
+                          int* done, int i, int c, T* sm, int* s_ok) {
   if (a.agate) {  // Tm's row block i and W_i come from a concurrent tile potrf
     if (threadIdx.x == 0) {
       const int* f = a.agate + (i64)i * a.agate_stride;
@@ -911,10 +863,10 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
           rr += __ffs(~m) - 1;
           break;
         }
-        if (lane == 0) {
-          if (rr > q + 1) fence_acquire();
-          s_ready_sh = rr;
-        }
+        // every lane that did a relaxed load of a flag orders it before the
+        // barrier with its own fence (rr is warp-uniform; one MEMBAR per warp)
+        if (rr > q + 1) fence_acquire();
+        if (lane == 0) s_ready_sh = rr;
       }
       __syncthreads();
       ready = s_ready_sh;
@@ -1028,7 +980,6 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   cp_async_wait<0>();
   __syncthreads();
   if (nprev > 0 && !*s_ok) return false;
-  if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
     // (the gate's flags cover 64-column chunks; c counts TN-wide blocks)
@@ -1100,7 +1051,6 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   if (tid == 0) {
     __threadfence();
     st_release(done + (i64)i * a.nc + c, 1);
-    if (tr) tr[3] = gtimer();
   }
   return true;
 }
@@ -1110,8 +1060,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
 template <typename T, bool AK, bool BKM, int TN>
 __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_cplx<T>::value) ? 1 : 3)))
     tile_trsm_kernel(View<T> Tm, View<T> B, const T* W,
-                                                        TrsmArgs a, int* sync, const int* info,
-                                                        unsigned long long* trace) {
+                                                        TrsmArgs a, int* sync, const int* info) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
@@ -1133,8 +1082,7 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
     if (t >= total) return;
     const int step = (int)(t / a.nc), c = (int)(t % a.nc);
     const int i = a.lower ? step : a.nb - 1 - step;
-    if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok, trace ? trace + 8 * t : nullptr))
-      return;
+    if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok)) return;
   }
 }
 
@@ -1152,402 +1100,18 @@ template <typename T, bool AK, bool BKM, int TN>
 int trsm_launch(View<T> Tm, View<T> B, const T* W, const TrsmArgs& a, int* sync, Ctx c) {
   auto kern = tile_trsm_kernel<T, AK, BKM, TN>;
   const size_t smem = trsm_smem_bytes<T, AK, BKM, TN>();
-  static const int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
-    return nb > 0 ? nb : 1;
-  }();
+  const int per_sm = kernel_setup(kern, TPT, smem);
   const long long tasks = (long long)a.nb * a.nc;
   long long grid = (long long)per_sm * num_sms();
   if (grid > tasks) grid = tasks;
-  static const char* trace_file = std::getenv("RFPK_TILE_TRACE");
-  unsigned long long* trace = nullptr;
-  if (trace_file) {
-    cudaMallocManaged(&trace, tasks * 8 * sizeof(unsigned long long));
-    cudaMemset(trace, 0, tasks * 8 * sizeof(unsigned long long));
-  }
-  kern<<<(unsigned)grid, TPT, smem, c.st>>>(Tm, B, W, a, sync, c.info, trace);
+  KernelClock kc(c.st);
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(Tm, B, W, a, sync, c.info);
   RFPK_CHECK_LAUNCH();
-  if (trace) {
-    cudaStreamSynchronize(c.st);
-    FILE* f = fopen(trace_file, "a");
-    if (f) {
-      fprintf(f, "# trsm n=%d nrhs=%d grid=%lld\n", a.n, a.nrhs, grid);
-      for (long long t = 0; t < tasks; ++t) {
-        const unsigned long long* r = trace + 8 * t;
-        fprintf(f, "%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", r[4] >> 16, r[4] & 0xffff, r[5], r[0],
-                r[1], r[2], r[3]);
-      }
-      fclose(f);
-    }
-    cudaFree(trace);
-  }
-  return 0;
-}
-
-// ------------------------------------------------------ two-region solve
-// One substitution sweep of pftrs (rfp.py:118-136) through BOTH triangles of
-// the RFP buffer in ONE dataflow launch (real data):
-//
-//   region 0:  op(Ta) X0 = B0                  (tasks as in tile_trsm_kernel)
-//   region 1:  op(Tb) X1 = B1 - P X0           (P = S1 or S1^T)
-//
-// A region-1 task's K loop first runs over P's 64-column chunks, chunk k
-// gated on region 0's done(k, c) -- the reference's GEMM between the two
-// solves, folded in as a prefix of the left-looking accumulation -- then over
-// its own triangle's chain.  The GEMM work thereby fills the chains' tails
-// and the three launches (trsm, gemm, trsm) become one.  T1, T2 and S1 come
-// in both orientations depending on TRANSR / UPLO and the sweep direction, so
-// the A operand's smem layout (K-major or M-major) is chosen per chunk and
-// recorded per pipeline stage; B is column- or row-major for the whole sweep.
-struct Trsm2Region {
-  View<double> Tm, B;  // n x n triangle (lower, or upper solved bottom-up), n x nrhs
-  const double* W;     // its 64-leaf inverses (lower form; wtrans for upper)
-  int n, nb;
-  int* done;           // nb x nc flags
-};
-struct Trsm2Args {
-  Trsm2Region r[2];
-  View<double> P;  // r[1].n x r[0].n
-  int nrhs, nc, lower;
-};
-
-template <typename LA, typename LB, int TN>
-__device__ __forceinline__ void stage_mma(const double* as, const double* bs,
-                                          double (&acc)[TrsmTile<TN>::MI][TrsmTile<TN>::NI][4]) {
-  using WL = TrsmTile<TN>;
-#pragma unroll
-  for (int kk = 0; kk < TileCfg<double>::BK; kk += 4) {
-    double af[WL::MI][2], bf[WL::NI];
-#pragma unroll
-    for (int mi = 0; mi < WL::MI; ++mi) {
-      af[mi][0] = as[kk * LA::KS + (mi * 16) * LA::RS];
-      af[mi][1] = as[kk * LA::KS + (mi * 16 + 8) * LA::RS];
-    }
-#pragma unroll
-    for (int ni = 0; ni < WL::NI; ++ni) bf[ni] = bs[kk * LB::KS + (ni * 8) * LB::RS];
-#pragma unroll
-    for (int mi = 0; mi < WL::MI; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < WL::NI; ++ni) dmma16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
-  }
-}
-
-template <bool BKM, int TN, bool PREW> struct Trsm2Smem {
-  using C = TileCfg<double>;
-  using LK = SmemLayout<double, TP, C::BK, true>;
-  using LM = SmemLayout<double, TP, C::BK, false>;
-  using LB = SmemLayout<double, TN, C::BK, BKM>;
-  static constexpr int ASZ = LK::SIZE > LM::SIZE ? LK::SIZE : LM::SIZE;
-  static constexpr int PIPE = STAGES * (ASZ + LB::SIZE);
-  static constexpr int STILE = (TN > TP ? TN : TP) * LD64;
-  // W'_i: prefetched at the task start past the pipeline, or read after the
-  // accumulation into the slot behind the S tile
-  static constexpr int WOFF = PREW ? (PIPE > STILE ? PIPE : STILE) : STILE;
-  static constexpr int END = WOFF + TP * LD64;
-  static constexpr size_t BYTES = (size_t)(END > PIPE ? END : PIPE) * sizeof(double);
-};
-
-template <bool BKM, int TN, bool PREW>
-__device__ void trsm2_task(const Trsm2Args& a, int reg, int i, int c, double* sm, int& s_ready) {
-  using T = double;
-  using C = TileCfg<T>;
-  using SM = Trsm2Smem<BKM, TN, PREW>;
-  using LK = typename SM::LK;
-  using LM = typename SM::LM;
-  using LB = typename SM::LB;
-  using WL = TrsmTile<TN>;
-  constexpr int MI = WL::MI, NI = WL::NI, BK = C::BK, SPC = C::SPC;
-  const Trsm2Region& R = a.r[reg];
-  const Trsm2Region& R0 = a.r[0];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WL::WMW, wn = warp / WL::WMW, gq = lane >> 2, tq = lane & 3;
-  T* As = sm;
-  T* Bs = sm + STAGES * SM::ASZ;
-  T* const Wpre = sm + SM::WOFF;
-  if constexpr (PREW) {  // W'_i depends on no task: fetch it now (oldest cp.async group)
-    const T* w = R.W + (i64)i * TP * TP;
-    const bool wt = !a.lower;
-    for (int e = tid; e < TP * TP; e += TPT) {
-      const int r = e & 63, k = e >> 6;
-      cp_async8(wt ? Wpre + (k + r * LD64) : Wpre + (r + k * LD64), w + e, true);
-    }
-    cp_async_commit();
-  }
-  const int nprev = a.lower ? i : R.nb - 1 - i;
-  const int npre = reg ? R0.nb : 0;
-  const int KT = (npre + nprev) * SPC;
-
-  TileLoader<T, TP, BK, TPT, true> lk;
-  TileLoader<T, TP, BK, TPT, false> lm;
-  TileLoader<T, TN, BK, TPT, BKM> lb;
-  double acc[MI][NI][4];
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[mi][ni][r] = 0.0;
-
-  int kvalid = TP;
-  bool akm = false;       // layout of the chunk being loaded
-  unsigned kmbits = 0;    // bit s: pipeline slot s holds a K-major A stage
-  const int nq = npre + nprev;
-  auto chunk_of = [&](int q) {
-    return q < npre ? (a.lower ? q : npre - 1 - q) : (a.lower ? q - npre : R.nb - 1 - (q - npre));
-  };
-  auto flag_of = [&](int q) { return (q < npre ? R0.done : R.done) + (i64)chunk_of(q) * a.nc + c; };
-  // chunks [0, ready) are known published: a chunk beyond waits for its flag,
-  // then warp 0 scans ahead 32 flags per round trip and one acquire fence
-  // covers every chunk found published (one barrier instead of one per chunk)
-  int ready = 0;
-  auto open_chunk = [&](int q) {
-    if (q >= ready) {
-      if (warp == 0) {
-        if (lane == 0) spin_wait_acquire(flag_of(q));  // the chain's critical wait: no fence
-        __syncwarp();
-        int rr = q + 1;
-        for (;;) {
-          const int qq = rr + lane;
-          const bool ok = qq < nq && ld_relaxed(flag_of(qq));
-          const unsigned m = __ballot_sync(0xffffffffu, ok);
-          if (m == 0xffffffffu) { rr += 32; continue; }
-          rr += __ffs(~m) - 1;
-          break;
-        }
-        if (lane == 0) {
-          if (rr > q + 1) fence_acquire();
-          s_ready = rr;
-        }
-      }
-      __syncthreads();
-      ready = s_ready;
-    }
-    const bool pre = q < npre;
-    const int kk = chunk_of(q);
-    const View<T>& A = pre ? a.P : R.Tm;
-    const View<T>& Bv = pre ? R0.B : R.B;
-    akm = A.rs != 1;
-    if (akm) lk.init(A.p + (i64)kk * TP, A.rs, i * TP, R.n, tid);
-    else lm.init(A.p + (i64)kk * TP * A.cs, A.cs, i * TP, R.n, tid);
-    lb.init(Bv.p + (i64)kk * TP * Bv.rs, BKM ? Bv.cs : Bv.rs, c * TN, a.nrhs, tid);
-    const int kn = pre ? R0.n : R.n;
-    kvalid = kn - kk * TP < TP ? kn - kk * TP : TP;
-  };
-  auto load_stage = [&](int stage, int q) {
-    const int k0 = (q % SPC) * BK;
-    T* as = As + stage * SM::ASZ;
-    if (akm) {
-      if (kvalid == TP) lk.load(as);
-      else lk.load_pred(as, k0, kvalid, 0, A_FULL);
-      lk.advance();
-      kmbits |= 1u << stage;
-    } else {
-      if (kvalid == TP) lm.load(as);
-      else lm.load_pred(as, k0, kvalid, 0, A_FULL);
-      lm.advance();
-      kmbits &= ~(1u << stage);
-    }
-    if (kvalid == TP) lb.load(Bs + stage * LB::SIZE);
-    else lb.load_pred(Bs + stage * LB::SIZE, k0, kvalid, 0, A_FULL);
-    lb.advance();
-  };
-
-  constexpr bool BPRE = TN < TP;  // narrow tiles: B(i, c) into registers now
-  T bpre[BPRE ? MI : 1][BPRE ? NI : 1][4];
-  const i64 i0 = (i64)i * TP, c0 = (i64)c * TN;
-  const int mrows = R.n - (int)i0 < TP ? R.n - (int)i0 : TP;
-  const int ncols = a.nrhs - (int)c0 < TN ? a.nrhs - (int)c0 : TN;
-  if constexpr (BPRE) {
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
-          bpre[mi][ni][r] = (row < mrows && col < ncols) ? *R.B.at(i0 + row, c0 + col) : 0.0;
-        }
-  }
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) {
-      if (s % SPC == 0) open_chunk(s / SPC);
-      load_stage(s, s);
-    }
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int slot = kt % STAGES;
-    const bool km = (kmbits >> slot) & 1u;  // read before the refill below
-    const int nk = kt + STAGES - 1;
-    if (nk < KT) {
-      if (nk % SPC == 0) open_chunk(nk / SPC);
-      load_stage(nk % STAGES, nk);
-    }
-    cp_async_commit();
-    const T* bs = Bs + slot * LB::SIZE + (wn * WL::CW + gq) * LB::RS + tq * LB::KS;
-    if (km) {
-      const T* as = As + slot * SM::ASZ + (wm * WL::RW + gq) * LK::RS + tq * LK::KS;
-      stage_mma<LK, LB, TN>(as, bs, acc);
-    } else {
-      const T* as = As + slot * SM::ASZ + (wm * WL::RW + gq) * LM::RS + tq * LM::KS;
-      stage_mma<LM, LB, TN>(as, bs, acc);
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-
-  // S = B(i, c) - acc (zero outside the matrix), X = W'_i S
-  T* S = sm;
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
-        const bool in = row < mrows && col < ncols;
-        T bv;
-        if constexpr (BPRE) bv = bpre[mi][ni][r];
-        else bv = in ? *R.B.at(i0 + row, c0 + col) : 0.0;
-        S[row + col * LD64] = in ? bv - acc[mi][ni][r] : 0.0;
-      }
-  if constexpr (!PREW) {
-    const T* w = R.W + (i64)i * TP * TP;
-    const bool wt = !a.lower;
-    for (int e = tid; e < TP * TP; e += TPT) {
-      const int r = e & 63, k = e >> 6;
-      Wpre[wt ? k + r * LD64 : r + k * LD64] = __ldcg(w + e);
-    }
-  }
-  __syncthreads();
-  double x[1][MI][NI][4];
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) x[0][mi][ni][r] = 0.0;
-  smem_mm_ab<T, TN>(Wpre, S, x);
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
-        if (row < mrows && col < ncols) *R.B.at(i0 + row, c0 + col) = x[0][mi][ni][r];
-      }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release(R.done + (i64)i * a.nc + c, 1);
-  }
-}
-
-template <bool BKM, int TN, bool PREW>
-__global__ void __launch_bounds__(TPT, (PREW && TN == TP) ? 2 : 3)
-    tile_trsm2_kernel(Trsm2Args a, int* counter, const int* info) {
-  extern __shared__ __align__(16) double smem_d[];
-  __shared__ int s_task, s_ready;
-  if (info && *info) return;
-  const long long t0 = (long long)a.r[0].nb * a.nc;
-  const long long total = t0 + (long long)a.r[1].nb * a.nc;
-  for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
-    __syncthreads();
-    const long long t = s_task;
-    __syncthreads();
-    if (t >= total) return;
-    const int reg = t >= t0;
-    const long long u = reg ? t - t0 : t;
-    const int step = (int)(u / a.nc), c = (int)(u % a.nc);
-    const int i = a.lower ? step : a.r[reg].nb - 1 - step;
-    trsm2_task<BKM, TN, PREW>(a, reg, i, c, smem_d, s_ready);
-  }
-}
-
-template <bool BKM, int TN, bool PREW> int trsm2_launch(Trsm2Args a, int* counter, Ctx c) {
-  auto kern = tile_trsm2_kernel<BKM, TN, PREW>;
-  const size_t smem = Trsm2Smem<BKM, TN, PREW>::BYTES;
-  static const int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPT, smem);
-    return nb > 0 ? nb : 1;
-  }();
-  const long long tasks = (long long)(a.r[0].nb + a.r[1].nb) * a.nc;
-  long long grid = (long long)per_sm * num_sms();
-  if (grid > tasks) grid = tasks;
-  kern<<<(unsigned)grid, TPT, smem, c.st>>>(a, counter, c.info);
-  RFPK_CHECK_LAUNCH();
+  kc.stop("tile_trsm", Tm.m, B.n);
   return 0;
 }
 
 }  // namespace
-
-// One pftrs sweep through both RFP triangles (see tile_trsm2_kernel):
-// op(Ta) X0 = B0, then op(Tb) X1 = B1 - P X0, in place on B0 / B1, in ONE
-// launch.  lower: both triangles lower (forward sweep); else both upper,
-// solved bottom-up with their W taken transposed.  Returns -100 when the
-// operands do not fit the kernel (the caller then runs trsm, gemm, trsm).
-int trsm2_tiles(Ctx c, bool lower, View<double> Ta, View<double> B0, const double* Wa,
-                View<double> Tb, View<double> B1, const double* Wb, View<double> P) {
-  if (Ta.m == 0 || Tb.m == 0 || B0.n == 0) return -100;
-  // opt-in (RFPK_TRSM2=1): measured slower than trsm + gemm + trsm on the
-  // B200 (config 3's pftrs 22.8 vs 19.5 ms, n = 4000 0.78 vs 0.72 ms; see
-  // DESIGN.md section 9), kept parity-tested for the record
-  const char* on = std::getenv("RFPK_TRSM2");
-  if (!on || std::atoi(on) == 0 || InputGate::flags()) return -100;
-  auto unit_stride = [](const View<double>& v) { return v.rs == 1 || v.cs == 1; };
-  if (!unit_stride(Ta) || !unit_stride(Tb) || !unit_stride(P)) return -100;
-  // a degenerate (single-row / single-column) view: one fixed orientation
-  if ((Ta.rs == 1 && Ta.cs == 1) || (Tb.rs == 1 && Tb.cs == 1) || (P.rs == 1 && P.cs == 1))
-    return -100;
-  const bool bkm = B0.rs == 1 && B1.rs == 1;
-  if (!bkm && !(B0.cs == 1 && B1.cs == 1)) return -100;
-  if (B0.n != B1.n || P.m != Tb.m || P.n != Ta.m) return -100;
-  Trsm2Args a;
-  a.nrhs = (int)B0.n;
-  a.lower = lower ? 1 : 0;
-  a.P = P;
-  static const int narrow_max = [] {
-    const char* v = std::getenv("RFPK_TRSM_NARROW");
-    return v ? std::atoi(v) : 256;
-  }();
-  const int nb0 = (int)((Ta.m + TP - 1) / TP), nb1 = (int)((Tb.m + TP - 1) / TP);
-  const long long tasks64 = (long long)(nb0 + nb1) * ((B0.n + TP - 1) / TP);
-  const int tn = (B0.n <= narrow_max || tasks64 <= 10LL * num_sms()) ? 16 : TP;
-  a.nc = (int)((B0.n + tn - 1) / tn);
-  const size_t ints = SYNC_HDR + (size_t)(nb0 + nb1) * a.nc;
-  int* sync = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
-  if (e != cudaSuccess) return (int)e;
-  if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
-  a.r[0] = Trsm2Region{Ta, B0, Wa, (int)Ta.m, nb0, sync + SYNC_HDR};
-  a.r[1] = Trsm2Region{Tb, B1, Wb, (int)Tb.m, nb1, sync + SYNC_HDR + (size_t)nb0 * a.nc};
-  int rc;
-  // 64-wide tiles: W'_i prefetched at two CTAs per SM, or read late at three
-  static const bool prew = [] {
-    const char* v = std::getenv("RFPK_TRSM2_PREW");
-    return v && std::atoi(v) != 0;
-  }();
-  if (tn == 16) rc = bkm ? trsm2_launch<true, 16, true>(a, sync, c)
-                         : trsm2_launch<false, 16, true>(a, sync, c);
-  else if (prew) rc = bkm ? trsm2_launch<true, TP, true>(a, sync, c)
-                          : trsm2_launch<false, TP, true>(a, sync, c);
-  else rc = bkm ? trsm2_launch<true, TP, false>(a, sync, c)
-                : trsm2_launch<false, TP, false>(a, sync, c);
-  cudaFreeAsync(sync, c.st);
-  return rc;
-}
 
 // conj?(Tm) X = B in place with the dataflow kernel (W: lower-form 64-block
 // inverses; wtrans for Tm upper).  Returns -100 for unsupported strides.
@@ -1569,21 +1133,13 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   // SM: pftrf's S1 solve at n = 4000 0.72 -> 0.52 ms, n = 1000 0.16 ->
   // 0.07 ms); measured slower with more tasks (S1 at n = 6000 1.48 vs 1.31
   // ms, 16384 26.8 vs 17.6 ms; pftrs 16384 x 1024 3.4 vs 2.7 ms per solve)
-  static const int narrow_max = [] {
-    const char* v = std::getenv("RFPK_TRSM_NARROW");
-    return v ? std::atoi(v) : 256;
-  }();
+  constexpr int narrow_max = 256;
   // (a 64 x 128 tile with 2 x 2 warps of 32 x 64 measured slower on the S1
   // solve of config 3: 255 registers with spills, two CTAs per SM, 18.4 vs
   // 17.7 ms)
   const long long tasks64 = (long long)a.nb * ((B.n + TP - 1) / TP);
-  static const int tn_force = [] {
-    const char* v = std::getenv("RFPK_TRSM_TN");
-    return v ? std::atoi(v) : 0;
-  }();
-  int tn = (!is_cplx<T>::value &&
-            (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;
-  if (!is_cplx<T>::value && (tn_force == 16 || tn_force == 32 || tn_force == 64)) tn = tn_force;
+  const int tn = (!is_cplx<T>::value &&
+                  (B.n <= narrow_max || tasks64 <= 10LL * num_sms())) ? 16 : TP;
   a.nc = (int)((B.n + tn - 1) / tn);
   a.lower = lower ? 1 : 0;
   a.conj = conj ? 1 : 0;
@@ -1595,11 +1151,7 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.aabort = aabort;
   a.aguard = agate ? aabort - 1 : nullptr;  // the producer's task counter (sync[0])
   a.aguard_keep = num_sms();
-  static const int scan = [] {
-    const char* v = std::getenv("RFPK_TRSM_SCAN");
-    return v ? std::atoi(v) : 1;
-  }();
-  a.scan = scan;
+  a.scan = 1;
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
@@ -1608,16 +1160,7 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   // B operand = X^T (nrhs x K): K-major when B is column-major
   const bool bkm = B.rs == 1;
   int rc;
-  if (tn == 32) {
-    if constexpr (!is_cplx<T>::value) {
-      if (ak) rc = bkm ? trsm_launch<T, true, true, 32>(Tm, B, W, a, sync, c)
-                       : trsm_launch<T, true, false, 32>(Tm, B, W, a, sync, c);
-      else rc = bkm ? trsm_launch<T, false, true, 32>(Tm, B, W, a, sync, c)
-                    : trsm_launch<T, false, false, 32>(Tm, B, W, a, sync, c);
-    } else {
-      rc = -100;
-    }
-  } else if (tn == 16) {
+  if (tn == 16) {
     if constexpr (!is_cplx<T>::value) {
       if (ak) rc = bkm ? trsm_launch<T, true, true, 16>(Tm, B, W, a, sync, c)
                        : trsm_launch<T, true, false, 16>(Tm, B, W, a, sync, c);
@@ -1682,11 +1225,12 @@ template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
   return potrf_panel_tiles(c, A, A.m, base, W);
 }
 
+// Library side streams for the overlapped steps, per host thread and device
+// (thread_local): two callers on their own streams never share a fork/join
+// event or a side stream, so a join can never silently lose a dependency.
 OverlapStreams& overlap_streams() {
-  static OverlapStreams per_dev[16];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  OverlapStreams& S = per_dev[dev & 15];
+  static thread_local OverlapStreams per_dev[MAX_DEVICES];
+  OverlapStreams& S = per_dev[cur_device() & (MAX_DEVICES - 1)];
   if (!S.ok) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -1697,6 +1241,31 @@ OverlapStreams& overlap_streams() {
   }
   return S;
 }
+
+OverlapStreams::~OverlapStreams() {
+  if (!ok) return;
+  cudaStreamDestroy(hi);
+  cudaStreamDestroy(lo);
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+namespace {
+// Device-wide order of the spin-coupled potrf || trsm pairs: the solve's
+// waiting CTAs need the potrf's CTAs to become resident beside them, which
+// one pair at a time guarantees (at most num_sms() waiting CTAs, see aguard)
+// but several pairs from different host threads could not -- enough waiting
+// CTAs of several solves could fill every slot.  Each pair's fork therefore
+// waits (stream-ordered, never spinning) for the previous pair's join on the
+// same device.
+struct PairChain {
+  std::mutex mu;
+  cudaEvent_t last = nullptr;
+};
+PairChain& pair_chain() {
+  static PairChain chains[MAX_DEVICES];
+  return chains[cur_device() & (MAX_DEVICES - 1)];
+}
+}  // namespace
 
 // potrf('L', A) and the solve conj?(A) X = B that consumes its factor, as
 // two CONCURRENT dataflow launches: the tile potrf on a high-priority stream
@@ -1719,11 +1288,7 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* 
   if constexpr (is_cplx<T>::value) {
     return -100;
   } else {
-    static const bool off = [] {
-      const char* v = std::getenv("RFPK_NO_OVERLAP");
-      return v && std::atoi(v) != 0;
-    }();
-    if (off || A.m <= TP || B.empty() || !W) return -100;
+    if (!tune(TK_OVERLAP) || A.m <= TP || B.empty() || !W) return -100;
     // row-major B only: the column-major-B trsm variants take ~250 registers
     // and do not fit beside two potrf CTAs on an SM (UPLO='U' at n = 12000:
     // 11.18 ms overlapped vs 10.9 in sequence)
@@ -1745,9 +1310,13 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* 
       if (psync) cudaFreeAsync(psync, c.st);
       return (int)e;
     }
+    PairChain& pc = pair_chain();
+    std::lock_guard<std::mutex> lk(pc.mu);
     e = cudaEventRecord(S.ev[0], c.st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.hi, S.ev[0], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(S.lo, S.ev[0], 0);
+    if (e == cudaSuccess && pc.last) e = cudaStreamWaitEvent(S.hi, pc.last, 0);
+    if (e == cudaSuccess && pc.last) e = cudaStreamWaitEvent(S.lo, pc.last, 0);
     if (e != cudaSuccess) {
       cudaFreeAsync(psync, c.st);
       return (int)e;
@@ -1769,6 +1338,13 @@ int potrf_trsm_overlap(Ctx c, View<T> A, T* W, bool conj, View<T> B, const int* 
     cudaEventRecord(S.ev[2], S.lo);
     cudaStreamWaitEvent(c.st, S.ev[1], 0);
     cudaStreamWaitEvent(c.st, S.ev[2], 0);
+    // this pair's join becomes the next pair's fork dependency
+    cudaEvent_t joined = nullptr;
+    if (cudaEventCreateWithFlags(&joined, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(joined, c.st);
+      if (pc.last) cudaEventDestroy(pc.last);  // pending waits keep their snapshot
+      pc.last = joined;
+    }
     cudaFreeAsync(psync, c.st);
     return rc;
   }

@@ -244,34 +244,25 @@ def test_syrk_large(K, uplo, trans):
     assert np.array_equal(cd.cpu().numpy()[other], c[other])
 
 
-def test_forced_wide_tiles_triangular():
-    """RFPK_TILE=64128 forces the 64 x 128 tiles onto SYRK too (the non-square
-    triangular tile enumeration); the env is read once per process, so this
-    runs in a child interpreter."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch
-from oracle import rfp_oracle as O
-from paper_0901_1696_b200 import kernels as K
-for uplo in "LU":
-    g = np.random.default_rng(5)
-    a = np.asfortranarray(g.standard_normal((700, 19)))
-    c = np.asfortranarray(g.standard_normal((700, 700)))
-    want = c.copy(); O.syrk_herk(uplo, "N", -1.0, a, 1.0, want, False)
-    cd = torch.from_numpy(c).cuda(); K.syrk_herk(uplo, "N", -1.0, torch.from_numpy(a).cuda(), 1.0, cd)
-    got = cd.cpu().numpy()
-    assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max(), uplo
-    other = np.triu(np.ones((700, 700), bool), 1) if uplo == "L" else np.tril(np.ones((700, 700), bool), -1)
-    assert np.array_equal(got[other], c[other]), uplo
-print("ok")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, RFPK_TILE="64128", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
-                         text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+def test_forced_wide_tiles_triangular(K):
+    """Tuning gemm_wide=1 forces the 64 x 128 tiles onto SYRK too (the
+    non-square triangular tile enumeration): other triangle untouched,
+    values against the oracle."""
+    from paper_0901_1696_b200 import _capi
+    with _capi.tuning(gemm_wide=1):
+        for uplo in "LU":
+            g = np.random.default_rng(5)
+            a = np.asfortranarray(g.standard_normal((700, 19)))
+            c = np.asfortranarray(g.standard_normal((700, 700)))
+            want = c.copy()
+            O.syrk_herk(uplo, "N", -1.0, a, 1.0, want, False)
+            cd = torch.from_numpy(c).cuda()
+            K.syrk_herk(uplo, "N", -1.0, torch.from_numpy(a).cuda(), 1.0, cd)
+            got = cd.cpu().numpy()
+            assert np.abs(got - want).max() <= TOL * np.abs(want).max(), uplo
+            other = (np.triu(np.ones((700, 700), bool), 1) if uplo == "L"
+                     else np.tril(np.ones((700, 700), bool), -1))
+            assert np.array_equal(got[other], c[other]), uplo
 
 
 @pytest.mark.parametrize("cplx", [False, True])

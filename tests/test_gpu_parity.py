@@ -564,6 +564,87 @@ def test_concurrent_host_threads_on_own_streams(P):
 
 
 # ---------------------------------------------------------------- SPEC acceptance checks
+@pytest.mark.slow
+def test_reentrant_large_orders_on_own_streams(P):
+    """Re-entrancy at orders where the library forks its own side streams:
+    n1 > 4096, so pftrf runs potrf(T1) || S1 solve as two spin-coupled
+    launches and pfsv runs pftrs part 1 beside potrf(T2).  Four host threads,
+    each on its own stream, run pftrf and pfsv on their own matrices five
+    times; every result must be bit-identical to the same call made alone
+    (single thread, nothing else on the device)."""
+    import threading
+    conv, rfp = P.convert, P.rfp
+    cases = [(8194, "L", "N"), (9001, "L", "N"), (9500, "U", "N"), (10000, "L", "T")]
+    inputs_ = []
+    for k, (n, uplo, transr) in enumerate(cases):
+        g = torch.Generator(device="cuda").manual_seed(50 + k)
+        bm = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+        a = bm @ bm.t() / n
+        a.diagonal().add_(1.0)
+        del bm
+        src = conv.trttf(a, uplo, transr).data
+        b = torch.randn(64, n, dtype=torch.float64, device="cuda", generator=g).t()
+        inputs_.append((src, b))
+        del a
+
+    def run(k):
+        n, uplo, transr = cases[k]
+        src, b = inputs_[k]
+        d = P.layout.make_descriptor(n, uplo, transr)
+        r1 = conv.RfpTriangle(src.clone(), d)
+        assert rfp.pftrf(r1) == 0
+        r2 = conv.RfpTriangle(src.clone(), d)
+        x = b.clone()
+        assert rfp.pfsv(r2, x) == 0
+        torch.cuda.current_stream().synchronize()
+        return r1.data, r2.data, x
+
+    alone = [run(k) for k in range(len(cases))]
+    torch.cuda.synchronize()
+    errs = []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(5):
+                    got = run(k)
+                    for u, v in zip(got, alone[k]):
+                        if not torch.equal(u, v):
+                            errs.append(f"thread {k} rep {rep}: result differs")
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "a thread hung"
+    assert not errs, errs
+
+
+def test_stream_of_another_device_is_served_on_its_device(P):
+    """The C ABI switches to the device owning the caller's stream (and back):
+    a pftrf on cuda:0's stream issued while another device is current.  With
+    one GPU the check is that the current device is restored and the call
+    succeeds from a non-default current stream."""
+    conv, rfp = P.convert, P.rfp
+    n = 300
+    a = O.spd_matrix(n, 3, "n")
+    f = O.trttf(a, "L", "N")
+    assert O.pftrf(f, n, "L", "N") == 0
+    ndev = torch.cuda.device_count()
+    other = 1 if ndev > 1 else 0
+    r = conv.trttf(a, "L", "N")
+    s = torch.cuda.Stream(device=0)
+    with torch.cuda.device(other):
+        with torch.cuda.stream(s):
+            assert rfp.pftrf(r) == 0
+        assert torch.cuda.current_device() == other
+    assert rel(r.data, f) <= TOL
+
+
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
 @pytest.mark.parametrize("cplx", [False, True])
@@ -691,126 +772,117 @@ def test_pftrf_panel_path(P, transr, bad):
         assert want == bad + 1
 
 
-def _pftrs_split_vs_fused(P, r, b, monkeypatch):
-    """pftrs with the two-region sweeps (opt-in RFPK_TRSM2=1) and with the
-    default split trsm / gemm / trsm sequence."""
-    monkeypatch.setenv("RFPK_TRSM2", "1")
-    x = b.clone()
-    P.rfp.pftrs(r, x)
-    monkeypatch.delenv("RFPK_TRSM2")
-    y = b.clone()
-    P.rfp.pftrs(r, y)
-    return x, y
+def _kernel_launches(prefix, fn):
+    """Launches of library kernels whose kernel-clock label starts with
+    ``prefix`` (e.g. "kernel tile_copy") during fn(), and fn()'s result."""
+    from paper_0901_1696_b200 import _capi
+    torch.cuda.synchronize()
+    with _capi.phase_clock() as pc:
+        out = fn()
+        torch.cuda.synchronize()
+    return out, sum(c for lab, (_, c) in pc.table().items() if lab.startswith(prefix))
 
 
-@pytest.mark.parametrize("uplo", "LU")
-@pytest.mark.parametrize("transr", "NT")
-@pytest.mark.parametrize("n,nrhs,rowmajor", [(300, 5, False), (1001, 100, False),
-                                             (2049, 300, True), (1100, 17, True)])
-def test_pftrs_two_region_sweeps_vs_oracle(P, monkeypatch, uplo, transr, n, nrhs, rowmajor):
-    """The fused forward / backward sweeps (trsm2_tiles: both triangles and the
-    S1 product in one launch each) against the oracle and the split sequence,
-    for column- and row-major right-hand sides, odd and even n."""
-    conv, rfp = P.convert, P.rfp
-    a = O.spd_matrix(n, 7 + n, "n")
-    buf = O.trttf(a, uplo, transr)
-    f = buf.copy()
-    assert O.pftrf(f, n, uplo, transr) == 0
-    r = conv.trttf(a, uplo, transr)
-    assert rfp.pftrf(r) == 0
-    bh = np.random.default_rng(n + nrhs).standard_normal((n, nrhs))
-    b = torch.from_numpy(np.ascontiguousarray(bh) if rowmajor else np.asfortranarray(bh)).cuda()
-    assert (b.stride(1) == 1) == rowmajor
-    x, y = _pftrs_split_vs_fused(P, r, b, monkeypatch)
-    xo = np.asfortranarray(bh)
-    O.pftrs(f, n, uplo, transr, xo)
-    assert rel(x, xo) <= TOL
-    assert rel(x, y) <= TOL
-
-
-@pytest.mark.parametrize("uplo,transr", [("L", "N"), ("U", "T")])
-def test_pftrs_two_region_wide_tiles(P, monkeypatch, uplo, transr):
-    """n = 6000, nrhs = 1024: enough tasks for the 64-wide tiles of the fused
-    sweeps; residual and agreement with the split sequence."""
-    conv, rfp = P.convert, P.rfp
-    n, nrhs = 6000, 1024
-    g = torch.Generator(device="cuda").manual_seed(11)
-    bm = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
-    a = bm @ bm.t() / n
-    a.diagonal().add_(1.0)
-    r = conv.trttf(a, uplo, transr)
-    assert rfp.pftrf(r) == 0
-    b = torch.randn(nrhs, n, dtype=torch.float64, device="cuda", generator=g).t()
-    x, y = _pftrs_split_vs_fused(P, r, b, monkeypatch)
-    res = float((a @ x - b).norm() / (a.norm() * x.norm() * n * 2.0 ** -53))
-    assert res <= 10
-    assert rel(x, y) <= TOL
+def _phase_count(label, fn):
+    """Number of SRPA phases named ``label`` the phase clock saw during fn()
+    (direct calls only -- the forced paths below are never graph-captured
+    because every call gets fresh buffers)."""
+    import ctypes
+    from paper_0901_1696_b200 import _capi
+    lib = _capi.lib()
+    lib.rfpk_phase_clock(1)
+    try:
+        out = fn()
+        ms, cnt = ctypes.c_double(0.0), ctypes.c_int64(0)
+        lib.rfpk_phase_time(label.encode(), ctypes.byref(ms), ctypes.byref(cnt))
+    finally:
+        lib.rfpk_phase_clock(0)
+    return out, int(cnt.value)
 
 
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
 @pytest.mark.parametrize("n", [777, 1299])
 @pytest.mark.parametrize("cplx", [False, True])
-def test_potrf_row_major_block_copy(P, monkeypatch, uplo, transr, n, cplx):
+def test_potrf_row_major_block_copy(P, uplo, transr, n, cplx):
     """A diagonal block whose lower view is row-major (T2 for TRANSR='N', T1
-    for 'T') is factored in a column-major copy (forced here with
-    RFPK_T2_COPY_MIN=64; default from order 2048 up, real data only -- the
-    complex cases check that the direct path is unaffected): factor within
-    TOL of the oracle, and failure indices inside either block are the
-    reference's."""
+    for 'T') is factored in a column-major copy (forced here with tuning
+    t2_copy_min=64 -- the copies show up as extra launches; default from
+    order 2048 up, real data only -- the complex cases check that the direct
+    path is unaffected): factor within TOL of the oracle, and failure indices
+    inside either block are the reference's."""
+    from paper_0901_1696_b200 import _capi
     conv, rfp = P.convert, P.rfp
-    monkeypatch.setenv("RFPK_T2_COPY_MIN", "64")
     a = O.spd_matrix(n, 31 + n, "n", complex_=cplx)
     f = O.trttf(a, uplo, transr)
     assert O.pftrf(f, n, uplo, transr) == 0
-    r = conv.trttf(a, uplo, transr)
-    assert rfp.pftrf(r) == 0
-    assert rel(r.data, f) <= TOL
-    for k in (2, n - 3):  # inside the leading block, inside the trailing one
-        bad = a.copy()
-        bad[k, k] = -1.0
-        fb = O.trttf(bad, uplo, transr)
-        want = O.pftrf(fb, n, uplo, transr)
-        assert want == k + 1
-        rb = conv.trttf(bad, uplo, transr)
-        assert rfp.pftrf(rb) == want
+    info0, plain = _kernel_launches("kernel tile_copy",
+                                    lambda: rfp.pftrf(conv.trttf(a, uplo, transr)))
+    with _capi.tuning(t2_copy_min=64):
+        r = conv.trttf(a, uplo, transr)
+        info, forced = _kernel_launches("kernel tile_copy", lambda: rfp.pftrf(r))
+        assert info == info0 == 0
+        assert rel(r.data, f) <= TOL
+        # real data, TRANSR='N': T2's lower view is row-major and goes through
+        # the copy (two more tile copies); 'T': T1 is the row-major one, but it
+        # is factored in the [T1; S1] panel at these orders either way
+        assert forced - plain == (2 if (not cplx and transr == "N") else 0)
+        for k in (2, n - 3):  # inside the leading block, inside the trailing one
+            bad = a.copy()
+            bad[k, k] = -1.0
+            fb = O.trttf(bad, uplo, transr)
+            want = O.pftrf(fb, n, uplo, transr)
+            assert want == k + 1
+            rb = conv.trttf(bad, uplo, transr)
+            assert rfp.pftrf(rb) == want
 
 
 @pytest.mark.parametrize("uplo", "LU")
-def test_potrf_trsm_overlap_info_and_factor(P, monkeypatch, uplo):
-    """Above the panel limit (forced low: RFPK_PANEL_MAX=256) potrf(T1) and the
-    S1 solve run as two concurrent launches, the solve gated on the potrf's
-    diagonal flags: factor within TOL of the oracle, and a failure inside T1
-    (every gated solve task must then exit) returns the reference's index
-    without hanging."""
+def test_potrf_trsm_overlap_info_and_factor(P, uplo):
+    """Above the panel limit (forced low: tuning panel_max=256) potrf(T1) and
+    the S1 solve run as two concurrent launches, the solve gated on the
+    potrf's diagonal flags (the phase clock sees the overlapped phase; 'U'
+    keeps the sequence, its column-major-B solve does not fit beside the
+    potrf): factor within TOL of the oracle, and a failure inside T1 (every
+    gated solve task must then exit) returns the reference's index without
+    hanging."""
+    from paper_0901_1696_b200 import _capi
     conv, rfp = P.convert, P.rfp
-    monkeypatch.setenv("RFPK_PANEL_MAX", "256")
     n = 1403
     a = O.spd_matrix(n, 99, "n")
     f = O.trttf(a, uplo, "N")
     assert O.pftrf(f, n, uplo, "N") == 0
-    r = conv.trttf(a, uplo, "N")
-    assert rfp.pftrf(r) == 0
-    assert rel(r.data, f) <= TOL
-    for k in (1, 300, 650):
-        bad = a.copy()
-        bad[k, k] = -1.0
-        want = O.pftrf(O.trttf(bad, uplo, "N"), n, uplo, "N")
-        assert want == k + 1
-        assert rfp.pftrf(conv.trttf(bad, uplo, "N")) == want
+    with _capi.tuning(panel_max=256):
+        r = conv.trttf(a, uplo, "N")
+        info, seen = _phase_count("pftrf potrf(T1)||trsm(S1)", lambda: rfp.pftrf(r))
+        assert info == 0
+        assert seen == (1 if uplo == "L" else 0)
+        assert rel(r.data, f) <= TOL
+        for k in (1, 300, 650):
+            bad = a.copy()
+            bad[k, k] = -1.0
+            want = O.pftrf(O.trttf(bad, uplo, "N"), n, uplo, "N")
+            assert want == k + 1
+            assert rfp.pftrf(conv.trttf(bad, uplo, "N")) == want
 
 
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
 @pytest.mark.parametrize("n", [1, 130, 1501, 2049])
 @pytest.mark.parametrize("cplx", [False, True])
-def test_pfsv_device_matches_pftrf_pftrs(P, monkeypatch, uplo, transr, n, cplx):
+def test_pfsv_device_matches_pftrf_pftrs(P, uplo, transr, n, cplx):
     """rfp.pfsv (the first T1 solve and the S1 product run beside potrf(T2);
-    forced from T2 order 64 here) gives pftrf + pftrs's factor and solution
-    within TOL of the oracle; a failing factorization leaves b untouched and
-    returns the reference's index."""
+    forced from T2 order 64 here, and the phase clock must see that phase
+    whenever T2 reaches it) gives pftrf + pftrs's factor and solution within
+    TOL of the oracle; a failing factorization leaves b untouched and returns
+    the reference's index."""
+    from paper_0901_1696_b200 import _capi
+    with _capi.tuning(pfsv_overlap_min=64):
+        _pfsv_case(P, uplo, transr, n, cplx)
+
+
+def _pfsv_case(P, uplo, transr, n, cplx):
     conv, rfp = P.convert, P.rfp
-    monkeypatch.setenv("RFPK_PFSV_OVERLAP_MIN", "64")
     a = O.spd_matrix(n, 5 + n, "n", complex_=cplx)
     f = O.trttf(a, uplo, transr)
     assert O.pftrf(f, n, uplo, transr) == 0
@@ -820,7 +892,10 @@ def test_pfsv_device_matches_pftrf_pftrs(P, monkeypatch, uplo, transr, n, cplx):
     O.pftrs(f, n, uplo, transr, xo)
     r = conv.trttf(a, uplo, transr)
     b = torch.from_numpy(np.asfortranarray(bh)).cuda()
-    assert rfp.pfsv(r, b) == 0
+    info, seen = _phase_count("pftrf potrf(T2)||pftrs(T1,S1)", lambda: rfp.pfsv(r, b))
+    assert info == 0
+    t2_order = n // 2 if uplo == "L" else (n + 1) // 2
+    assert seen == (1 if t2_order >= 64 and n > 1 else 0)
     assert r.state is conv.FactorState.CHOLESKY
     assert rel(r.data, f) <= TOL
     assert rel(b, xo) <= TOL
