@@ -93,34 +93,46 @@ template <bool T> struct RV {
   __device__ __forceinline__ RV<!T> t() const { return RV<!T>{p}; }
 };
 
-// One warp: right-looking Cholesky of the 16 columns [c0, c0 + 16) of the
-// lower 32x32 view at p, rows c0 .. 31 (lane i holds row i's 16 panel
-// entries; lanes above c0 idle).  The pivot column is broadcast through colk
-// (double-buffered, 16-byte pairs); the next pivot comes straight from lane
-// p+1's registers.  16-wide rows halve the broadcast volume of a 32-wide
-// right-looking sweep.  Returns 0 or the failing pivot (1-based in the view;
+// 1/sqrt(x) for a positive normal x: the MUFU seed (rsqrt.approx.f64) and
+// one cubic Newton step, y (1 + e/2 + 3e^2/8) with e = 1 - x y^2 (the seed's
+// error cubed: below double rounding).  No range checks: a pivot that is not
+// > 0 is reported before its rsqrt is used, and the library's own rsqrt()
+// spends ~12 instructions per pivot on those checks.
+__device__ __forceinline__ double rsqrt_pivot(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
+// One warp: right-looking Cholesky of the 16 columns [C0, C0 + 16) of the
+// lower 32x32 view at p, rows C0 .. 31 (lane i holds row i's 16 panel
+// entries).  The pivot column is broadcast through colk (double-buffered,
+// 16-byte pairs); the next pivot comes straight from lane p+1's registers.
+// 16-wide rows halve the broadcast volume of a 32-wide right-looking sweep.
+// The view orientation T and the panel C0 are compile-time, so every row
+// slot is an immediate offset from the lane's row pointer.  Lanes whose row
+// lies above the panel (and the slots of a row above its diagonal, which
+// belong to the other RFP block) load and update garbage that is never
+// broadcast or stored.  Returns 0 or the failing pivot (1-based in the view;
 // NaN fails like the reference's `not d > 0`, kernels.py:436).
-__device__ __noinline__ int panel16(double* p, double* colk, int c0, bool T) {
+template <bool T, int C0>
+__device__ __noinline__ int panel16(double* p, double* colk) {
   __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(colk));
-  __builtin_assume(c0 == 0 || c0 == 16);
   const int lane = threadIdx.x & 31;
-  // row `lane`, panel column j: prow[T ? j : colstart(j)] (colstart is
-  // additive over the 16-aligned c0, so one body serves both panels and, with
-  // the orientation a runtime select, both views: 4 uses per matrix of one
-  // copy in the instruction cache)
-  double* prow = p + (T ? colstart(lane) + c0 : lane + colstart(c0));
+  double* prow = p + (T ? colstart(lane) + C0 : lane + colstart(C0));
   double r[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) r[j] = (c0 + j <= lane) ? prow[T ? j : colstart(j)] : 0.0;
-  int fail = 0;
-  double dkk = shfl(r[0], c0);
-  const double* cbase = colk + c0;
+  for (int j = 0; j < 16; ++j) r[j] = prow[T ? j : colstart(j)];
+  unsigned bad = 0;
+  double dkk = shfl(r[0], C0);
+  const double* cbase = colk + C0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const int pv = c0 + k;
-    if (!(dkk > 0.0)) fail = fail ? fail : pv + 1;
-    const double rd = rsqrt(dkk);
+    const int pv = C0 + k;
+    bad |= (dkk > 0.0) ? 0u : (1u << k);
+    const double rd = rsqrt_pivot(dkk);
     const double lk = (lane == pv) ? dkk * rd : rd * r[k];
     r[k] = lk;
     double dnext = 0.0;
@@ -136,10 +148,10 @@ __device__ __noinline__ int panel16(double* p, double* colk, int c0, bool T) {
     }
     dkk = dnext;
   }
-  if (fail) return fail;
+  if (bad) return C0 + __ffs(bad);
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    if (c0 + j <= lane) prow[T ? j : colstart(j)] = r[j];
+    if (C0 + j <= lane) prow[T ? j : colstart(j)] = r[j];
   __syncwarp();
   return 0;
 }
@@ -149,7 +161,7 @@ __device__ __noinline__ int panel16(double* p, double* colk, int c0, bool T) {
 // L21), V22 -= L21 L21^T on DMMA (m16n8k4, lower tiles), panel [16, 32).
 template <bool T>
 __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* colk) {
-  int f = panel16(p, colk, 0, T);
+  int f = panel16<T, 0>(p, colk);
   if (f) return f;
   const RV<T> V{p};
   double acc[2][4];
@@ -176,7 +188,7 @@ __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* col
       }
     }
   __syncwarp();
-  return panel16(p, colk, 16, T);
+  return panel16<T, 16>(p, colk);
 }
 
 // In-place inverse of the lower 32x32 view (only its lower triangle is read
@@ -421,8 +433,8 @@ __device__ __forceinline__ void load_rect(double* R, const double* g) {
       const double* s = g + 65 * c + lane;
       cp8(d, s);
       cp8(d + 32, s + 32);
-      if (lane == 0) cp8(d + 64, s + 64);
     }
+    cp8(R + 64 + colstart(lane), g + 65 * lane + 64);  // row 64 of every column
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncwarp();

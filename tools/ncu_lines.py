@@ -2,29 +2,21 @@
 
 usage: python tools/ncu_lines.py REPORT.ncu-rep [TOP]
 
-Aggregates the CUDA-source view (`--page source --print-source cuda`) and
-prints the lines with the most shared-memory wavefronts, the most executed
-instructions and the most warp-stall samples."""
+Reads the mixed CUDA/SASS source view (`--page source --print-source
+cuda,sass`): the source-line rows carry the metrics of their SASS, summed.
+Prints totals per matrix-independent unit (whole launch), the lines with the
+most shared-memory wavefronts, instructions and stall samples, and the SASS
+opcode mix."""
 import csv
 import subprocess
 import sys
+from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr_i = next(i for i, r in enumerate(rows) if any("Source" == c or c.startswith("# ") for c in r)
-             or ("Source" in r))
-hdr = rows[hdr_i]
-body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
-
-
-def col(*subs):
-    for i, h in enumerate(hdr):
-        if all(s.lower() in h.lower() for s in subs):
-            return i
-    return None
 
 
 def num(s):
@@ -34,20 +26,40 @@ def num(s):
         return 0.0
 
 
-src = col("source")
-file_i = col("file") if col("file") is not None else None
-line_i = col("line") if col("line") is not None else col("#")
-wf = col("l1 wavefronts shared") if col("l1 wavefronts shared") is not None else col("wavefronts", "shared")
-ins = col("instructions executed")
-smp = col("warp stall sampling (all")
-print("columns:", " | ".join(h for h in hdr[:40]))
-tot = {k: sum(num(r[i]) for r in body) for k, i in (("wf", wf), ("ins", ins), ("smp", smp)) if i is not None}
-print("totals:", tot)
-for key, i in (("shared wavefronts", wf), ("instructions", ins), ("stall samples", smp)):
-    if i is None:
+hdr = None
+cur = ""
+lines = []
+ops = defaultdict(lambda: [0.0, 0.0])
+for r in rows:
+    if len(r) >= 2 and r[0] == "File Path":
+        cur = r[1].split("/")[-1]
         continue
-    print(f"--- top by {key}")
-    for r in sorted(body, key=lambda r: -num(r[i]))[:top]:
-        vals = " ".join(f"{num(r[j]):>10.0f}" for j in (wf, ins, smp) if j is not None)
-        loc = r[line_i] if line_i is not None else ""
-        print(f"{vals}  {loc:>5}  {r[src].strip()[:90] if src is not None else ''}")
+    if r and r[0] == "Line No":
+        hdr = r
+        ix = {h: i for i, h in enumerate(hdr)}
+        WF, INS, SMP = ix["L1 Wavefronts Shared"], ix["Instructions Executed"], ix[
+            "Warp Stall Sampling (All Samples)"]
+        SRC2 = 3
+        continue
+    if hdr is None or len(r) != len(hdr):
+        continue
+    if r[0]:
+        lines.append((num(r[WF]), num(r[INS]), num(r[SMP]), f"{cur}:{r[0]}", r[1].strip()))
+    else:
+        op = r[SRC2].split()[0] if r[SRC2].split() else "?"
+        if op.startswith("@"):
+            op = r[SRC2].split()[1]
+        op = op.split(".")[0]
+        ops[op][0] += num(r[INS])
+        ops[op][1] += num(r[WF])
+
+tot = [sum(x[i] for x in lines) for i in range(3)]
+print(f"totals: shared wavefronts {tot[0]:.4g}  instructions {tot[1]:.4g}  samples {tot[2]:.4g}")
+for key, i in (("shared wavefronts", 0), ("instructions", 1), ("stall samples", 2)):
+    print(f"--- top by {key}   (wf  ins  samples  %samples)")
+    for x in sorted(lines, key=lambda x: -x[i])[:top]:
+        print(f"{x[0]:>11.0f} {x[1]:>11.0f} {x[2]:>7.0f} {100 * x[2] / max(tot[2], 1):5.1f}%  "
+              f"{x[3]:<22} {x[4][:80]}")
+print("--- SASS opcode mix (instructions, shared wavefronts)")
+for op, (n, w) in sorted(ops.items(), key=lambda kv: -kv[1][0])[:20]:
+    print(f"{op:<10} {n:>12.0f} {w:>12.0f}")
