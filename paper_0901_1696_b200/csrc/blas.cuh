@@ -56,9 +56,14 @@ struct InputGate {
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
 // the same on a tall panel P (m x n): potrf of its n x n head + solve of the
 // rows below (pftrf's potrf(T1) and S1 <- S1 T1^-H in one launch); -100 if
-// the layout is not supported (m > n needs n % 64 == 0)
+// the layout is not supported
 template <typename T>
 int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync = nullptr);
+// the whole SRPA pftrf of an RFP (rfp.py:70-89) as ONE dataflow launch: P =
+// [T1; S] (n x n1 tall panel, T1 lower), V = lower view of T2^T (n2 x n2);
+// global info = base + first failing pivot of the n x n chain.  Real only;
+// W = ws_alloc(n + 64).  -100 if not applicable.
+template <typename T> int potrf_rfp_tiles(Ctx c, View<T> P, View<T> V, int base, T* W);
 // dataflow tile trsm: conj?(Tm) X = B in place (tile_potrf.cu); W = lower-form
 // 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
 // agate: row block i of Tm (and W_i) readable once agate[i * agate_stride]

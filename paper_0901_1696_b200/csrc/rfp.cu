@@ -277,6 +277,34 @@ template <typename T> static int potrf_block(Ctx c, char uplo, View<T> blk, int 
 
 static i64 panel_max() { return tune(TK_PANEL_MAX); }
 
+// The whole SRPA chain (rfp.py:70-89 / :81-89) as ONE dataflow launch over
+// the global lower triangle (potrf_rfp_tiles): region 0 = [T1; S] with S =
+// S1 ('L') or S1^T ('U'), region 1 = T2^T.  'L': [T1; S1] are contiguous
+// rows of the normal rectangle, so the panel is read in place; 'U': S1 lies
+// above T1 and enters transposed, so T1's lower triangle and S1^T are copied
+// into a column-major workspace panel first (and back after).  T2^T is
+// factored in place.  -100: not applicable.
+template <typename T>
+static int chol_srpa_fused(Ctx c, const RfpDesc& d, View<T> t1, View<T> t2, View<T> s1, T* W) {
+  const i64 k = t1.m, m = d.n - k;
+  if (d.lower) {
+    View<T> panel{t1.p, d.n, k, t1.rs, t1.cs};
+    return potrf_rfp_tiles(c, panel, t2.t(), 0, W);
+  }
+  const View<T> s = s1.t();
+  View<T> P;
+  int rc = ws_colmajor(c, d.n, k, P);
+  if (rc) return rc;
+  View<T> p1 = P.sub(0, 0, k, k), p2 = P.sub(k, 0, m, k);
+  rc = tile_copy(c, t1, p1, true);
+  if (!rc) rc = tile_copy(c, s, p2, false);
+  if (!rc) rc = potrf_rfp_tiles(c, P, t2.t(), 0, W);
+  if (!rc) rc = tile_copy(c, p1, t1, true);
+  if (!rc) rc = tile_copy(c, p2, s, false);
+  cudaFreeAsync(P.p, c.st);
+  return rc;
+}
+
 struct WsPair {  // two leaf-inverse workspaces, freed stream-ordered
   cudaStream_t st;
   void* p[2] = {nullptr, nullptr};
@@ -301,9 +329,19 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
   // one workspace for the leaf inverses: T1's are reused by the S1 solve,
   // then the buffer is reused for T2's potrf
   T* W = nullptr;
-  TRY(ws_alloc(&W, d.n1, c.st));
+  TRY(ws_alloc(&W, d.n + LEAF, c.st));
   int rc = 0;
   PhaseTrace tr(c.st, "pftrf");
+  // mid orders, device-resident input: the whole chain in one launch
+  if (!is_cplx<T>::value && !s1_ready && !cflags && d.n2 && t1.m <= panel_max()) {
+    rc = chol_srpa_fused(c, d, t1, t2, s1, W);
+    if (rc != -100) {
+      tr.mark("potrf(T1)+trsm(S1)+syrk(T2)+potrf(T2)");
+      ws_free(W, c.st);
+      return rc;
+    }
+    rc = 0;
+  }
   // potrf(T2); with a pfsv plan, beside pftrs part 1 (see pfsv)
   auto t2_step = [&](int base) -> int {
     const i64 min_t2 = tune(TK_PFSV_OVERLAP_MIN);

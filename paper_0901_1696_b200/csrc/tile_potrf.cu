@@ -119,10 +119,13 @@ template <typename T, bool KM> struct PipeCfg {
   static constexpr int SPC = TP / BK;
 };
 
-template <typename T, bool KM> size_t tile_smem_bytes() {
+template <typename T, bool KM> size_t pipe_smem_elems() {
   using P = PipeCfg<T, KM>;
-  using L = SmemLayout<T, TP, P::BK, KM>;
-  const size_t pipe = (size_t)P::ST * 2 * L::SIZE;
+  return (size_t)P::ST * 2 * SmemLayout<T, TP, P::BK, KM>::SIZE;
+}
+template <typename T, bool KM0, bool KM1> size_t tile_smem_bytes() {
+  const size_t p0 = pipe_smem_elems<T, KM0>(), p1 = pipe_smem_elems<T, KM1>();
+  const size_t pipe = p0 > p1 ? p0 : p1;
   const size_t leaf = (size_t)2 * TP * LD64 + 128;
   return (pipe > leaf ? pipe : leaf) * sizeof(T);
 }
@@ -198,16 +201,44 @@ __device__ __forceinline__ void smem_mm_yh(const T* X, const T* Y,
 // with no flag round trip between the sub-diagonal tile and the next leaf.
 enum TaskKind : int { TK_DIAG0 = 0, TK_SUPER = 1, TK_NORMAL = 2, TK_PARTIAL = 3 };
 
-template <typename T> struct CholCtx {
-  View<T> A;
+// The factored matrix is one or two REGIONS of the global lower triangle:
+// region 0 = columns [0, n1) of view A (all m rows: for a tall panel the
+// rows below n1 are solved, not factored), region 1 = the trailing
+// (n - n1) x (n - n1) lower block at global offset (n1, n1), its own view B
+// (an RFP's T2^T beside the [T1; S] panel: pftrf's whole SRPA chain in one
+// launch).  Row and column tiles restart at n1, so the last tile of region
+// 0 may be ragged; off / sz give every tile's global offset and order.
+template <typename T, bool TWO = false> struct CholCtx {
+  View<T> A, B;
   T* W;
   int* info;
-  int* done;    // nt x nt tile flags
+  int* done;    // mt x nt tile flags
   int* pready;  // nt flags: diagonal partial sums written
   int* abort;
   int base, n, nt;  // columns (the factored order) and their tiles
   int m, mt;        // rows and row tiles (m >= n: a tall panel [L11; L21])
+  int n1, nt1;      // region 0's columns and column tiles (n1 == n: one region)
   const int* ext;   // optional input gate: column block j readable once ext[j]
+  // (TWO = false: one region, tiles on the plain 64-grid -- the kernel's
+  // code stays small, which the latency-bound chain measurably needs)
+  __device__ __forceinline__ int off(int I) const {
+    if constexpr (!TWO) return I * TP;
+    return I < nt1 ? I * TP : n1 + (I - nt1) * TP;
+  }
+  __device__ __forceinline__ int sz(int I) const {
+    const int e = (TWO && I >= nt1 ? m : (I < nt1 ? n1 : m)) - off(I);
+    return e < TP ? e : TP;
+  }
+  // tile (I, J) as a view (origin, order sz(I) x sz(J), the region's strides)
+  __device__ __forceinline__ View<T> tile(int I, int J) const {
+    const int r = off(I), c = off(J);
+    if (!TWO || J < nt1) return View<T>{A.p + (i64)r * A.rs + (i64)c * A.cs, sz(I), sz(J), A.rs, A.cs};
+    return View<T>{B.p + (i64)(r - n1) * B.rs + (i64)(c - n1) * B.cs, sz(I), sz(J), B.rs, B.cs};
+  }
+  // the tile's view is row-major (loads with lanes along columns)
+  __device__ __forceinline__ bool rowmajor(int J) const {
+    return ((!TWO || J < nt1) ? A.rs : B.rs) != 1;
+  }
 };
 
 template <typename T>
@@ -246,12 +277,14 @@ __device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok) {
   return *s_ok != 0;
 }
 
-// acc += sum_{k < kend} L(i, k) L(j, k)^H, chunk k loaded only once tiles
-// (i, k) and (j, k) are published.  3-stage cp.async pipeline; returns false
-// on abort.  Leaves the pipeline drained and the CTA synchronised.
-template <typename T, bool KM>
-__device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, int* s_ok,
-                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+// acc += sum_{kb <= k < ke} L(i, k) L(j, k)^H over the chunks of ONE region
+// (view V, global offset roff), chunk k loaded only once tiles (i, k) and
+// (j, k) are published.  Pipelined cp.async; a ragged chunk (region 0's last
+// tile) is zero-filled past its width.  Returns false on abort.  Leaves the
+// pipeline drained and the CTA synchronised.
+template <typename T, bool KM, bool TWO>
+__device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, int i, int j, int kb,
+                          int ke, T* sm, int* s_ok, double (&acc)[TileCfg<T>::NACC][2][4][4]) {
   using C = TileCfg<T>;
   using P = PipeCfg<T, KM>;
   using LA = SmemLayout<T, TP, P::BK, KM>;
@@ -260,15 +293,18 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
   const int wm = warp & 1, wn = warp >> 1, gq = lane >> 2, tq = lane & 3;
   T* As = sm;
   T* Bs = sm + STAGES * LA::SIZE;
-  const i64 ld = KM ? X.A.rs : X.A.cs;
+  const i64 ld = KM ? V.rs : V.cs;
+  // element (r, k) of the region in GLOBAL coordinates, k from chunk kb
+  const T* base = V.p - (i64)roff * V.rs + (i64)(X.off(kb) - roff) * V.cs;
   TileLoader<T, TP, BK, TPT, KM> la, lb;
-  la.init(X.A.p, ld, i * TP, X.m, tid);
-  lb.init(X.A.p, ld, j * TP, X.m, tid);
+  const int ri = X.off(i), rj = X.off(j);
+  la.init(base, ld, ri, ri + X.sz(i), tid);
+  lb.init(base, ld, rj, rj + X.sz(j), tid);
   // chunk kc's tiles are final.  Thread 0 also scans ahead over chunks that
   // are already published, so a task whose inputs are all done pays ONE
   // barrier instead of one per chunk.  *s_ok = 1 + last verified chunk, or 0
   // on abort (read by all threads before the loop's next barrier).
-  int known = -1;
+  int known = kb - 1;
   auto ready = [&](int kc) -> bool {
     if (kc <= known) return true;
     if (tid == 0) {
@@ -276,7 +312,7 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
       if (ok && i != j) ok = spin_wait(X.done + (i64)j * X.nt + kc, X.abort);
       int k2 = kc;
       if (ok)
-        while (k2 + 1 < kend && ld_relaxed(X.done + (i64)i * X.nt + k2 + 1) &&
+        while (k2 + 1 < ke && ld_relaxed(X.done + (i64)i * X.nt + k2 + 1) &&
                (i == j || ld_relaxed(X.done + (i64)j * X.nt + k2 + 1)))
           ++k2;
       fence_acquire();
@@ -286,21 +322,27 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
     known = *s_ok - 1;
     return known >= kc;
   };
-  auto load_stage = [&](int stage) {
-    la.load(As + stage * LA::SIZE);
-    lb.load(Bs + stage * LA::SIZE);
+  auto load_stage = [&](int stage, int q) {
+    const int kw = TWO ? X.sz(kb + q / SPC) : TP;
+    if (kw == TP) {
+      la.load(As + stage * LA::SIZE);
+      lb.load(Bs + stage * LA::SIZE);
+    } else {
+      la.load_pred(As + stage * LA::SIZE, (q % SPC) * BK, kw, ri, 0);
+      lb.load_pred(Bs + stage * LA::SIZE, (q % SPC) * BK, kw, rj, 0);
+    }
     la.advance();
     lb.advance();
   };
-  const int KT = kend * SPC;
+  const int KT = (ke - kb) * SPC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
-      if (s % SPC == 0 && !ready(s / SPC)) {
+      if (s % SPC == 0 && !ready(kb + s / SPC)) {
         cp_async_wait<0>();
         return false;
       }
-      load_stage(s);
+      load_stage(s, s);
     }
     cp_async_commit();
   }
@@ -309,11 +351,11 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
     __syncthreads();
     const int nk = kt + STAGES - 1;
     if (nk < KT) {
-      if (nk % SPC == 0 && !ready(nk / SPC)) {
+      if (nk % SPC == 0 && !ready(kb + nk / SPC)) {
         cp_async_wait<0>();
         return false;
       }
-      load_stage(nk % STAGES);
+      load_stage(nk % STAGES, nk);
     }
     cp_async_commit();
     const T* as = As + (kt % STAGES) * LA::SIZE + (wm * 32 + gq) * LA::RS + tq * LA::KS;
@@ -364,15 +406,40 @@ __device__ bool accumulate(const CholCtx<T>& X, int i, int j, int kend, T* sm, i
   return true;
 }
 
+template <typename T, bool KM0, bool KM1, bool TWO>
+__device__ bool accumulate(const CholCtx<T, TWO>& X, int i, int j, int kend, T* sm, int* s_ok,
+                           double (&acc)[TileCfg<T>::NACC][2][4][4]) {
+  if constexpr (!TWO) {
+    return acc_range<T, KM0, TWO>(X, X.A, 0, i, j, 0, kend, sm, s_ok, acc);
+  } else if constexpr (KM0 == KM1) {
+    // one copy of the pipeline for both regions (a second inlined copy grew
+    // the kernel by a third and slowed the latency-bound chain)
+#pragma unroll 1
+    for (int rg = 0; rg < 2; ++rg) {
+      const int kb = rg ? X.nt1 : 0, ke = rg ? kend : (kend < X.nt1 ? kend : X.nt1);
+      if (ke <= kb) continue;
+      if (!acc_range<T, KM0, TWO>(X, rg ? X.B : X.A, rg ? X.n1 : 0, i, j, kb, ke, sm, s_ok, acc))
+        return false;
+    }
+    return true;
+  } else {
+    const int k0 = kend < X.nt1 ? kend : X.nt1;
+    if (k0 > 0 && !acc_range<T, KM0, TWO>(X, X.A, 0, i, j, 0, k0, sm, s_ok, acc)) return false;
+    if (kend > X.nt1 && !acc_range<T, KM1, TWO>(X, X.B, X.n1, i, j, X.nt1, kend, sm, s_ok, acc))
+      return false;
+    return true;
+  }
+}
+
 // Off-diagonal tile (i, j) in two halves so that everything not needing W_j
 // happens before the wait for it:
 //   build_c: S = A(i, j) - acc (rows past the matrix zeroed)
 //   apply_w: Ws = W_j, x = S W_j^H; X written to A(i, j) and to smem tile Xs
-template <typename T>
-__device__ void build_c(const CholCtx<T>& X, int i, int j,
+template <typename T, bool TWO>
+__device__ void build_c(const CholCtx<T, TWO>& X, int i, int j,
                         const double (&acc)[TileCfg<T>::NACC][2][4][4], T* S) {
-  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
-  const int mrows = X.m - (int)i0 < TP ? X.m - (int)i0 : TP;
+  const View<T> tv = X.tile(i, j);
+  const int mrows = (int)tv.m, ncols = (int)tv.n;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -381,16 +448,17 @@ __device__ void build_c(const CholCtx<T>& X, int i, int j,
       for (int r = 0; r < 4; ++r) {
         int row, col;
         frag_rc(mi, ni, r, row, col);
-        S[row + col * LD64] =
-            row < mrows ? *X.A.at(i0 + row, j0 + col) - frag<T>(acc, mi, ni, r) : zero_<T>();
+        S[row + col * LD64] = row < mrows && col < ncols
+                                  ? *tv.at(row, col) - frag<T>(acc, mi, ni, r)
+                                  : zero_<T>();
       }
 }
-template <typename T>
-__device__ void apply_w(const CholCtx<T>& X, int i, int j, T* S, T* Ws,
+template <typename T, bool TWO>
+__device__ void apply_w(const CholCtx<T, TWO>& X, int i, int j, T* S, T* Ws,
                         double (&x)[TileCfg<T>::NACC][2][4][4], T* Xs) {
   const int tid = threadIdx.x;
-  const i64 i0 = (i64)i * TP, j0 = (i64)j * TP;
-  const int mrows = X.m - (int)i0 < TP ? X.m - (int)i0 : TP;
+  const View<T> tv = X.tile(i, j);
+  const int mrows = (int)tv.m, ncols = (int)tv.n;
   const T* w = X.W + (i64)j * TP * TP;
 #pragma unroll 8
   for (int e = tid; e < TP * TP; e += TPT) {
@@ -414,34 +482,36 @@ __device__ void apply_w(const CholCtx<T>& X, int i, int j, T* S, T* Ws,
         int row, col;
         frag_rc(mi, ni, r, row, col);
         const T v = frag<T>(x, mi, ni, r);
+        // (columns past a ragged tile come out exactly 0: S is zero there and
+        // W_j identity-padded)
         Xs[row + col * LD64] = row < mrows ? v : zero_<T>();
-        if (row < mrows) *X.A.at(i0 + row, j0 + col) = v;
+        if (row < mrows && col < ncols) *tv.at(row, col) = v;
       }
 }
 
 // Diagonal tile d from S (lower, identity-padded, ready): leaf -> L(d, d)
 // into A and W_d into its slab, then publish done(d, d).  false = failure.
-template <typename T>
-__device__ bool finish_diag(const CholCtx<T>& X, int d, T* S, T* Ws, T* scr, int* s_ok) {
+template <typename T, bool TWO>
+__device__ bool finish_diag(const CholCtx<T, TWO>& X, int d, T* S, T* Ws, T* scr, int* s_ok) {
   const int tid = threadIdx.x;
-  const i64 d0 = (i64)d * TP;
-  const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+  const View<T> tv = X.tile(d, d);
+  const int d0 = X.off(d), m = (int)tv.m;
   const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
   if (f) {
     if (tid == 0) {
-      *X.info = X.base + (int)d0 + f;
+      *X.info = X.base + d0 + f;
       __threadfence();
       st_release(X.abort, 1);
     }
     return false;
   }
   __syncthreads();
-  const bool km = X.A.rs != 1;
+  const bool km = X.rowmajor(d);
   for (int e = tid; e < TP * TP; e += TPT) {
     int r, c;
     if (km) { c = e & 63; r = e >> 6; }  // lanes along the unit-stride dimension
     else { r = e & 63; c = e >> 6; }
-    if (r < m && c <= r) *X.A.at(d0 + r, d0 + c) = S[r + c * LD64];
+    if (r < m && c <= r) *tv.at(r, c) = S[r + c * LD64];
   }
   T* w = X.W + (i64)d * TP * TP;
   for (int e = tid; e < TP * TP; e += TPT) w[e] = Ws[(e & 63) + (e >> 6) * LD64];
@@ -451,16 +521,17 @@ __device__ bool finish_diag(const CholCtx<T>& X, int d, T* S, T* Ws, T* scr, int
 
 // S <- identity-padded lower part of A(d, d) (read from L2: it may have been
 // written by another CTA)
-template <typename T> __device__ void load_diag(const CholCtx<T>& X, int d, T* S) {
-  const i64 d0 = (i64)d * TP;
-  const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+template <typename T, bool TWO> __device__ void load_diag(const CholCtx<T, TWO>& X, int d, T* S) {
+  const View<T> tv = X.tile(d, d);
+  const int m = (int)tv.m;
+  const bool km = X.rowmajor(d);
   for (int e = threadIdx.x; e < TP * TP; e += TPT) {
     int r, c;
-    if (X.A.rs != 1) { c = e & 63; r = e >> 6; }
+    if (km) { c = e & 63; r = e >> 6; }
     else { r = e & 63; c = e >> 6; }
     T v = (r == c) ? one_<T>() : zero_<T>();
     if (r < m && c < m && c <= r) {
-      const T* src = X.A.at(d0 + r, d0 + c);
+      const T* src = tv.at(r, c);
       if constexpr (is_cplx<T>::value) {
         const double2 q = __ldcg(reinterpret_cast<const double2*>(src));
         v = Z{q.x, q.y};
@@ -473,14 +544,14 @@ template <typename T> __device__ void load_diag(const CholCtx<T>& X, int d, T* S
 }
 
 // the input gate (if any): column block j of A's original data has landed
-template <typename T>
-__device__ __forceinline__ bool wait_input(const CholCtx<T>& X, int j, int* s_ok) {
+template <typename T, bool TWO>
+__device__ __forceinline__ bool wait_input(const CholCtx<T, TWO>& X, int j, int* s_ok) {
   if (!X.ext) return true;
   return wait_flag(const_cast<int*>(X.ext) + j, X.abort, s_ok);
 }
 
-template <typename T, bool KM>
-__device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int* s_ok) {
+template <typename T, bool KM0, bool KM1, bool TWO>
+__device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm, int* s_ok) {
   using C = TileCfg<T>;
   T* S = sm;
   T* Ws = S + TP * LD64;
@@ -497,10 +568,10 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   if (kind == TK_PARTIAL) {
     // A(d, d) <- A(d, d) - sum_{k < d-1} L(d, k) L(d, k)^H  (lower part)
     const int d = a;
-    if (!accumulate<T, KM>(X, d, d, d - 1, sm, s_ok, acc)) return false;
+    if (!accumulate<T, KM0, KM1, TWO>(X, d, d, d - 1, sm, s_ok, acc)) return false;
     if (!wait_input(X, d, s_ok)) return false;
-    const i64 d0 = (i64)d * TP;
-    const int m = X.n - (int)d0 < TP ? X.n - (int)d0 : TP;
+    const View<T> tv = X.tile(d, d);
+    const int m = (int)tv.m;
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -510,7 +581,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
           int row, col;
           frag_rc(mi, ni, r, row, col);
           if (row < m && col <= row) {
-            T* p = X.A.at(d0 + row, d0 + col);
+            T* p = tv.at(row, col);
             *p = *p - frag<T>(acc, mi, ni, r);
           }
         }
@@ -519,19 +590,19 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
   }
   // TK_NORMAL (i, j) and TK_SUPER (j + 1, j)
   const int i = a, j = b;
-  if (!accumulate<T, KM>(X, i, j, j, sm, s_ok, acc)) return false;
+  if (!accumulate<T, KM0, KM1, TWO>(X, i, j, j, sm, s_ok, acc)) return false;
   if (!wait_input(X, j, s_ok)) return false;
   // (diag 1 has no partial task: its original tile is read below)
   if (kind == TK_SUPER && i == 1 && !wait_input(X, 1, s_ok)) return false;
   build_c(X, i, j, acc, S);
   const int d = i;  // super: the diagonal tile factored next
-  const int m = X.n - d * TP < TP ? X.n - d * TP : TP;
+  const int m = X.sz(d);
   // real: prefetch the diagonal partial sum into acc (fragment layout, lower
   // part, identity padding) while W_j is still being produced; complex (no
   // spare registers) reloads it after the solve instead
   if (kind == TK_SUPER && !C::CPLX) {
     if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
-    const i64 d0 = (i64)d * TP;
+    const View<T> tv = X.tile(d, d);
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -542,7 +613,7 @@ __device__ bool run_task(const CholCtx<T>& X, int kind, int a, int b, T* sm, int
           frag_rc(mi, ni, r, row, col);
           T v = (row == col) ? one_<T>() : zero_<T>();
           if (row < m && col < m && col <= row) {
-            const T* src = X.A.at(d0 + row, d0 + col);
+            const T* src = tv.at(row, col);
             if constexpr (is_cplx<T>::value) {
               const double2 q = __ldcg(reinterpret_cast<const double2*>(src));
               v = Z{q.x, q.y};
@@ -607,16 +678,17 @@ __host__ __device__ inline long long chol_task_count(int nt, int mt) {
   return t;
 }
 
-template <typename T, bool KM>
+template <typename T, bool KM0, bool KM1, bool TWO>
 __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
-    tile_potrf_kernel(View<T> A, int ncols, T* W, int* info, int base, int* sync, int nt, int mt,
-                      const int* ext) {
+    tile_potrf_kernel(View<T> A, View<T> B, int n1, int nt1, int ncols, T* W, int* info, int base,
+                      int* sync, int nt, int mt, const int* ext) {
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
   if (*info) return;  // an earlier step of the chain failed
-  CholCtx<T> X;
+  CholCtx<T, TWO> X;
   X.A = A;
+  X.B = B;
   X.W = W;
   X.info = info;
   X.abort = sync + 1;
@@ -625,8 +697,10 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
   X.base = base;
   X.n = ncols;
   X.nt = nt;
-  X.m = (int)A.m;
+  X.m = nt1 < nt ? ncols : (int)A.m;
   X.mt = mt;
+  X.n1 = n1;
+  X.nt1 = nt1;
   X.ext = ext;
   const long long total = chol_task_count(nt, mt);
   int g = 0;
@@ -655,14 +729,15 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
       else if ((o -= sup) < nnorm) { kind = TK_NORMAL; a = first + o; b = g; }
       else { kind = TK_PARTIAL; a = g + 2; b = 0; }
     }
-    if (!run_task<T, KM>(X, kind, a, b, sm, &s_ok)) return;
+    if (!run_task<T, KM0, KM1, TWO>(X, kind, a, b, sm, &s_ok)) return;
   }
 }
 
-template <typename T, bool KM>
-int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, int mt) {
-  auto kern = tile_potrf_kernel<T, KM>;
-  const size_t smem = tile_smem_bytes<T, KM>();
+template <typename T, bool KM0, bool KM1, bool TWO>
+int tile_launch(View<T> A, View<T> B, int n1, int nt1, int ncols, T* W, Ctx c, int base, int* sync,
+                int nt, int mt) {
+  auto kern = tile_potrf_kernel<T, KM0, KM1, TWO>;
+  const size_t smem = tile_smem_bytes<T, KM0, KM1>();
   const int per_sm = kernel_setup(kern, TPT, smem);
   const long long tasks = chol_task_count(nt, mt);
   // two CTAs per SM up to ~12k columns: the diagonal chain's CTA then shares
@@ -672,7 +747,7 @@ int tile_launch(View<T> A, int ncols, T* W, Ctx c, int base, int* sync, int nt, 
   long long grid = (long long)ps * num_sms();
   if (grid > tasks) grid = tasks;
   KernelClock kc(c.st);
-  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, ncols, W, c.info, base, sync, nt, mt,
+  kern<<<(unsigned)grid, TPT, smem, c.st>>>(A, B, n1, nt1, ncols, W, c.info, base, sync, nt, mt,
                                             InputGate::flags());
   RFPK_CHECK_LAUNCH();
   kc.stop("tile_potrf", A.m, ncols);
@@ -1190,7 +1265,8 @@ size_t potrf_sync_ints(int nt, int mt) { return SYNC_HDR + (size_t)mt * nt + nt;
 // Factor the tall lower panel P (m x n, m >= n, col- or row-major): the
 // Cholesky of its leading n x n block and the solve of the rows below it,
 // P = [L11; L21] with L21 = P21 L11^-H, in one dataflow launch.  m == n is
-// potrf.  W (leaf-inverse slabs for ceil(n/64) tiles) is required.
+// potrf.  W (leaf-inverse slabs for the column tiles) is required; the row
+// tiles restart at n, so n need not be a multiple of 64.
 template <typename T>
 int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) {
   const i64 m = P.m;
@@ -1198,9 +1274,7 @@ int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) 
   if (!W || m < n) return -100;
   const bool km = !(P.rs == 1);
   if (km && P.cs != 1) return -100;
-  const int nt = (int)((n + TP - 1) / TP), mt = (int)((m + TP - 1) / TP);
-  // the row tiles must break at n: the rows below are off-diagonal tiles
-  if (mt > nt && n % TP) return -100;
+  const int nt = (int)((n + TP - 1) / TP), mt = nt + (int)((m - n + TP - 1) / TP);
   const size_t ints = potrf_sync_ints(nt, mt);
   int* sync = keep_sync ? *keep_sync : nullptr;  // a caller-provided, zeroed array
   if (!sync) {
@@ -1208,8 +1282,8 @@ int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) 
     if (e != cudaSuccess) return (int)e;
     if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
   }
-  int rc = km ? tile_launch<T, true>(P, (int)n, W, c, base, sync, nt, mt)
-              : tile_launch<T, false>(P, (int)n, W, c, base, sync, nt, mt);
+  int rc = km ? tile_launch<T, true, true, false>(P, P, (int)n, nt, (int)n, W, c, base, sync, nt, mt)
+              : tile_launch<T, false, false, false>(P, P, (int)n, nt, (int)n, W, c, base, sync, nt, mt);
   // keep_sync: the caller gates a concurrent kernel on the done flags
   // (done(i, j) at sync + SYNC_HDR + i * nt + j; abort at sync + 1; the task
   // counter at sync[0] is nonzero once a CTA has started) and frees the array
@@ -1219,6 +1293,39 @@ int potrf_panel_tiles(Ctx c, View<T> P, i64 n, int base, T* W, int** keep_sync) 
   if (keep_sync) *keep_sync = sync;
   else cudaFreeAsync(sync, c.st);
   return rc;
+}
+
+// The whole SRPA factorization in one dataflow launch: region 0 = the tall
+// panel P = [T1; S] (n x n1, T1 lower), region 1 = the lower view V of T2^T
+// (n2 x n2, n = n1 + n2).  Every tile of the global lower triangle is a task
+// of the one DAG, so potrf(T1), the S solve, T2 -= S S^H and potrf(T2) are a
+// single chain of diagonal tiles with all other work overlapping it
+// (rfp.py:70-89 in one kernel).  Real only; W needs ceil(n1/64) +
+// ceil(n2/64) slabs.  -100: unsupported strides.
+template <typename T> int potrf_rfp_tiles(Ctx c, View<T> P, View<T> V, int base, T* W) {
+  if constexpr (is_cplx<T>::value) {
+    return -100;
+  } else {
+    const i64 n1 = P.n, n2 = V.m, n = n1 + n2;
+    if (n2 == 0) return potrf_panel_tiles(c, P, n1, base, W);
+    if (!W || P.m != n || V.n != n2 || n1 == 0) return -100;
+    const bool k0 = !(P.rs == 1), k1 = !(V.rs == 1);
+    if ((k0 && P.cs != 1) || (k1 && V.cs != 1)) return -100;
+    const int nt1 = (int)((n1 + TP - 1) / TP), nt = nt1 + (int)((n2 + TP - 1) / TP);
+    const size_t ints = potrf_sync_ints(nt, nt);
+    int* sync = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
+    if (e != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+    const int a = (int)n1, b = (int)n;
+    int rc = -100;
+    if (k0 && !k1) rc = tile_launch<T, true, false, true>(P, V, a, nt1, b, W, c, base, sync, nt, nt);
+    else if (!k0 && k1) rc = tile_launch<T, false, true, true>(P, V, a, nt1, b, W, c, base, sync, nt, nt);
+    else if (!k0 && !k1) rc = tile_launch<T, false, false, true>(P, V, a, nt1, b, W, c, base, sync, nt, nt);
+    // (both row-major: no RFP layout produces it)
+    cudaFreeAsync(sync, c.st);
+    return rc;
+  }
 }
 
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W) {
@@ -1356,6 +1463,7 @@ template int potrf_trsm_overlap<Z>(Ctx, View<Z>, Z*, bool, View<Z>, const int*, 
 template int potrf_panel_tiles<double>(Ctx, View<double>, i64, int, double*, int**);
 template int potrf_panel_tiles<Z>(Ctx, View<Z>, i64, int, Z*, int**);
 template int potrf_tiles<double>(Ctx, View<double>, int, double*);
+template int potrf_rfp_tiles<double>(Ctx, View<double>, View<double>, int, double*);
 template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
 
 }  // namespace rfpk

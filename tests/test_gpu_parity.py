@@ -520,8 +520,17 @@ def test_phase_clock_times_srpa_steps(P):
     a = O.spd_matrix(n, 9, "n")
     lib.rfpk_phase_clock(1)
     r = P.convert.trttf(a, "L", "N")
-    assert P.rfp.pftrf(r) == 0  # first call of this shape: direct
+    assert P.rfp.pftrf(r) == 0  # first call of this shape: direct (the one-launch chain)
     tot, cnt = ctypes.c_double(0), ctypes.c_int64(0)
+    assert lib.rfpk_phase_time(b"pftrf potrf(T1)+trsm(S1)+syrk(T2)+potrf(T2)", ctypes.byref(tot),
+                               ctypes.byref(cnt)) == 0
+    assert cnt.value >= 1 and tot.value > 0
+    assert lib.rfpk_phase_time(b"kernel tile_potrf 1037x1037", ctypes.byref(tot),
+                               ctypes.byref(cnt)) == 0
+    assert cnt.value >= 1 and tot.value > 0
+    with _capi.tuning(panel_max=0):  # the step-by-step SRPA sequence
+        r = P.convert.trttf(a, "L", "N")
+        assert P.rfp.pftrf(r) == 0
     assert lib.rfpk_phase_time(b"pftrf syrk(T2)", ctypes.byref(tot), ctypes.byref(cnt)) == 0
     assert cnt.value >= 1 and tot.value > 0
     assert lib.rfpk_phase_time(b"no such phase", ctypes.byref(tot), ctypes.byref(cnt)) == 1
@@ -749,10 +758,11 @@ def test_batched_from_host_pipelined(P, nrhs):
 @pytest.mark.parametrize("transr", "NT")
 @pytest.mark.parametrize("bad", [None, 100, 460, 700])
 def test_pftrf_panel_path(P, transr, bad):
-    """n = 1000 'L': potrf(T1) + the S1 solve run as one tall-panel launch over
-    the first 448 columns and the trailing 52 columns separately; factor
-    parity with the oracle, and the reference's failure index for a non-PD
-    pivot in the panel (100), in the trailing block (460) and in T2 (700)."""
+    """n = 1000 'L': the whole SRPA chain runs as one dataflow launch whose
+    region-0 tiles end with a ragged 52-column tile (448..499) before T2's
+    tiles restart at 500; factor parity with the oracle, and the reference's
+    failure index for a non-PD pivot in T1's full tiles (100), in the ragged
+    tile (460) and in T2 (700)."""
     conv, rfp = P.convert, P.rfp
     n = 1000
     a = O.spd_matrix(n, 21, "n")
@@ -816,17 +826,18 @@ def test_potrf_row_major_block_copy(P, uplo, transr, n, cplx):
     a = O.spd_matrix(n, 31 + n, "n", complex_=cplx)
     f = O.trttf(a, uplo, transr)
     assert O.pftrf(f, n, uplo, transr) == 0
-    info0, plain = _kernel_launches("kernel tile_copy",
-                                    lambda: rfp.pftrf(conv.trttf(a, uplo, transr)))
-    with _capi.tuning(t2_copy_min=64):
+    with _capi.tuning(panel_max=0):  # the step-by-step sequence (potrf_block)
+        info0, plain = _kernel_launches("kernel tile_copy",
+                                        lambda: rfp.pftrf(conv.trttf(a, uplo, transr)))
+    with _capi.tuning(t2_copy_min=64, panel_max=0):
         r = conv.trttf(a, uplo, transr)
         info, forced = _kernel_launches("kernel tile_copy", lambda: rfp.pftrf(r))
         assert info == info0 == 0
         assert rel(r.data, f) <= TOL
-        # real data, TRANSR='N': T2's lower view is row-major and goes through
-        # the copy (two more tile copies); 'T': T1 is the row-major one, but it
-        # is factored in the [T1; S1] panel at these orders either way
-        assert forced - plain == (2 if (not cplx and transr == "N") else 0)
+        # real data: the row-major block (T2's lower view for TRANSR='N', T1's
+        # for 'T', outside the one-launch paths) goes through the copy (two
+        # more tile copies); complex never does
+        assert forced - plain == (0 if cplx else 2)
         for k in (2, n - 3):  # inside the leading block, inside the trailing one
             bad = a.copy()
             bad[k, k] = -1.0
@@ -877,8 +888,39 @@ def test_pfsv_device_matches_pftrf_pftrs(P, uplo, transr, n, cplx):
     TOL of the oracle; a failing factorization leaves b untouched and returns
     the reference's index."""
     from paper_0901_1696_b200 import _capi
-    with _capi.tuning(pfsv_overlap_min=64):
+    # (panel_max=0: the step-by-step sequence whose potrf(T2) the solve
+    # overlaps; the one-launch chain is covered by test_pfsv_fused_chain)
+    with _capi.tuning(pfsv_overlap_min=64, panel_max=0):
         _pfsv_case(P, uplo, transr, n, cplx)
+
+
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("transr", "NT")
+@pytest.mark.parametrize("n", [130, 1501, 2049, 4001])
+def test_pfsv_fused_chain(P, uplo, transr, n):
+    """Real mid orders factor through the one-launch SRPA chain (every tile of
+    T1, S, T2 in one dataflow kernel; the phase clock sees that phase and no
+    separate syrk(T2) step); pfsv then solves after it: factor and solution
+    within TOL of the oracle, failure index inside T2 the reference's."""
+    conv, rfp = P.convert, P.rfp
+    a = O.spd_matrix(n, 77 + n, "n")
+    f = O.trttf(a, uplo, transr)
+    assert O.pftrf(f, n, uplo, transr) == 0
+    rng = np.random.default_rng(n + 1)
+    bh = rng.standard_normal((n, 5))
+    xo = np.asfortranarray(bh.copy())
+    O.pftrs(f, n, uplo, transr, xo)
+    r = conv.trttf(a, uplo, transr)
+    b = torch.from_numpy(np.asfortranarray(bh)).cuda()
+    info, seen = _phase_count("pftrf potrf(T1)+trsm(S1)+syrk(T2)+potrf(T2)",
+                              lambda: rfp.pfsv(r, b))
+    assert info == 0 and seen == 1
+    assert rel(r.data, f) <= TOL
+    assert rel(b, xo) <= TOL
+    bad = a.copy()
+    bad[n - 2, n - 2] = -1.0
+    want = O.pftrf(O.trttf(bad, uplo, transr), n, uplo, transr)
+    assert rfp.pftrf(conv.trttf(bad, uplo, transr)) == want == n - 1
 
 
 def _pfsv_case(P, uplo, transr, n, cplx):

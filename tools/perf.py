@@ -227,6 +227,11 @@ if __name__ == "__main__":
                 for t in "NT":
                     rfp_bench(n, u, t, 64)
         rfp_bench(16384, "L", "N", 1024, reps=3)
+    if w == "mid":
+        for n in (1000, 2000, 3000, 4000, 4001, 6000, 8000, 8193):
+            for u in "LU":
+                for t in "NT":
+                    rfp_bench(n, u, t, 64, reps=5)
     if w == "big":
         rfp_bench(16384, "L", "N", 1024, reps=3)
         rfp_bench(4000, "L", "N", 64)
