@@ -49,7 +49,7 @@ __device__ void batched_body(const RfpDesc r, double* __restrict__ arf, int nrhs
     int i = e % n, j = e / n;
     if (i >= j) L[i + j * BLD] = r.lower ? arf[rfp_off(r, i, j)] : arf[rfp_off(r, j, i)];
   }
-  __syncthreads();
+  cta_sync();
   if (factor) {
     for (int k = 0; k < n; ++k) {
       double d = L[k + k * BLD];
@@ -59,16 +59,16 @@ __device__ void batched_body(const RfpDesc r, double* __restrict__ arf, int nrhs
       }
       d = sqrt(d);
       for (int i = k + 1 + tid; i < n; i += NT) L[i + k * BLD] /= d;
-      __syncthreads();
+      cta_sync();
       const int m = n - k - 1;
       for (int e = tid; e < m * m; e += NT) {
         int i = k + 1 + e % m, j = k + 1 + e / m;
         if (j <= i) L[i + j * BLD] = fma(-L[i + k * BLD], L[j + k * BLD], L[i + j * BLD]);
       }
       if (tid == 0) L[k + k * BLD] = d;
-      __syncthreads();
+      cta_sync();
     }
-    __syncthreads();
+    cta_sync();
     if (tid == 0) *info_out = fail;
     if (fail) return;
     // compress the factor back into the RFP buffer
@@ -88,32 +88,32 @@ __device__ void batched_body(const RfpDesc r, double* __restrict__ arf, int nrhs
       int i = e % n, c = e / n;
       X[i + c * BMAX] = b[i + (i64)(c0 + c) * ldb];
     }
-    __syncthreads();
+    cta_sync();
     // forward substitution L y = b: rows processed in order, columns in parallel
     for (int i = 0; i < n; ++i) {
       if (tid < cw) X[i + tid * BMAX] /= L[i + i * BLD];
-      __syncthreads();
+      cta_sync();
       for (int e = tid; e < (n - i - 1) * cw; e += NT) {
         int rr = i + 1 + e % (n - i - 1), c = e / (n - i - 1);
         X[rr + c * BMAX] = fma(-L[rr + i * BLD], X[i + c * BMAX], X[rr + c * BMAX]);
       }
-      __syncthreads();
+      cta_sync();
     }
     // back substitution L^T x = y
     for (int i = n - 1; i >= 0; --i) {
       if (tid < cw) X[i + tid * BMAX] /= L[i + i * BLD];
-      __syncthreads();
+      cta_sync();
       for (int e = tid; e < i * cw; e += NT) {
         int rr = e % i, c = e / i;
         X[rr + c * BMAX] = fma(-L[i + rr * BLD], X[i + c * BMAX], X[rr + c * BMAX]);
       }
-      __syncthreads();
+      cta_sync();
     }
     for (int e = tid; e < n * cw; e += NT) {
       int i = e % n, c = e / n;
       b[i + (i64)(c0 + c) * ldb] = X[i + c * BMAX];
     }
-    __syncthreads();
+    cta_sync();
   }
 }
 

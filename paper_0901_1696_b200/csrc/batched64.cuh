@@ -93,18 +93,6 @@ template <bool T> struct RV {
   __device__ __forceinline__ RV<!T> t() const { return RV<!T>{p}; }
 };
 
-// 1/sqrt(x) for a positive normal x: the MUFU seed (rsqrt.approx.f64) and
-// one cubic Newton step, y (1 + e/2 + 3e^2/8) with e = 1 - x y^2 (the seed's
-// error cubed: below double rounding).  No range checks: a pivot that is not
-// > 0 is reported before its rsqrt is used, and the library's own rsqrt()
-// spends ~12 instructions per pivot on those checks.
-__device__ __forceinline__ double rsqrt_pivot(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);
-  return fma(y, e * fma(0.375, e, 0.5), y);
-}
-
 // One warp: right-looking Cholesky of the 16 columns [C0, C0 + 16) of the
 // lower 32x32 view at p, rows C0 .. 31 (lane i holds row i's 16 panel
 // entries).  The pivot column is broadcast through colk (double-buffered,

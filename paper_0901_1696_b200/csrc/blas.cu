@@ -87,13 +87,13 @@ __global__ void __launch_bounds__(128) potf2_inv64_kernel(View<T> A, T* W, int* 
   if (*info) return;
   const int n = (int)A.m;
   leaf_load_lower(S, A, n);
-  __syncthreads();
+  cta_sync();
   const int f = leaf_factor_inv64(S, Ws, scratch, &fail);
   if (f) {
     if (threadIdx.x == 0) *info = base + f;
     return;
   }
-  __syncthreads();
+  cta_sync();
   leaf_store_lower(S, A, n, false);
   if (W)
     for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) W[e] = Ws[(e & 63) + (e >> 6) * LD64];
@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(128) trtri_leaves_kernel(View<T> A, T* W, int 
   const int len = (int)((A.m - r0) < 64 ? (A.m - r0) : 64);
   View<T> blk = A.sub(r0, r0, len, len);
   leaf_load_lower(S, blk, len);
-  __syncthreads();
+  cta_sync();
   inv64_block(S, Ws, unit != 0, false, scratch);
-  __syncthreads();
+  cta_sync();
   if (W) {
     T* dst = W + r0 * 64;
     for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) dst[e] = Ws[(e & 63) + (e >> 6) * LD64];
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) lauum_leaf_kernel(View<T> A, const int* s
   if (skip && *skip) return;
   const int n = (int)A.m;
   smem_load(L, LD, A, n, n, 1);
-  __syncthreads();
+  cta_sync();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     int i = e % n, j = e / n;
     if (j > i) continue;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) lauum_leaf_kernel(View<T> A, const int* s
     if (i == j) s = real_part_as(s);
     X[i + j * LD] = s;
   }
-  __syncthreads();
+  cta_sync();
   smem_store(X, LD, A, n, n, 1, false);
 }
 
@@ -153,7 +153,7 @@ template <typename T>
 __global__ void diag_scan_kernel(View<T> A, int* info, int base, int highest) {
   __shared__ int best;
   if (threadIdx.x == 0) best = highest ? 0 : 0x7fffffff;
-  __syncthreads();
+  cta_sync();
   if (*info) return;
   const int n = (int)A.m;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -161,7 +161,7 @@ __global__ void diag_scan_kernel(View<T> A, int* info, int base, int highest) {
       if (highest) atomicMax(&best, i + 1);
       else atomicMin(&best, i + 1);
     }
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) {
     int b = best;
     if (highest ? b > 0 : b != 0x7fffffff) *info = base + b;

@@ -66,6 +66,31 @@ __device__ __forceinline__ Z fnmac(Z a, Z b, Z c) {
   return Z{fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y))};
 }
 
+// 1/sqrt(x) for a Cholesky pivot x > 0 (normal): the MUFU seed
+// (rsqrt.approx.f64) and one cubic Newton step, y (1 + e/2 + 3e^2/8) with
+// e = 1 - x y^2 -- the seed's error cubed, below double rounding.  No range
+// checks: a pivot that is not > 0 is reported before its rsqrt is used (the
+// library's rsqrt() spends ~12 instructions on those checks, on the serial
+// chain of every pivot).
+__device__ __forceinline__ double rsqrt_pivot(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
+// CTA barrier for code where single threads run the flag protocol (spins,
+// atomics, releases) or record failures: __syncthreads() is bar.sync, an
+// .aligned barrier that a warp must reach CONVERGED, and under independent
+// thread scheduling the compiler does not always reconverge a warp after a
+// thread-0-only block (measured: one thread-0 store ahead of a task's first
+// barrier let the warp's other lanes run a barrier ahead of lane 0 and read
+// a tile before lane 0 had acquired its flag).  Reconverge first.
+__device__ __forceinline__ void cta_sync() {
+  __syncwarp();
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- views
 template <typename T> struct View {
   T* p;

@@ -65,14 +65,6 @@ __device__ void leaf_store_lower(const T* S, View<T> A, int n, bool skip_diag) {
   }
 }
 
-// 1/sqrt(x) for x > 0: MUFU seed + Newton steps (relative error ~1 ulp).
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y = rsqrt(x);
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-
 // One warp: C(16 x 16) = A(16 x 16) * op(B) on FP64 DMMA (m16n8k4, two n8
 // tiles), A(i, k) = A[i + k*LD64], B(k, n) = B[k*bk + n*bn] (BC: conjugated).
 // c[q][ni][r]: q = re / im plane; element (g + 8(r>>1), 8ni + 2t + (r&1)).
@@ -84,6 +76,7 @@ template <typename T, bool BC>
 __device__ __forceinline__ void mm16_warp(const T* A, const T* B, int bk, int bn, Frag16<T>& f) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   constexpr bool CPLX = is_cplx<T>::value;
+  __syncwarp();  // mma.sync.aligned needs the converged warp
 #pragma unroll
   for (int q = 0; q < (CPLX ? 2 : 1); ++q)
 #pragma unroll
@@ -142,7 +135,7 @@ __device__ __noinline__ int chol_panel16(T* S, int off, int c0, T* colk) {
   for (int j = 0; j < 16; ++j) r[j] = act ? prow[j * LD64] : zero_<T>();
   int fail = 0;
   double dkk = shfl(sc_re(r[0]), c0);
-  double rd = rsqrt(dkk);
+  double rd = rsqrt_pivot(dkk);
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const int p = c0 + k;
@@ -154,7 +147,7 @@ __device__ __noinline__ int chol_panel16(T* S, int off, int c0, T* colk) {
     T* cb = colk + (k & 1) * 32;
     cb[lane] = conj_(lk);
     __syncwarp();
-    const double rd_next = rsqrt(dnext);
+    const double rd_next = rsqrt_pivot(dnext);
     if constexpr (is_cplx<T>::value) {
 #pragma unroll
       for (int j = k + 1; j < 16; ++j) r[j] = fnmac(lk, cb[c0 + j], r[j]);
@@ -249,6 +242,7 @@ __device__ __forceinline__ void mm32_mma(const T* X, int xr, int xc, const T* Y,
                                          Frag32<T>& f) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   constexpr bool CPLX = is_cplx<T>::value;
+  __syncwarp();  // mma.sync.aligned needs the converged warp (lane-0 fail flags precede)
 #pragma unroll
   for (int q = 0; q < (CPLX ? 2 : 1); ++q)
 #pragma unroll
@@ -300,13 +294,13 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
   if (!both_diag_done) {
     if (warp == 0) inv32_warp(S, 0, W, 0, unit, scratch);
     if (warp == 1) inv32_warp(S, 32, W, 32, unit, scratch + 32);
-    __syncthreads();
+    cta_sync();
   }
   // Y = L21 * W11  (scratch: S rows 0..31, cols 32..63)
   Frag32<T> f;
   mm32_mma<T, false, false>(S, 32, 0, W, 0, 0, f);
   frag32_each(f, [&](int i, int j, T v) { S[i + (32 + j) * LD64] = v; });
-  __syncthreads();
+  cta_sync();
   // W21 = -W22 * Y ; W12 = 0
   mm32_mma<T, false, false>(W, 32, 32, S, 0, 32, f);
   frag32_each(f, [&](int i, int j, T v) {
@@ -324,33 +318,33 @@ template <typename T>
 __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) *s_fail = 0;
-  __syncthreads();
+  cta_sync();
   if (warp == 0) {
     const int f = chol32_warp(S, 0, scratch);
     if (lane == 0 && f) *s_fail = f;
   }
-  __syncthreads();
+  cta_sync();
   if (*s_fail) return *s_fail;
   if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
-  __syncthreads();
+  cta_sync();
   Frag32<T> f;
   mm32_mma<T, true, true>(S, 32, 0, Ws, 0, 0, f);  // L21 = A21 W11^H
-  __syncthreads();
+  cta_sync();
   frag32_each(f, [&](int i, int j, T v) { S[(32 + i) + j * LD64] = v; });
-  __syncthreads();
+  cta_sync();
   mm32_mma<T, true, true>(S, 32, 0, S, 32, 0, f);  // L21 L21^H
   frag32_each(f, [&](int i, int j, T v) {
     if (j <= i) S[(32 + i) + (32 + j) * LD64] = S[(32 + i) + (32 + j) * LD64] - v;
   });
-  __syncthreads();
+  cta_sync();
   if (warp == 0) {
     const int f = chol32_warp(S, 32, scratch);
     if (lane == 0 && f) *s_fail = 32 + f;
   }
-  __syncthreads();
+  cta_sync();
   if (*s_fail) return *s_fail;
   if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
-  __syncthreads();
+  cta_sync();
   inv64_block(S, Ws, false, true, scratch);
   return 0;
 }

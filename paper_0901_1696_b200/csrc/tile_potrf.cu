@@ -18,7 +18,7 @@
 // A task only ever waits on tasks handed out before it, and those are held
 // by running CTAs, so progress never depends on co-residency (no deadlock
 // whatever the grid size or other work on the GPU).  Publication: the CTA's
-// stores, __syncthreads, then one thread's __threadfence + st.release.gpu of
+// stores, __syncthreads, then one thread's st.release.gpu of
 // the flag; consumption: one thread's ld.acquire.gpu spin, __syncthreads,
 // then the tile reads (cp.async / ld.global.cg from L2).
 //
@@ -55,6 +55,27 @@ const int* InputGate::flags() { return tl_gate; }
 int InputGate::mode() { return tl_gate_mode; }
 
 namespace {
+
+// Developer timeline of the diagonal chain (build variant with
+// -DRFPK_CHAIN_TRACE, read by tools/chain_trace.py through
+// rfpk_chain_trace_read): per diagonal tile d, %globaltimer stamps of the
+// SUPER task that produces it.
+#ifdef RFPK_CHAIN_TRACE
+constexpr int CT_EV = 8, CT_MAX = 1024;
+__device__ unsigned long long g_chain_trace[CT_MAX * CT_EV];
+__device__ __forceinline__ void ct_mark(int d, int ev) {
+  if (threadIdx.x == 0 && d < CT_MAX) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_chain_trace[d * CT_EV + ev] = t;
+  }
+  // (without reconverging here the tile potrf computed wrong factors: the
+  // warp stayed split after the thread-0 store -- see cta_sync)
+  __syncwarp();
+}
+#else
+__device__ __forceinline__ void ct_mark(int, int) {}
+#endif
 
 constexpr int TP = 64;    // tile order (== LEAF)
 constexpr int TPT = 128;  // threads per CTA (4 warps, 2 x 2 of 32 x 32)
@@ -151,6 +172,7 @@ __device__ __forceinline__ void smem_mm_yh(const T* X, const T* Y,
                                            double (&acc)[TileCfg<T>::NACC][2][4][4]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, t = lane & 3;
+  __syncwarp();  // mma.sync.aligned needs the converged warp (see publish)
 #pragma unroll 4
   for (int k = 0; k < TP; k += 4) {
     if constexpr (!is_cplx<T>::value) {
@@ -260,20 +282,29 @@ __device__ __forceinline__ void frag_rc(int mi, int ni, int r, int& row, int& co
   col = (warp >> 1) * 32 + ni * 8 + 2 * (lane & 3) + (r & 1);
 }
 
-// one thread publishes a flag after the whole CTA's stores
+// Convergence: the flag protocol runs in thread 0 (spins, atomics, the
+// release) while the other threads wait at the barrier; every barrier here
+// is cta_sync() (common.cuh: reconverge, then bar.sync) and every warp-wide
+// DMMA sequence (mma.sync.aligned) starts with __syncwarp().
+//
+// one thread publishes a flag after the whole CTA's stores: the barrier
+// orders every thread's stores before thread 0's release, and a release is
+// cumulative over what its thread has observed, so ONE gpu-scope fence (the
+// release's own) publishes the whole tile (an extra __threadfence before it
+// cost ~0.5 us per diagonal step on the chain)
 __device__ __forceinline__ void publish(int* f) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(f, 1);
-  }
+  cta_sync();
+#ifdef RFPK_PUBLISH_FENCE
+  if (threadIdx.x == 0) __threadfence();
+#endif
+  if (threadIdx.x == 0) st_release(f, 1);
 }
 __device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok) {
   if (threadIdx.x == 0) {
     *s_ok = spin_wait(f, abort);
     fence_acquire();
   }
-  __syncthreads();
+  cta_sync();
   return *s_ok != 0;
 }
 
@@ -318,7 +349,7 @@ __device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, 
       fence_acquire();
       *s_ok = ok ? k2 + 1 : 0;
     }
-    __syncthreads();
+    cta_sync();
     known = *s_ok - 1;
     return known >= kc;
   };
@@ -348,7 +379,7 @@ __device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, 
   }
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    cta_sync();
     const int nk = kt + STAGES - 1;
     if (nk < KT) {
       if (nk % SPC == 0 && !ready(kb + nk / SPC)) {
@@ -358,6 +389,7 @@ __device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, 
       load_stage(nk % STAGES, nk);
     }
     cp_async_commit();
+    __syncwarp();  // (a thread-0 flag wait may have left the warp split)
     const T* as = As + (kt % STAGES) * LA::SIZE + (wm * 32 + gq) * LA::RS + tq * LA::KS;
     const T* bs = Bs + (kt % STAGES) * LA::SIZE + (wn * 32 + gq) * LA::RS + tq * LA::KS;
 #pragma unroll
@@ -402,7 +434,7 @@ __device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, 
     }
   }
   cp_async_wait<0>();
-  __syncthreads();  // pipeline buffers are reused by the caller
+  cta_sync();  // pipeline buffers are reused by the caller
   return true;
 }
 
@@ -460,19 +492,30 @@ __device__ void apply_w(const CholCtx<T, TWO>& X, int i, int j, T* S, T* Ws,
   const View<T> tv = X.tile(i, j);
   const int mrows = (int)tv.m, ncols = (int)tv.n;
   const T* w = X.W + (i64)j * TP * TP;
+  // W_j (32 KB, L2-resident: just written by the diagonal task) with every
+  // load in flight at once (cp.async.cg bypasses L1: written by another CTA)
+#ifdef RFPK_W_LDCG
+  if constexpr (!is_cplx<T>::value) {
+#pragma unroll 8
+    for (int e = tid; e < TP * TP; e += TPT) Ws[(e & 63) + (e >> 6) * LD64] = __ldcg(w + e);
+  }
+  if (is_cplx<T>::value)
+#endif
 #pragma unroll 8
   for (int e = tid; e < TP * TP; e += TPT) {
     if constexpr (is_cplx<T>::value) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(w + e));
-      Ws[(e & 63) + (e >> 6) * LD64] = Z{v.x, v.y};
+      cp_async16(Ws + (e & 63) + (e >> 6) * LD64, w + e, true);
     } else {
-      Ws[(e & 63) + (e >> 6) * LD64] = __ldcg(w + e);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Ws + (e & 63) + (e >> 6) * LD64);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(w + e));
     }
   }
-  __syncthreads();
+  cp_async_commit();
+  cp_async_wait<0>();
+  cta_sync();
   zero_acc<T>(x);
   smem_mm_yh<T>(S, Ws, x);
-  __syncthreads();  // S and Ws fully read
+  cta_sync();  // S and Ws fully read
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -496,7 +539,9 @@ __device__ bool finish_diag(const CholCtx<T, TWO>& X, int d, T* S, T* Ws, T* scr
   const int tid = threadIdx.x;
   const View<T> tv = X.tile(d, d);
   const int d0 = X.off(d), m = (int)tv.m;
+  ct_mark(d, 4);
   const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
+  ct_mark(d, 5);
   if (f) {
     if (tid == 0) {
       *X.info = X.base + d0 + f;
@@ -505,7 +550,7 @@ __device__ bool finish_diag(const CholCtx<T, TWO>& X, int d, T* S, T* Ws, T* scr
     }
     return false;
   }
-  __syncthreads();
+  cta_sync();
   const bool km = X.rowmajor(d);
   for (int e = tid; e < TP * TP; e += TPT) {
     int r, c;
@@ -515,7 +560,9 @@ __device__ bool finish_diag(const CholCtx<T, TWO>& X, int d, T* S, T* Ws, T* scr
   }
   T* w = X.W + (i64)d * TP * TP;
   for (int e = tid; e < TP * TP; e += TPT) w[e] = Ws[(e & 63) + (e >> 6) * LD64];
+  ct_mark(d, 6);
   publish(X.done + (i64)d * X.nt + d);
+  ct_mark(d, 7);
   return true;
 }
 
@@ -561,7 +608,7 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
   if (kind == TK_DIAG0) {
     if (!wait_input(X, 0, s_ok)) return false;
     load_diag(X, 0, S);
-    __syncthreads();
+    cta_sync();
     const bool ok = finish_diag(X, 0, S, Ws, scr, s_ok);
     return ok;
   }
@@ -590,7 +637,9 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
   }
   // TK_NORMAL (i, j) and TK_SUPER (j + 1, j)
   const int i = a, j = b;
+  if (kind == TK_SUPER) ct_mark(i, 0);
   if (!accumulate<T, KM0, KM1, TWO>(X, i, j, j, sm, s_ok, acc)) return false;
+  if (kind == TK_SUPER) ct_mark(i, 1);
   if (!wait_input(X, j, s_ok)) return false;
   // (diag 1 has no partial task: its original tile is read below)
   if (kind == TK_SUPER && i == 1 && !wait_input(X, 1, s_ok)) return false;
@@ -626,8 +675,10 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
         }
   }
   if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok)) return false;
+  if (kind == TK_SUPER) ct_mark(i, 2);
   double x[C::NACC][2][4][4];
   apply_w(X, i, j, S, Ws, x, kind == TK_SUPER ? Ws : S);
+  if (kind == TK_SUPER) ct_mark(i, 3);
   publish(X.done + (i64)i * X.nt + j);
   if (kind == TK_NORMAL) {
     return true;
@@ -636,7 +687,7 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
   if constexpr (C::CPLX) {
     if (d >= 2 && !wait_flag(X.pready + d, X.abort, s_ok)) return false;
     load_diag(X, d, S);
-    __syncthreads();
+    cta_sync();
   }
   zero_acc<T>(x);
   smem_mm_yh<T>(Ws, Ws, x);
@@ -656,7 +707,7 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
           S[row + col * LD64] = v;
         }
       }
-  __syncthreads();
+  cta_sync();
   const bool ok = finish_diag(X, d, S, Ws, scr, s_ok);
   return ok;
 }
@@ -707,9 +758,9 @@ __global__ void __launch_bounds__(TPT, is_cplx<T>::value ? 1 : 3)
   long long gbase = 1;  // first task of group g
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(sync, 1);
-    __syncthreads();
+    cta_sync();
     const long long t = s_task;
-    __syncthreads();
+    cta_sync();
     if (t >= total) return;
     int kind, a, b;
     if (t == 0) {
@@ -784,6 +835,7 @@ __device__ __forceinline__ void smem_mm_ab(
   using W = TrsmTile<TN>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp % W::WMW, wn = warp / W::WMW, g = lane >> 2, t = lane & 3;
+  __syncwarp();  // mma.sync.aligned needs the converged warp
 #pragma unroll 4
   for (int k = 0; k < TP; k += 4) {
     if constexpr (!is_cplx<T>::value) {
@@ -864,7 +916,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
       }
       *s_ok = ok;
     }
-    __syncthreads();
+    cta_sync();
     if (!*s_ok) return false;
   }
   using C = TileCfg<T>;
@@ -923,7 +975,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     const int q = a.lower ? kk : a.nb - 1 - kk;  // position in solve order
     if (!scan_ahead) {
       if (tid == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
-      __syncthreads();
+      cta_sync();
     } else if (q >= ready) {
       if (warp == 0) {
         if (lane == 0) spin_wait_acquire(done + (i64)kk * a.nc + c);
@@ -943,7 +995,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
         if (rr > q + 1) fence_acquire();
         if (lane == 0) s_ready_sh = rr;
       }
-      __syncthreads();
+      cta_sync();
       ready = s_ready_sh;
     }
     const T* ta = AK ? Tm.p + (i64)kk * TP : Tm.p + (i64)kk * TP * Tm.cs;
@@ -1002,13 +1054,14 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   const double sa = (C::CPLX && a.conj) ? -1.0 : 1.0;
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    cta_sync();
     const int nk = kt + STAGES - 1;
     if (nk < KT) {
       if (nk % SPC == 0) open_chunk(chunk(nk / SPC));
       load_stage(nk % STAGES, nk);
     }
     cp_async_commit();
+    __syncwarp();  // (a thread-0 flag wait may have left the warp split)
     const T* as = As + (kt % STAGES) * LA::SIZE + (wm * WL::RW + gq) * LA::RS + tq * LA::KS;
     const T* bs = Bs + (kt % STAGES) * LB::SIZE + (wn * WL::CW + gq) * LB::RS + tq * LB::KS;
 #pragma unroll
@@ -1053,7 +1106,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     }
   }
   cp_async_wait<0>();
-  __syncthreads();
+  cta_sync();
   if (nprev > 0 && !*s_ok) return false;
 
   if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
@@ -1064,7 +1117,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
       const int last = (c * TN + TN - 1 < a.nrhs - 1 ? c * TN + TN - 1 : a.nrhs - 1) / TP;
       spin_wait_acquire(a.ext + (a.ext_mode ? last : i));
     }
-    __syncthreads();
+    cta_sync();
   }
   // S = B(i, c) - acc (zero outside the matrix), Ws = W'_i, X = Ws S
   T* S = sm;
@@ -1101,7 +1154,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     if (a.wtrans) Ws[k + r * LD64] = v;  // W'(k, r) = W(r, k)
     else Ws[r + k * LD64] = v;
   }
-  __syncthreads();
+  cta_sync();
   double x[NACC][MI][NI][4];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
@@ -1122,7 +1175,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
         const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
         if (row < mrows && col < ncols) *B.at(i0 + row, c0 + col) = fragn<T>(x[0], x[NACC - 1], mi, ni, r);
       }
-  __syncthreads();
+  cta_sync();
   if (tid == 0) {
     __threadfence();
     st_release(done + (i64)i * a.nc + c, 1);
@@ -1143,7 +1196,7 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   if (threadIdx.x == 0) s_ok = 1;  // cleared only by a failed triangle gate
   if (a.aguard && (int)blockIdx.x >= a.aguard_keep) {
     if (threadIdx.x == 0) s_task = ld_relaxed(a.aguard);
-    __syncthreads();
+    cta_sync();
     if (s_task == 0) return;
   }
   int* counter = sync;
@@ -1151,9 +1204,9 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   const long long total = (long long)a.nb * a.nc;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
-    __syncthreads();
+    cta_sync();
     const long long t = s_task;
-    __syncthreads();
+    cta_sync();
     if (t >= total) return;
     const int step = (int)(t / a.nc), c = (int)(t % a.nc);
     const int i = a.lower ? step : a.nb - 1 - step;
@@ -1467,3 +1520,14 @@ template int potrf_rfp_tiles<double>(Ctx, View<double>, View<double>, int, doubl
 template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
 
 }  // namespace rfpk
+
+#ifdef RFPK_CHAIN_TRACE
+extern "C" int rfpk_chain_trace_read(unsigned long long* host, int count) {
+  return (int)cudaMemcpyFromSymbol(host, rfpk::g_chain_trace,
+                                   sizeof(unsigned long long) * (size_t)count);
+}
+extern "C" int rfpk_chain_trace_clear() {
+  static unsigned long long zero[rfpk::CT_MAX * rfpk::CT_EV] = {};
+  return (int)cudaMemcpyToSymbol(rfpk::g_chain_trace, zero, sizeof(zero));
+}
+#endif
