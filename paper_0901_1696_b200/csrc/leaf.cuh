@@ -13,6 +13,10 @@
 #include "common.cuh"
 #include "dmma.cuh"
 
+#ifndef LEAF_MARK
+#define LEAF_MARK(d, ev)
+#endif
+
 namespace rfpk {
 
 constexpr int LD64 = 65;
@@ -315,7 +319,7 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
 // failing pivot, uniform over the CTA (s_fail: a __shared__ int).  Callers
 // sync before (S ready) and after.
 template <typename T>
-__device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
+__device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail, int trace_id = -1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) *s_fail = 0;
   cta_sync();
@@ -324,28 +328,35 @@ __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail) {
     if (lane == 0 && f) *s_fail = f;
   }
   cta_sync();
+  LEAF_MARK(trace_id, 8);
   if (*s_fail) return *s_fail;
   if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
   cta_sync();
+  LEAF_MARK(trace_id, 9);
   Frag32<T> f;
   mm32_mma<T, true, true>(S, 32, 0, Ws, 0, 0, f);  // L21 = A21 W11^H
   cta_sync();
   frag32_each(f, [&](int i, int j, T v) { S[(32 + i) + j * LD64] = v; });
   cta_sync();
+  LEAF_MARK(trace_id, 10);
   mm32_mma<T, true, true>(S, 32, 0, S, 32, 0, f);  // L21 L21^H
   frag32_each(f, [&](int i, int j, T v) {
     if (j <= i) S[(32 + i) + (32 + j) * LD64] = S[(32 + i) + (32 + j) * LD64] - v;
   });
   cta_sync();
+  LEAF_MARK(trace_id, 11);
   if (warp == 0) {
     const int f = chol32_warp(S, 32, scratch);
     if (lane == 0 && f) *s_fail = 32 + f;
   }
   cta_sync();
+  LEAF_MARK(trace_id, 12);
   if (*s_fail) return *s_fail;
   if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
   cta_sync();
+  LEAF_MARK(trace_id, 13);
   inv64_block(S, Ws, false, true, scratch);
+  LEAF_MARK(trace_id, 14);
   return 0;
 }
 

@@ -30,6 +30,33 @@
 // Failure: the failing diagonal task writes info = base + pivot and raises
 // an abort flag that every waiting CTA checks (kernels.py:441-442 semantics:
 // the first failing pivot; later tiles are never factored).
+#include <cuda_runtime.h>
+
+namespace rfpk {
+// Developer timeline of the diagonal chain (build variant with
+// -DRFPK_CHAIN_TRACE, read by tools/chain_trace.py through
+// rfpk_chain_trace_read): per diagonal tile d, %globaltimer stamps of the
+// SUPER task that produces it.
+#ifdef RFPK_CHAIN_TRACE
+constexpr int CT_EV = 16, CT_MAX = 1024;
+__device__ unsigned long long g_chain_trace[CT_MAX * CT_EV];
+__device__ __forceinline__ void ct_mark(int d, int ev) {
+  if (threadIdx.x == 0 && d >= 0 && d < CT_MAX) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_chain_trace[d * CT_EV + ev] = t;
+  }
+  // (without reconverging here the tile potrf computed wrong factors: the
+  // warp stayed split after the thread-0 store -- see cta_sync)
+  __syncwarp();
+}
+#define LEAF_MARK(d, ev) ::rfpk::ct_mark(d, ev)
+#else
+__device__ __forceinline__ void ct_mark(int, int) {}
+#endif
+
+}  // namespace rfpk
+
 #include "blas.cuh"
 #include "dmma.cuh"
 #include "leaf.cuh"
@@ -55,27 +82,6 @@ const int* InputGate::flags() { return tl_gate; }
 int InputGate::mode() { return tl_gate_mode; }
 
 namespace {
-
-// Developer timeline of the diagonal chain (build variant with
-// -DRFPK_CHAIN_TRACE, read by tools/chain_trace.py through
-// rfpk_chain_trace_read): per diagonal tile d, %globaltimer stamps of the
-// SUPER task that produces it.
-#ifdef RFPK_CHAIN_TRACE
-constexpr int CT_EV = 8, CT_MAX = 1024;
-__device__ unsigned long long g_chain_trace[CT_MAX * CT_EV];
-__device__ __forceinline__ void ct_mark(int d, int ev) {
-  if (threadIdx.x == 0 && d < CT_MAX) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_chain_trace[d * CT_EV + ev] = t;
-  }
-  // (without reconverging here the tile potrf computed wrong factors: the
-  // warp stayed split after the thread-0 store -- see cta_sync)
-  __syncwarp();
-}
-#else
-__device__ __forceinline__ void ct_mark(int, int) {}
-#endif
 
 constexpr int TP = 64;    // tile order (== LEAF)
 constexpr int TPT = 128;  // threads per CTA (4 warps, 2 x 2 of 32 x 32)
@@ -540,7 +546,7 @@ __device__ bool finish_diag(const CholCtx<T, TWO>& X, int d, T* S, T* Ws, T* scr
   const View<T> tv = X.tile(d, d);
   const int d0 = X.off(d), m = (int)tv.m;
   ct_mark(d, 4);
-  const int f = leaf_factor_inv64(S, Ws, scr, s_ok);
+  const int f = leaf_factor_inv64(S, Ws, scr, s_ok, d);
   ct_mark(d, 5);
   if (f) {
     if (tid == 0) {
