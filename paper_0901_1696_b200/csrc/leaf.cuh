@@ -76,17 +76,19 @@ template <typename T> struct Frag16 {
   double c[is_cplx<T>::value ? 2 : 1][2][4];
 };
 
-template <typename T, bool BC>
+template <typename T, bool BC, bool ACC = false>
 __device__ __forceinline__ void mm16_warp(const T* A, const T* B, int bk, int bn, Frag16<T>& f) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   constexpr bool CPLX = is_cplx<T>::value;
   __syncwarp();  // mma.sync.aligned needs the converged warp
+  if constexpr (!ACC) {
 #pragma unroll
-  for (int q = 0; q < (CPLX ? 2 : 1); ++q)
+    for (int q = 0; q < (CPLX ? 2 : 1); ++q)
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) f.c[q][ni][r] = 0.0;
+        for (int r = 0; r < 4; ++r) f.c[q][ni][r] = 0.0;
+  }
 #pragma unroll
   for (int k0 = 0; k0 < 16; k0 += 4) {
     const int k = k0 + t;
@@ -190,6 +192,114 @@ __device__ __noinline__ int chol32_warp(T* S, int off, T* colk) {
   });
   __syncwarp();
   return chol_panel16(S, off, 16, colk);
+}
+
+// The same panel over the 64 x 32 block [A11; A21] of the leaf (S at 0, 0):
+// lane i also carries row 32 + i, which the pivot column broadcasts update
+// too, so L21 = A21 L11^-H comes out of the factorization's own broadcasts
+// (no inverse of L11 on the critical path).  Returns 0 or the failing pivot.
+template <typename T>
+__device__ __noinline__ int chol_panel16x2(T* S, int c0, T* colk) {
+  const int lane = threadIdx.x & 31;
+  const bool act = lane >= c0;
+  T* prow = S + lane + c0 * LD64;
+  T* qrow = prow + 32;
+  T r[16], q[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    r[j] = act ? prow[j * LD64] : zero_<T>();
+    q[j] = qrow[j * LD64];
+  }
+  int fail = 0;
+  double dkk = shfl(sc_re(r[0]), c0);
+  double rd = rsqrt_pivot(dkk);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int p = c0 + k;
+    if (!(dkk > 0.0)) fail = fail ? fail : p + 1;
+    const T lk = (lane == p) ? sc_from<T>(dkk * rd) : rd * r[k];
+    const T mk = rd * q[k];
+    r[k] = lk;
+    q[k] = mk;
+    double dnext = 1.0;
+    if (k + 1 < 16) dnext = shfl(sc_re(fnmac(lk, conj_(lk), r[k + 1])), p + 1);
+    T* cb = colk + (k & 1) * 32;
+    cb[lane] = conj_(lk);
+    __syncwarp();
+    const double rd_next = rsqrt_pivot(dnext);
+    if constexpr (is_cplx<T>::value) {
+#pragma unroll
+      for (int j = k + 1; j < 16; ++j) {
+        const T c = cb[c0 + j];
+        r[j] = fnmac(lk, c, r[j]);
+        q[j] = fnmac(mk, c, q[j]);
+      }
+    } else {
+#pragma unroll
+      for (int jj = (k + 1) & ~1; jj < 16; jj += 2) {
+        const double2 c2 = *reinterpret_cast<const double2*>(cb + c0 + jj);
+        if (jj >= k + 1) {
+          r[jj] = fnmac(lk, c2.x, r[jj]);
+          q[jj] = fnmac(mk, c2.x, q[jj]);
+        }
+        r[jj + 1] = fnmac(lk, c2.y, r[jj + 1]);
+        q[jj + 1] = fnmac(mk, c2.y, q[jj + 1]);
+      }
+    }
+    dkk = dnext;
+    rd = rd_next;
+  }
+  if (fail) return fail;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (act && c0 + j <= lane) prow[j * LD64] = r[j];
+    qrow[j * LD64] = q[j];
+  }
+  __syncwarp();
+  return 0;
+}
+
+// One warp: L11 and L21 of the leaf's first 32 columns, [A11; A21] =
+// [L11; L21] L11^H: panel [0, 16) over 64 rows, rows 16..63 of columns
+// [16, 32) -= (their first 16 columns) L(16..31, 0..15)^H on DMMA, panel
+// [16, 32) over rows 16..63.  Returns 0 or the 1-based failing pivot.
+template <typename T>
+__device__ __noinline__ int chol64x32_warp(T* S, T* colk) {
+  int f = chol_panel16x2(S, 0, colk);
+  if (f) return f;
+  const T* Lb = S + 16;  // B(k, n) = conj(L(16 + n, k))
+#pragma unroll 1
+  for (int rb = 16; rb < 64; rb += 16) {
+    Frag16<T> fr;
+    mm16_warp<T, true>(S + rb, Lb, LD64, 1, fr);
+    T* C = S + rb + 16 * LD64;
+    const bool diag = rb == 16;
+    frag16_each(fr, [&](int i, int j, T v) {
+      if (!diag || j <= i) C[i + j * LD64] = C[i + j * LD64] - v;
+    });
+  }
+  __syncwarp();
+  return chol_panel16x2(S, 16, colk);
+}
+
+// One warp: Y = L21 W11 (32 x 32, W11 lower) into Y (LD64 smem), as four
+// 16 x 16 blocks (the block above W11's diagonal skipped)
+template <typename T>
+__device__ __noinline__ void mm_l21_w11_warp(const T* L21, const T* W11, T* Y) {
+#pragma unroll 1
+  for (int bi = 0; bi < 2; ++bi)
+#pragma unroll 1
+    for (int bj = 0; bj < 2; ++bj) {
+      Frag16<T> fr;
+      // sum over kb >= bj (W11(kb, bj) = 0 for kb < bj)
+      mm16_warp<T, false>(L21 + 16 * bi + 16 * bj * LD64, W11 + 16 * bj + 16 * bj * LD64, 1,
+                          LD64, fr);
+      if (bj == 0)
+        mm16_warp<T, false, true>(L21 + 16 * bi + 16 * LD64, W11 + 16, 1, LD64, fr);
+      T* Yb = Y + 16 * bi + 16 * bj * LD64;
+      frag16_each(fr, [&](int i, int j, T v) { Yb[i + j * LD64] = v; });
+    }
+  __syncwarp();
 }
 
 // One warp: W(offw.., offw..) = inverse of the 32 x 32 lower block of S at
@@ -320,43 +430,47 @@ __device__ void inv64_block(T* S, T* W, bool unit, bool both_diag_done, T* scrat
 // sync before (S ready) and after.
 template <typename T>
 __device__ int leaf_factor_inv64(T* S, T* Ws, T* scratch, int* s_fail, int trace_id = -1) {
+  // warp 0 carries the pivot chain: [L11; L21] in one 64-row panel, then
+  // L22 after the 4-warp update A22 -= L21 L21^H; meanwhile warp 1 inverts
+  // L11 and forms Y = L21 W11 (staged in S's unused upper-right block), so
+  // only L22's inverse and W21 = -W22 Y follow the chain
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) *s_fail = 0;
   cta_sync();
   if (warp == 0) {
-    const int f = chol32_warp(S, 0, scratch);
+    const int f = chol64x32_warp(S, scratch);
     if (lane == 0 && f) *s_fail = f;
   }
   cta_sync();
   LEAF_MARK(trace_id, 8);
   if (*s_fail) return *s_fail;
-  if (warp == 0) inv32_warp(S, 0, Ws, 0, false, scratch);
-  cta_sync();
-  LEAF_MARK(trace_id, 9);
   Frag32<T> f;
-  mm32_mma<T, true, true>(S, 32, 0, Ws, 0, 0, f);  // L21 = A21 W11^H
-  cta_sync();
-  frag32_each(f, [&](int i, int j, T v) { S[(32 + i) + j * LD64] = v; });
-  cta_sync();
-  LEAF_MARK(trace_id, 10);
   mm32_mma<T, true, true>(S, 32, 0, S, 32, 0, f);  // L21 L21^H
   frag32_each(f, [&](int i, int j, T v) {
     if (j <= i) S[(32 + i) + (32 + j) * LD64] = S[(32 + i) + (32 + j) * LD64] - v;
   });
   cta_sync();
-  LEAF_MARK(trace_id, 11);
+  LEAF_MARK(trace_id, 9);
   if (warp == 0) {
-    const int f = chol32_warp(S, 32, scratch);
-    if (lane == 0 && f) *s_fail = 32 + f;
+    const int fl = chol32_warp(S, 32, scratch);
+    if (lane == 0 && fl) *s_fail = 32 + fl;
+  } else if (warp == 1) {
+    inv32_warp(S, 0, Ws, 0, false, scratch + 64);
+    mm_l21_w11_warp(S + 32, Ws, S + 32 * LD64);
   }
   cta_sync();
-  LEAF_MARK(trace_id, 12);
+  LEAF_MARK(trace_id, 10);
   if (*s_fail) return *s_fail;
-  if (warp == 1) inv32_warp(S, 32, Ws, 32, false, scratch + 32);
+  if (warp == 0) inv32_warp(S, 32, Ws, 32, false, scratch);
   cta_sync();
-  LEAF_MARK(trace_id, 13);
-  inv64_block(S, Ws, false, true, scratch);
-  LEAF_MARK(trace_id, 14);
+  LEAF_MARK(trace_id, 11);
+  // W21 = -W22 Y ; W12 = 0
+  mm32_mma<T, false, false>(Ws, 32, 32, S, 0, 32, f);
+  frag32_each(f, [&](int i, int j, T v) {
+    Ws[(32 + i) + j * LD64] = zero_<T>() - v;
+    Ws[i + (32 + j) * LD64] = zero_<T>();
+  });
+  LEAF_MARK(trace_id, 12);
   return 0;
 }
 

@@ -116,7 +116,7 @@ __device__ void spin_wait_acquire(const int* f) {
   }
 }
 // one thread: wait for *f != 0 (true) or an abort (false; abort may be null);
-// the caller issues fence_acquire() before trusting data guarded by *f
+// the caller issues fence_acquire() before trusting data guarded by *f.
 __device__ bool spin_wait(const int* f, const int* abort) {
   unsigned ns = 32;
   for (;;) {
@@ -305,10 +305,20 @@ __device__ __forceinline__ void publish(int* f) {
 #endif
   if (threadIdx.x == 0) st_release(f, 1);
 }
-__device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok) {
+__device__ __forceinline__ bool wait_flag(int* f, int* abort, int* s_ok, bool hot = false) {
   if (threadIdx.x == 0) {
-    *s_ok = spin_wait(f, abort);
-    fence_acquire();
+    if (hot) {
+      // the chain's wait: acquire polls (no separate fence after the flag)
+      int ok;
+      for (;;) {
+        if (ld_acquire(f)) { ok = 1; break; }
+        if (ld_relaxed(abort)) { ok = 0; break; }
+      }
+      *s_ok = ok;
+    } else {
+      *s_ok = spin_wait(f, abort);
+      fence_acquire();
+    }
   }
   cta_sync();
   return *s_ok != 0;
@@ -680,7 +690,7 @@ __device__ bool run_task(const CholCtx<T, TWO>& X, int kind, int a, int b, T* sm
           else acc[0][mi][ni][r] = v;
         }
   }
-  if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok)) return false;
+  if (!wait_flag(X.done + (i64)j * X.nt + j, X.abort, s_ok, kind == TK_SUPER)) return false;
   if (kind == TK_SUPER) ct_mark(i, 2);
   double x[C::NACC][2][4][4];
   apply_w(X, i, j, S, Ws, x, kind == TK_SUPER ? Ws : S);

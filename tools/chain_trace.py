@@ -54,13 +54,11 @@ for n in [int(x) for x in (sys.argv[1:] or ["2000", "4000"])]:
           "publish diag (stored -> publ)": [t[d, 7] - t[d, 6] for d in mid],
           "STEP (publ d-1 -> publ d)": [t[d, 7] - t[d - 1, 7] for d in mid],
           "acc ready before flag (flag - acc)": [t[d, 2] - t[d, 1] for d in mid],
-          "  leaf: chol32 #1": [t[d, 8] - t[d, 4] for d in mid],
-          "  leaf: inv32 #1": [t[d, 9] - t[d, 8] for d in mid],
-          "  leaf: L21 = A21 W11^H": [t[d, 10] - t[d, 9] for d in mid],
-          "  leaf: A22 -= L21 L21^H": [t[d, 11] - t[d, 10] for d in mid],
-          "  leaf: chol32 #2": [t[d, 12] - t[d, 11] for d in mid],
-          "  leaf: inv32 #2": [t[d, 13] - t[d, 12] for d in mid],
-          "  leaf: W21 products": [t[d, 14] - t[d, 13] for d in mid]}
+          "  leaf: chol [A11; A21]": [t[d, 8] - t[d, 4] for d in mid],
+          "  leaf: A22 -= L21 L21^H": [t[d, 9] - t[d, 8] for d in mid],
+          "  leaf: chol32(A22) || inv32(L11), Y": [t[d, 10] - t[d, 9] for d in mid],
+          "  leaf: inv32(L22)": [t[d, 11] - t[d, 10] for d in mid],
+          "  leaf: W21 = -W22 Y": [t[d, 12] - t[d, 11] for d in mid]}
     print(f"n={n}: {ms:.3f} ms, {nt} diagonal tiles, {ms * 1e3 / nt:.1f} us per tile")
     for k, v in iv.items():
         print(f"   {np.mean(v) / 1e3:8.2f} us  {k}")
