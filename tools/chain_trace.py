@@ -54,11 +54,18 @@ for n in [int(x) for x in (sys.argv[1:] or ["2000", "4000"])]:
           "publish diag (stored -> publ)": [t[d, 7] - t[d, 6] for d in mid],
           "STEP (publ d-1 -> publ d)": [t[d, 7] - t[d - 1, 7] for d in mid],
           "acc ready before flag (flag - acc)": [t[d, 2] - t[d, 1] for d in mid],
+          "  super: start -> acc done (publ d-1 relative)": [t[d, 1] - t[d - 1, 7] for d in mid],
+          "  super: acc -> prog ready": [t[d, 13] - t[d, 1] for d in mid],
+          "  super: prog -> pready (PARTIAL d)": [t[d, 14] - t[d, 13] for d in mid],
+          "  super: pready -> W flag": [t[d, 2] - t[d, 14] for d in mid],
           "  leaf: chol [A11; A21]": [t[d, 8] - t[d, 4] for d in mid],
           "  leaf: A22 -= L21 L21^H": [t[d, 9] - t[d, 8] for d in mid],
           "  leaf: chol32(A22) || inv32(L11), Y": [t[d, 10] - t[d, 9] for d in mid],
           "  leaf: inv32(L22)": [t[d, 11] - t[d, 10] for d in mid],
           "  leaf: W21 = -W22 Y": [t[d, 12] - t[d, 11] for d in mid]}
     print(f"n={n}: {ms:.3f} ms, {nt} diagonal tiles, {ms * 1e3 / nt:.1f} us per tile")
+    pub = (t[1:, 7] - t[1, 0]) / 1e3
+    print("   diag published at (us from the first SUPER's start), every nt/16 tiles:",
+          " ".join(f"{d}:{pub[d - 1]:.0f}" for d in range(1, nt, max(1, nt // 16))))
     for k, v in iv.items():
         print(f"   {np.mean(v) / 1e3:8.2f} us  {k}")
