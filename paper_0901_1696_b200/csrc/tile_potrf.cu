@@ -51,8 +51,20 @@ __device__ __forceinline__ void ct_mark(int d, int ev) {
   __syncwarp();
 }
 #define LEAF_MARK(d, ev) ::rfpk::ct_mark(d, ev)
+// per-task start / end stamps of the tile trsm (task index t < TT_MAX)
+constexpr int TT_MAX = 1 << 16;
+__device__ unsigned long long g_task_trace[2 * TT_MAX];
+__device__ __forceinline__ void tt_mark(long long t, int ev) {
+  if (threadIdx.x == 0 && t >= 0 && t < TT_MAX) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_task_trace[2 * t + ev] = v;
+  }
+  __syncwarp();
+}
 #else
 __device__ __forceinline__ void ct_mark(int, int) {}
+__device__ __forceinline__ void tt_mark(long long, int) {}
 #endif
 
 }  // namespace rfpk
@@ -1226,7 +1238,9 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
     if (t >= total) return;
     const int step = (int)(t / a.nc), c = (int)(t % a.nc);
     const int i = a.lower ? step : a.nb - 1 - step;
+    tt_mark(t, 0);
     if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok)) return;
+    tt_mark(t, 1);
   }
 }
 
@@ -1540,6 +1554,10 @@ template int potrf_tiles<Z>(Ctx, View<Z>, int, Z*);
 #ifdef RFPK_CHAIN_TRACE
 extern "C" int rfpk_chain_trace_read(unsigned long long* host, int count) {
   return (int)cudaMemcpyFromSymbol(host, rfpk::g_chain_trace,
+                                   sizeof(unsigned long long) * (size_t)count);
+}
+extern "C" int rfpk_task_trace_read(unsigned long long* host, int count) {
+  return (int)cudaMemcpyFromSymbol(host, rfpk::g_task_trace,
                                    sizeof(unsigned long long) * (size_t)count);
 }
 extern "C" int rfpk_chain_trace_clear() {
