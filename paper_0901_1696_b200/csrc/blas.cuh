@@ -52,6 +52,28 @@ struct InputGate {
   static int mode();
 };
 
+// Row-completion hook for the host-buffer drivers (rfpk_?pfsv_host): while a
+// RowHook is installed on this host thread, the NEXT tile trsm launch counts,
+// per 64-row block i of its right-hand side, the finished column tasks in
+// rowcnt[i] (released after the block's stores), records `launched` on its
+// stream just before the launch and fills nb / nc / forward; the caller can
+// then copy each row block back as soon as rowcnt[i] reaches nc (a
+// stream-ordered wait on device memory) instead of after the whole solve.
+struct RowDoneHook {
+  int* rowcnt = nullptr;   // >= ceil(rows / 64) ints, device memory
+  cudaEvent_t launched = nullptr;
+  int nb = 0, nc = 0;
+  bool forward = true;     // row blocks finish in ascending order
+  bool used = false;
+};
+struct RowHook {
+  RowDoneHook* prev;
+  explicit RowHook(RowDoneHook* h);
+  ~RowHook();
+  static RowDoneHook* current();
+  static void consumed();  // the hook applies to one launch only
+};
+
 // dataflow tile Cholesky of a lower view (tile_potrf.cu); W required
 template <typename T> int potrf_tiles(Ctx c, View<T> A, int base, T* W);
 // the same on a tall panel P (m x n): potrf of its n x n head + solve of the

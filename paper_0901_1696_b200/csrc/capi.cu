@@ -242,6 +242,32 @@ static int h2d_rfp_begin(const RfpDesc& d, const void* h, void* dv, cudaStream_t
   return (int)cudaEventRecord(in_done, copy);
 }
 
+// cuStreamWaitValue32 (GEQ) through the runtime's driver entry point (no
+// link-time dependency on libcuda); null if the driver does not offer it
+using WaitValueFn = int (*)(cudaStream_t, const int*, unsigned);
+namespace {
+typedef int (*cu_wait_value32_t)(void* stream, unsigned long long addr, unsigned value,
+                                 unsigned flags);
+cu_wait_value32_t g_cu_wait = nullptr;
+int wait_value_geq(cudaStream_t s, const int* addr, unsigned value) {
+  return g_cu_wait((void*)s, (unsigned long long)(uintptr_t)addr, value, 0x0 /* GEQ */);
+}
+}  // namespace
+static WaitValueFn stream_wait_value_fn() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_cu_wait = reinterpret_cast<cu_wait_value32_t>(fn);
+    else
+      cudaGetLastError();
+  });
+  return g_cu_wait ? wait_value_geq : nullptr;
+}
+
 // ---------------------------------------------------------------- pftrf from host
 // The factorization of a pinned HOST RFP buffer with the transfer streamed:
 // the rows holding T1/T2 are copied on `st` and potrf(T1) starts as soon as
@@ -325,10 +351,56 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   // skips on *info
   const i64 split = d.lower ? d.n1 : d.n2;  // first row of the trailing block
   const bool trail = nrhs > 0 && n - split > 0 && !(d.lower && d.n2 == 0);
+  // the head block [0, split) is final only as the last solve ends each of its
+  // 64-row blocks: with the row-completion hook every block is copied back as
+  // soon as its column tasks are done (a stream-ordered wait on the solve's
+  // per-row counter), so only the last block's copy follows the solve
+  static thread_local cudaEvent_t launched = [] {
+    cudaEvent_t ev_;
+    cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming);
+    return ev_;
+  }();
+  // the previous call's row-block waits (side stream) read the same counter
+  // buffer: order this call's use of it after them, whatever stream it is on
+  static thread_local cudaEvent_t last_join = [] {
+    cudaEvent_t ev_;
+    cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming);
+    cudaEventRecord(ev_, 0);
+    return ev_;
+  }();
+  cudaStreamWaitEvent(st, last_join, 0);
+  RowDoneHook hook;
+  hook.launched = launched;
+  const int nbh = (int)((split + 63) / 64);
+  // (a plain cudaMalloc buffer, kept per host thread and device and grown as
+  // needed: stream memory operations reject stream-ordered pool allocations)
+  static thread_local int* rc_buf[MAX_DEVICES] = {};
+  static thread_local int rc_len[MAX_DEVICES] = {};
+  int* rowcnt = nullptr;
+  if (trail && stream_wait_value_fn()) {
+    const int dev = cur_device() & (MAX_DEVICES - 1);
+    if (rc_len[dev] < nbh) {
+      cudaStreamSynchronize(st);  // (a previous call's waits may still read the old buffer)
+      cudaStreamSynchronize(side);
+      if (rc_buf[dev]) cudaFree(rc_buf[dev]);
+      rc_buf[dev] = nullptr;
+      rc_len[dev] = 0;
+      if (cudaMalloc((void**)&rc_buf[dev], (size_t)nbh * sizeof(int)) == cudaSuccess)
+        rc_len[dev] = nbh;
+      else
+        cudaGetLastError();
+    }
+    if (rc_len[dev] >= nbh) rowcnt = rc_buf[dev];
+    if (rowcnt) hook.rowcnt = rowcnt;
+  }
   int rcf = pfsv<T>(Ctx{st, info}, d, (T*)d_arf, V<T>(d_b, n, nrhs, 1, ldb), s1_done, cflags,
-                    sflags, b_done, trail ? b2_final : nullptr);
+                    sflags, b_done, trail ? b2_final : nullptr, rowcnt ? &hook : nullptr);
   if (cflags) cudaFreeAsync(cflags, st);
-  if (rcf) return rcf;
+  auto free_rowcnt = [&]() {};  // (the counter buffer is kept for the next call)
+  if (rcf) {
+    free_rowcnt();
+    return rcf;
+  }
   if (nrhs == 0) return 0;
   if (trail) {
     cudaStreamWaitEvent(side, b2_final, 0);
@@ -337,11 +409,41 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
                           side);
     if (e != cudaSuccess) return (int)e;
   }
-  e = cudaMemcpy2DAsync(h_x, pitch, d_b, pitch, (size_t)(trail ? split : n) * sizeof(T),
-                        (size_t)nrhs, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return (int)e;
+  bool rows_copied = false;
+  if (hook.used && hook.nb == nbh) {
+    cudaStreamWaitEvent(side, hook.launched, 0);
+    auto wait32 = stream_wait_value_fn();
+    for (int k = 0; k < nbh; ++k) {
+      const int i = hook.forward ? k : nbh - 1 - k;
+      const i64 r0 = (i64)i * 64, rows = split - r0 < 64 ? split - r0 : 64;
+      const int we = wait32(side, rowcnt + i, (unsigned)hook.nc);
+      if (we != 0) {
+        if (k == 0) {  // not offered for this memory / device: copy after the solve
+          static bool once = [&] {
+            fprintf(stderr, "rfpk: cuStreamWaitValue32 unavailable (CUresult %d): the "
+                            "solution is copied back after the last solve\n", we);
+            return true;
+          }();
+          (void)once;
+          break;
+        }
+        return (int)cudaErrorUnknown;
+      }
+      e = cudaMemcpy2DAsync((T*)h_x + r0, pitch, (const T*)d_b + r0, pitch, (size_t)rows * sizeof(T),
+                            (size_t)nrhs, cudaMemcpyDeviceToHost, side);
+      if (e != cudaSuccess) return (int)e;
+      rows_copied = true;
+    }
+  }
+  if (!rows_copied) {
+    e = cudaMemcpy2DAsync(h_x, pitch, d_b, pitch, (size_t)(trail ? split : n) * sizeof(T),
+                          (size_t)nrhs, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return (int)e;
+  }
   cudaEventRecord(fork, side);  // join the side stream back into `st`
   cudaStreamWaitEvent(st, fork, 0);
+  cudaEventRecord(last_join, side);
+  free_rowcnt();
   return 0;
 }
 

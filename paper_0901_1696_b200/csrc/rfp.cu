@@ -316,7 +316,7 @@ struct WsPair {  // two leaf-inverse workspaces, freed stream-ordered
 
 template <typename T>
 static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T* W2,
-                      cudaEvent_t b2_final, int part);
+                      cudaEvent_t b2_final, int part, RowDoneHook* last_hook = nullptr);
 
 // SRPA factorization (rfp.py:55-91)
 template <typename T>
@@ -369,7 +369,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     if (rt2) return rt2;
     if (r) return r;
     r = blas_leaf_inverses(c, t2.t(), W2);
-    if (!r) r = pftrs_part(c, d, (const T*)arf, plan->b, W1, W2, plan->b2_final, 2);
+    if (!r) r = pftrs_part(c, d, (const T*)arf, plan->b, W1, W2, plan->b2_final, 2, plan->head_rows);
     plan->done = true;
     return r;
   };
@@ -563,7 +563,7 @@ int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* s
 // formed once and shared by the two solves with each triangle.
 template <typename T>
 static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T* W2,
-                      cudaEvent_t b2_final, int part) {
+                      cudaEvent_t b2_final, int part, RowDoneHook* last_hook) {
   View<T> t1, t2, s1;
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
   const i64 n1 = d.n1, n2 = d.n2, r = b.n;
@@ -588,7 +588,10 @@ static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T
       TRY(blas_gemm(c, 'C', 'N', m_one<T>(), s1, b2, one<T>(), b1));
       tr.mark("gemm2");
     }
-    TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false, W1));
+    {
+      RowHook h(last_hook);  // the head block's rows are final as this solve ends them
+      TRY(blas_trsm(c, 'L', 'L', 'C', 'N', one<T>(), t1, b1, false, W1));
+    }
     tr.mark("trsm4");
     return 0;
   }
@@ -605,13 +608,14 @@ static int pftrs_part(Ctx c, const RfpDesc& d, const T* arf, View<T> b, T* W1, T
   if (b2_final) cudaEventRecord(b2_final, c.st);
   if (n2) {
     TRY(blas_gemm(c, 'N', 'N', m_one<T>(), s1, b2, one<T>(), b1));
+    RowHook h(last_hook);  // the head block's rows are final as this solve ends them
     TRY(blas_trsm(c, 'L', 'L', 'T', 'N', one<T>(), t1, b1, false, W1));
   }
   return 0;
 }
 
 template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
-                                cudaEvent_t b2_final) {
+                                cudaEvent_t b2_final, RowDoneHook* head_rows) {
   if (d.n == 0 || b.n == 0) return 0;
   View<T> t1, t2, s1;
   rfp_blocks(d, const_cast<T*>(arf), t1, t2, s1);
@@ -625,7 +629,7 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
     fr.p[1] = W2;
     TRY(blas_leaf_inverses(c, t2.t(), W2));
   }
-  return pftrs_part(c, d, arf, b, W1, W2, b2_final, 0);
+  return pftrs_part(c, d, arf, b, W1, W2, b2_final, 0, head_rows);
 }
 
 // pftrf + pftrs in one driver (the public pfsv paths).  The first solve with
@@ -635,12 +639,12 @@ template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b
 // the solve fills.  No flags cross the two: they touch disjoint blocks.
 template <typename T>
 int pfsv(Ctx c, const RfpDesc& d, T* arf, View<T> b, cudaEvent_t s1_ready, const int* cflags,
-         const int* sflags, cudaEvent_t b_ready, cudaEvent_t b2_final) {
-  PfsvPlan<T> plan{b, b_ready, b2_final, false};
+         const int* sflags, cudaEvent_t b_ready, cudaEvent_t b2_final, RowDoneHook* head_rows) {
+  PfsvPlan<T> plan{b, b_ready, b2_final, false, head_rows};
   const int rc = pftrf<T>(c, d, arf, s1_ready, cflags, sflags, b.n ? &plan : nullptr);
   if (rc || plan.done || b.n == 0 || d.n == 0) return rc;
   if (b_ready) cudaStreamWaitEvent(c.st, b_ready, 0);
-  return pftrs<T>(c, d, arf, b, b2_final);
+  return pftrs<T>(c, d, arf, b, b2_final, head_rows);
 }
 
 // triangular inverse in RFP (rfp.py:286-325)
@@ -1245,10 +1249,10 @@ int lansf(cudaStream_t st, const RfpDesc& d, char norm, const T* arf, double* ou
   template void rfp_blocks<T>(const RfpDesc&, T*, View<T>&, View<T>&, View<T>&);             \
   template int pftrf<T>(Ctx, const RfpDesc&, T*, cudaEvent_t, const int*, const int*, PfsvPlan<T>*); \
   template int pfsv<T>(Ctx, const RfpDesc&, T*, View<T>, cudaEvent_t, const int*, const int*,      \
-                       cudaEvent_t, cudaEvent_t);                               \
+                       cudaEvent_t, cudaEvent_t, RowDoneHook*);                 \
   template int rfp_h2d_split<T>(const RfpDesc&, const T*, T*, cudaStream_t, cudaStream_t);   \
   template int rfp_h2d_chunked<T>(const RfpDesc&, const T*, T*, int*, int*, cudaStream_t);                                            \
-  template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>, cudaEvent_t);                             \
+  template int pftrs<T>(Ctx, const RfpDesc&, const T*, View<T>, cudaEvent_t, RowDoneHook*);               \
   template int tftri<T>(Ctx, const RfpDesc&, char, T*);                                      \
   template int pftri<T>(Ctx, const RfpDesc&, T*);                                            \
   template int convert<T>(const Storage&, const T*, const Storage&, T*, bool, cudaStream_t);  \

@@ -28,6 +28,7 @@ template <typename T> struct PfsvPlan {
   cudaEvent_t b_ready;
   cudaEvent_t b2_final;
   bool done;
+  RowDoneHook* head_rows = nullptr;  // hook for the last solve (the head block's rows)
 };
 template <typename T>
 int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr,
@@ -37,7 +38,8 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready = nullptr,
 template <typename T>
 int pfsv(Ctx c, const RfpDesc& d, T* arf, View<T> b, cudaEvent_t s1_ready = nullptr,
          const int* cflags = nullptr, const int* sflags = nullptr,
-         cudaEvent_t b_ready = nullptr, cudaEvent_t b2_final = nullptr);
+         cudaEvent_t b_ready = nullptr, cudaEvent_t b2_final = nullptr,
+         RowDoneHook* head_rows = nullptr);
 // (s1_ready: the S1 rows' transfer; with cflags / sflags the input is being
 //  streamed in 64-column chunks of the normal rectangle, chunk j of the T1/T2
 //  rows flagged in cflags[j] and of the S1 rows in sflags[j], and s1_ready
@@ -54,7 +56,9 @@ template <typename T>
 int rfp_h2d_chunked(const RfpDesc& d, const T* host, T* dev, int* cflags, int* sflags,
                     cudaStream_t copy);
 template <typename T> int pftrs(Ctx c, const RfpDesc& d, const T* arf, View<T> b,
-                                cudaEvent_t b2_final = nullptr);
+                                cudaEvent_t b2_final = nullptr, RowDoneHook* head_rows = nullptr);
+// (head_rows: see RowHook -- the last solve, which finalizes the head block
+//  rows [0, n1) for 'L' / [0, n2) for 'U', reports its row blocks as done)
 // (b2_final: recorded once the trailing block of b -- rows [n1, n) for 'L',
 //  [n2, n) for 'U' -- holds its final values, before the last two steps)
 template <typename T> int tftri(Ctx c, const RfpDesc& d, char diag, T* arf);

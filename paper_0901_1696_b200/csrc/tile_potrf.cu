@@ -94,6 +94,14 @@ const int* InputGate::flags() { return tl_gate; }
 int InputGate::mode() { return tl_gate_mode; }
 
 namespace {
+thread_local RowDoneHook* tl_rowhook = nullptr;
+}  // namespace
+RowHook::RowHook(RowDoneHook* h) : prev(tl_rowhook) { tl_rowhook = h; }
+RowHook::~RowHook() { tl_rowhook = prev; }
+RowDoneHook* RowHook::current() { return tl_rowhook; }
+void RowHook::consumed() { tl_rowhook = nullptr; }
+
+namespace {
 
 constexpr int TP = 64;    // tile order (== LEAF)
 constexpr int TPT = 128;  // threads per CTA (4 warps, 2 x 2 of 32 x 32)
@@ -928,6 +936,7 @@ struct TrsmArgs {
   const int* aguard;
   int aguard_keep;
   int scan;  // scan-ahead chunk waits (see trsm_task's open_chunk)
+  int* rowcnt;  // RowHook: finished column tasks per row block (or null)
 };
 
 template <typename T, bool AK, bool BKM, int TN>
@@ -1205,8 +1214,9 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
       }
   cta_sync();
   if (tid == 0) {
-    __threadfence();
     st_release(done + (i64)i * a.nc + c, 1);
+    if (a.rowcnt)  // (a release of its own: ordered after this task's stores)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.rowcnt + i) : "memory");
   }
   return true;
 }
@@ -1220,7 +1230,13 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   extern __shared__ __align__(16) double smem_d[];
   T* sm = reinterpret_cast<T*>(smem_d);
   __shared__ int s_task, s_ok;
-  if (info && *info) return;
+  if (info && *info) {
+    // skipped (an earlier step failed): a row-completion watcher must not
+    // wait forever -- report every row block as done (b stays untouched)
+    if (a.rowcnt && blockIdx.x == 0)
+      for (int r = threadIdx.x; r < a.nb; r += blockDim.x) atomicExch(a.rowcnt + r, a.nc);
+    return;
+  }
   if (threadIdx.x == 0) s_ok = 1;  // cleared only by a failed triangle gate
   if (a.aguard && (int)blockIdx.x >= a.aguard_keep) {
     if (threadIdx.x == 0) s_task = ld_relaxed(a.aguard);
@@ -1310,11 +1326,24 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.aguard = agate ? aabort - 1 : nullptr;  // the producer's task counter (sync[0])
   a.aguard_keep = num_sms();
   a.scan = 1;
+  a.rowcnt = nullptr;
+  RowDoneHook* hook = RowHook::current();
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
   if (e != cudaSuccess) return (int)e;
   if ((e = cudaMemsetAsync(sync, 0, ints * sizeof(int), c.st)) != cudaSuccess) return (int)e;
+  if (hook && hook->rowcnt && !(tn == 16 && is_cplx<T>::value)) {
+    if ((e = cudaMemsetAsync(hook->rowcnt, 0, (size_t)a.nb * sizeof(int), c.st)) != cudaSuccess)
+      return (int)e;
+    a.rowcnt = hook->rowcnt;
+    hook->nb = a.nb;
+    hook->nc = a.nc;
+    hook->forward = lower;
+    hook->used = true;
+    cudaEventRecord(hook->launched, c.st);
+    RowHook::consumed();
+  }
   // B operand = X^T (nrhs x K): K-major when B is column-major
   const bool bkm = B.rs == 1;
   int rc;

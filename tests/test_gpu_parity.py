@@ -695,6 +695,29 @@ def test_inverse_residual_and_determinism(P, n):
         assert outs[0] == outs[1]
 
 
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("uplo", "LU")
+@pytest.mark.parametrize("n", [1100, 2049])
+def test_pfsv_from_host_failure_returns(P, uplo, n):
+    """A non-PD host problem: the solves skip on info, and the head block's
+    per-row-block copies (which wait on the last solve's row counters) must
+    still be released -- the call returns the reference's failure index
+    (the solution is unspecified on failure, as documented)."""
+    conv, rfp = P.convert, P.rfp
+    a = O.spd_matrix(n, 17 + n, "n")
+    bad = n // 3
+    a[bad, bad] = -1.0
+    buf = O.trttf(a, uplo, "N")
+    want = O.pftrf(buf.copy(), n, uplo, "N")
+    assert want == bad + 1
+    b = np.random.default_rng(n).standard_normal((n, 7))
+    hb = torch.from_numpy(b.T.copy()).pin_memory().t()
+    out = torch.from_numpy(np.full((7, n), np.nan)).pin_memory().t()
+    r, info = rfp.pfsv_from_host(torch.from_numpy(buf.copy()).pin_memory(), hb, n, uplo, "N",
+                                 out=out)
+    assert info == want
+
+
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
 @pytest.mark.parametrize("n", [1, 2, 130, 601, 1100, 2049])
