@@ -1,0 +1,67 @@
+"""Rebuild profiles/ncu_traffic.json from an ncu launch list of one bench step.
+
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+      --clock-control none --csv --log-file profiles/rNN_ncu_step_launches.csv \
+      python bench.py --steps 1 --warmup 3 --no-cpu --no-configs --no-batched --no-e2e
+  python tools/ncu_traffic.py profiles/rNN_ncu_step_launches.csv
+
+The library's kernels of the LAST bench step (the timed one) are the last
+`per_step` rfpk launches; each is keyed by the kernel-clock label bench.py
+uses (config 3: n1 = n2 = 8192, nrhs = 1024)."""
+import csv
+import json
+import sys
+from collections import defaultdict
+
+src = sys.argv[1]
+per_step = int(sys.argv[2]) if len(sys.argv) > 2 else 14
+rows = [r for r in csv.reader(open(src)) if len(r) > 10]
+hdr = rows[0]
+ix = {h: i for i, h in enumerate(hdr)}
+launch = defaultdict(dict)
+names = {}
+for r in rows[1:]:
+    lid = int(r[ix["ID"]])
+    names[lid] = r[ix["Kernel Name"]]
+    v = float(r[ix["Metric Value"]].replace(",", ""))
+    launch[lid][r[ix["Metric Name"]]] = v if r[ix["Metric Unit"]] not in ("nsecond", "ns") else v / 1e6
+ours = [lid for lid in sorted(launch) if "rfpk::" in names[lid]]
+step = ours[-per_step:]
+
+
+def label(lid):
+    nm, d = names[lid], launch[lid]
+    ms = d.get("gpu__time_duration.sum", 0.0)
+    if "tile_potrf_kernel" in nm:
+        return "kernel tile_potrf 8192x8192"
+    if "tile_trsm_kernel" in nm:
+        return "kernel tile_trsm 8192x8192" if ms > 8.0 else "kernel tile_trsm 8192x1024"
+    if "tile_copy_kernel" in nm:
+        return "kernel tile_copy 8192x8192"
+    if "gemm_kernel" in nm:
+        return "kernel syrk 8192x8192x8192" if ms > 12.0 else "kernel gemm 8192x1024x8192"
+    return "other " + nm.split("(")[0].replace("void ", "")[:80]
+
+
+acc = defaultdict(lambda: {"bytes": 0.0, "read": 0.0, "write": 0.0, "ms_ncu": 0.0, "n": 0})
+for lid in step:
+    d = launch[lid]
+    a = acc[label(lid)]
+    a["read"] += d.get("dram__bytes_read.sum", 0.0)
+    a["write"] += d.get("dram__bytes_write.sum", 0.0)
+    a["ms_ncu"] += d.get("gpu__time_duration.sum", 0.0)
+    a["n"] += 1
+out = {"_note": ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch, keyed by "
+                 "the library's kernel-clock label; averaged over the launches of one config-3 "
+                 f"step. Source: {src} (the last {per_step} library launches = the timed step; "
+                 "tools/ncu_traffic.py). Serialised, cold-cache per-launch times ('ms_ncu') are "
+                 "for the share of the step, not absolute.")}
+for k, a in sorted(acc.items(), key=lambda kv: -kv[1]["ms_ncu"]):
+    n = a["n"]
+    out[k] = {"bytes": (a["read"] + a["write"]) / n, "read": a["read"] / n,
+              "write": a["write"] / n, "ms_ncu": a["ms_ncu"] / n, "launches_in_step": n}
+json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
+tot = sum(a["ms_ncu"] for a in acc.values())
+for k, a in sorted(acc.items(), key=lambda kv: -kv[1]["ms_ncu"]):
+    print(f"{a['ms_ncu']:9.3f} ms {100 * a['ms_ncu'] / tot:5.1f}%  x{a['n']}  "
+          f"{(a['read'] + a['write']) / a['n'] / 1e9:7.2f} GB/launch  {k}")
