@@ -268,6 +268,28 @@ static WaitValueFn stream_wait_value_fn() {
   return g_cu_wait ? wait_value_geq : nullptr;
 }
 
+// Side stream and events of the host-buffer drivers, per host thread and
+// DEVICE (streams and events belong to the device current at creation; a
+// thread may serve streams of several devices, see StreamDevice)
+struct HostPathRes {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, s1_done = nullptr, b_done = nullptr, b2_final = nullptr,
+              launched = nullptr, last_join = nullptr;
+  int* rowcnt = nullptr;  // row-block counters (plain cudaMalloc: stream memory
+  int rowcnt_len = 0;     // operations reject stream-ordered pool allocations)
+};
+static HostPathRes& host_path_res() {
+  static thread_local HostPathRes per_dev[MAX_DEVICES];
+  HostPathRes& r = per_dev[cur_device() & (MAX_DEVICES - 1)];
+  if (!r.side) {
+    cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
+    for (cudaEvent_t* e : {&r.fork, &r.s1_done, &r.b_done, &r.b2_final, &r.launched, &r.last_join})
+      cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    cudaEventRecord(r.last_join, r.side);
+  }
+  return r;
+}
+
 // ---------------------------------------------------------------- pftrf from host
 // The factorization of a pinned HOST RFP buffer with the transfer streamed:
 // the rows holding T1/T2 are copied on `st` and potrf(T1) starts as soon as
@@ -285,21 +307,9 @@ int pftrf_host_t(char transr, char uplo, int64_t n, const void* h_arf, void* d_a
   if (int rc = reset_info(info, st)) return rc;
   if (n == 0) return 0;
   const RfpDesc d = rfp_desc(n, uplo, transr);
-  static thread_local cudaStream_t side = [] {
-    cudaStream_t s;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    return s;
-  }();
-  static thread_local cudaEvent_t fork = [] {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    return e;
-  }();
-  static thread_local cudaEvent_t s1_done = [] {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    return e;
-  }();
+  HostPathRes& R = host_path_res();
+  cudaStream_t side = R.side;
+  cudaEvent_t fork = R.fork, s1_done = R.s1_done;
   int* cflags;
   int* sflags;
   if (int rc = h2d_rfp_begin<T>(d, h_arf, d_arf, st, side, fork, s1_done, &cflags, &sflags))
@@ -326,15 +336,12 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   if (int rc = reset_info(info, st)) return rc;
   if (n == 0) return 0;
   const RfpDesc d = rfp_desc(n, uplo, transr);
-  static thread_local cudaStream_t side = [] {
-    cudaStream_t s;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    return s;
-  }();
-  static thread_local cudaEvent_t ev[4] = {};
-  if (!ev[0])
-    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  cudaEvent_t fork = ev[0], s1_done = ev[1], b_done = ev[2], b2_final = ev[3];
+  HostPathRes& R = host_path_res();
+  cudaStream_t side = R.side;
+  cudaEvent_t fork = R.fork, s1_done = R.s1_done, b_done = R.b_done, b2_final = R.b2_final;
+  // the previous call's row-block waits (side stream) read the same counter
+  // buffer: order this call after them, whatever stream it is on
+  cudaStreamWaitEvent(st, R.last_join, 0);
   int* cflags;
   int* sflags;
   if (int rc = h2d_rfp_begin<T>(d, h_arf, d_arf, st, side, fork, s1_done, &cflags, &sflags))
@@ -355,52 +362,28 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   // 64-row blocks: with the row-completion hook every block is copied back as
   // soon as its column tasks are done (a stream-ordered wait on the solve's
   // per-row counter), so only the last block's copy follows the solve
-  static thread_local cudaEvent_t launched = [] {
-    cudaEvent_t ev_;
-    cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming);
-    return ev_;
-  }();
-  // the previous call's row-block waits (side stream) read the same counter
-  // buffer: order this call's use of it after them, whatever stream it is on
-  static thread_local cudaEvent_t last_join = [] {
-    cudaEvent_t ev_;
-    cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming);
-    cudaEventRecord(ev_, 0);
-    return ev_;
-  }();
-  cudaStreamWaitEvent(st, last_join, 0);
   RowDoneHook hook;
-  hook.launched = launched;
+  hook.launched = R.launched;
   const int nbh = (int)((split + 63) / 64);
-  // (a plain cudaMalloc buffer, kept per host thread and device and grown as
-  // needed: stream memory operations reject stream-ordered pool allocations)
-  static thread_local int* rc_buf[MAX_DEVICES] = {};
-  static thread_local int rc_len[MAX_DEVICES] = {};
   int* rowcnt = nullptr;
   if (trail && stream_wait_value_fn()) {
-    const int dev = cur_device() & (MAX_DEVICES - 1);
-    if (rc_len[dev] < nbh) {
-      cudaStreamSynchronize(st);  // (a previous call's waits may still read the old buffer)
-      cudaStreamSynchronize(side);
-      if (rc_buf[dev]) cudaFree(rc_buf[dev]);
-      rc_buf[dev] = nullptr;
-      rc_len[dev] = 0;
-      if (cudaMalloc((void**)&rc_buf[dev], (size_t)nbh * sizeof(int)) == cudaSuccess)
-        rc_len[dev] = nbh;
+    if (R.rowcnt_len < nbh) {
+      cudaStreamSynchronize(side);  // (a previous call's waits may still read the old buffer)
+      if (R.rowcnt) cudaFree(R.rowcnt);
+      R.rowcnt = nullptr;
+      R.rowcnt_len = 0;
+      if (cudaMalloc((void**)&R.rowcnt, (size_t)nbh * sizeof(int)) == cudaSuccess)
+        R.rowcnt_len = nbh;
       else
         cudaGetLastError();
     }
-    if (rc_len[dev] >= nbh) rowcnt = rc_buf[dev];
-    if (rowcnt) hook.rowcnt = rowcnt;
+    if (R.rowcnt_len >= nbh) rowcnt = R.rowcnt;
+    hook.rowcnt = rowcnt;
   }
   int rcf = pfsv<T>(Ctx{st, info}, d, (T*)d_arf, V<T>(d_b, n, nrhs, 1, ldb), s1_done, cflags,
                     sflags, b_done, trail ? b2_final : nullptr, rowcnt ? &hook : nullptr);
   if (cflags) cudaFreeAsync(cflags, st);
-  auto free_rowcnt = [&]() {};  // (the counter buffer is kept for the next call)
-  if (rcf) {
-    free_rowcnt();
-    return rcf;
-  }
+  if (rcf) return rcf;
   if (nrhs == 0) return 0;
   if (trail) {
     cudaStreamWaitEvent(side, b2_final, 0);
@@ -442,8 +425,7 @@ int pfsv_host_t(char transr, char uplo, int64_t n, int64_t nrhs, const void* h_a
   }
   cudaEventRecord(fork, side);  // join the side stream back into `st`
   cudaStreamWaitEvent(st, fork, 0);
-  cudaEventRecord(last_join, side);
-  free_rowcnt();
+  cudaEventRecord(R.last_join, side);
   return 0;
 }
 
