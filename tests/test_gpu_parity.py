@@ -919,7 +919,7 @@ def test_pfsv_device_matches_pftrf_pftrs(P, uplo, transr, n, cplx):
 
 @pytest.mark.parametrize("uplo", "LU")
 @pytest.mark.parametrize("transr", "NT")
-@pytest.mark.parametrize("n", [130, 1501, 2049, 4001])
+@pytest.mark.parametrize("n", [128, 130, 257, 1501, 2049, 4001])
 def test_pfsv_fused_chain(P, uplo, transr, n):
     """Real mid orders factor through the one-launch SRPA chain (every tile of
     T1, S, T2 in one dataflow kernel; the phase clock sees that phase and no
