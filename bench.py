@@ -574,9 +574,15 @@ def run_c3(args, rank, world, local):
     ee.record(st)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(es.elapsed_time(ee) / e2e_steps, world)
+    # the host path's solution against the device step's (same kernels, same
+    # summation order: expected bit-identical; the head block came back row
+    # block by row block while the last solve still ran)
+    xd = x.t().contiguous().cpu()
+    e2e_diff = float((out_x - xd).abs().max() / xd.abs().max())
     del pristine, work, host_rfp
     line["e2e"] = {"value": world * flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                   "max_rel_diff_vs_device_solution": e2e_diff,
                    "path": "rfp.pfsv_from_host (public API): pinned host RFP + RHS in, solution "
                            "out, transfers overlapped with pftrf/pftrs"}
     return line
