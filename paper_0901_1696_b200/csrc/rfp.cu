@@ -389,7 +389,7 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     // tiles fill the SMs the diagonal chain leaves idle.  Measured 10-16%
     // faster for n1 up to 4096 (pftrf 4096: 2.71 -> 2.27 ms, 8192: 8.82 ->
     // 7.89) and slower above (16384: 25.6 vs 24.8 ms), so used up to
-    // RFPK_PANEL_MAX (default 4096) columns.  (Row-major blocks, TRANSR='T',
+    // tuning panel_max (default 4096) columns.  (Row-major blocks, TRANSR='T',
     // run the panel in place too: a column-major workspace copy measured
     // 2.48 vs 2.39 ms at n = 4000 and 1.67 vs 1.65 at 3000.)
     int fused = -100;
