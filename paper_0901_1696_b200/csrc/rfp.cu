@@ -203,50 +203,6 @@ template <typename T> static int ws_colmajor(Ctx c, i64 m, i64 n, View<T>& v) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-// Cholesky of the k x k lower view t1 and the solve of the m x k block s1
-// below it, L21 = S L11^-H, in ONE dataflow launch over the tall panel
-// [t1; s1] (s1 must continue t1's rows in the same strided view).  The
-// panel's row tiles must break at its column count, so it factors the first
-// k' = 64*floor(k/64) columns; the r < 64 remaining ones follow as
-// T22 -= L21 L21^H, S2 -= L31 L21^H, potrf(T22), S2 <- S2 L22^-H (the same
-// blocked Cholesky, info offsets unchanged).  -100: k < 64.
-template <typename T> static int panel_chol(Ctx c, View<T> t1, View<T> s1, T* W) {
-  const i64 k = t1.m, m = s1.m, ka = k / 64 * 64, rr = k - ka;
-  if (ka < 64) return -100;
-  View<T> panel{t1.p, k + m, ka, t1.rs, t1.cs};
-  int rc = potrf_panel_tiles(c, panel, ka, 0, W);
-  if (!rc && rr) {
-    const bool herm = is_cplx<T>::value;
-    View<T> L21 = t1.sub(ka, 0, rr, ka), T22 = t1.sub(ka, ka, rr, rr);
-    View<T> L31 = s1.sub(0, 0, m, ka), S12 = s1.sub(0, ka, m, rr);
-    rc = blas_syrk(c, 'L', 'N', -1.0, L21, 1.0, T22, herm);
-    if (!rc) rc = blas_gemm(c, 'N', 'C', m_one<T>(), L31, L21, one<T>(), S12);
-    if (!rc) rc = blas_potrf(c, 'L', T22, (int)ka, (T*)nullptr);
-    if (!rc) rc = blas_trsm(c, 'R', 'L', 'C', 'N', one<T>(), T22, S12, false);
-  }
-  return rc;
-}
-
-// The same through a column-major workspace panel when T1 and S are not one
-// strided view (UPLO='U': S1 sits above T1 in the rectangle and enters
-// transposed): copy T1's lower triangle and S in, factor, copy back --
-// O(n^2) coalesced copies buy the one-launch panel.
-template <typename T> static int panel_chol_ws(Ctx c, View<T> t1, View<T> s, T* W) {
-  const i64 k = t1.m, m = s.m;
-  if (k / 64 * 64 < 64) return -100;
-  View<T> P;
-  int rc = ws_colmajor(c, k + m, k, P);
-  if (rc) return rc;
-  View<T> p1 = P.sub(0, 0, k, k), p2 = P.sub(k, 0, m, k);
-  rc = tile_copy(c, t1, p1, true);
-  if (!rc) rc = tile_copy(c, s, p2, false);
-  if (!rc) rc = panel_chol(c, p1, p2, W);
-  if (!rc) rc = tile_copy(c, p1, t1, true);
-  if (!rc) rc = tile_copy(c, p2, s, false);
-  cudaFreeAsync(P.p, c.st);
-  return rc;
-}
-
 // potrf('U', T2) (rfp.py:89 / :84).  The lower view the Cholesky factors is
 // T2^T; for TRANSR='N' that view is row-major with the RFP's odd leading
 // dimension, where every 16-wide K slice of a row straddles an extra sector
@@ -384,35 +340,19 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
     if (gated && !rc && s1_ready) rc = (int)cudaStreamWaitEvent(c.st, s1_ready, 0);
   };
   if (d.lower) {
-    // potrf(T1) and S1 <- S1 T1^-H as ONE dataflow launch over the tall panel
-    // [T1; S1] (contiguous rows of the normal rectangle; panel_chol): the S1
-    // tiles fill the SMs the diagonal chain leaves idle.  Measured 10-16%
-    // faster for n1 up to 4096 (pftrf 4096: 2.71 -> 2.27 ms, 8192: 8.82 ->
-    // 7.89) and slower above (16384: 25.6 vs 24.8 ms), so used up to
-    // tuning panel_max (default 4096) columns.  (Row-major blocks, TRANSR='T',
-    // run the panel in place too: a column-major workspace copy measured
-    // 2.48 vs 2.39 ms at n = 4000 and 1.67 vs 1.65 at 3000.)
+    // (mid orders took the one-launch chain above.)  potrf(T1) and the S1
+    // solve as two concurrent launches, the solve gated row block by row
+    // block on the factorization (device-resident input, real, column-major
+    // T1: potrf_trsm_overlap); streamed input: each launch keeps its chunk
+    // gate (B = S1^T, block row i <-> column chunk i)
     int fused = -100;
-    if (!is_cplx<T>::value && !s1_ready && d.n2 && d.n1 <= panel_max())
-      fused = panel_chol(c, t1, s1, W);
+    if (d.n2 && (gated || !s1_ready))
+      fused = potrf_trsm_overlap(c, t1, W, herm, s1.t(), cflags, sflags, 0);
     if (fused != -100) {
       rc = fused;
-      tr.mark("potrf(T1)+trsm(S1)");
+      after_s1();
+      tr.mark("potrf(T1)||trsm(S1)");
     } else {
-      // potrf(T1) and the S1 solve as two concurrent launches, the solve gated
-      // row block by row block on the factorization (device-resident input,
-      // real, column-major T1: potrf_trsm_overlap)
-      // (streamed input: each launch keeps its chunk gate; B = S1^T, block
-      // row i <-> column chunk i)
-      if (d.n2 && (gated || !s1_ready))
-        fused = potrf_trsm_overlap(c, t1, W, herm, s1.t(), cflags, sflags, 0);
-      if (fused != -100) {
-        rc = fused;
-        after_s1();
-        tr.mark("potrf(T1)||trsm(S1)");
-      }
-    }
-    if (fused == -100) {
       {
         InputGate g(cflags, 0);
         rc = gated ? blas_potrf(c, 'L', t1, 0, W) : potrf_block(c, 'L', t1, 0, W);
@@ -433,19 +373,9 @@ int pftrf(Ctx c, const RfpDesc& d, T* arf, cudaEvent_t s1_ready, const int* cfla
       tr.mark(plan && plan->done ? "pftrs(rest)" : "potrf(T2)");
     }
   } else {
-    // UPLO='U': S1 <- T1^-H S1 is the tall panel [T1; S1^T] transposed; S1
-    // lies above T1 in the rectangle, so the one-launch panel runs on a
-    // column-major workspace copy (panel_chol_ws), same limit as 'L' (config
-    // 2, n = 4000/4001 'U': pftrf 2.59-2.71 -> 2.38-2.52 ms)
+    // UPLO='U' (mid orders took the one-launch chain above)
     int fused = -100;
-    if (!is_cplx<T>::value && !s1_ready && !gated && d.n2 && d.n2 <= panel_max())
-      fused = panel_chol_ws(c, t1, s1.t(), W);
-    if (fused != -100) {
-      rc = fused;
-      tr.mark("potrf(T1)+trsm(S1)");
-      if (!rc) rc = blas_syrk(c, 'U', 'C', -1.0, s1, 1.0, t2, herm);
-      tr.mark("syrk(T2)");
-    } else if (d.n2) {
+    if (d.n2) {
       // larger leading blocks: potrf(T1) and the S1 solve concurrently (as 'L')
       if (gated || !s1_ready)  // B = S1: block column c <-> column chunk c
         fused = potrf_trsm_overlap(c, t1, W, herm, s1, cflags, sflags, 1);
