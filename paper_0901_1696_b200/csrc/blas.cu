@@ -662,7 +662,7 @@ template <typename T> int trtri_oop(Ctx c, bool unit, View<T> A) {
   if (!rc) rc = leaf_inverses(c, A, unit, W);
   if (!rc) rc = ws_matrix(c, n, n, X, is_rowmajor(A));
   if (!rc) rc = tri_copy(c, X, X, CP_EYE);
-  if (!rc) rc = trsm_tiles(c, true, false, A, X, (const T*)W, false);
+  if (!rc) rc = trsm_tiles(c, true, false, A, X, (const T*)W, false, nullptr, 0, nullptr, true);
   // (unit diagonal: the stored diagonal is never referenced nor written)
   if (!rc) rc = tri_copy(c, X, A, unit ? CP_SLOWER_ONLY : CP_LOWER_ONLY);
   if (X.p) cudaFreeAsync(X.p, c.st);

@@ -90,9 +90,12 @@ template <typename T> int potrf_rfp_tiles(Ctx c, View<T> P, View<T> V, int base,
 // 64-block inverses, wtrans when Tm is upper; -100 = unsupported strides
 // agate: row block i of Tm (and W_i) readable once agate[i * agate_stride]
 // is set by a concurrent producer (aabort != 0: it failed)
+// tri_rhs: B is lower-triangular (a forward solve's identity in trtri): the
+// zero blocks of X above its diagonal are neither summed nor solved
 template <typename T>
 int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans,
-               const int* agate = nullptr, int agate_stride = 0, const int* aabort = nullptr);
+               const int* agate = nullptr, int agate_stride = 0, const int* aabort = nullptr,
+               bool tri_rhs = false);
 // per-device streams for concurrent launches: hi = greatest priority (the
 // critical-path kernel), lo = least; ev = scratch fork/join events
 // Per host thread and device (thread_local; see tile_potrf.cu)

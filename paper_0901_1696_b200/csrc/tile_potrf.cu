@@ -937,6 +937,10 @@ struct TrsmArgs {
   int aguard_keep;
   int scan;  // scan-ahead chunk waits (see trsm_task's open_chunk)
   int* rowcnt;  // RowHook: finished column tasks per row block (or null)
+  // forward solve whose right-hand side is lower-triangular (B(r, j) = 0 for
+  // r < j: trtri's identity): X(r, j) = 0 for r < j too, so task (i, c)
+  // sums only chunks k >= c TN / 64 and the tasks above that are no-ops
+  int tri_rhs;
 };
 
 template <typename T, bool AK, bool BKM, int TN>
@@ -968,6 +972,9 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   T* Bs = sm + STAGES * LA::SIZE;
   const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
   const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
+  // (triangular right-hand side: chunks before q0 hold zeros of X)
+  const int q0 = (a.tri_rhs && a.lower) ? (c * TN) / TP : 0;
+  if (nprev < q0) return true;  // X(i, c) = 0: the workspace already holds it
   // (wide tiles only: the narrow, chain-bound solves measured slower with
   // the extra scan on their critical wait -- pftrs n = 4000 0.73 -> 0.755 ms)
   const bool scan_ahead = TN == TP && a.scan != 0;
@@ -1007,7 +1014,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   // warp 0 scans ahead 32 flags per round trip and one acquire fence covers
   // every further chunk found published -- one barrier for the long run of
   // chunks solved well before this task instead of one per chunk
-  int ready = 0;
+  int ready = q0;
   auto open_chunk = [&](int kk) -> bool {
     const int q = a.lower ? kk : a.nb - 1 - kk;  // position in solve order
     if (!scan_ahead) {
@@ -1079,11 +1086,11 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
           }
     }
   }
-  const int KT = nprev * SPC;
+  const int KT = (nprev - q0) * SPC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
-      if (s % SPC == 0) open_chunk(chunk(s / SPC));
+      if (s % SPC == 0) open_chunk(chunk(q0 + s / SPC));
       load_stage(s, s);
     }
     cp_async_commit();
@@ -1094,7 +1101,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     cta_sync();
     const int nk = kt + STAGES - 1;
     if (nk < KT) {
-      if (nk % SPC == 0) open_chunk(chunk(nk / SPC));
+      if (nk % SPC == 0) open_chunk(chunk(q0 + nk / SPC));
       load_stage(nk % STAGES, nk);
     }
     cp_async_commit();
@@ -1291,7 +1298,7 @@ int trsm_launch(View<T> Tm, View<T> B, const T* W, const TrsmArgs& a, int* sync,
 // inverses; wtrans for Tm upper).  Returns -100 for unsupported strides.
 template <typename T>
 int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, bool wtrans,
-               const int* agate, int agate_stride, const int* aabort) {
+               const int* agate, int agate_stride, const int* aabort, bool tri_rhs) {
   const i64 n = Tm.m;
   if (n == 0 || B.n == 0) return 0;
   const bool ak = !(Tm.rs == 1);
@@ -1327,6 +1334,7 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.aguard_keep = num_sms();
   a.scan = 1;
   a.rowcnt = nullptr;
+  a.tri_rhs = tri_rhs && lower ? 1 : 0;
   RowDoneHook* hook = RowHook::current();
   const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
   int* sync = nullptr;
@@ -1368,9 +1376,9 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
 }
 
 template int trsm_tiles<double>(Ctx, bool, bool, View<double>, View<double>, const double*, bool,
-                                const int*, int, const int*);
+                                const int*, int, const int*, bool);
 template int trsm_tiles<Z>(Ctx, bool, bool, View<Z>, View<Z>, const Z*, bool, const int*, int,
-                           const int*);
+                           const int*, bool);
 
 size_t potrf_sync_ints(int nt, int mt) { return SYNC_HDR + (size_t)mt * nt + nt; }
 
