@@ -233,11 +233,11 @@ namespace {
 // G = conj?(Gv) (n x k) and op(G) = G^H (herm) or G^T.
 template <typename T>
 int herk_core(Ctx c, int tri, double alpha, View<T> Gv, bool gconj, double beta, View<T> C,
-              bool herm) {
+              bool herm, int g_tri = A_FULL) {
   const bool cplx = is_cplx<T>::value;
   const bool bconj = cplx ? (herm ? !gconj : gconj) : false;
   return gemm<T>(tri, sc_from<T>(alpha), Gv, cplx && gconj, Gv.t(), bconj, sc_from<T>(beta), C,
-                 cplx && herm, c.info, c.st);
+                 cplx && herm, c.info, c.st, g_tri);
 }
 
 // Inverses of all 64-leaves of the lower-in-view triangle L into W slabs.
@@ -705,8 +705,9 @@ template <typename T> int lauum_oop(Ctx c, View<T> A) {
   View<T> Lw;
   int rc = ws_matrix(c, A.m, A.m, Lw, is_rowmajor(A));
   if (!rc) rc = tri_copy(c, A, Lw, CP_LOWER0);
-  // L^H L = G G^H with G = conj(L^T)
-  if (!rc) rc = herk_core(c, TRI_LOWER, 1.0, Lw.t(), is_cplx<T>::value, 0.0, A, true);
+  // L^H L = G G^H with G = conj(L^T), upper triangular with its zeros in Lw:
+  // the lower output tile (i, j) only needs K from row i on (1/3 the flops)
+  if (!rc) rc = herk_core(c, TRI_LOWER, 1.0, Lw.t(), is_cplx<T>::value, 0.0, A, true, A_UBAND);
   if (Lw.p) cudaFreeAsync(Lw.p, c.st);
   return rc;
 }

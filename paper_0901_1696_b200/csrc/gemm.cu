@@ -102,15 +102,16 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs<T>& g, int tm, int tn, 
   TileLoader<T, BN, BK, NT, BKM> lb;
   la.init(g.A, g.lda, m0, M, tid);
   lb.init(g.B, g.ldb, n0, N, tid);
-  const bool masked = g.a_tri != A_FULL || g.b_tri != A_FULL;
+  const bool masked = (g.a_tri != A_FULL && g.a_tri != A_UBAND) ||
+                      (g.b_tri != A_FULL && g.b_tri != A_UBAND);
   // a triangular operand is zero outside a band of K for this tile: lower
   // (k <= row) ends the K loop at the tile's last row, upper (k >= row)
   // starts it at the tile's first -- half the flops of a masked trmm GEMM
   int kbeg = 0, kend = g.K;
   if (g.a_tri == A_LOWER || g.a_tri == A_SLOWER) kend = min(kend, m0 + BM);
-  if (g.a_tri == A_UPPER || g.a_tri == A_SUPPER) kbeg = max(kbeg, m0);
+  if (g.a_tri == A_UPPER || g.a_tri == A_SUPPER || g.a_tri == A_UBAND) kbeg = max(kbeg, m0);
   if (g.b_tri == A_LOWER || g.b_tri == A_SLOWER) kend = min(kend, n0 + BN);
-  if (g.b_tri == A_UPPER || g.b_tri == A_SUPPER) kbeg = max(kbeg, n0);
+  if (g.b_tri == A_UPPER || g.b_tri == A_SUPPER || g.b_tri == A_UBAND) kbeg = max(kbeg, n0);
   const int kt0 = kbeg / BK;
   la.skip(kt0);
   lb.skip(kt0);

@@ -32,7 +32,7 @@ template <typename T> struct GemmArgs {
   int herm_diag;      // complex TRI modes: force Im(C_ii) = 0
   const int* skip;    // device flag: nonzero -> do nothing (failed factorization)
   int tiles_m;        // tiles along M (for the triangular mapping)
-  int a_tri;          // A operand mask: 0 none, 1 lower, 2 upper, 3 strict lower, 4 strict upper
+  int a_tri;          // A operand mask: 0 none, 1 lower, 2 upper, 3 strict lower, 4 strict upper, 5 upper band
   int b_tri;          // same mask applied to B (k, n) as if it were A (n, k) (transposed problems)
   long long ntiles;   // tiles of the launch (CTAs stride over them)
   int band;           // TRI square tiles: rows per band of the rasterised order (0: row by row)
@@ -40,7 +40,9 @@ template <typename T> struct GemmArgs {
 
 
 // A-operand triangle masks (for triangular-times-matrix leaves)
-enum ATri : int { A_FULL = 0, A_LOWER = 1, A_UPPER = 2, A_SLOWER = 3, A_SUPPER = 4 };
+// A_UBAND: upper-triangular operand whose lower part is already zero in
+// memory -- only the K band is narrowed, no per-element mask
+enum ATri : int { A_FULL = 0, A_LOWER = 1, A_UPPER = 2, A_SLOWER = 3, A_SUPPER = 4, A_UBAND = 5 };
 
 
 template <typename T>
