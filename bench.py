@@ -137,16 +137,32 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- dist
+def _backend():
+    """NCCL on the GPUs; BENCH_DIST_BACKEND=gloo lets the CPU tests drive the
+    rank logic (barrier, max over ranks, gathers) with world_size 2."""
+    return os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
+def _coll_device():
+    return "cuda" if _backend() == "nccl" else "cpu"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
 def dist_setup():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = dist_env()
     if world > 1:
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _backend() == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(_backend())
     return rank, world, local
 
 
@@ -161,7 +177,7 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -171,7 +187,7 @@ def all_ranks(x, world):
         return [x]
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     out = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(out, t)
     return [float(v.item()) for v in out]
@@ -500,6 +516,23 @@ def run_c3(args, rank, world, local):
     del a
     dgemm = measured_dgemm(dev)
 
+    # the dominant kernel's largest launch ALONE (pftrf's S1 solve, n2 x n1
+    # right-hand sides on the factored T1 of the last step's buffer, as pftrf
+    # issues it): the in-step launch below shares the SMs with potrf(T1)
+    ld = n + 1 - (n & 1)
+    shift = 1 - (n & 1)
+    t1p = work.data_ptr() + 8 * shift
+    s1p = work.data_ptr() + 8 * (n1 + shift)
+
+    def s1_solve():
+        rc = lib.rfpk_dtrsm(b"R", b"L", b"C", b"N", 1.0, t1p, n1, 1, ld, s1p, n2, n1, 1, ld,
+                            info.data_ptr(), sh)
+        if rc:
+            raise RuntimeError(f"rfpk_dtrsm failed rc={rc}")
+
+    alone_ms = ev_time(s1_solve, 3)
+    alone_tf = n1 * n1 * n2 / (alone_ms * 1e-3) / 1e12
+
     kernels = kernel_table(table, args.steps)
     phases = phase_table(table, args.steps, n1, n2, nrhs, dgemm)
     # the dominant kernel: the most device time per step summed over its
@@ -524,6 +557,10 @@ def run_c3(args, rank, world, local):
         "algorithmic_flops_per_launch": d_fl / d_launches, "ms_per_launch": d_ms / d_launches,
         "launches": [{k: r_[k] for k in ("shape", "launches_per_step", "ms_per_launch", "tflops",
                                          "frac_nominal") if k in r_} for r_ in drows],
+        "alone": {"launch": f"S1 solve {n2}x{n1} by itself (rfpk_dtrsm on the same views, median "
+                            "of 3 after the timed steps)", "ms_per_launch": alone_ms,
+                  "achieved": alone_tf, "frac": alone_tf / NOMINAL_FP64_TFLOPS,
+                  "frac_measured_dgemm": alone_tf / dgemm},
         "timing": ("live: CUDA events around every launch on the stream it runs on, inside the "
                    f"{args.steps} timed steps (the S1 solve's launch spans its run beside "
                    "potrf(T1), flag waits included)"),
@@ -902,11 +939,14 @@ def main():
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the N ranks
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    rank, world, local = dist_setup()
     if args.impl == "reference":
+        # rank 0 alone times the CPU path; the other ranks exit 0 without work
+        # (no process group: nothing here is collective)
+        rank, world, _ = dist_env()
         run_reference(args, rank, world)
-    else:
-        run_b200(args, rank, world, local)
+        return
+    rank, world, local = dist_setup()
+    run_b200(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
