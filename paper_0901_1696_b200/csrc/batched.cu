@@ -149,20 +149,22 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
   const i64 k = blockIdx.x;
   double* g = arf + k * stride_arf;
   load_rect<TRANS>(R, g);
-  // the first 8-column chunk of the right-hand side goes into its B-operand
-  // registers now: the load latency then hides under the factorization
-  // instead of sitting between the inverses and the solve (column g8, rows
-  // 4s + t4 of b1 / b2)
-  double x1p[8], x2p[8];
+  // the first 8-column chunk of the right-hand side goes into its registers
+  // now (transposed accumulator layout, see vmm: right-hand side g8, rows
+  // 8j + 2 t4 + e of b1 / b2): the load latency then hides under the
+  // factorization instead of sitting between the inverses and the solve
+  double y1p[4][2], y2p[4][2];
   if (SOLVE) {
     const int g8 = lane >> 2, t4 = lane & 3;
     const int cw = nrhs < 8 ? nrhs : 8;
-    const double* bc = b + k * stride_b + (i64)g8 * ldb;
+    const double* bc = b + k * stride_b + (i64)g8 * ldb + 2 * t4;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      x1p[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
-      x2p[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        y1p[j][e] = g8 < cw ? bc[8 * j + e] : 0.0;
+        y2p[j][e] = g8 < cw ? bc[32 + 8 * j + e] : 0.0;
+      }
   }
   // T1 / T2 / S1 of the normal 65 x 32 rectangle (convert.py:142-153, d = 1):
   // V1 = T1 (L1, lower), V2 = T2^T (L2, lower), S = S1 ('L') | S1^T ('U')
@@ -206,64 +208,65 @@ __global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_a
   const int g8 = lane >> 2, t4 = lane & 3;
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int cw = nrhs - c0 < 8 ? nrhs - c0 : 8;
-    // b1 / b2 straight into the B-operand registers (column g8, rows 4s+t4)
-    double x1[8], x2[8], c[2][4];
+    // b1^T / b2^T (8 x 32 each) in the transposed accumulator layout
+    double y1[4][2], y2[4][2], z[4][2];
     if (c0 == 0) {
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        x1[s] = x1p[s];
-        x2[s] = x2p[s];
-      }
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          y1[j][e] = y1p[j][e];
+          y2[j][e] = y2p[j][e];
+        }
     } else {
-      const double* bc = bk + (i64)(c0 + g8) * ldb;
+      const double* bc = bk + (i64)(c0 + g8) * ldb + 2 * t4;
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        x1[s] = g8 < cw ? bc[4 * s + t4] : 0.0;
-        x2[s] = g8 < cw ? bc[32 + 4 * s + t4] : 0.0;
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          y1[j][e] = g8 < cw ? bc[8 * j + e] : 0.0;
+          y2[j][e] = g8 < cw ? bc[32 + 8 * j + e] : 0.0;
+        }
+    }
+    auto zero = [](double (&v)[4][2]) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j][0] = v[j][1] = 0.0;
+    };
+    auto negate = [](double (&v)[4][2]) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j][0] = -v[j][0];
+        v[j][1] = -v[j][1];
+      }
+    };
+    zero(z);
+    vmm<1>(o, W1, y1, z);       // z = (W1 b1)^T
+    negate(z);
+    vmm<0>(o, S, z, y2);        // b2 -= S (W1 b1)
+    zero(y1);
+    vmm<1>(o, W2, y2, y1);      // y1 <- (W2 b2)^T
+    zero(y2);
+    vmm<2>(o, W2.t(), y1, y2);  // y2 = x2^T = (W2^T W2 b2)^T: final
+    double* bc = bk + (i64)(c0 + g8) * ldb + 2 * t4;
+    if (g8 < cw) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bc[32 + 8 * j] = y2[j][0];
+        bc[32 + 8 * j + 1] = y2[j][1];
       }
     }
-    zero_c(c);
-    mm32r<1>(o, W1, x1, c);                      // b1 = W1 b1
-    c2b(c, x1);
-    zero_c(c);
-    mm32r<0>(o, S, x1, c);                       // S b1
-    {
-      double d[8];
-      c2b(c, d);
+    // z = -(W1 b1)^T; b1' = W1 b1 - S^T x2 = -(z + S^T x2)
+    vmm<0>(o, S.t(), y2, z);
+    negate(z);
+    zero(y1);
+    vmm<2>(o, W1.t(), z, y1);   // x1^T = (W1^T b1')^T
+    if (g8 < cw) {
 #pragma unroll
-      for (int s = 0; s < 8; ++s) x2[s] -= d[s];  // b2 -= S b1
-    }
-    zero_c(c);
-    mm32r<1>(o, W2, x2, c);                      // b2 = W2 b2
-    c2b(c, x2);
-    zero_c(c);
-    mm32r<2>(o, W2.t(), x2, c);                  // b2 = W2^T b2
-    c2b(c, x2);
-    // b2 is final: store it from the accumulator layout
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = mi * 16 + g8 + ((r & 2) ? 8 : 0), col = 2 * t4 + (r & 1);
-        if (col < cw) bk[32 + row + (i64)(c0 + col) * ldb] = c[mi][r];
+      for (int j = 0; j < 4; ++j) {
+        bc[8 * j] = y1[j][0];
+        bc[8 * j + 1] = y1[j][1];
       }
-    zero_c(c);
-    mm32r<0>(o, S.t(), x2, c);                   // S^T b2
-    {
-      double d[8];
-      c2b(c, d);
-#pragma unroll
-      for (int s = 0; s < 8; ++s) x1[s] -= d[s];  // b1 -= S^T b2
     }
-    zero_c(c);
-    mm32r<2>(o, W1.t(), x1, c);                  // b1 = W1^T b1
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int row = mi * 16 + g8 + ((r & 2) ? 8 : 0), col = 2 * t4 + (r & 1);
-        if (col < cw) bk[row + (i64)(c0 + col) * ldb] = c[mi][r];
-      }
   }
 }
 

@@ -14,7 +14,10 @@
 // with S = S1 for UPLO 'L' and S = S1^T for 'U' (the two compositions of
 // rfp.py:70-89 / 118-136 are the same algebra on a transposed S1), the 32x32
 // Cholesky and inverse on the warp's registers and every product on FP64 DMMA
-// (mma.m16n8k4) fragments read from shared memory.  Only __syncwarp is needed,
+// fragments read from shared memory (mma.m16n8k4 for the factorization's
+// products; the solve runs transposed on mma.m8n8k4 with the right-hand side
+// in accumulator-layout registers, so its six products chain without a
+// shuffle, see vmm).  Only __syncwarp is needed,
 // so twelve matrices (warps) are resident per SM.
 //
 // Shared-memory layout.  The kernel is bound by shared-memory wavefronts
@@ -340,51 +343,42 @@ __device__ __forceinline__ void store_acc(const LaneOff& o, VC C, double acc[2][
     }
 }
 
-// ---- the right-hand side in registers
-// A 32 x 8 block X is held as the m16n8k4 B operand: lane (g, t) owns
-// xb[s] = X(4s + t, g), s = 0..7.  Products land in the accumulator layout
-// c[mi][r] = C(16 mi + g + 8 (r >> 1), 2t + (r & 1)).
-
-// c (32 x 8) += A (32 x 32 view, triangle mask TA) * X (registers)
-template <int TA, class VA>
-__device__ __forceinline__ void mm32r(const LaneOff& o, VA A, const double (&xb)[8],
-                                      double (&c)[2][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int kk = 4 * s + t;
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      if (TA == 1 && mi == 0 && s >= 4) continue;  // strip above the lower triangle
-      if (TA == 2 && mi == 1 && s < 4) continue;   // strip below the upper triangle
-      const int r0 = mi * 16 + g, r1 = r0 + 8;
-      const double a0 =
-          (TA == 1 && kk > r0) || (TA == 2 && kk < r0) ? 0.0 : A.gt(o, mi * 16, 4 * s);
-      const double a1 =
-          (TA == 1 && kk > r1) || (TA == 2 && kk < r1) ? 0.0 : A.gt(o, mi * 16 + 8, 4 * s);
-      mma(c[mi], a0, a1, xb[s]);
-    }
-  }
+// ---- the right-hand side TRANSPOSED in registers (the solve of the fused
+// kernel).  Y = X^T is 8 x 32 (row g = right-hand side g) and lives in the
+// m8n8k4 accumulator layout: lane (g, t) holds y[j][e] = Y(g, 8j + 2t + e).
+// The same registers ARE the A operand of the next product when its k-step
+// (j, e) takes the four k = 8j + 2t + e of lanes t = 0..3 -- a permutation of
+// the summation order only -- so the six products of the solve chain hand
+// their results on without any shuffle.  The B operand of that k-step is
+// M(8jp + g, 8j + 2t + e): exactly the accumulator access pattern of the view
+// (conflict-free in the swizzle for both orientations).
+__device__ __forceinline__ void mma8(double (&c)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
 }
 
-// accumulator layout -> B-operand layout (16 shuffles)
-__device__ __forceinline__ void c2b(const double (&c)[2][4], double (&xb)[8]) {
+// out (8 x 32) += Y (8 x 32) M^T for a 32 x 32 view M indexed (n, k).
+// TRI 1: M lower (k <= n), 2: M upper (k >= n); the other triangle holds
+// unrelated data and reads as zero.
+template <int TRI, class VM>
+__device__ __forceinline__ void vmm(const LaneOff& o, VM M, const double (&y)[4][2],
+                                    double (&out)[4][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int mi = s >> 2, half = (s & 3) >> 1;
-    const int src = (4 * (s & 1) + t) * 4 + (g >> 1);
-    const double v0 = __shfl_sync(0xffffffffu, c[mi][half * 2], src);
-    const double v1 = __shfl_sync(0xffffffffu, c[mi][half * 2 + 1], src);
-    xb[s] = (g & 1) ? v1 : v0;
-  }
-}
-
-__device__ __forceinline__ void zero_c(double (&c)[2][4]) {
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+    for (int e = 0; e < 2; ++e)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) c[mi][r] = 0.0;
+      for (int jp = 0; jp < 4; ++jp) {
+        if (TRI == 1 && j > jp) continue;
+        if (TRI == 2 && j < jp) continue;
+        const int k = 2 * t + e;
+        const bool off = j == jp && ((TRI == 1 && k > g) || (TRI == 2 && k < g));
+        const double b = off ? 0.0 : M.acc(o, 8 * jp, 8 * j, e);
+        mma8(out[jp], y[j][e], b);
+      }
 }
 
 template <int NC>

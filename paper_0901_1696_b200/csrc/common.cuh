@@ -213,6 +213,7 @@ enum TuneKey : int {
   TK_GEMM_WIDE,            // force the 64 x 128 GEMM tile for every product (0)
   TK_BATCHED_GENERIC,      // force the generic batched kernel at n = 64 (0)
   TK_TRACE,                // print per-phase SRPA times to stderr (0)
+  TK_TRSM_SPLIT,           // tile trsm: split tasks: 0 off, 1 automatic, > 1 kept chunks (1)
   TK_COUNT
 };
 long long tune(TuneKey k);  // defined in capi.cu

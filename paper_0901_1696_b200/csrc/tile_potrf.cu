@@ -941,11 +941,20 @@ struct TrsmArgs {
   // r < j: trtri's identity): X(r, j) = 0 for r < j too, so task (i, c)
   // sums only chunks k >= c TN / 64 and the tasks above that are no-ops
   int tri_rhs;
+  // split tasks (shorter tail): the task of solve position p >= split_from
+  // sums only its last split_m chunks; a PRE task handed out split_m + 1
+  // steps earlier (its chunks are all handed out by then) sums the chunks
+  // before that and subtracts them from B(i, c) in place, then sets
+  // pre[i * nc + c].  0 = off.
+  int split_m, split_from;
+  int* pre;
 };
 
 template <typename T, bool AK, bool BKM, int TN>
 __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const TrsmArgs& a,
-                          int* done, int i, int c, T* sm, int* s_ok) {
+                          int* done, int i, int c, T* sm, int* s_ok, int kind = 0) {
+  // kind 0: the whole task; 1: the task of a split position (its last
+  // split_m chunks, then B(i, c) once the PRE task has updated it); 2: PRE
   if (a.agate) {  // Tm's row block i and W_i come from a concurrent tile potrf
     if (threadIdx.x == 0) {
       const int* f = a.agate + (i64)i * a.agate_stride;
@@ -973,7 +982,9 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   const i64 lda = AK ? Tm.rs : Tm.cs, ldb = BKM ? B.cs : B.rs;
   const int nprev = a.lower ? i : a.nb - 1 - i;  // chunks solved before block i
   // (triangular right-hand side: chunks before q0 hold zeros of X)
-  const int q0 = (a.tri_rhs && a.lower) ? (c * TN) / TP : 0;
+  const int q0 = kind == 1 ? nprev - a.split_m
+                           : ((a.tri_rhs && a.lower) ? (c * TN) / TP : 0);
+  const int qend = kind == 2 ? nprev - a.split_m : nprev;  // chunks [q0, qend)
   if (nprev < q0) return true;  // X(i, c) = 0: the workspace already holds it
   // (wide tiles only: the narrow, chain-bound solves measured slower with
   // the extra scan on their critical wait -- pftrs n = 4000 0.73 -> 0.755 ms)
@@ -983,7 +994,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   constexpr int PIPE = STAGES * (LA::SIZE + LB::SIZE);
   constexpr int STILE = (TN > TP ? TN : TP) * LD64;  // the S tile (64 x TN, LD64 columns)
   T* const Wpre = sm + (PIPE > STILE ? PIPE : STILE);  // PREW only
-  if constexpr (PREW) {
+  if (PREW && kind != 2) {
     // W'_i does not depend on any task: fetch it now (oldest cp.async group,
     // complete before the first pipeline wait returns)
     const T* w = W + (i64)i * TP * TP;
@@ -1028,7 +1039,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
         for (;;) {
           const int qq = rr + lane;
           const int k2 = a.lower ? qq : a.nb - 1 - qq;
-          const bool ok = qq < nprev && ld_relaxed(done + (i64)k2 * a.nc + c);
+          const bool ok = qq < qend && ld_relaxed(done + (i64)k2 * a.nc + c);
           const unsigned m = __ballot_sync(0xffffffffu, ok);
           if (m == 0xffffffffu) { rr += 32; continue; }
           rr += __ffs(~m) - 1;
@@ -1086,7 +1097,7 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
           }
     }
   }
-  const int KT = (nprev - q0) * SPC;
+  const int KT = (qend - q0) * SPC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
@@ -1152,6 +1163,32 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
   cp_async_wait<0>();
   cta_sync();
   if (nprev > 0 && !*s_ok) return false;
+
+  if (kind == 2) {  // PRE: B(i, c) -= the partial sum, in place
+    const i64 pi0 = (i64)i * TP, pc0 = (i64)c * TN;
+    const int pm = a.n - (int)pi0 < TP ? a.n - (int)pi0 : TP;
+    const int pn = a.nrhs - (int)pc0 < TN ? a.nrhs - (int)pc0 : TN;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = wm * WL::RW + mi * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = wn * WL::CW + ni * 8 + 2 * tq + (r & 1);
+          if (row < pm && col < pn) {
+            T* bp = B.at(pi0 + row, pc0 + col);
+            *bp = *bp - fragn<T>(acc[0], acc[NACC - 1], mi, ni, r);
+          }
+        }
+    cta_sync();
+    if (tid == 0) st_release(a.pre + (i64)i * a.nc + c, 1);
+    return true;
+  }
+  if (kind == 1) {  // B(i, c) as the PRE task left it
+    if (tid == 0) spin_wait_acquire(a.pre + (i64)i * a.nc + c);
+    cta_sync();
+  }
 
   if (a.ext) {  // B's original block (i, c) streamed in by the copy engine
     // (the gate's flags cover 64-column chunks; c counts TN-wide blocks)
@@ -1252,17 +1289,39 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
   }
   int* counter = sync;
   int* done = sync + SYNC_HDR;
-  const long long total = (long long)a.nb * a.nc;
+  const int npre = a.split_m ? a.nb - a.split_from : 0;
+  const long long total = (long long)(a.nb + npre) * a.nc;
+  // hand-out order: step by step the tasks of solve position `step`, and
+  // (split solves) behind them the PRE tasks of position step + split_m + 1
+  const int s1 = a.split_from - a.split_m - 1;
+  const long long t1 = (long long)s1 * a.nc, span = (long long)npre * 2 * a.nc;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
     cta_sync();
     const long long t = s_task;
     cta_sync();
     if (t >= total) return;
-    const int step = (int)(t / a.nc), c = (int)(t % a.nc);
+    int step, c, kind = 0;
+    if (TN != TP || !a.split_m || t < t1) {
+      step = (int)(t / a.nc), c = (int)(t % a.nc);
+    } else if (t - t1 < span) {
+      const long long u = t - t1;
+      step = s1 + (int)(u / (2 * a.nc));
+      c = (int)(u % (2 * a.nc));
+      if (c >= a.nc) {
+        c -= a.nc;
+        step += a.split_m + 1;
+        kind = 2;
+      }
+    } else {
+      const long long u = t - t1 - span;
+      step = s1 + npre + (int)(u / a.nc), c = (int)(u % a.nc);
+    }
+    if (TN == TP && a.split_m && kind == 0 && step >= a.split_from) kind = 1;
     const int i = a.lower ? step : a.nb - 1 - step;
     tt_mark(t, 0);
-    if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok)) return;
+    if (!trsm_task<T, AK, BKM, TN>(Tm, B, W, a, done, i, c, sm, &s_ok, TN == TP ? kind : 0))
+      return;
     tt_mark(t, 1);
   }
 }
@@ -1335,8 +1394,32 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
   a.scan = 1;
   a.rowcnt = nullptr;
   a.tri_rhs = tri_rhs && lower ? 1 : 0;
+  // split tasks: plain wide-tile solves only (a PRE task of row block i would
+  // sit on the triangle gate of a concurrent potrf, or on the input gate, long
+  // before its turn), and only where the tail is a few long tasks per CTA
+  a.split_m = a.split_from = 0;
+  a.pre = nullptr;
+  {
+    // tuning "trsm_split": 0 off, 1 automatic, > 1 the kept chunks.  The tail
+    // of a solve is its last tasks (nb chunks each) running out one by one:
+    // about 2 grid / (nb nc) of the run, so it only matters for few columns
+    // (config 3's pftrs solves, 128 x 16 tasks: 2.76 -> 2.60 ms; kept chunks
+    // 16 / 24 / 32: 2.70 / 2.60 / 2.64 ms)
+    const long long v = tune(TK_TRSM_SPLIT);
+    int m = (int)v;
+    if (v == 1) {
+      m = (a.nb * 3 / 16) & ~7;
+      if (m < 16) m = 16;
+      if (m > 64) m = 64;
+      if ((long long)a.nb * a.nc > 48LL * num_sms()) m = 0;
+    }
+    if (m > 0 && tn == TP && !agate && !a.ext && !a.tri_rhs && a.nb >= 4 * m) {
+      a.split_m = m;
+      a.split_from = 2 * m;
+    }
+  }
   RowDoneHook* hook = RowHook::current();
-  const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc;
+  const size_t ints = SYNC_HDR + (size_t)a.nb * a.nc * (a.split_m ? 2 : 1);
   int* sync = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&sync, ints * sizeof(int), c.st);
   if (e != cudaSuccess) return (int)e;
@@ -1352,6 +1435,7 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
     cudaEventRecord(hook->launched, c.st);
     RowHook::consumed();
   }
+  if (a.split_m) a.pre = sync + SYNC_HDR + (size_t)a.nb * a.nc;
   // B operand = X^T (nrhs x K): K-major when B is column-major
   const bool bkm = B.rs == 1;
   int rc;

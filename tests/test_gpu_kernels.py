@@ -195,6 +195,30 @@ def test_tile_trsm_widths(K, side, uplo, trans, r):
     assert rel(bd, want) <= TOL
 
 
+@pytest.mark.parametrize("side,uplo,trans", [("L", "L", "N"), ("L", "L", "T"), ("L", "U", "N"),
+                                             ("L", "U", "T"), ("R", "L", "T"), ("R", "U", "N")])
+def test_tile_trsm_split_tasks(K, side, uplo, trans):
+    """Split tasks of the wide-tile dataflow trsm (tuning trsm_split): from
+    solve position 6 on, a PRE task sums all but the last 3 chunks of every
+    tile and updates B in place, the tile's own task waits for it.  Ragged
+    last tiles in both dimensions, forward and backward sweeps, against the
+    oracle and against the unsplit solve."""
+    from paper_0901_1696_b200 import _capi
+    n, r = 1800, 4000
+    a = tri_matrix(n, False, 21, rowmajor=(uplo == "U"))
+    b = rnd((n, r) if side == "L" else (r, n), False, 22, rowmajor=(side == "R"))
+    want = b.copy()
+    O.trsm(side, uplo, trans, "N", 1.0, a, want)
+    got = {}
+    for split in (0, 3):
+        with _capi.tuning(trsm_split=split):
+            bd = dev(b)
+            K.trsm(side, uplo, trans, "N", 1.0, dev(a), bd)
+            got[split] = bd.cpu().numpy()
+            assert rel(got[split], want) <= TOL, split
+    assert not np.array_equal(got[0], got[3])  # the split path ran (other summation order)
+
+
 @pytest.mark.parametrize("cplx", [False, True])
 def test_gemm_splitk_deterministic(K, cplx):
     """Few output tiles and a long K take the split-K path (partials reduced
