@@ -1413,7 +1413,7 @@ int trsm_tiles(Ctx c, bool lower, bool conj, View<T> Tm, View<T> B, const T* W, 
       if (m > 64) m = 64;
       if ((long long)a.nb * a.nc > 48LL * num_sms()) m = 0;
     }
-    if (m > 0 && tn == TP && !agate && !a.ext && !a.tri_rhs && a.nb >= 4 * m) {
+    if (m > 0 && tn == TP && !agate && !a.ext && !a.tri_rhs && a.nb >= (v == 1 ? 4 : 3) * m) {
       a.split_m = m;
       a.split_from = 2 * m;
     }

@@ -14,9 +14,12 @@ m = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 torch.manual_seed(1)
 g = torch.randn(n, n, dtype=torch.float64, device=dev) / n ** 0.5
 L = (torch.tril(g) + 2 * torch.eye(n, dtype=torch.float64, device=dev)).t().contiguous().t()
-b0 = torch.randn(m, n, dtype=torch.float64, device=dev).t()
+ROWMAJOR = len(sys.argv) > 3 and sys.argv[3] == "row"
+b0 = torch.randn(n, m, dtype=torch.float64, device=dev) if ROWMAJOR else \
+    torch.randn(m, n, dtype=torch.float64, device=dev).t()
+rsb, csb = (m, 1) if ROWMAJOR else (1, n)
 ref = {}
-for split in (0, 1, 16, 24, 32, 48):
+for split in (0, 1, 16, 24, 32, 40):
     _capi.set_tuning("trsm_split", split)
     for trans in (b"N", b"T"):
         b = b0.clone()
@@ -26,7 +29,7 @@ for split in (0, 1, 16, 24, 32, 48):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             rc = lib.rfpk_dtrsm(b"L", b"L", trans, b"N", 1.0, L.data_ptr(), n, 1, n, b.data_ptr(),
-                                n, m, 1, n, info.data_ptr(), st)
+                                n, m, rsb, csb, info.data_ptr(), st)
             e1.record()
             torch.cuda.synchronize()
             assert rc == 0
