@@ -654,6 +654,34 @@ def make_c4_inputs(start, stop, n, nrhs, seed0, dev):
     return a, arf, rhs
 
 
+def cpu_baseline_c4(arf_host, rhs_host, n, nrhs, sample=2048):
+    """Config 4 on the host: the unmodified reference's rfp.pftrf + rfp.pftrs
+    per matrix (rfp.py:55-136) over the first `sample` matrices of the same
+    inputs, ONE process (the reference has no batched entry point; a matrix of
+    order 64 is interpreter-bound, so its BLAS threads do not help)."""
+    ref = _reference_module()
+    m = min(sample, arf_host.shape[0])
+    t0 = time.perf_counter()
+    if ref is not None:
+        desc = ref.layout.make_descriptor(n, "U", "N")
+        for k in range(m):
+            r = ref.convert.RfpTriangle(arf_host[k].copy(), desc)
+            assert ref.rfp.pftrf(r) == 0
+            ref.rfp.pftrs(r, np.asfortranarray(rhs_host[k]))
+    else:
+        from oracle import rfp_oracle as O
+        for k in range(m):
+            buf = arf_host[k].copy()
+            assert O.pftrf(buf, n, "U", "N") == 0
+            O.pftrs(buf, n, "U", "N", np.asfortranarray(rhs_host[k]))
+    dt = time.perf_counter() - t0
+    return {"value": m / dt, "unit": "matrices/s", "cores": 1,
+            "kind": "reference" if ref is not None else "port",
+            "sample": f"first {m} of the 65,536 matrices, one host process, "
+                      f"{'reference rfpk (baseline/_ref)' if ref is not None else 'oracle port'} "
+                      f"rfp.pftrf + rfp.pftrs(nrhs={nrhs}) per matrix: {dt:.2f} s"}
+
+
 def run_c4(args, rank, world, local):
     """Config 4: 65,536 independent n = 64 matrices sharded by contiguous
     ranges; one fused batched launch per step per rank; the only collective
@@ -738,6 +766,10 @@ def run_c4(args, rank, world, local):
     if rank == 0:
         block["failed_matrices"] = int((gi != 0).sum())
         block["max_residual_scaled"] = float(gr.max())
+    if rank == 0 and world == 1 and not args.no_cpu:
+        m = min(2048, count)
+        block["cpu_baseline"] = cpu_baseline_c4(arf0[:m].cpu().numpy(), rhs0[:m].cpu().numpy(),
+                                                n, nrhs, m)
     if args.no_e2e:
         return block
     # e2e through the public API with pinned host buffers

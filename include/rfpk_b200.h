@@ -55,7 +55,7 @@ int rfpk_graph_cache_clear(void);
 /* Path thresholds (process-wide; there are no environment knobs).  Names and
    defaults: "oop_max" 4096, "t2_copy_min" 2048, "panel_max" 4096,
    "pfsv_overlap_min" 512, "overlap" 1, "graphs" 1, "graph_max_n" 8192,
-   "gemm_wide" 0, "batched_generic" 0, "trace" 0, "trsm_split" 1 (see
+   "gemm_wide" 0, "batched_generic" 0, "trace" 0, "trsm_split" 1, "zpotrf_split_min" 9000 (see
    DESIGN.md section 4).
    Setting a value drops every cached graph.  Returns 0, or -1 for an
    unknown name.  Not meant to be changed while other threads are inside

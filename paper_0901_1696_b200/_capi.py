@@ -158,7 +158,8 @@ class phase_clock:
 
 TUNING_DEFAULTS = {"oop_max": 4096, "t2_copy_min": 2048, "panel_max": 4096,
                    "pfsv_overlap_min": 512, "overlap": 1, "graphs": 1, "graph_max_n": 8192,
-                   "gemm_wide": 0, "batched_generic": 0, "trace": 0, "trsm_split": 1}
+                   "gemm_wide": 0, "batched_generic": 0, "trace": 0, "trsm_split": 1,
+                   "zpotrf_split_min": 9000}
 
 
 def set_tuning(name: str, value: int) -> None:

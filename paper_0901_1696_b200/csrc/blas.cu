@@ -630,8 +630,22 @@ template <typename T> int potrf_node(Ctx c, View<T> A, int base, T* W, int depth
 template <typename T> int potrf_lower(Ctx c, View<T> A, int base, T* W) {
   // the dataflow tile kernel (tile_potrf.cu) at every order above one leaf
   // (measured faster than the recursion everywhere)
-  if (A.m > LEAF && W)
+  if (A.m > LEAF && W) {
+    // complex, large: one split level, the halves on the tile kernel and the
+    // panel solve / update on the GEMM kernel (34 TFLOP/s against the complex
+    // tile kernel's 26 at n = 12000, one CTA per SM: zpotrf 12000 88.7 ms
+    // whole; real orders stay whole -- potrf 8192 6.9 ms vs ~8.2 split)
+    if (is_cplx<T>::value && A.m >= tune(TK_ZPOTRF_SPLIT_MIN)) {
+      const i64 n1 = split_point(A.m), n2 = A.m - n1;
+      View<T> A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
+      int rc;
+      if ((rc = potrf_tiles(c, A11, base, W))) return rc;
+      if ((rc = trsm_rec(c, true, true, A11, A21.t(), W, false))) return rc;
+      if ((rc = herk_core(c, TRI_LOWER, -1.0, A21, false, 1.0, A22, true))) return rc;
+      return potrf_tiles(c, A22, base + (int)n1, W + n1 * 64);
+    }
     return potrf_tiles(c, A, base, W);
+  }
   // (fallback / n <= 64: the recursive driver with look-ahead streams)
   if (A.m < LA_MIN) return potrf_node(c, A, base, W, 0);
   return on_hi_stream(c, [&](Ctx h) { return potrf_node(h, A, base, W, 0); });

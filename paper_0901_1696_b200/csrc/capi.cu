@@ -179,11 +179,12 @@ constexpr TuneTable kTune[TK_COUNT] = {
     {"oop_max", 4096},       {"t2_copy_min", 2048}, {"panel_max", 4096},
     {"pfsv_overlap_min", 512}, {"overlap", 1},      {"graphs", 1},
     {"graph_max_n", 8192},   {"gemm_wide", 0},      {"batched_generic", 0},
-    {"trace", 0},            {"trsm_split", 1}};
+    {"trace", 0},            {"trsm_split", 1},
+    {"zpotrf_split_min", 9000}};
 std::atomic<long long> g_tune[TK_COUNT] = {
     {kTune[0].dflt}, {kTune[1].dflt}, {kTune[2].dflt}, {kTune[3].dflt}, {kTune[4].dflt},
     {kTune[5].dflt}, {kTune[6].dflt}, {kTune[7].dflt}, {kTune[8].dflt}, {kTune[9].dflt},
-    {kTune[10].dflt}};
+    {kTune[10].dflt}, {kTune[11].dflt}};
 int tune_index(const char* name) {
   if (!name) return -1;
   for (int i = 0; i < TK_COUNT; ++i)

@@ -214,6 +214,7 @@ enum TuneKey : int {
   TK_BATCHED_GENERIC,      // force the generic batched kernel at n = 64 (0)
   TK_TRACE,                // print per-phase SRPA times to stderr (0)
   TK_TRSM_SPLIT,           // tile trsm: split tasks: 0 off, 1 automatic, > 1 kept chunks (1)
+  TK_ZPOTRF_SPLIT_MIN,     // complex potrf: one GEMM-level split from this order (9000)
   TK_COUNT
 };
 long long tune(TuneKey k);  // defined in capi.cu

@@ -142,6 +142,28 @@ def test_potrf_failure_and_trtri_zero(K):
     assert np.array_equal(td.cpu().numpy(), t)  # untouched (kernels.py:526-529)
 
 
+@pytest.mark.parametrize("uplo", "LU")
+def test_zpotrf_split_level(K, uplo):
+    """Complex potrf with the GEMM-level split forced at a small order (tuning
+    zpotrf_split_min): the halves on the tile kernel, the panel solve and the
+    HERK between them; the factor against the oracle, and a failing pivot in
+    each half reported at its global index."""
+    from paper_0901_1696_b200 import _capi
+    n = 700
+    g = rnd((n, n), True, 31)
+    a = np.asfortranarray(g @ np.conj(g.T) + n * np.eye(n))
+    want = a.copy(order="F")
+    assert O.potrf(uplo, want) == 0
+    with _capi.tuning(zpotrf_split_min=300):
+        ad = dev(a)
+        assert K.potrf_ref(uplo, ad) == 0
+        assert rel(ad, want) <= TOL
+        for bad in (100, 500):
+            b = a.copy(order="F")
+            b[bad, bad] = -1.0
+            assert K.potrf_ref(uplo, dev(b)) == O.potrf(uplo, b.copy(order="F")) == bad + 1
+
+
 # ---------------------------------------------------------------- dataflow tile kernels
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("uplo", "LU")

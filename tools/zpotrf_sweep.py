@@ -4,6 +4,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.ins
 from paper_0901_1696_b200 import _capi
 lib = _capi.lib(); dev = torch.device("cuda:0"); st = _capi.stream_handle(dev)
 info = torch.zeros(1, dtype=torch.int32, device=dev)
+if "ZSPLIT" in os.environ:  # tuning zpotrf_split_min (a huge value = never split)
+    _capi.set_tuning("zpotrf_split_min", int(os.environ["ZSPLIT"]))
 for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1000,3000,6000").split(",")]:
     g = torch.randn(n, n, dtype=torch.complex128, device=dev); a = g @ g.mH / n; a.diagonal().add_(1.0)
     pad = int(os.environ.get("LDPAD", "0"))
