@@ -75,8 +75,10 @@ __device__ __forceinline__ Z fnmac(Z a, Z b, Z c) {
 __device__ __forceinline__ double rsqrt_pivot(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);
-  return fma(y, e * fma(0.375, e, 0.5), y);
+  // (four dependent FP64 operations after the seed: y^2 | e | {3e/8 + 1/2,
+  // y e} | the sum -- this value heads the serial chain of every pivot)
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 // CTA barrier for code where single threads run the flag protocol (spins,
