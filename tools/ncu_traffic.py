@@ -66,6 +66,18 @@ for k, a in sorted(acc.items(), key=lambda kv: -kv[1]["ms_ncu"]):
     n = a["n"]
     out[k] = {"bytes": (a["read"] + a["write"]) / n, "read": a["read"] / n,
               "write": a["write"] / n, "ms_ncu": a["ms_ncu"] / n, "launches_in_step": n}
+# config 4's kernel: from the summary of its own `ncu --set full` capture
+# (tools/ncu_summary.py prints the DRAM counters in GB)
+import glob
+import re
+caps = sorted(glob.glob("profiles/r*_prof_batched_v*_summary.txt"),
+              key=lambda f: [int(x) for x in re.findall(r"\d+", f)])
+if caps:
+    vals = dict(l.split()[:2] for l in open(caps[-1]) if l.startswith(("dram__", "gpu__time")))
+    rd, wr = float(vals["dram__bytes_read.sum"]) * 1e9, float(vals["dram__bytes_write.sum"]) * 1e9
+    out["kernel batched64 65536x8"] = {"bytes": rd + wr, "read": rd, "write": wr,
+                                       "ms_ncu": float(vals["gpu__time_duration.sum"]),
+                                       "launches_in_step": 1, "source": caps[-1]}
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 tot = sum(a["ms_ncu"] for a in acc.values())
 for k, a in sorted(acc.items(), key=lambda kv: -kv[1]["ms_ncu"]):
