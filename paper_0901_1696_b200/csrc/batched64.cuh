@@ -101,14 +101,18 @@ template <bool T> struct RV {
 // entries).  The pivot column is broadcast through colk (double-buffered,
 // 16-byte pairs); the next pivot comes straight from lane p+1's registers.
 // 16-wide rows halve the broadcast volume of a 32-wide right-looking sweep.
-// The view orientation T and the panel C0 are compile-time, so every row
-// slot is an immediate offset from the lane's row pointer.  Lanes whose row
+// The view orientation T is compile-time, so every row slot is an immediate
+// offset from the lane's row pointer; the panel C0 (0 or 16) is a run-time
+// argument -- two instantiations instead of four shrink the fused kernel from
+// 73 to 56 KB of straight-line code, which its three warps per scheduler
+// fetch at different places (ncu: no_instruction 13% of the stall cycles;
+// 59.9 -> 61.0 M matrices/s).  Lanes whose row
 // lies above the panel (and the slots of a row above its diagonal, which
 // belong to the other RFP block) load and update garbage that is never
 // broadcast or stored.  Returns 0 or the failing pivot (1-based in the view;
 // NaN fails like the reference's `not d > 0`, kernels.py:436).
-template <bool T, int C0>
-__device__ __noinline__ int panel16(double* p, double* colk) {
+template <bool T>
+__device__ __noinline__ int panel16(double* p, double* colk, int C0) {
   __builtin_assume(__isShared(p));
   __builtin_assume(__isShared(colk));
   const int lane = threadIdx.x & 31;
@@ -152,7 +156,7 @@ __device__ __noinline__ int panel16(double* p, double* colk) {
 // L21), V22 -= L21 L21^T on DMMA (m16n8k4, lower tiles), panel [16, 32).
 template <bool T>
 __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* colk) {
-  int f = panel16<T, 0>(p, colk);
+  int f = panel16<T>(p, colk, 0);
   if (f) return f;
   const RV<T> V{p};
   double acc[2][4];
@@ -179,7 +183,7 @@ __device__ __forceinline__ int factor32(const LaneOff& o, double* p, double* col
       }
     }
   __syncwarp();
-  return panel16<T, 16>(p, colk);
+  return panel16<T>(p, colk, 16);
 }
 
 // In-place inverse of the lower 32x32 view (only its lower triangle is read
