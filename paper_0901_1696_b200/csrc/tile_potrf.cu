@@ -150,7 +150,6 @@ __device__ bool spin_wait(const int* f, const int* abort) {
 template <typename T> struct TileCfg {
   static constexpr bool CPLX = is_cplx<T>::value;
   static constexpr int BK = CPLX ? 8 : 16;
-  static constexpr int SPC = TP / BK;  // k-slices per 64-chunk
   static constexpr int NACC = CPLX ? 2 : 1;
 };
 
@@ -159,19 +158,26 @@ template <typename T> struct TileCfg {
 // slice of a row (128 B real) straddles 5 sectors instead of 4; 32-wide
 // slices (256 B: 9 instead of 8) with two stages keep three CTAs per SM and
 // measured 9.1 -> ~7.8 ms on potrf(8192) with ld 8193.
-template <typename T, bool KM> struct PipeCfg {
+// Column-major (MN-major) real operands of the single-region kernel (the
+// large orders): four stages of 8 k instead of three of 16, as in the GEMM
+// kernel -- alone the potrf does not change (8192: 6.93 vs 6.94 ms), beside
+// the gated S1 solve and beside pftrs part 1 it does (config 3: 23.8 -> 23.2
+// and 13.9 -> 13.2 ms).  The two-region chain of the mid orders keeps 16 x 3
+// (config 2 measured +-1% either way).
+template <typename T, bool KM, bool TWO> struct PipeCfg {
   static constexpr bool CPLX = is_cplx<T>::value;
-  static constexpr int BK = KM ? (CPLX ? 16 : 32) : (CPLX ? 8 : 16);
-  static constexpr int ST = (KM && !CPLX) ? 2 : 3;
+  static constexpr bool FINE = !KM && !CPLX && !TWO;
+  static constexpr int BK = KM ? (CPLX ? 16 : 32) : (CPLX || FINE ? 8 : 16);
+  static constexpr int ST = (KM && !CPLX) ? 2 : (FINE ? 4 : 3);
   static constexpr int SPC = TP / BK;
 };
 
-template <typename T, bool KM> size_t pipe_smem_elems() {
-  using P = PipeCfg<T, KM>;
+template <typename T, bool KM, bool TWO> size_t pipe_smem_elems() {
+  using P = PipeCfg<T, KM, TWO>;
   return (size_t)P::ST * 2 * SmemLayout<T, TP, P::BK, KM>::SIZE;
 }
-template <typename T, bool KM0, bool KM1> size_t tile_smem_bytes() {
-  const size_t p0 = pipe_smem_elems<T, KM0>(), p1 = pipe_smem_elems<T, KM1>();
+template <typename T, bool KM0, bool KM1, bool TWO> size_t tile_smem_bytes() {
+  const size_t p0 = pipe_smem_elems<T, KM0, TWO>(), p1 = pipe_smem_elems<T, KM1, TWO>();
   const size_t pipe = p0 > p1 ? p0 : p1;
   const size_t leaf = (size_t)2 * TP * LD64 + 128;
   return (pipe > leaf ? pipe : leaf) * sizeof(T);
@@ -353,7 +359,7 @@ template <typename T, bool KM, bool TWO>
 __device__ bool acc_range(const CholCtx<T, TWO>& X, const View<T>& V, int roff, int i, int j, int kb,
                           int ke, T* sm, int* s_ok, double (&acc)[TileCfg<T>::NACC][2][4][4]) {
   using C = TileCfg<T>;
-  using P = PipeCfg<T, KM>;
+  using P = PipeCfg<T, KM, TWO>;
   using LA = SmemLayout<T, TP, P::BK, KM>;
   constexpr int BK = P::BK, SPC = P::SPC, STAGES = P::ST;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -824,7 +830,7 @@ template <typename T, bool KM0, bool KM1, bool TWO>
 int tile_launch(View<T> A, View<T> B, int n1, int nt1, int ncols, T* W, Ctx c, int base, int* sync,
                 int nt, int mt) {
   auto kern = tile_potrf_kernel<T, KM0, KM1, TWO>;
-  const size_t smem = tile_smem_bytes<T, KM0, KM1>();
+  const size_t smem = tile_smem_bytes<T, KM0, KM1, TWO>();
   const int per_sm = kernel_setup(kern, TPT, smem);
   const long long tasks = chol_task_count(nt, mt);
   // two CTAs per SM up to ~12k columns: the diagonal chain's CTA then shares
@@ -918,6 +924,16 @@ __device__ __forceinline__ void smem_mm_ab(
 // register budget already limits the kernel to two CTAs per SM (the
 // column-major-B variants), so the extra 33 KB costs no occupancy
 template <typename T, bool BKM> constexpr bool trsm_prew() { return BKM && !is_cplx<T>::value; }
+// the solve's cp.async pipeline: real wide tiles take four stages of 8 k
+// (S1 solve of config 3 alone 17.51 -> 17.19 ms, pftrs's 8192 x 1024 solves
+// 2.59 -> 2.54 ms); the narrow, chain-bound tiles keep three of 16 (pftrs at
+// n = 4000, nrhs = 64: 0.716 vs 0.750 ms)
+template <typename T, int TN> struct TrsmPipe {
+  static constexpr bool FINE = !is_cplx<T>::value && TN >= TP;
+  static constexpr int BK = FINE ? 8 : TileCfg<T>::BK;
+  static constexpr int ST = FINE ? 4 : STAGES;
+  static constexpr int SPC = TP / BK;
+};
 
 struct TrsmArgs {
   int n, nrhs, nb, nc;
@@ -970,11 +986,13 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     if (!*s_ok) return false;
   }
   using C = TileCfg<T>;
-  using LA = SmemLayout<T, TP, C::BK, AK>;
-  using LB = SmemLayout<T, TN, C::BK, BKM>;
+  using PP = TrsmPipe<T, TN>;
+  constexpr int STAGES = PP::ST;  // (shadows the file-wide default)
+  using LA = SmemLayout<T, TP, PP::BK, AK>;
+  using LB = SmemLayout<T, TN, PP::BK, BKM>;
   using WL = TrsmTile<TN>;
   constexpr int MI = WL::MI, NI = WL::NI;
-  constexpr int NACC = C::NACC, BK = C::BK, SPC = C::SPC;
+  constexpr int NACC = C::NACC, BK = PP::BK, SPC = PP::SPC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WL::WMW, wn = warp / WL::WMW, gq = lane >> 2, tq = lane & 3;
   T* As = sm;
@@ -1328,8 +1346,9 @@ __global__ void __launch_bounds__(TPT, TN < TP ? 3 : (TN > TP ? 2 : ((BKM || is_
 
 template <typename T, bool AK, bool BKM, int TN> size_t trsm_smem_bytes() {
   using C = TileCfg<T>;
-  const size_t pipe = (size_t)STAGES * (SmemLayout<T, TP, C::BK, AK>::SIZE +
-                                        SmemLayout<T, TN, C::BK, BKM>::SIZE);
+  using PP = TrsmPipe<T, TN>;
+  const size_t pipe = (size_t)PP::ST * (SmemLayout<T, TP, PP::BK, AK>::SIZE +
+                                        SmemLayout<T, TN, PP::BK, BKM>::SIZE);
   const size_t stile = (size_t)(TN > TP ? TN : TP) * LD64, one = (size_t)TP * LD64;
   if (trsm_prew<T, BKM>()) return ((pipe > stile ? pipe : stile) + one) * sizeof(T);
   const size_t tiles = stile + one;  // S and W'_i
