@@ -243,7 +243,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs<T>& g, int tm, int tn, 
 
 template <typename T, int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int MODE>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
-                                  (BM * BN <= 64 * 64) ? (is_cplx<T>::value ? 2 : 4) : 1)
+                                  (BM * BN <= 64 * 64) ? (is_cplx<T>::value ? 2 : (STAGES <= 3 ? 4 : 3)) : 1)
     gemm_kernel(GemmArgs<T> g) {
   using LA = SmemLayout<T, BM, BK, AK>;
   extern __shared__ __align__(16) double smem_d[];
@@ -555,13 +555,15 @@ int gemm(int tri_mode, T alpha, View<T> A, bool conjA, View<T> B, bool conjB, T 
       return launch_mode<T, 64, 64, 8, 32, 32, 4>(g, tri_mode, ak, bk, st);
     return launch_mode<T, 32, 32, 8, 16, 16, 3>(g, tri_mode, ak, bk, st);
   } else {
-    // 64 x 64 tiles, 4 warps of 32 x 32, FOUR stages of EIGHT k, 4 CTAs per
-    // SM (128 registers): the measured best FP64 config.  Against the former
-    // three stages of 16 k (same tile, 52 KB of shared memory per CTA instead
-    // of 35): config 3's SYRK 16.73 -> 16.40 ms (tools/dom_syrk.py; 16 k x 4
-    // stages 16.80, 8 k x 3 / 5 / 6 stages 17.07 / 17.28 / 18.23, 32 k x 2
-    // 17.80, 4 k x 8 19.33; 8 k x 4 at three CTAs per SM and 150 registers
-    // 16.45).  (33 TFLOP/s at 8192^3 vs 31 for a 1-CTA/SM 128 x 128 tile:
+    // 64 x 64 tiles, 4 warps of 32 x 32, FOUR stages of EIGHT k, three CTAs
+    // per SM at 150 registers: the measured best FP64 config.  Against the
+    // former three stages of 16 k at four CTAs per SM (128 registers, 52 KB of
+    // shared memory per CTA instead of 35): config 3's SYRK 16.73 -> 16.45 ms
+    // by itself (tools/dom_syrk.py; 16 k x 4 stages 16.80, 8 k x 3 / 5 / 6
+    // stages 17.07 / 17.28 / 18.23, 32 k x 2 17.80, 4 k x 8 19.33) and 16.42
+    // -> 16.20 ms inside the bench step; capped at 128 registers for four
+    // CTAs per SM it is 16.40 ms alone but 16.45 in the step (bench 65.00 vs
+    // 64.50 ms).  (33 TFLOP/s at 8192^3 vs 31 for a 1-CTA/SM 128 x 128 tile:
     // more resident CTAs hide the per-stage barrier.)
     const bool force_wide = tune(TK_GEMM_WIDE) != 0;
     // 64 x 128 tiles (4 warps of 32 x 64: 12 fragment loads per 16 DMMAs
