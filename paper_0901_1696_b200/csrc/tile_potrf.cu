@@ -1204,6 +1204,10 @@ __device__ bool trsm_task(const View<T>& Tm, const View<T>& B, const T* W, const
     return true;
   }
   if (kind == 1) {  // B(i, c) as the PRE task left it
+    // (release/acquire through thread 0 and the CTA barriers on both sides,
+    // as for the done flags: the PRE task's stores happen before every
+    // thread's loads of the tile below.  Reading the tile with ld.global.cg
+    // instead was measured: the changed register allocation costs 2.7%.)
     if (tid == 0) spin_wait_acquire(a.pre + (i64)i * a.nc + c);
     cta_sync();
   }
