@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(NT) batched_kernel(RfpDesc r, double* arf, i64
 constexpr int B64_SMEM_DOUBLES = b64::RECT + 96;
 
 template <bool LOWER, int TRANS, bool FACTOR, bool SOLVE>
-__global__ void __launch_bounds__(32) batched64_kernel(double* arf, i64 stride_arf, int nrhs,
+__global__ void __launch_bounds__(32, 12) batched64_kernel(double* arf, i64 stride_arf, int nrhs,
                                                        double* b, i64 ldb, i64 stride_b,
                                                        int* info) {
   using namespace b64;
